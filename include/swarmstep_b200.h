@@ -1,0 +1,157 @@
+/*
+ * swarmstep_b200.h -- C ABI of the B200 quadrotor-group library
+ * (paper_2308_12698_b200/libswarmstep_b200.so).
+ *
+ * The reference (swarmstep, /root/reference/pkg/src/swarmstep) has no FFI:
+ * its World duck-types homogeneous groups (core.py:308-318, 455-475) and the
+ * quadrotor group's hot path is QuadGroup.step (core.py:166-202).  These
+ * entry points are what that group protocol needs underneath; the Python
+ * host class paper_2308_12698_b200.group.B200QuadGroup binds them with
+ * ctypes and implements the reference's group protocol on top.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Device memory is borrowed (the caller
+ *    owns it); nothing here allocates except the library's own error string.
+ *  - Every call returns an int status: SWARMSTEP_OK (0) or a negative code;
+ *    swarmstep_last_error() returns the thread-local message.  Nothing throws
+ *    across the ABI.
+ *  - `stream` is a cudaStream_t passed as void*; every launch is async on it.
+ *    Calls on distinct streams over distinct groups are thread-safe.
+ *  - State is structure-of-arrays float32, one column per scalar component,
+ *    each column `stride` floats long (stride >= n, multiple of 32, 16-byte
+ *    aligned).  Rows in [n, stride) must have flags == 0 (dead padding).
+ */
+#ifndef SWARMSTEP_B200_H
+#define SWARMSTEP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SWARMSTEP_ABI_VERSION 1
+
+enum {
+    SWARMSTEP_OK = 0,
+    SWARMSTEP_EINVAL = -1,   /* bad argument (maps to ValidationError) */
+    SWARMSTEP_ECUDA = -2,    /* CUDA launch / runtime error            */
+    SWARMSTEP_ENODEV = -3    /* no usable sm_100 device                */
+};
+
+/* per-row flag byte (the reference's alive / has_prev / cmd_level columns:
+ * state.py:57-65, control.py:100-104, core.py:98-104) */
+#define SWARMSTEP_FLAG_ALIVE     0x01u
+#define SWARMSTEP_FLAG_HAS_PREV  0x02u
+#define SWARMSTEP_LEVEL_SHIFT    2
+#define SWARMSTEP_LEVEL_MASK     0x0Cu
+enum { SWARMSTEP_LEVEL_POS = 0, SWARMSTEP_LEVEL_RATE = 1, SWARMSTEP_LEVEL_MOTOR = 2 }; /* core.py:73 */
+
+/* Per-type constants, float32 (QuadParams quad.py:39-69, PidGains
+ * control.py:40-53, OuterGains control.py:56-68).  G / G_inv are the 4x4
+ * allocation matrix and its inverse (quad.py:106-122), row-major. */
+typedef struct swarmstep_quad_params {
+    float m, inv_m, g;
+    float inv_ixx, inv_iyy, inv_izz;
+    float ixx, iyy, izz;
+    float k_t, omega_max, f_max, fc_max;      /* fc_max = 4 * f_max (control.py:253) */
+    float G[16];
+    float G_inv[16];
+    float kp[3], ki[3], kd[3], i_limit[3];
+    float kp_pos[3], kv[3], k_att[3];
+    float omega_sp_max, a_cmd_min;
+    float _pad[2];
+} swarmstep_quad_params;
+
+/* Column block offsets inside `cols` (each block is k columns of `stride`). */
+enum {
+    SWARMSTEP_COL_POS = 0,      /* px py pz          (state.py:57)          */
+    SWARMSTEP_COL_VEL = 3,      /* vx vy vz                                 */
+    SWARMSTEP_COL_QUAT = 6,     /* qw qx qy qz (scalar-first Hamilton)      */
+    SWARMSTEP_COL_OMEGA = 10,   /* wx wy wz (body rates)                    */
+    SWARMSTEP_COL_POS_LO = 13,  /* compensated-position low words           */
+    SWARMSTEP_COL_INTEGRAL = 16,/* RatePidState.integral (control.py:103)   */
+    SWARMSTEP_COL_PREV = 19,    /* RatePidState.prev_omega                  */
+    SWARMSTEP_COL_SP = 22,      /* QuadGroup.omega_sp xyz, f_c_sp (core.py:109-110) */
+    SWARMSTEP_COL_CMD = 26,     /* QuadGroup.cmd_values[0..6] (core.py:99)  */
+    SWARMSTEP_COL_OVERLAY = 33, /* QuadGroup.v_overlay (core.py:106)        */
+    SWARMSTEP_NCOL = 36
+};
+
+/* A borrowed view of one group's device columns. */
+typedef struct swarmstep_group_view {
+    int64_t n;              /* live rows                                    */
+    int64_t stride;         /* floats per column (>= n, multiple of 32)     */
+    float *cols;            /* [SWARMSTEP_NCOL][stride] float32             */
+    uint8_t *flags;         /* [stride]                                     */
+    uint32_t *counters;     /* device [4]: 0 fault count, 1 scratch count   */
+    uint64_t *fault_log;    /* device [fault_cap]: (substep << 40) | row    */
+    int64_t fault_cap;
+    int32_t compensated;    /* 1: position = hi + lo (COL_POS_LO in use)    */
+    int32_t _pad;
+} swarmstep_group_view;
+
+/* Library / device info.  Returns SWARMSTEP_ABI_VERSION. */
+int swarmstep_abi_version(void);
+const char *swarmstep_last_error(void);
+/* Fills sm count and compute capability of the current device. */
+int swarmstep_device_info(int *sm_count, int *cc_major, int *cc_minor);
+
+/* One launch = k_substeps successive QuadGroup.step(dt) calls
+ * (core.py:166-202) with commands held fixed: setpoint selection by level,
+ * position_outer_loop (control.py:222-294), rate_pid_step (control.py:136-187),
+ * mix_to_motors (quad.py:143-168), raw-motor override (core.py:189-197) and
+ * rk4_step (quad.py:350-437) including fault revert + kill.  The overlay
+ * column block is added to v_sp on substep 0 only when overlay_active != 0
+ * (core.py:172-175, 199-201); the caller clears it afterwards.
+ * Faulted rows are appended to fault_log and counted in counters[0]
+ * (the caller zeroes counters[0] before the launch).
+ * Replaces: QuadGroup.step (core.py:166).  Errors: dt <= 0 or k < 1 ->
+ * SWARMSTEP_EINVAL (quad.py:359-360, control.py:154-155). */
+int swarmstep_quad_step(const swarmstep_group_view *g, const swarmstep_quad_params *p,
+                        float dt, int k_substeps, int overlay_active, void *stream);
+
+/* Latest-wins command scatter (QuadGroup.apply_command, core.py:117-135).
+ * rows[i] (int64), levels[i] (uint8, SWARMSTEP_LEVEL_*), values[i*7..]
+ * (float32; RATE/MOTOR entries carry 4 values and zeros) are device arrays;
+ * rows must be unique.  Dead rows are skipped on device as well. */
+int swarmstep_quad_apply_commands(const swarmstep_group_view *g, const int64_t *rows,
+                                  const uint8_t *levels, const float *values,
+                                  int64_t count, void *stream);
+
+/* Bulk device setpoints: every row in [row0, row0+count) gets `level` and
+ * values from the column block `values` ([7][ld] float32, device), alive
+ * rows only.  The device-resident setpoint feed. */
+int swarmstep_quad_set_setpoints(const swarmstep_group_view *g, int64_t row0, int64_t count,
+                                 int level, const float *values, int64_t ld, void *stream);
+
+/* mark_dead (core.py:151-158): rows[i] unique device int64; was_alive[i]
+ * (uint8, device) receives 1 where the row was alive before the call. */
+int swarmstep_quad_mark_dead(const swarmstep_group_view *g, const int64_t *rows,
+                             uint8_t *was_alive, int64_t count, void *stream);
+
+/* retarget_waypoint (core.py:141-149): alive rows with |p - point| < radius
+ * switch to POS level with p_sp = point, v_sp = 0, yaw_sp = quat_yaw(q)
+ * (quat.py:139-143).  counters[1] += number of rows retargeted. */
+int swarmstep_quad_retarget_waypoint(const swarmstep_group_view *g, const double *point3,
+                                     double radius, void *stream);
+
+/* Device-side snapshot packing (batch_snapshot, state.py:193-204): writes
+ * float64 row-major pos (n,3), vel (n,3), quat (n,4), omega (n,3) and
+ * alive (n,) u8 / level (n,) u8 into the device buffers given (any may be
+ * NULL).  Position is hi + lo when compensated. */
+int swarmstep_quad_pack_f64(const swarmstep_group_view *g, double *pos, double *vel,
+                            double *quat, double *omega, uint8_t *alive, void *stream);
+
+/* Inverse of the above: loads float64 row-major host-layout columns (device
+ * pointers) into the float32 SoA columns, splitting position into hi + lo
+ * when compensated.  Flags: alive from `alive` (u8), has_prev cleared,
+ * level left unchanged. */
+int swarmstep_quad_unpack_f64(const swarmstep_group_view *g, const double *pos,
+                              const double *vel, const double *quat, const double *omega,
+                              const uint8_t *alive, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SWARMSTEP_B200_H */

@@ -1,0 +1,106 @@
+"""ctypes binding of libswarmstep_b200.so (declarations: include/swarmstep_b200.h).
+
+There is no fallback: if the library is missing or cannot be loaded, every
+product entry point raises ``NativeLibraryError``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from pathlib import Path
+
+from .errors import NativeLibraryError, ValidationError
+
+LIB_PATH = Path(__file__).resolve().parent / "libswarmstep_b200.so"
+
+SWARMSTEP_OK, SWARMSTEP_EINVAL, SWARMSTEP_ECUDA, SWARMSTEP_ENODEV = 0, -1, -2, -3
+ABI_VERSION = 1
+
+# column block offsets (SWARMSTEP_COL_*)
+COL_POS, COL_VEL, COL_QUAT, COL_OMEGA = 0, 3, 6, 10
+COL_POS_LO, COL_INTEGRAL, COL_PREV, COL_SP, COL_CMD, COL_OVERLAY = 13, 16, 19, 22, 26, 33
+NCOL = 36
+FLAG_ALIVE, FLAG_HAS_PREV, LEVEL_SHIFT, LEVEL_MASK = 0x01, 0x02, 2, 0x0C
+
+# every symbol include/swarmstep_b200.h declares
+EXPORTS = (
+    "swarmstep_abi_version", "swarmstep_last_error", "swarmstep_device_info",
+    "swarmstep_quad_step", "swarmstep_quad_apply_commands", "swarmstep_quad_set_setpoints",
+    "swarmstep_quad_mark_dead", "swarmstep_quad_retarget_waypoint",
+    "swarmstep_quad_pack_f64", "swarmstep_quad_unpack_f64",
+)
+
+
+class GroupView(ctypes.Structure):
+    """ctypes mirror of ``swarmstep_group_view``."""
+
+    _fields_ = [
+        ("n", ctypes.c_int64), ("stride", ctypes.c_int64),
+        ("cols", ctypes.c_void_p), ("flags", ctypes.c_void_p),
+        ("counters", ctypes.c_void_p), ("fault_log", ctypes.c_void_p),
+        ("fault_cap", ctypes.c_int64),
+        ("compensated", ctypes.c_int32), ("_pad", ctypes.c_int32),
+    ]
+
+
+_lock = threading.Lock()
+_lib = None
+
+
+def _declare(lib) -> None:
+    vp, i64, i32, f32, f64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_float, ctypes.c_double
+    view = ctypes.POINTER(GroupView)
+    lib.swarmstep_abi_version.restype = i32
+    lib.swarmstep_abi_version.argtypes = []
+    lib.swarmstep_last_error.restype = ctypes.c_char_p
+    lib.swarmstep_last_error.argtypes = []
+    lib.swarmstep_device_info.restype = i32
+    lib.swarmstep_device_info.argtypes = [ctypes.POINTER(i32)] * 3
+    lib.swarmstep_quad_step.restype = i32
+    lib.swarmstep_quad_step.argtypes = [view, vp, f32, i32, i32, vp]
+    lib.swarmstep_quad_apply_commands.restype = i32
+    lib.swarmstep_quad_apply_commands.argtypes = [view, vp, vp, vp, i64, vp]
+    lib.swarmstep_quad_set_setpoints.restype = i32
+    lib.swarmstep_quad_set_setpoints.argtypes = [view, i64, i64, i32, vp, i64, vp]
+    lib.swarmstep_quad_mark_dead.restype = i32
+    lib.swarmstep_quad_mark_dead.argtypes = [view, vp, vp, i64, vp]
+    lib.swarmstep_quad_retarget_waypoint.restype = i32
+    lib.swarmstep_quad_retarget_waypoint.argtypes = [view, ctypes.POINTER(f64), f64, vp]
+    lib.swarmstep_quad_pack_f64.restype = i32
+    lib.swarmstep_quad_pack_f64.argtypes = [view, vp, vp, vp, vp, vp, vp]
+    lib.swarmstep_quad_unpack_f64.restype = i32
+    lib.swarmstep_quad_unpack_f64.argtypes = [view, vp, vp, vp, vp, vp, vp]
+
+
+def load():
+    """Load (once) and return the native library; raises if it is unavailable."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not LIB_PATH.exists():
+            raise NativeLibraryError(
+                f"{LIB_PATH.name} is not built; run `python -m paper_2308_12698_b200._build` "
+                "(there is no CPU fallback)")
+        try:
+            lib = ctypes.CDLL(str(LIB_PATH))
+        except OSError as exc:
+            raise NativeLibraryError(f"cannot load {LIB_PATH}: {exc}") from exc
+        _declare(lib)
+        if lib.swarmstep_abi_version() != ABI_VERSION:
+            raise NativeLibraryError("ABI version mismatch between Python binding and library")
+        _lib = lib
+        return _lib
+
+
+def check(status: int) -> None:
+    """Map a C-ABI status onto the exception hierarchy."""
+    if status == SWARMSTEP_OK:
+        return
+    msg = (load().swarmstep_last_error() or b"").decode(errors="replace")
+    if status == SWARMSTEP_EINVAL:
+        raise ValidationError(msg)
+    raise NativeLibraryError(f"swarmstep status {status}: {msg}")

@@ -1,0 +1,401 @@
+// swarmstep_b200.cu -- sm_100a kernels and the C ABI (include/swarmstep_b200.h).
+//
+// Hot path: quad_step_kernel = K fused QuadGroup.step(dt) calls
+// (core.py:166-202) per launch, one agent per thread, state register-resident
+// across the K substeps.  Columns are float32 SoA (one column per scalar
+// component), so every warp-wide load/store of a component is one fully
+// coalesced 128-byte line.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "swarmstep_b200.h"
+#include "quad_math.cuh"
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int set_err(int code, const char *msg)
+{
+    snprintf(g_err, sizeof(g_err), "%s", msg);
+    return code;
+}
+
+int cuda_status(const char *where)
+{
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
+        return SWARMSTEP_ECUDA;
+    }
+    return SWARMSTEP_OK;
+}
+
+int check_view(const swarmstep_group_view *g)
+{
+    if (!g || !g->cols || !g->flags) return set_err(SWARMSTEP_EINVAL, "null group view");
+    if (g->n < 0 || g->stride < g->n || (g->stride % 32) != 0)
+        return set_err(SWARMSTEP_EINVAL, "bad n/stride (stride must be >= n and a multiple of 32)");
+    if ((reinterpret_cast<uintptr_t>(g->cols) & 15u) != 0)
+        return set_err(SWARMSTEP_EINVAL, "cols must be 16-byte aligned");
+    return SWARMSTEP_OK;
+}
+
+constexpr int kBlock = 256;
+
+struct Cols {
+    float *c;
+    int64_t s;
+    __device__ __forceinline__ float *col(int k) const { return c + (int64_t)k * s; }
+};
+
+// ---------------------------------------------------------------------------
+// The fused step kernel.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kBlock)
+quad_step_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t n, int64_t stride,
+                 uint32_t *__restrict__ counters, uint64_t *__restrict__ fault_log,
+                 int64_t fault_cap, int compensated, int overlay_active,
+                 const swarmstep_quad_params P, float dt, int K)
+{
+    const int64_t r = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    if (r >= n) return;
+    uint8_t fl = flags[r];
+    if (!(fl & SWARMSTEP_FLAG_ALIVE)) return;  // dead rows are frozen (quad.py:395-437)
+    const int level = (fl & SWARMSTEP_LEVEL_MASK) >> SWARMSTEP_LEVEL_SHIFT;
+    const Cols C{cols, stride};
+
+    // ---- load state (register-resident for all K substeps) ----
+    float p_hi[3], p_lo[3], v[3], q[4], w[3], integ[3], prev[3];
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+        p_hi[i] = __ldcs(C.col(SWARMSTEP_COL_POS + i) + r);
+        v[i] = __ldcs(C.col(SWARMSTEP_COL_VEL + i) + r);
+        w[i] = __ldcs(C.col(SWARMSTEP_COL_OMEGA + i) + r);
+        integ[i] = __ldcs(C.col(SWARMSTEP_COL_INTEGRAL + i) + r);
+        prev[i] = __ldcs(C.col(SWARMSTEP_COL_PREV + i) + r);
+        p_lo[i] = compensated ? __ldcs(C.col(SWARMSTEP_COL_POS_LO + i) + r) : 0.0f;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; i++) q[i] = __ldcs(C.col(SWARMSTEP_COL_QUAT + i) + r);
+    bool has_prev = (fl & SWARMSTEP_FLAG_HAS_PREV) != 0;
+
+    // ---- per-launch setpoint inputs (commands are fixed across substeps) ----
+    float cmd[7];
+    float w_sp[3], f_sp;
+    float mot_fc = 0.0f, mot_tau[3] = {0.0f, 0.0f, 0.0f};
+    float cy = 1.0f, sy = 0.0f, ov[3] = {0.0f, 0.0f, 0.0f};
+    if (level == SWARMSTEP_LEVEL_POS) {
+#pragma unroll
+        for (int i = 0; i < 7; i++) cmd[i] = __ldg(C.col(SWARMSTEP_COL_CMD + i) + r);
+        sincosf(cmd[6], &sy, &cy);
+        if (overlay_active) {
+#pragma unroll
+            for (int i = 0; i < 3; i++) ov[i] = __ldg(C.col(SWARMSTEP_COL_OVERLAY + i) + r);
+        }
+        w_sp[0] = w_sp[1] = w_sp[2] = f_sp = 0.0f;
+    } else if (level == SWARMSTEP_LEVEL_RATE) {
+#pragma unroll
+        for (int i = 0; i < 4; i++) cmd[i] = __ldg(C.col(SWARMSTEP_COL_CMD + i) + r);
+        w_sp[0] = cmd[0]; w_sp[1] = cmd[1]; w_sp[2] = cmd[2]; f_sp = cmd[3];
+    } else {
+        // MOTOR: PID runs on the stale setpoints (core.py:109-110, 184-186);
+        // the rk4 wrench comes from the rotor model.
+#pragma unroll
+        for (int i = 0; i < 4; i++) cmd[i] = __ldg(C.col(SWARMSTEP_COL_CMD + i) + r);
+        w_sp[0] = __ldg(C.col(SWARMSTEP_COL_SP + 0) + r);
+        w_sp[1] = __ldg(C.col(SWARMSTEP_COL_SP + 1) + r);
+        w_sp[2] = __ldg(C.col(SWARMSTEP_COL_SP + 2) + r);
+        f_sp = __ldg(C.col(SWARMSTEP_COL_SP + 3) + r);
+        ssb::motor_wrench(cmd, P, mot_fc, mot_tau);
+    }
+
+    const float inv_dt = 1.0f / dt;
+    bool alive = true;
+    for (int k = 0; k < K; k++) {
+        if (level == SWARMSTEP_LEVEL_POS) {
+            float p_err[3], v_sp[3];
+#pragma unroll
+            for (int i = 0; i < 3; i++) {
+                p_err[i] = (cmd[i] - p_hi[i]) - p_lo[i];
+                v_sp[i] = (k == 0) ? cmd[3 + i] + ov[i] : cmd[3 + i];
+            }
+            ssb::outer_row(p_err, v, q, v_sp, cy, sy, P, w_sp, f_sp);
+        }
+        float tau[3], f_c = f_sp;
+        ssb::pid_row(w, w_sp, P, dt, inv_dt, integ, prev, has_prev, tau);
+        ssb::mix_row(f_c, tau, P);
+        if (level == SWARMSTEP_LEVEL_MOTOR) {
+            f_c = mot_fc;
+            tau[0] = mot_tau[0]; tau[1] = mot_tau[1]; tau[2] = mot_tau[2];
+        }
+        float p_hi_n[3], p_lo_n[3], v_n[3], q_n[4], w_n[3];
+        const bool ok = ssb::rk4_row(p_hi, p_lo, v, q, w, f_c, tau, P, dt, compensated != 0,
+                                     p_hi_n, p_lo_n, v_n, q_n, w_n);
+        if (!ok) {
+            // fault: revert to pre-step values, kill, report (quad.py:425-436)
+            alive = false;
+            const uint32_t slot = atomicAdd(&counters[0], 1u);
+            if ((int64_t)slot < fault_cap) fault_log[slot] = ((uint64_t)k << 40) | (uint64_t)r;
+            break;
+        }
+#pragma unroll
+        for (int i = 0; i < 3; i++) { p_hi[i] = p_hi_n[i]; p_lo[i] = p_lo_n[i]; v[i] = v_n[i]; w[i] = w_n[i]; }
+#pragma unroll
+        for (int i = 0; i < 4; i++) q[i] = q_n[i];
+    }
+
+    // ---- store ----
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+        __stcs(C.col(SWARMSTEP_COL_POS + i) + r, p_hi[i]);
+        __stcs(C.col(SWARMSTEP_COL_VEL + i) + r, v[i]);
+        __stcs(C.col(SWARMSTEP_COL_OMEGA + i) + r, w[i]);
+        __stcs(C.col(SWARMSTEP_COL_INTEGRAL + i) + r, integ[i]);
+        __stcs(C.col(SWARMSTEP_COL_PREV + i) + r, prev[i]);
+        if (compensated) __stcs(C.col(SWARMSTEP_COL_POS_LO + i) + r, p_lo[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; i++) __stcs(C.col(SWARMSTEP_COL_QUAT + i) + r, q[i]);
+    if (level != SWARMSTEP_LEVEL_MOTOR) {
+        // the last substep's setpoints become the stale setpoints a later
+        // MOTOR command runs the PID on (core.py:178-182)
+        __stcs(C.col(SWARMSTEP_COL_SP + 0) + r, w_sp[0]);
+        __stcs(C.col(SWARMSTEP_COL_SP + 1) + r, w_sp[1]);
+        __stcs(C.col(SWARMSTEP_COL_SP + 2) + r, w_sp[2]);
+        __stcs(C.col(SWARMSTEP_COL_SP + 3) + r, f_sp);
+    }
+    uint8_t nfl = (uint8_t)((fl & SWARMSTEP_LEVEL_MASK) | (alive ? SWARMSTEP_FLAG_ALIVE : 0u) |
+                            (has_prev ? SWARMSTEP_FLAG_HAS_PREV : 0u));
+    if (nfl != fl) flags[r] = nfl;
+}
+
+// ---------------------------------------------------------------------------
+// Command / bookkeeping kernels (off the per-tick hot loop).
+// ---------------------------------------------------------------------------
+__global__ void apply_commands_kernel(float *cols, uint8_t *flags, int64_t stride,
+                                      const int64_t *rows, const uint8_t *levels,
+                                      const float *values, int64_t count)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const int64_t r = rows[i];
+    const uint8_t fl = flags[r];
+    if (!(fl & SWARMSTEP_FLAG_ALIVE)) return;
+    flags[r] = (uint8_t)((fl & ~SWARMSTEP_LEVEL_MASK) | ((levels[i] & 3u) << SWARMSTEP_LEVEL_SHIFT));
+#pragma unroll
+    for (int c = 0; c < 7; c++) cols[(int64_t)(SWARMSTEP_COL_CMD + c) * stride + r] = values[i * 7 + c];
+}
+
+__global__ void set_setpoints_kernel(float *cols, uint8_t *flags, int64_t stride, int64_t row0,
+                                     int64_t count, int level, const float *values, int64_t ld)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const int64_t r = row0 + i;
+    const uint8_t fl = flags[r];
+    if (!(fl & SWARMSTEP_FLAG_ALIVE)) return;
+    const uint8_t nfl = (uint8_t)((fl & ~SWARMSTEP_LEVEL_MASK) | ((level & 3) << SWARMSTEP_LEVEL_SHIFT));
+    if (nfl != fl) flags[r] = nfl;
+    const int nv = level == SWARMSTEP_LEVEL_POS ? 7 : 4;
+    for (int c = 0; c < 7; c++)
+        cols[(int64_t)(SWARMSTEP_COL_CMD + c) * stride + r] = c < nv ? values[(int64_t)c * ld + i] : 0.0f;
+}
+
+__global__ void mark_dead_kernel(uint8_t *flags, const int64_t *rows, uint8_t *was_alive, int64_t count)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const int64_t r = rows[i];
+    const uint8_t fl = flags[r];
+    if (was_alive) was_alive[i] = (fl & SWARMSTEP_FLAG_ALIVE) ? 1 : 0;
+    flags[r] = (uint8_t)(fl & ~SWARMSTEP_FLAG_ALIVE);
+}
+
+__global__ void retarget_kernel(float *cols, uint8_t *flags, int64_t n, int64_t stride, int compensated,
+                                double px, double py, double pz, double radius, uint32_t *counters)
+{
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const uint8_t fl = flags[r];
+    if (!(fl & SWARMSTEP_FLAG_ALIVE)) return;
+    double p[3];
+    for (int i = 0; i < 3; i++) {
+        p[i] = (double)cols[(int64_t)(SWARMSTEP_COL_POS + i) * stride + r];
+        if (compensated) p[i] += (double)cols[(int64_t)(SWARMSTEP_COL_POS_LO + i) * stride + r];
+    }
+    const double dx = p[0] - px, dy = p[1] - py, dz = p[2] - pz;
+    const double d = sqrt(dx * dx + dy * dy + dz * dz);
+    if (!(d < radius)) return;
+    const double w = cols[(int64_t)(SWARMSTEP_COL_QUAT + 0) * stride + r];
+    const double x = cols[(int64_t)(SWARMSTEP_COL_QUAT + 1) * stride + r];
+    const double y = cols[(int64_t)(SWARMSTEP_COL_QUAT + 2) * stride + r];
+    const double z = cols[(int64_t)(SWARMSTEP_COL_QUAT + 3) * stride + r];
+    const double yaw = atan2(2.0 * (w * z + x * y), 1.0 - 2.0 * (y * y + z * z));  // quat.py:139-143
+    flags[r] = (uint8_t)(fl & ~SWARMSTEP_LEVEL_MASK);  // POS level
+    const float vals[7] = {(float)px, (float)py, (float)pz, 0.0f, 0.0f, 0.0f, (float)yaw};
+    for (int c = 0; c < 7; c++) cols[(int64_t)(SWARMSTEP_COL_CMD + c) * stride + r] = vals[c];
+    atomicAdd(&counters[1], 1u);
+}
+
+__global__ void pack_f64_kernel(const float *cols, const uint8_t *flags, int64_t n, int64_t stride,
+                                int compensated, double *pos, double *vel, double *quat,
+                                double *omega, uint8_t *alive)
+{
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    for (int i = 0; i < 3; i++) {
+        if (pos) {
+            double p = cols[(int64_t)(SWARMSTEP_COL_POS + i) * stride + r];
+            if (compensated) p += (double)cols[(int64_t)(SWARMSTEP_COL_POS_LO + i) * stride + r];
+            pos[r * 3 + i] = p;
+        }
+        if (vel) vel[r * 3 + i] = cols[(int64_t)(SWARMSTEP_COL_VEL + i) * stride + r];
+        if (omega) omega[r * 3 + i] = cols[(int64_t)(SWARMSTEP_COL_OMEGA + i) * stride + r];
+    }
+    if (quat)
+        for (int i = 0; i < 4; i++) quat[r * 4 + i] = cols[(int64_t)(SWARMSTEP_COL_QUAT + i) * stride + r];
+    if (alive) alive[r] = (flags[r] & SWARMSTEP_FLAG_ALIVE) ? 1 : 0;
+}
+
+__global__ void unpack_f64_kernel(float *cols, uint8_t *flags, int64_t n, int64_t stride, int compensated,
+                                  const double *pos, const double *vel, const double *quat,
+                                  const double *omega, const uint8_t *alive)
+{
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    for (int i = 0; i < 3; i++) {
+        if (pos) {
+            const double p = pos[r * 3 + i];
+            const float hi = (float)p;
+            cols[(int64_t)(SWARMSTEP_COL_POS + i) * stride + r] = hi;
+            cols[(int64_t)(SWARMSTEP_COL_POS_LO + i) * stride + r] = compensated ? (float)(p - (double)hi) : 0.0f;
+        }
+        if (vel) cols[(int64_t)(SWARMSTEP_COL_VEL + i) * stride + r] = (float)vel[r * 3 + i];
+        if (omega) cols[(int64_t)(SWARMSTEP_COL_OMEGA + i) * stride + r] = (float)omega[r * 3 + i];
+    }
+    if (quat)
+        for (int i = 0; i < 4; i++) cols[(int64_t)(SWARMSTEP_COL_QUAT + i) * stride + r] = (float)quat[r * 4 + i];
+    if (alive) {
+        const uint8_t fl = flags[r];
+        flags[r] = (uint8_t)((fl & SWARMSTEP_LEVEL_MASK) | (alive[r] ? SWARMSTEP_FLAG_ALIVE : 0u));
+    }
+}
+
+inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 1) / block); }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int swarmstep_abi_version(void) { return SWARMSTEP_ABI_VERSION; }
+
+const char *swarmstep_last_error(void) { return g_err; }
+
+int swarmstep_device_info(int *sm_count, int *cc_major, int *cc_minor)
+{
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return cuda_status("cudaGetDevice");
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) return cuda_status("cudaGetDeviceProperties");
+    if (sm_count) *sm_count = prop.multiProcessorCount;
+    if (cc_major) *cc_major = prop.major;
+    if (cc_minor) *cc_minor = prop.minor;
+    if (prop.major != 10) return set_err(SWARMSTEP_ENODEV, "device is not sm_100 (B200)");
+    return SWARMSTEP_OK;
+}
+
+int swarmstep_quad_step(const swarmstep_group_view *g, const swarmstep_quad_params *p, float dt,
+                        int k_substeps, int overlay_active, void *stream)
+{
+    int st = check_view(g);
+    if (st) return st;
+    if (!p) return set_err(SWARMSTEP_EINVAL, "null params");
+    if (!(dt > 0.0f)) return set_err(SWARMSTEP_EINVAL, "dt must be positive");
+    if (k_substeps < 1) return set_err(SWARMSTEP_EINVAL, "k_substeps must be >= 1");
+    if (!g->counters) return set_err(SWARMSTEP_EINVAL, "null counters");
+    if (g->n == 0) return SWARMSTEP_OK;
+    quad_step_kernel<<<grid_for(g->n, kBlock), kBlock, 0, (cudaStream_t)stream>>>(
+        g->cols, g->flags, g->n, g->stride, g->counters, g->fault_log, g->fault_log ? g->fault_cap : 0,
+        g->compensated, overlay_active, *p, dt, k_substeps);
+    return cuda_status("quad_step_kernel");
+}
+
+int swarmstep_quad_apply_commands(const swarmstep_group_view *g, const int64_t *rows, const uint8_t *levels,
+                                  const float *values, int64_t count, void *stream)
+{
+    int st = check_view(g);
+    if (st) return st;
+    if (count < 0) return set_err(SWARMSTEP_EINVAL, "negative count");
+    if (count == 0) return SWARMSTEP_OK;
+    if (!rows || !levels || !values) return set_err(SWARMSTEP_EINVAL, "null command arrays");
+    apply_commands_kernel<<<grid_for(count, 256), 256, 0, (cudaStream_t)stream>>>(
+        g->cols, g->flags, g->stride, rows, levels, values, count);
+    return cuda_status("apply_commands_kernel");
+}
+
+int swarmstep_quad_set_setpoints(const swarmstep_group_view *g, int64_t row0, int64_t count, int level,
+                                 const float *values, int64_t ld, void *stream)
+{
+    int st = check_view(g);
+    if (st) return st;
+    if (row0 < 0 || count < 0 || row0 + count > g->n) return set_err(SWARMSTEP_EINVAL, "row range out of bounds");
+    if (level < 0 || level > 2) return set_err(SWARMSTEP_EINVAL, "bad level");
+    if (count == 0) return SWARMSTEP_OK;
+    if (!values || ld < count) return set_err(SWARMSTEP_EINVAL, "bad values / ld");
+    set_setpoints_kernel<<<grid_for(count, 256), 256, 0, (cudaStream_t)stream>>>(
+        g->cols, g->flags, g->stride, row0, count, level, values, ld);
+    return cuda_status("set_setpoints_kernel");
+}
+
+int swarmstep_quad_mark_dead(const swarmstep_group_view *g, const int64_t *rows, uint8_t *was_alive,
+                             int64_t count, void *stream)
+{
+    int st = check_view(g);
+    if (st) return st;
+    if (count <= 0) return count < 0 ? set_err(SWARMSTEP_EINVAL, "negative count") : SWARMSTEP_OK;
+    if (!rows) return set_err(SWARMSTEP_EINVAL, "null rows");
+    mark_dead_kernel<<<grid_for(count, 256), 256, 0, (cudaStream_t)stream>>>(g->flags, rows, was_alive, count);
+    return cuda_status("mark_dead_kernel");
+}
+
+int swarmstep_quad_retarget_waypoint(const swarmstep_group_view *g, const double *point3, double radius,
+                                     void *stream)
+{
+    int st = check_view(g);
+    if (st) return st;
+    if (!point3 || !g->counters) return set_err(SWARMSTEP_EINVAL, "null point / counters");
+    if (g->n == 0) return SWARMSTEP_OK;
+    retarget_kernel<<<grid_for(g->n, 256), 256, 0, (cudaStream_t)stream>>>(
+        g->cols, g->flags, g->n, g->stride, g->compensated, point3[0], point3[1], point3[2], radius, g->counters);
+    return cuda_status("retarget_kernel");
+}
+
+int swarmstep_quad_pack_f64(const swarmstep_group_view *g, double *pos, double *vel, double *quat,
+                            double *omega, uint8_t *alive, void *stream)
+{
+    int st = check_view(g);
+    if (st) return st;
+    if (g->n == 0) return SWARMSTEP_OK;
+    pack_f64_kernel<<<grid_for(g->n, 256), 256, 0, (cudaStream_t)stream>>>(
+        g->cols, g->flags, g->n, g->stride, g->compensated, pos, vel, quat, omega, alive);
+    return cuda_status("pack_f64_kernel");
+}
+
+int swarmstep_quad_unpack_f64(const swarmstep_group_view *g, const double *pos, const double *vel,
+                              const double *quat, const double *omega, const uint8_t *alive, void *stream)
+{
+    int st = check_view(g);
+    if (st) return st;
+    if (g->n == 0) return SWARMSTEP_OK;
+    unpack_f64_kernel<<<grid_for(g->n, 256), 256, 0, (cudaStream_t)stream>>>(
+        g->cols, g->flags, g->n, g->stride, g->compensated, pos, vel, quat, omega, alive);
+    return cuda_status("unpack_f64_kernel");
+}
+
+}  // extern "C"

@@ -1,0 +1,422 @@
+"""B200QuadGroup: the reference's homogeneous quadrotor group, on one B200.
+
+Drop-in for ``swarmstep.core.QuadGroup`` (core.py:76-205): it implements the
+duck-typed group protocol the reference ``World`` calls (core.py:308-505) --
+``kind``, ``type_id``, ``batch``, ``params``, ``step(dt)``,
+``apply_command``, ``mark_dead``, ``add_velocity_overlay``,
+``retarget_waypoint``, ``snapshot``, ``rows_for``, ``cmd_values`` /
+``cmd_level`` -- and adds the bulk / fused entry points the B200 path is
+built for: ``step_k(dt, k)`` (k fused ticks per launch), ``set_setpoints``
+(device-resident setpoint feed) and ``step_async`` / ``collect_faults``.
+
+Device layout: one float32 buffer of ``NCOL`` columns x
+``stride`` rows (structure of arrays, one column per scalar component) plus a
+uint8 flag column (alive | has_prev | level).  The float64 host views the
+reference exposes (``batch.pos`` ...) are mirrors synchronised lazily: a
+read after a step packs the device columns to float64 on the device and
+copies them down once.  Writes into those mirror arrays do not reach the
+device; use ``push_host_state()`` after editing them.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Iterable
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import (COL_CMD, COL_OVERLAY, FLAG_ALIVE, LEVEL_MASK, LEVEL_SHIFT, NCOL, GroupView)
+from .commands import LEVEL_MOTOR, LEVEL_POS, LEVEL_RATE, level_code
+from .errors import InvalidStateError, NativeLibraryError, ValidationError
+from .params import (default_outer_gains, default_quad_params, default_rate_gains,
+                     pack_device_params)
+from .state import AgentBatch, batch_snapshot, quat_yaw
+
+_ROW_ALIGN = 128  # stride multiple: whole 512-byte column tiles, 16-byte aligned
+
+
+def _round_up(x: int, m: int) -> int:
+    return (x + m - 1) // m * m
+
+
+def _ptr(t: torch.Tensor) -> int:
+    return t.data_ptr()
+
+
+class B200QuadGroup:
+    """One quadrotor type stepped by the sm_100a fused kernel."""
+
+    kind = "quadrotor"
+
+    def __init__(self, type_id: int, batch, params=None, rate_gains=None, outer_gains=None, *,
+                 device=None, compensated: bool = True, fault_capacity: int | None = None):
+        lib = _lib.load()
+        if not torch.cuda.is_available():
+            raise NativeLibraryError("B200QuadGroup needs a CUDA device (there is no CPU fallback)")
+        n = int(batch.agent_ids.shape[0])
+        if n < 1:
+            raise ValidationError("a group needs at least one agent")
+        self._lib = lib
+        self.type_id = int(type_id)
+        self.params = params if params is not None else default_quad_params()
+        self.rate_gains = rate_gains if rate_gains is not None else default_rate_gains()
+        self.outer_gains = outer_gains if outer_gains is not None else default_outer_gains()
+        self._dparams = pack_device_params(self.params, self.rate_gains, self.outer_gains)
+        self.compensated = bool(compensated)
+        self.n = n
+        self.stride = _round_up(n, _ROW_ALIGN)
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
+        with torch.cuda.device(self.device):
+            self.stream = torch.cuda.Stream(self.device)
+            with torch.cuda.stream(self.stream):
+                self._cols = torch.zeros((NCOL, self.stride), dtype=torch.float32, device=self.device)
+                self._flags = torch.zeros(self.stride, dtype=torch.uint8, device=self.device)
+                self._counters = torch.zeros(4, dtype=torch.int32, device=self.device)
+                cap = int(fault_capacity) if fault_capacity is not None else n
+                self._fault_cap = max(1, cap)
+                self._fault_log = torch.zeros(self._fault_cap, dtype=torch.int64, device=self.device)
+            self._counters_host = torch.zeros(4, dtype=torch.int32, pin_memory=True)
+        self._view = GroupView(n=n, stride=self.stride, cols=_ptr(self._cols), flags=_ptr(self._flags),
+                               counters=_ptr(self._counters), fault_log=_ptr(self._fault_log),
+                               fault_cap=self._fault_cap, compensated=int(self.compensated))
+        self._view_ref = ctypes.byref(self._view)
+        self._params_ref = ctypes.byref(self._dparams)
+
+        # host mirrors (the reference's numpy columns)
+        self._batch = AgentBatch(
+            type_id=int(getattr(batch, "type_id", type_id)),
+            agent_ids=np.array(batch.agent_ids, dtype=np.uint64),
+            pos=np.array(batch.pos, dtype=float).reshape(n, 3),
+            vel=np.array(batch.vel, dtype=float).reshape(n, 3),
+            quat=np.array(batch.quat, dtype=float).reshape(n, 4),
+            omega=np.array(batch.omega, dtype=float).reshape(n, 3),
+            alive=np.array(batch.alive, dtype=bool).reshape(n),
+        )
+        self._row = {int(a): i for i, a in enumerate(self._batch.agent_ids)}
+        self._alive = self._batch.alive  # exact: changes only via mark_dead / faults
+        self._state_stale = False        # device state newer than the host mirror
+        # command store (core.py:98-104): position hold at the initial pose
+        self._cmd_level = np.full(n, LEVEL_POS, dtype=np.uint8)
+        self._cmd_values = np.zeros((n, 7))
+        self._cmd_values[:, :3] = self._batch.pos
+        self._cmd_values[:, 6] = quat_yaw(self._batch.quat)
+        self._cmd_stale = False          # device command store newer than host mirror
+        self._pending: dict[int, tuple[int, np.ndarray]] = {}
+        self._nonfinite_rows: set[int] = set()
+        self._overlay_active = False
+        self._overlay_poison = False
+        self._fault_batches: list[np.ndarray] = []  # fault ids per substep of the last launch
+
+        self.push_host_state(upload_commands=True)
+
+    # ------------------------------------------------------------------ utils
+    def _call(self, fn, *args) -> None:
+        with torch.cuda.device(self.device):
+            _lib.check(fn(self._view_ref, *args))
+
+    def _sync(self) -> None:
+        self.stream.synchronize()
+
+    @property
+    def cols(self) -> torch.Tensor:
+        """The device SoA buffer [NCOL, stride] (float32)."""
+        return self._cols
+
+    @property
+    def flags(self) -> torch.Tensor:
+        return self._flags
+
+    # --------------------------------------------------------- host <-> device
+    def push_host_state(self, upload_commands: bool = False) -> None:
+        """Upload the host mirror (pos/vel/quat/omega/alive) to the device columns."""
+        b = self._batch
+        with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
+            pos = torch.from_numpy(np.ascontiguousarray(b.pos)).to(self.device, non_blocking=False)
+            vel = torch.from_numpy(np.ascontiguousarray(b.vel)).to(self.device)
+            quat = torch.from_numpy(np.ascontiguousarray(b.quat)).to(self.device)
+            omega = torch.from_numpy(np.ascontiguousarray(b.omega)).to(self.device)
+            alive = torch.from_numpy(b.alive.astype(np.uint8)).to(self.device)
+            self._call(self._lib.swarmstep_quad_unpack_f64, _ptr(pos), _ptr(vel), _ptr(quat),
+                       _ptr(omega), _ptr(alive), ctypes.c_void_p(self.stream.cuda_stream))
+            if upload_commands:
+                vals = torch.from_numpy(self._cmd_values.T.astype(np.float32).copy()).to(self.device)
+                self._cols[COL_CMD:COL_CMD + 7, :self.n].copy_(vals)
+                lv = torch.from_numpy(self._cmd_level.astype(np.uint8)).to(self.device)
+                fl = self._flags[:self.n]
+                fl.copy_((fl & (0xFF ^ LEVEL_MASK)) | (lv << LEVEL_SHIFT))
+            self._sync()
+        self._alive = b.alive
+        self._state_stale = False
+
+    def _pull_state(self) -> None:
+        if not self._state_stale:
+            return
+        n = self.n
+        b = self._batch
+        with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
+            buf = torch.empty(n * 13, dtype=torch.float64, device=self.device)
+            alive = torch.empty(n, dtype=torch.uint8, device=self.device)
+            p = _ptr(buf)
+            self._call(self._lib.swarmstep_quad_pack_f64, p, p + n * 3 * 8, p + n * 6 * 8, p + n * 10 * 8,
+                       _ptr(alive), ctypes.c_void_p(self.stream.cuda_stream))
+            host = buf.cpu().numpy()
+            alive_h = alive.cpu().numpy()
+        b.pos[:] = host[: n * 3].reshape(n, 3)
+        b.vel[:] = host[n * 3: n * 6].reshape(n, 3)
+        b.quat[:] = host[n * 6: n * 10].reshape(n, 4)
+        b.omega[:] = host[n * 10:].reshape(n, 3)
+        b.alive[:] = alive_h.astype(bool)
+        self._state_stale = False
+
+    def _pull_commands(self) -> None:
+        if not self._cmd_stale:
+            return
+        with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
+            vals = self._cols[COL_CMD:COL_CMD + 7, :self.n].T.double().cpu().numpy()
+            lv = ((self._flags[:self.n] & LEVEL_MASK) >> LEVEL_SHIFT).cpu().numpy()
+        self._cmd_values[:] = vals
+        self._cmd_level[:] = lv
+        self._cmd_stale = False
+
+    def _flush_commands(self) -> None:
+        if not self._pending:
+            return
+        rows = np.fromiter(self._pending.keys(), dtype=np.int64, count=len(self._pending))
+        levels = np.empty(rows.shape[0], dtype=np.uint8)
+        vals = np.empty((rows.shape[0], 7), dtype=np.float32)
+        for i, (lvl, v) in enumerate(self._pending.values()):
+            levels[i] = lvl
+            vals[i] = v
+        self._pending.clear()
+        with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
+            d_rows = torch.from_numpy(rows).to(self.device)
+            d_lv = torch.from_numpy(levels).to(self.device)
+            d_vals = torch.from_numpy(vals).to(self.device)
+            self._call(self._lib.swarmstep_quad_apply_commands, _ptr(d_rows), _ptr(d_lv), _ptr(d_vals),
+                       ctypes.c_int64(rows.shape[0]), ctypes.c_void_p(self.stream.cuda_stream))
+            # keep the staging tensors alive until the kernel has consumed them
+            self._staging = (d_rows, d_lv, d_vals)
+
+    # ------------------------------------------------------- group protocol
+    @property
+    def batch(self) -> AgentBatch:
+        """Host float64 view of the state table, synchronised on access."""
+        self._pull_state()
+        return self._batch
+
+    @property
+    def cmd_values(self) -> np.ndarray:
+        self._pull_commands()
+        return self._cmd_values
+
+    @property
+    def cmd_level(self) -> np.ndarray:
+        self._pull_commands()
+        return self._cmd_level
+
+    def rows_for(self, agent_id: int) -> int | None:
+        return self._row.get(int(agent_id))
+
+    def apply_command(self, cmd) -> bool:
+        """Latest-wins command write (core.py:117-135)."""
+        row = self._row.get(int(cmd.agent_id))
+        if row is None or not self._alive[row]:
+            return False
+        lvl = level_code(cmd.level)
+        if lvl is None:
+            return False
+        vals = np.asarray(cmd.values, dtype=float).ravel()
+        want = 7 if lvl == LEVEL_POS else 4
+        if vals.shape[0] != want:
+            raise ValidationError(f"level takes {want} values, got {vals.shape[0]}")
+        self._pull_commands()
+        full = np.zeros(7)
+        full[:want] = vals
+        self._cmd_level[row] = lvl
+        self._cmd_values[row] = full
+        if np.all(np.isfinite(full)):
+            self._nonfinite_rows.discard(row)
+        else:
+            self._nonfinite_rows.add(row)
+        self._pending[row] = (lvl, full.astype(np.float32))
+        return True
+
+    def set_setpoints(self, values, level=LEVEL_POS, row0: int = 0) -> None:
+        """Bulk device setpoints for rows [row0, row0 + count) (alive rows only).
+
+        ``values`` is a (count, 7|4) array-like or a device tensor of that
+        shape; it is written straight into the device command columns.  This
+        is the device-resident setpoint feed that replaces per-agent
+        ``apply_command`` calls for whole swarms.
+        """
+        lvl = level_code(level) if not isinstance(level, int) else level
+        if lvl not in (LEVEL_POS, LEVEL_RATE, LEVEL_MOTOR):
+            raise ValidationError(f"bad level {level!r}")
+        want = 7 if lvl == LEVEL_POS else 4
+        with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
+            t = values if isinstance(values, torch.Tensor) else torch.from_numpy(np.asarray(values, dtype=np.float32))
+            if t.dim() != 2 or t.shape[1] != want:
+                raise ValidationError(f"setpoints must be (count, {want})")
+            count = int(t.shape[0])
+            if row0 < 0 or row0 + count > self.n:
+                raise ValidationError("setpoint rows out of range")
+            if not bool(torch.isfinite(t).all()):
+                raise ValidationError("setpoints must be finite")
+            tcols = t.to(self.device, torch.float32).T.contiguous()
+            self._flush_commands()
+            self._call(self._lib.swarmstep_quad_set_setpoints, ctypes.c_int64(row0), ctypes.c_int64(count),
+                       int(lvl), _ptr(tcols), ctypes.c_int64(count), ctypes.c_void_p(self.stream.cuda_stream))
+            self._staging_sp = tcols
+        if self._nonfinite_rows:
+            self._nonfinite_rows = {r for r in self._nonfinite_rows if not (row0 <= r < row0 + count)}
+        self._cmd_stale = True
+
+    def add_velocity_overlay(self, offsets) -> None:
+        """One-tick velocity offsets added to v_sp of POS rows (core.py:137-139)."""
+        with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
+            t = offsets if isinstance(offsets, torch.Tensor) else torch.from_numpy(np.asarray(offsets, dtype=np.float32))
+            t = t.to(self.device, torch.float32).reshape(self.n, 3)
+            if not bool(torch.isfinite(t).all()):
+                self._overlay_poison = True
+            if not self._overlay_active:
+                self._cols[COL_OVERLAY:COL_OVERLAY + 3].zero_()
+            self._cols[COL_OVERLAY:COL_OVERLAY + 3, :self.n] += t.T
+        self._overlay_active = True
+
+    def retarget_waypoint(self, point, radius: float) -> None:
+        """Alive rows within ``radius`` of ``point`` go to POS hold there (core.py:141-149)."""
+        pt = (ctypes.c_double * 3)(*[float(x) for x in np.asarray(point, dtype=float).ravel()[:3]])
+        self._flush_commands()
+        self._pull_commands()
+        with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
+            self._call(self._lib.swarmstep_quad_retarget_waypoint, pt, ctypes.c_double(float(radius)),
+                       ctypes.c_void_p(self.stream.cuda_stream))
+        self._cmd_stale = True
+        # rows rewritten by the waypoint carry finite values now
+        if self._nonfinite_rows:
+            self._pull_commands()
+            self._nonfinite_rows = {r for r in self._nonfinite_rows
+                                    if not np.all(np.isfinite(self._cmd_values[r]))}
+
+    def mark_dead(self, agent_ids: Iterable[int]) -> list[int]:
+        """Kill agents; returns the ids that were alive (core.py:151-158)."""
+        killed, rows = [], []
+        for aid in agent_ids:
+            row = self._row.get(int(aid))
+            if row is not None and self._alive[row]:
+                self._alive[row] = False
+                killed.append(int(aid))
+                rows.append(row)
+        if rows:
+            with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
+                d_rows = torch.tensor(rows, dtype=torch.int64).to(self.device)
+                self._call(self._lib.swarmstep_quad_mark_dead, _ptr(d_rows), None,
+                           ctypes.c_int64(len(rows)), ctypes.c_void_p(self.stream.cuda_stream))
+                self._staging_dead = d_rows
+        return killed
+
+    def snapshot(self, tick: int):
+        return batch_snapshot(self.batch, tick)
+
+    # ------------------------------------------------------------ stepping
+    def _any_pos_rows(self) -> bool:
+        self._pull_commands()
+        return bool(np.any(self._cmd_level == LEVEL_POS))
+
+    def step_async(self, dt: float, k: int = 1) -> None:
+        """Launch k fused ticks; fault ids are gathered by ``collect_faults()``."""
+        if not dt > 0.0:
+            raise ValidationError(f"dt must be positive, got {dt}")
+        if k < 1:
+            raise ValidationError(f"k must be >= 1, got {k}")
+        if (self._nonfinite_rows or self._overlay_poison) and self._any_pos_rows():
+            # the reference's outer loop runs quat_mul over every row whenever
+            # a POS row exists and raises on non-finite input (quat.py:84)
+            self._overlay_reset()
+            raise InvalidStateError("non-finite quaternion input")
+        self._flush_commands()
+        stream = ctypes.c_void_p(self.stream.cuda_stream)
+        with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
+            self._counters[0].zero_()
+            self._call(self._lib.swarmstep_quad_step, self._params_ref, ctypes.c_float(dt), int(k),
+                       int(self._overlay_active), stream)
+            self._overlay_reset()
+            self._counters_host.copy_(self._counters, non_blocking=True)
+        self._state_stale = True
+        self._launch_k = k
+
+    def _overlay_reset(self) -> None:
+        if self._overlay_active:
+            with torch.cuda.stream(self.stream):
+                self._cols[COL_OVERLAY:COL_OVERLAY + 3].zero_()
+        self._overlay_active = False
+        self._overlay_poison = False
+
+    def collect_faults(self) -> list[np.ndarray]:
+        """Wait for the last launch; fault ids per substep (row order within a substep)."""
+        self._sync()
+        count = int(self._counters_host[0])
+        k = getattr(self, "_launch_k", 1)
+        if count == 0:
+            return [np.empty(0, dtype=np.uint64) for _ in range(k)]
+        if count > self._fault_cap:
+            raise NativeLibraryError("fault log overflow")
+        log = self._fault_log[:count].cpu().numpy().astype(np.uint64)
+        sub = (log >> np.uint64(40)).astype(np.int64)
+        rows = (log & np.uint64((1 << 40) - 1)).astype(np.int64)
+        order = np.lexsort((rows, sub))
+        sub, rows = sub[order], rows[order]
+        self._alive[rows] = False
+        ids = self._batch.agent_ids[rows]
+        return [ids[sub == s].copy() for s in range(k)]
+
+    def step_k(self, dt: float, k: int = 1) -> np.ndarray:
+        """k fused ticks (== k successive step(dt) calls with fixed commands)."""
+        self.step_async(dt, k)
+        per = self.collect_faults()
+        return np.concatenate(per) if len(per) > 1 else per[0]
+
+    def step(self, dt: float) -> np.ndarray:
+        """Advance one tick in place; returns fault ids (core.py:166-202)."""
+        return self.step_k(dt, 1)
+
+    # -------------------------------------------------------------- extras
+    def alive_count(self) -> int:
+        return int(self._alive.sum())
+
+    def pid_state(self) -> dict:
+        """Host float64 copy of the PID columns (RatePidState, control.py:100-114)."""
+        from ._lib import COL_INTEGRAL, COL_PREV, COL_SP, FLAG_HAS_PREV
+        with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
+            integ = self._cols[COL_INTEGRAL:COL_INTEGRAL + 3, :self.n].T.double().cpu().numpy()
+            prev = self._cols[COL_PREV:COL_PREV + 3, :self.n].T.double().cpu().numpy()
+            sp = self._cols[COL_SP:COL_SP + 4, :self.n].T.double().cpu().numpy()
+            hp = ((self._flags[:self.n] & FLAG_HAS_PREV) != 0).cpu().numpy()
+        return {"integral": integ, "prev_omega": prev, "has_prev": hp,
+                "omega_sp": sp[:, :3].copy(), "f_c_sp": sp[:, 3].copy()}
+
+    def set_pid_state(self, integral=None, prev_omega=None, has_prev=None, omega_sp=None, f_c_sp=None) -> None:
+        """Load PID / stale-setpoint columns (test and resume support)."""
+        from ._lib import COL_INTEGRAL, COL_PREV, COL_SP, FLAG_HAS_PREV
+        n = self.n
+        with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
+            def put(c0, arr, k):
+                t = torch.from_numpy(np.asarray(arr, dtype=np.float32).reshape(n, k).T.copy()).to(self.device)
+                self._cols[c0:c0 + k, :n].copy_(t)
+            if integral is not None:
+                put(COL_INTEGRAL, integral, 3)
+            if prev_omega is not None:
+                put(COL_PREV, prev_omega, 3)
+            if omega_sp is not None:
+                put(COL_SP, omega_sp, 3)
+            if f_c_sp is not None:
+                put(COL_SP + 3, f_c_sp, 1)
+            if has_prev is not None:
+                hp = torch.from_numpy(np.asarray(has_prev, dtype=np.uint8).reshape(n)).to(self.device)
+                fl = self._flags[:n]
+                fl.copy_((fl & (0xFF ^ FLAG_HAS_PREV)) | (hp * FLAG_HAS_PREV))
+            self._sync()

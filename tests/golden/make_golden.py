@@ -1,0 +1,183 @@
+"""Generate golden vectors by running the REFERENCE itself (swarmstep, float64).
+
+Run in the build container, where /root/reference exists:
+
+    python tests/golden/make_golden.py
+
+It imports ``swarmstep`` from /root/reference/pkg/src (read-only, via
+sys.path), drives its real hot-path functions and ``QuadGroup`` through the
+scenarios of tests/scenarios.py, and writes small .npz fixtures next to this
+file.  The fixtures are committed; nothing on the GPU box reads the reference.
+"""
+
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+sys.path.insert(0, str(HERE.parent))
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import scenarios  # noqa: E402
+from swarmstep.control import (PosSetpoint, RatePidState, RateSetpoint, default_outer_gains,  # noqa: E402
+                               default_rate_gains, position_outer_loop, rate_pid_step)
+from swarmstep.core import QuadGroup  # noqa: E402
+from swarmstep.quad import (QuadWorkspace, default_quad_params, dynamics_deriv, mix_to_motors,  # noqa: E402
+                            rk4_step)
+from swarmstep.state import batch_create  # noqa: E402
+from swarmstep.wire import AgentCommand, CommandLevel  # noqa: E402
+
+P = default_quad_params()
+LEVELS = {0: CommandLevel.POS, 1: CommandLevel.RATE, 2: CommandLevel.MOTOR, 3: CommandLevel.UNICYCLE}
+
+
+def make_cmd(agent_id, level_code, values):
+    return AgentCommand(int(agent_id), LEVELS[level_code], tuple(values))
+
+
+def state_of(g: QuadGroup) -> dict:
+    b = g.batch
+    return dict(pos=b.pos.copy(), vel=b.vel.copy(), quat=b.quat.copy(), omega=b.omega.copy(),
+                alive=b.alive.copy(), integral=g.pid_state.integral.copy(),
+                prev_omega=g.pid_state.prev_omega.copy(), has_prev=g.pid_state.has_prev.copy(),
+                omega_sp=g.omega_sp.copy(), f_c_sp=g.f_c_sp.copy(),
+                cmd_level=g.cmd_level.copy(), cmd_values=g.cmd_values.copy())
+
+
+def gen_scenario(name: str) -> None:
+    sc = scenarios.ALL[name]()
+    batch = batch_create(0, sc.n, sc.pos, quat=sc.quat, vel=sc.vel, omega=sc.omega)
+    init = dict(pos=batch.pos.copy(), vel=batch.vel.copy(), quat=batch.quat.copy(), omega=batch.omega.copy())
+    group = QuadGroup(0, batch, P)
+    records, cmd_ok, faults = scenarios.run_script(group, sc, make_cmd, state_of)
+    out = sc.to_arrays()
+    # batch_create renormalises quaternions: store the exact initial state used
+    out.update(init)
+    ticks = sorted(records)
+    out["rec_ticks"] = np.array(ticks, dtype=np.int64)
+    for key in records[ticks[0]] if ticks else []:
+        out[f"rec_{key}"] = np.stack([records[t][key] for t in ticks])
+    out["cmd_ok"] = cmd_ok
+    ft, fi, raise_tick = [], [], -1
+    for t, f in faults.items():
+        if isinstance(f, str):
+            raise_tick = t
+            continue
+        for a in f:
+            ft.append(t)
+            fi.append(a)
+    out["fault_tick"] = np.array(ft, dtype=np.int64)
+    out["fault_id"] = np.array(fi, dtype=np.int64)
+    out["raise_tick"] = np.array(raise_tick)
+    np.savez_compressed(HERE / f"scenario_{name}.npz", **out)
+    print(f"{name}: n={sc.n} ticks={sc.ticks} recorded={ticks} faults={len(fi)} raise_tick={raise_tick}")
+
+
+def gen_functions() -> None:
+    rng = np.random.default_rng(2024)
+    out = {}
+    # --- dynamics_deriv (quad.py:320-335)
+    n = 256
+    q = rng.standard_normal((n, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    b = batch_create(0, n, rng.uniform(-5, 5, (n, 3)), quat=q, vel=rng.uniform(-2, 2, (n, 3)),
+                     omega=rng.uniform(-3, 3, (n, 3)))
+    f_c = rng.uniform(0, 40, n)
+    tau = rng.uniform(-0.5, 0.5, (n, 3))
+    d = dynamics_deriv(b, f_c, tau, P)
+    out["deriv_state"] = np.hstack([b.pos, b.vel, b.quat, b.omega])
+    out["deriv_fc"], out["deriv_tau"] = f_c, tau
+    out["deriv_out"] = np.hstack([d.pos[:n], d.vel[:n], d.quat[:n], d.omega[:n]])
+
+    # --- rk4_step (quad.py:350-437): 20 steps, piecewise wrench, dead rows
+    n = 128
+    q = rng.standard_normal((n, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    b = batch_create(0, n, rng.uniform(-5, 5, (n, 3)), quat=q, vel=rng.uniform(-2, 2, (n, 3)),
+                     omega=rng.uniform(-1, 1, (n, 3)))
+    b.alive[[5, 77]] = False
+    out["rk4_state0"] = np.hstack([b.pos, b.vel, b.quat, b.omega])
+    out["rk4_alive0"] = b.alive.copy()
+    ws = QuadWorkspace(n)
+    fcs, taus = [], []
+    for k in range(20):
+        if k % 5 == 0:
+            f_c = rng.uniform(0.0, 2 * P.m * P.g, n)
+            tau = rng.uniform(-0.05, 0.05, (n, 3))
+        fcs.append(f_c.copy())
+        taus.append(tau.copy())
+        rk4_step(b, f_c, tau, P, 1e-3, ws)
+    out["rk4_fc"], out["rk4_tau"] = np.stack(fcs), np.stack(taus)
+    out["rk4_state20"] = np.hstack([b.pos, b.vel, b.quat, b.omega])
+    out["rk4_alive20"] = b.alive.copy()
+    # fault case (test_quad.py:171-179)
+    bf = batch_create(0, 2, np.zeros((2, 3)))
+    fids = rk4_step(bf, np.zeros(2), np.array([[0.0, 0.0, 0.0], [1e308, 0.0, 0.0]]), P, 1e6)
+    out["rk4_fault_ids"] = fids.astype(np.int64)
+    out["rk4_fault_state"] = np.hstack([bf.pos, bf.vel, bf.quat, bf.omega])
+    out["rk4_fault_alive"] = bf.alive.copy()
+
+    # --- mix_to_motors (quad.py:143-168), including saturation
+    n = 256
+    f_c = rng.uniform(-5, 70, n)
+    tau = rng.uniform(-1.0, 1.0, (n, 3)) * np.array([1.0, 1.0, 0.02])
+    mx = mix_to_motors(f_c, tau, P)
+    out["mix_fc"], out["mix_tau"] = f_c, tau
+    out["mix_motors"] = mx.motors.copy()
+    out["mix_realized"] = np.hstack([mx.f_c[:, None], mx.tau]).copy()
+    out["mix_sat"] = mx.saturated.copy()
+
+    # --- rate_pid_step (control.py:136-187): 30 steps, dead rows appear
+    n, steps, dt = 32, 30, 0.013
+    st = RatePidState(n)
+    alive = np.ones(n, dtype=bool)
+    om_s, sp_s, fsp_s, al_s, tau_s, fc_s, int_s = [], [], [], [], [], [], []
+    for k in range(steps):
+        if k == 10:
+            alive[[3, 17]] = False
+        om = rng.uniform(-3, 3, (n, 3))
+        sp = rng.uniform(-3, 3, (n, 3))
+        fsp = rng.uniform(0, 20, n)
+        fc, tq = rate_pid_step(om, RateSetpoint(sp, fsp), default_rate_gains(), dt, st, alive)
+        om_s.append(om); sp_s.append(sp); fsp_s.append(fsp); al_s.append(alive.copy())
+        tau_s.append(tq.copy()); fc_s.append(fc.copy()); int_s.append(st.integral.copy())
+    out["pid_omega"], out["pid_sp"], out["pid_fsp"] = np.stack(om_s), np.stack(sp_s), np.stack(fsp_s)
+    out["pid_alive"], out["pid_tau"], out["pid_fc"] = np.stack(al_s), np.stack(tau_s), np.stack(fc_s)
+    out["pid_integral"], out["pid_dt"] = np.stack(int_s), np.array(dt)
+
+    # --- position_outer_loop (control.py:222-294), incl. every branch
+    n = 512
+    q = rng.standard_normal((n, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    q[:128] = np.array([1.0, 0, 0, 0]) + 0.05 * rng.standard_normal((128, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    pos = rng.uniform(-5, 5, (n, 3))
+    vel = rng.uniform(-2, 2, (n, 3))
+    p_sp = pos + rng.uniform(-3, 3, (n, 3))
+    v_sp = rng.uniform(-1, 1, (n, 3))
+    yaw = rng.uniform(-np.pi, np.pi, n)
+    alive = rng.random(n) > 0.05
+    g = default_outer_gains()
+    # low-thrust rows: a_cmd = 0 exactly
+    p_sp[500:503] = pos[500:503] + np.array([0.0, 0.0, -P.g / 16.0])
+    v_sp[500:503] = vel[500:503]
+    # degenerate-yaw rows: z_des parallel to the heading (a = (16,0,0), yaw 0)
+    p_sp[503:506] = pos[503:506] + np.array([1.0, 0.0, -P.g / 16.0])
+    v_sp[503:506] = vel[503:506]
+    yaw[503:506] = 0.0
+    alive[500:506] = True
+    res = position_outer_loop(pos, vel, q, alive, PosSetpoint(p_sp, v_sp, yaw), P, g)
+    for k, v in dict(pos=pos, vel=vel, quat=q, p_sp=p_sp, v_sp=v_sp, yaw=yaw, alive=alive,
+                     omega_sp=res.setpoint.omega_sp, f_c=res.setpoint.f_c_sp, low=res.low_thrust).items():
+        out[f"outer_{k}"] = np.asarray(v).copy()
+    np.savez_compressed(HERE / "functions.npz", **out)
+    print("functions: deriv/rk4/mix/pid/outer written")
+
+
+if __name__ == "__main__":
+    gen_functions()
+    for name in scenarios.ALL:
+        gen_scenario(name)
