@@ -84,8 +84,8 @@ typedef struct swarmstep_group_view {
     int64_t stride;         /* floats per column (>= n, multiple of 32)     */
     float *cols;            /* [SWARMSTEP_NCOL][stride] float32             */
     uint8_t *flags;         /* [stride]                                     */
-    uint32_t *counters;     /* device [4]: 0 fault count, 1 scratch count   */
-    uint64_t *fault_log;    /* device [fault_cap]: (substep << 40) | row    */
+    uint32_t *counters;     /* device [4]: 0 faults logged (monotonic), 1 scratch count */
+    uint64_t *fault_log;    /* device [fault_cap]: (tick << 40) | row       */
     int64_t fault_cap;
     int32_t compensated;    /* 1: position = hi + lo (COL_POS_LO in use)    */
     int32_t _pad;
@@ -104,12 +104,15 @@ int swarmstep_device_info(int *sm_count, int *cc_major, int *cc_minor);
  * rk4_step (quad.py:350-437) including fault revert + kill.  The overlay
  * column block is added to v_sp on substep 0 only when overlay_active != 0
  * (core.py:172-175, 199-201); the caller clears it afterwards.
- * Faulted rows are appended to fault_log and counted in counters[0]
- * (the caller zeroes counters[0] before the launch).
+ * Faulted rows are appended to fault_log as ((tick_base + substep) mod 2^24)
+ * << 40 | row and counted in counters[0], which only ever grows: a row can
+ * fault at most once (dead rows never revive), so fault_cap >= n never
+ * overflows and no per-launch reset is needed.
  * Replaces: QuadGroup.step (core.py:166).  Errors: dt <= 0 or k < 1 ->
  * SWARMSTEP_EINVAL (quad.py:359-360, control.py:154-155). */
 int swarmstep_quad_step(const swarmstep_group_view *g, const swarmstep_quad_params *p,
-                        float dt, int k_substeps, int overlay_active, void *stream);
+                        float dt, int k_substeps, int overlay_active, uint32_t tick_base,
+                        void *stream);
 
 /* Latest-wins command scatter (QuadGroup.apply_command, core.py:117-135).
  * rows[i] (int64), levels[i] (uint8, SWARMSTEP_LEVEL_*), values[i*7..]

@@ -58,7 +58,7 @@ def _declare(lib) -> None:
     lib.swarmstep_device_info.restype = i32
     lib.swarmstep_device_info.argtypes = [ctypes.POINTER(i32)] * 3
     lib.swarmstep_quad_step.restype = i32
-    lib.swarmstep_quad_step.argtypes = [view, vp, f32, i32, i32, vp]
+    lib.swarmstep_quad_step.argtypes = [view, vp, f32, i32, i32, ctypes.c_uint32, vp]
     lib.swarmstep_quad_apply_commands.restype = i32
     lib.swarmstep_quad_apply_commands.argtypes = [view, vp, vp, vp, i64, vp]
     lib.swarmstep_quad_set_setpoints.restype = i32

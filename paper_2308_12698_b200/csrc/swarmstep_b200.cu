@@ -57,7 +57,7 @@ struct Cols {
 __global__ void __launch_bounds__(kBlock)
 quad_step_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t n, int64_t stride,
                  uint32_t *__restrict__ counters, uint64_t *__restrict__ fault_log,
-                 int64_t fault_cap, int compensated, int overlay_active,
+                 int64_t fault_cap, int compensated, int overlay_active, uint32_t tick_base,
                  const swarmstep_quad_params P, float dt, int K)
 {
     const int64_t r = (int64_t)blockIdx.x * kBlock + threadIdx.x;
@@ -138,7 +138,8 @@ quad_step_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t 
             // fault: revert to pre-step values, kill, report (quad.py:425-436)
             alive = false;
             const uint32_t slot = atomicAdd(&counters[0], 1u);
-            if ((int64_t)slot < fault_cap) fault_log[slot] = ((uint64_t)k << 40) | (uint64_t)r;
+            if ((int64_t)slot < fault_cap)
+                fault_log[slot] = ((uint64_t)((tick_base + (uint32_t)k) & 0xFFFFFFu) << 40) | (uint64_t)r;
             break;
         }
 #pragma unroll
@@ -311,7 +312,7 @@ int swarmstep_device_info(int *sm_count, int *cc_major, int *cc_minor)
 }
 
 int swarmstep_quad_step(const swarmstep_group_view *g, const swarmstep_quad_params *p, float dt,
-                        int k_substeps, int overlay_active, void *stream)
+                        int k_substeps, int overlay_active, uint32_t tick_base, void *stream)
 {
     int st = check_view(g);
     if (st) return st;
@@ -322,7 +323,7 @@ int swarmstep_quad_step(const swarmstep_group_view *g, const swarmstep_quad_para
     if (g->n == 0) return SWARMSTEP_OK;
     quad_step_kernel<<<grid_for(g->n, kBlock), kBlock, 0, (cudaStream_t)stream>>>(
         g->cols, g->flags, g->n, g->stride, g->counters, g->fault_log, g->fault_log ? g->fault_cap : 0,
-        g->compensated, overlay_active, *p, dt, k_substeps);
+        g->compensated, overlay_active, tick_base, *p, dt, k_substeps);
     return cuda_status("quad_step_kernel");
 }
 

@@ -109,7 +109,14 @@ class B200QuadGroup:
         self._nonfinite_rows: set[int] = set()
         self._overlay_active = False
         self._overlay_poison = False
-        self._fault_batches: list[np.ndarray] = []  # fault ids per substep of the last launch
+        self._tick = 0                   # ticks launched so far (fault-log tags)
+        self._launched: list[tuple[int, int]] = []  # (first tick, k) not yet collected
+        self._fault_seen = 0             # fault-log entries already returned
+        self._copy_stream = None         # side stream for host->device setpoint uploads
+        self._sp_stage = [None, None]    # double-buffered setpoint staging
+        self._sp_consumed = [None, None]
+        self._sp_src = [None, None]
+        self._sp_slot = 0
 
         self.push_host_state(upload_commands=True)
 
@@ -245,32 +252,69 @@ class B200QuadGroup:
         self._pending[row] = (lvl, full.astype(np.float32))
         return True
 
-    def set_setpoints(self, values, level=LEVEL_POS, row0: int = 0) -> None:
-        """Bulk device setpoints for rows [row0, row0 + count) (alive rows only).
+    def set_setpoints(self, values, level=LEVEL_POS, row0: int = 0, columns: bool = False) -> None:
+        """Bulk setpoints for rows [row0, row0 + count) (alive rows only).
 
-        ``values`` is a (count, 7|4) array-like or a device tensor of that
-        shape; it is written straight into the device command columns.  This
-        is the device-resident setpoint feed that replaces per-agent
-        ``apply_command`` calls for whole swarms.
+        ``values`` is (count, 7|4) -- or (7|4, count) with ``columns=True``,
+        the device's own SoA layout -- as numpy, a host tensor (pinned for
+        asynchronous upload) or a device tensor.  Host data is copied on a
+        side stream into one of two staging buffers, so an upload overlaps
+        the group's previous launch; a scatter kernel then writes the command
+        columns in stream order.  This is the device-resident setpoint feed
+        that replaces per-agent ``apply_command`` calls for whole swarms
+        (SURVEY.md 8(f) f1).  Unlike ``apply_command`` it does not screen for
+        non-finite values: those fault the affected rows.
         """
         lvl = level_code(level) if not isinstance(level, int) else level
         if lvl not in (LEVEL_POS, LEVEL_RATE, LEVEL_MOTOR):
             raise ValidationError(f"bad level {level!r}")
         want = 7 if lvl == LEVEL_POS else 4
-        with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
-            t = values if isinstance(values, torch.Tensor) else torch.from_numpy(np.asarray(values, dtype=np.float32))
-            if t.dim() != 2 or t.shape[1] != want:
-                raise ValidationError(f"setpoints must be (count, {want})")
-            count = int(t.shape[0])
-            if row0 < 0 or row0 + count > self.n:
-                raise ValidationError("setpoint rows out of range")
-            if not bool(torch.isfinite(t).all()):
-                raise ValidationError("setpoints must be finite")
-            tcols = t.to(self.device, torch.float32).T.contiguous()
-            self._flush_commands()
-            self._call(self._lib.swarmstep_quad_set_setpoints, ctypes.c_int64(row0), ctypes.c_int64(count),
-                       int(lvl), _ptr(tcols), ctypes.c_int64(count), ctypes.c_void_p(self.stream.cuda_stream))
-            self._staging_sp = tcols
+        t = values if isinstance(values, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(values, dtype=np.float32))
+        if t.dim() != 2 or (t.shape[0] if columns else t.shape[1]) != want:
+            raise ValidationError(f"setpoints must be ({want}, count) / (count, {want})")
+        count = int(t.shape[1] if columns else t.shape[0])
+        if row0 < 0 or row0 + count > self.n:
+            raise ValidationError("setpoint rows out of range")
+        if t.dtype != torch.float32:
+            t = t.float()
+        self._flush_commands()
+        with torch.cuda.device(self.device):
+            if t.is_cuda:
+                cols = t if columns else t.T
+                if cols.stride(1) != 1:
+                    cols = cols.contiguous()
+                with torch.cuda.stream(self.stream):
+                    self._call(self._lib.swarmstep_quad_set_setpoints, ctypes.c_int64(row0), ctypes.c_int64(count),
+                               int(lvl), _ptr(cols), ctypes.c_int64(cols.stride(0)),
+                               ctypes.c_void_p(self.stream.cuda_stream))
+                self._staging_sp = cols
+            else:
+                if not columns:
+                    t = t.T.contiguous()
+                slot = self._sp_slot
+                self._sp_slot ^= 1
+                if self._sp_stage[slot] is None or self._sp_stage[slot].shape[1] < count:
+                    self._sp_stage[slot] = torch.empty((7, max(count, 1)), dtype=torch.float32, device=self.device)
+                    self._sp_consumed[slot] = None
+                    if self._copy_stream is None:
+                        self._copy_stream = torch.cuda.Stream(self.device)
+                buf = self._sp_stage[slot][:want, :count]
+                with torch.cuda.stream(self._copy_stream):
+                    if self._sp_consumed[slot] is not None:
+                        self._copy_stream.wait_event(self._sp_consumed[slot])
+                    buf.copy_(t, non_blocking=True)
+                    copied = torch.cuda.Event()
+                    copied.record(self._copy_stream)
+                self.stream.wait_event(copied)
+                with torch.cuda.stream(self.stream):
+                    self._call(self._lib.swarmstep_quad_set_setpoints, ctypes.c_int64(row0), ctypes.c_int64(count),
+                               int(lvl), _ptr(buf), ctypes.c_int64(self._sp_stage[slot].shape[1]),
+                               ctypes.c_void_p(self.stream.cuda_stream))
+                    ev = torch.cuda.Event()
+                    ev.record(self.stream)
+                    self._sp_consumed[slot] = ev
+                # the source must outlive the asynchronous copy
+                self._sp_src[slot] = t
         if self._nonfinite_rows:
             self._nonfinite_rows = {r for r in self._nonfinite_rows if not (row0 <= r < row0 + count)}
         self._cmd_stale = True
@@ -328,26 +372,27 @@ class B200QuadGroup:
         return bool(np.any(self._cmd_level == LEVEL_POS))
 
     def step_async(self, dt: float, k: int = 1) -> None:
-        """Launch k fused ticks; fault ids are gathered by ``collect_faults()``."""
+        """Launch k fused ticks without waiting; ``collect_faults()`` gathers fault ids."""
         if not dt > 0.0:
             raise ValidationError(f"dt must be positive, got {dt}")
         if k < 1:
             raise ValidationError(f"k must be >= 1, got {k}")
         if (self._nonfinite_rows or self._overlay_poison) and self._any_pos_rows():
             # the reference's outer loop runs quat_mul over every row whenever
-            # a POS row exists and raises on non-finite input (quat.py:84)
+            # a POS row exists and raises on non-finite input (quat.py:84),
+            # before any state changes
             self._overlay_reset()
             raise InvalidStateError("non-finite quaternion input")
         self._flush_commands()
-        stream = ctypes.c_void_p(self.stream.cuda_stream)
         with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
-            self._counters[0].zero_()
             self._call(self._lib.swarmstep_quad_step, self._params_ref, ctypes.c_float(dt), int(k),
-                       int(self._overlay_active), stream)
+                       int(self._overlay_active), ctypes.c_uint32(self._tick & 0xFFFFFF),
+                       ctypes.c_void_p(self.stream.cuda_stream))
             self._overlay_reset()
             self._counters_host.copy_(self._counters, non_blocking=True)
+        self._launched.append((self._tick, k))
+        self._tick += k
         self._state_stale = True
-        self._launch_k = k
 
     def _overlay_reset(self) -> None:
         if self._overlay_active:
@@ -357,22 +402,25 @@ class B200QuadGroup:
         self._overlay_poison = False
 
     def collect_faults(self) -> list[np.ndarray]:
-        """Wait for the last launch; fault ids per substep (row order within a substep)."""
+        """Wait for the launches since the last call; fault ids per tick, in row order."""
         self._sync()
+        launched, self._launched = self._launched, []
+        ticks = [t0 + j for t0, k in launched for j in range(k)]
         count = int(self._counters_host[0])
-        k = getattr(self, "_launch_k", 1)
-        if count == 0:
-            return [np.empty(0, dtype=np.uint64) for _ in range(k)]
+        if count == self._fault_seen:
+            return [np.empty(0, dtype=np.uint64) for _ in ticks]
         if count > self._fault_cap:
             raise NativeLibraryError("fault log overflow")
-        log = self._fault_log[:count].cpu().numpy().astype(np.uint64)
-        sub = (log >> np.uint64(40)).astype(np.int64)
+        log = self._fault_log[self._fault_seen:count].cpu().numpy().astype(np.uint64)
+        self._fault_seen = count
+        tag = (log >> np.uint64(40)).astype(np.int64)
         rows = (log & np.uint64((1 << 40) - 1)).astype(np.int64)
-        order = np.lexsort((rows, sub))
-        sub, rows = sub[order], rows[order]
         self._alive[rows] = False
-        ids = self._batch.agent_ids[rows]
-        return [ids[sub == s].copy() for s in range(k)]
+        out = []
+        for t in ticks:
+            sel = np.sort(rows[tag == (t & 0xFFFFFF)])
+            out.append(self._batch.agent_ids[sel].copy())
+        return out
 
     def step_k(self, dt: float, k: int = 1) -> np.ndarray:
         """k fused ticks (== k successive step(dt) calls with fixed commands)."""

@@ -1,0 +1,74 @@
+"""Shared helpers for the GPU parity tests (CUDA float32 path vs float64 oracle)."""
+
+from __future__ import annotations
+
+import numpy as np
+
+from oracle import oracle as orc
+
+# Per-step parity metric (north_star: per-step relative error <= 1e-5 in FP32).
+# err_q = max |x32 - x64| / max(|x64|_inf(row), floor_q), per quantity q, taken
+# over all rows after ONE step from an identical (float32-representable) state.
+# The floors are each quantity's natural scale: positions are in metres
+# (|p| up to ~150 m here), velocities in m/s, unit quaternions, body rates in
+# rad/s, PID integral in rad (clamped to i_limit = 0.2).
+PER_STEP_TOL = 1e-5
+FLOORS = dict(pos=1.0, vel=1.0, quat=1.0, omega=1.0, integral=0.2)
+
+
+def make_group(sc_or_arrays, compensated=True, **kw):
+    from paper_2308_12698_b200 import B200QuadGroup, batch_create
+    s = sc_or_arrays
+    b = batch_create(0, s.n, s.pos, quat=s.quat, vel=s.vel, omega=s.omega)
+    return B200QuadGroup(0, b, compensated=compensated, **kw)
+
+
+def gpu_state(g) -> dict:
+    b = g.batch
+    ps = g.pid_state()
+    return dict(pos=b.pos.copy(), vel=b.vel.copy(), quat=b.quat.copy(), omega=b.omega.copy(),
+                alive=b.alive.copy(), integral=ps["integral"], prev_omega=ps["prev_omega"],
+                has_prev=ps["has_prev"], omega_sp=ps["omega_sp"], f_c_sp=ps["f_c_sp"],
+                cmd_level=g.cmd_level.copy(), cmd_values=g.cmd_values.copy())
+
+
+class _Batch:
+    def __init__(self, st):
+        n = st["pos"].shape[0]
+        self.agent_ids = np.arange(n, dtype=np.uint64)
+        self.pos, self.vel, self.quat, self.omega = st["pos"], st["vel"], st["quat"], st["omega"]
+        self.alive = st["alive"]
+
+
+def oracle_twin(g, st=None) -> orc.OracleGroup:
+    """float64 oracle group holding exactly the GPU group's current (float32) state."""
+    st = st or gpu_state(g)
+    og = orc.OracleGroup(0, _Batch(st))
+    og.integral[:] = st["integral"]
+    og.prev_omega[:] = st["prev_omega"]
+    og.has_prev[:] = st["has_prev"].astype(np.uint8)
+    og.omega_sp[:] = st["omega_sp"]
+    og.f_c_sp[:] = st["f_c_sp"]
+    og.cmd_level[:] = st["cmd_level"]
+    og.cmd_values[:] = st["cmd_values"].astype(np.float32).astype(np.float64)
+    return og
+
+
+def rel_errors(gst: dict, og: orc.OracleGroup, rows=None) -> dict:
+    rows = slice(None) if rows is None else rows
+    alive = og.alive.astype(bool)[rows]
+    out = {}
+    for q, want in (("pos", og.pos), ("vel", og.vel), ("quat", og.quat), ("omega", og.omega),
+                    ("integral", og.integral)):
+        w = want[rows][alive]
+        h = gst[q][rows][alive]
+        if w.size == 0:
+            out[q] = 0.0
+            continue
+        scale = np.maximum(np.max(np.abs(w), axis=1, keepdims=True), FLOORS[q])
+        out[q] = float(np.max(np.abs(h - w) / scale))
+    return out
+
+
+def f32(dt: float) -> float:
+    return float(np.float32(dt))

@@ -1,0 +1,96 @@
+"""CPU checks of the drop-in boundary: the C-ABI library loads, exports every
+symbol include/swarmstep_b200.h declares, and the ctypes mirrors match the C
+struct layouts.  No compute calls (no GPU here)."""
+
+import ctypes
+import re
+import subprocess
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+HEADER = ROOT / "include" / "swarmstep_b200.h"
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2308_12698_b200 import _build, _lib
+    _build.build()
+    return _lib.load()
+
+
+def declared_functions():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"^(?:int|const char \*)\s*(swarmstep_\w+)\s*\(", text, re.M)))
+
+
+def test_header_declares_what_binding_exports():
+    from paper_2308_12698_b200._lib import EXPORTS
+    assert declared_functions() == sorted(EXPORTS)
+
+
+def test_library_exports_every_declared_symbol(lib):
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+    assert lib.swarmstep_abi_version() == 1
+    out = subprocess.run(["nm", "-D", "--defined-only", str(ROOT / "paper_2308_12698_b200" / "libswarmstep_b200.so")],
+                         capture_output=True, text=True, check=True).stdout
+    for name in declared_functions():
+        assert re.search(rf"\bT {name}\b", out), f"{name} not exported with C linkage"
+
+
+def test_library_is_sm100a(lib):
+    so = ROOT / "paper_2308_12698_b200" / "libswarmstep_b200.so"
+    out = subprocess.run(["cuobjdump", "--list-elf", str(so)], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def _c_sizeof(expr: str, tmp_path) -> int:
+    src = tmp_path / "s.c"
+    src.write_text(f'#include "swarmstep_b200.h"\n#include <stdio.h>\n#include <stddef.h>\n'
+                   f'int main(void){{printf("%zu\\n", (size_t)({expr}));return 0;}}\n')
+    exe = tmp_path / "s"
+    subprocess.run(["gcc", f"-I{ROOT / 'include'}", "-o", str(exe), str(src)], check=True)
+    return int(subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout)
+
+
+def test_struct_layouts_match_header(tmp_path):
+    from paper_2308_12698_b200._lib import GroupView
+    from paper_2308_12698_b200.params import DeviceParams
+    assert ctypes.sizeof(DeviceParams) == _c_sizeof("sizeof(swarmstep_quad_params)", tmp_path)
+    assert ctypes.sizeof(GroupView) == _c_sizeof("sizeof(swarmstep_group_view)", tmp_path)
+    for f in ("G_inv", "kp_pos", "omega_sp_max", "a_cmd_min"):
+        assert getattr(DeviceParams, f).offset == _c_sizeof(f"offsetof(swarmstep_quad_params, {f})", tmp_path)
+    for f in ("cols", "fault_cap", "compensated"):
+        assert getattr(GroupView, f).offset == _c_sizeof(f"offsetof(swarmstep_group_view, {f})", tmp_path)
+
+
+def test_column_constants_match_header(tmp_path):
+    from paper_2308_12698_b200 import _lib as L
+    for name, val in (("SWARMSTEP_COL_POS_LO", L.COL_POS_LO), ("SWARMSTEP_COL_INTEGRAL", L.COL_INTEGRAL),
+                      ("SWARMSTEP_COL_SP", L.COL_SP), ("SWARMSTEP_COL_CMD", L.COL_CMD),
+                      ("SWARMSTEP_COL_OVERLAY", L.COL_OVERLAY), ("SWARMSTEP_NCOL", L.NCOL)):
+        assert _c_sizeof(name, tmp_path) == val, name
+
+
+def test_device_params_packing():
+    from paper_2308_12698_b200 import default_outer_gains, default_quad_params, default_rate_gains
+    from paper_2308_12698_b200.params import allocation_matrices, pack_device_params
+    p = default_quad_params()
+    d = pack_device_params(p, default_rate_gains(), default_outer_gains())
+    g, gi = allocation_matrices(p)
+    np.testing.assert_allclose(np.array(d.G[:]).reshape(4, 4), g, rtol=1e-7)
+    np.testing.assert_allclose(np.array(d.G_inv[:]).reshape(4, 4) @ g, np.eye(4), atol=1e-5)
+    assert d.f_max == pytest.approx(16.0) and d.fc_max == pytest.approx(64.0)
+    assert list(d.kp) == pytest.approx([0.25, 0.25, 0.1]) and list(d.k_att) == pytest.approx([12, 12, 3])
+
+
+def test_group_fails_loudly_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2308_12698_b200 import B200QuadGroup, NativeLibraryError, batch_create
+    with pytest.raises(NativeLibraryError):
+        B200QuadGroup(0, batch_create(0, 2, np.zeros((2, 3))))
