@@ -157,7 +157,9 @@ class B200QuadGroup:
                 fl.copy_((fl & (0xFF ^ LEVEL_MASK)) | (lv << LEVEL_SHIFT))
             self._sync()
         self._alive = b.alive
-        self._state_stale = False
+        # the device holds the float32 (hi + lo) image of what was pushed;
+        # re-read it so the host mirror always shows the device state
+        self._state_stale = True
 
     def _pull_state(self) -> None:
         if not self._state_stale:
