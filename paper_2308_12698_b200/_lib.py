@@ -7,12 +7,17 @@ product entry point raises ``NativeLibraryError``.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
 from .errors import NativeLibraryError, ValidationError
 
 LIB_PATH = Path(__file__).resolve().parent / "libswarmstep_b200.so"
+# tools/tune.py points this at variant builds; the product always uses LIB_PATH
+_OVERRIDE = os.environ.get("SWARMSTEP_B200_LIB_OVERRIDE")
+if _OVERRIDE:
+    LIB_PATH = Path(_OVERRIDE)
 
 SWARMSTEP_OK, SWARMSTEP_EINVAL, SWARMSTEP_ECUDA, SWARMSTEP_ENODEV = 0, -1, -2, -3
 ABI_VERSION = 1

@@ -2,22 +2,23 @@
 //
 // Each function restates one piece of the reference's batched numpy path for
 // a single agent held in registers:
-//   deriv            quad.py:222-310   (_deriv_kernel)
-//   rk4_row          quad.py:350-437   (rk4_step, one row)
-//   mix_row          quad.py:143-168   (mix_to_motors)
+//   deriv / rk4_row  quad.py:222-310, 350-437  (_deriv_kernel, rk4_step)
+//   mix_row          quad.py:143-168           (mix_to_motors)
 //   motor_wrench     quad.py:130-140 + core.py:189-197
-//   pid_row          control.py:136-187 (rate_pid_step)
-//   outer_row        control.py:190-294 (position_outer_loop, _rotmats_to_quats)
+//   pid_row          control.py:136-187        (rate_pid_step)
+//   outer_row        control.py:190-294        (position_outer_loop, _rotmats_to_quats)
 //
-// Numerics (float32 against the float64 reference):
-//  * clamps are written as compare-selects so NaN propagates like np.clip;
+// Numerics (float32 against the float64 reference, target <= 1e-5 relative
+// per step):
+//  * clamps are compare-selects so NaN propagates like np.clip;
 //  * the mixer returns the requested wrench unchanged for unsaturated rows
-//    (G * G^-1 * w == w exactly in R; the reference's float64 round trip
-//    differs by ~1 ulp, a float32 round trip would inject |f_c| * eps32 of
+//    (G G^-1 w == w in R; a float32 round trip would inject |f_c| eps32 of
 //    torque error -- SURVEY.md Appendix B);
-//  * position may be carried as an unevaluated sum hi + lo (TwoSum update),
-//    so that the float64 reference's sub-ulp increments at |p| ~ 100 m are
-//    kept.
+//  * position can be carried as an unevaluated sum hi + lo (TwoSum update) so
+//    the reference's sub-ulp increments at |p| ~ 100 m are kept;
+//  * sqrt / 1/x / 1/sqrt use the SFU (MUFU) approximations (<= 2 ulp) and
+//    atan2 a degree-8 minimax polynomial (9e-8 relative): all well inside the
+//    1e-5 budget, and branch-free of the IEEE slow paths.
 #pragma once
 #include <cuda_runtime.h>
 #include <math.h>
@@ -31,95 +32,129 @@ __device__ __forceinline__ float clip(float x, float lo, float hi)
     return x < lo ? lo : (x > hi ? hi : x);
 }
 
-// d/dt of (v, q, w); p-dot = v is handled by the caller.
-// fc_m = f_c / m.  quad.py:222-310.
-__device__ __forceinline__ void deriv(const float q[4], const float w[3], float fc_m,
-                                      const float tau[3], const swarmstep_quad_params &P,
+__device__ __forceinline__ float rsqrt_a(float x)
+{
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ float sqrt_a(float x)
+{
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ float rcp_a(float x)
+{
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Per-tick constants derived from the per-type struct (hoisted out of the
+// substep loop by the caller).
+struct Derived {
+    float g;
+    float gx, gy, gz;        // gyroscopic coefficients (I_zz-I_yy)/I_xx, ...
+    float kd_dt[3];          // kd / dt
+};
+
+__device__ __forceinline__ Derived derive(const swarmstep_quad_params &P, float inv_dt)
+{
+    Derived d;
+    d.g = P.g;
+    d.gx = (P.izz - P.iyy) * P.inv_ixx;
+    d.gy = (P.ixx - P.izz) * P.inv_iyy;
+    d.gz = (P.iyy - P.ixx) * P.inv_izz;
+#pragma unroll
+    for (int i = 0; i < 3; i++) d.kd_dt[i] = P.kd[i] * inv_dt;
+    return d;
+}
+
+// d/dt of (v, q, w) at (q, w) for a held wrench (quad.py:222-310):
+//   vdot = (f_c/m) R(q) e_z - g e_z ; qdot = q (x) (0, w) / 2 ;
+//   wdot = I^-1 (tau - w x (I w)) = tau/I - (gyro coefficient) w_j w_k.
+// fc2 = 2 f_c / m, fcg = f_c / m - g, tI = tau / I (per axis).
+__device__ __forceinline__ void deriv(const float q[4], const float w[3], float fc2, float fcg,
+                                      const float tI[3], const Derived &D,
                                       float dv[3], float dq[4], float dw[3])
 {
     const float qw = q[0], qx = q[1], qy = q[2], qz = q[3];
-    const float ox = w[0], oy = w[1], oz = w[2];
-    dv[0] = 2.0f * (qx * qz + qw * qy) * fc_m;
-    dv[1] = 2.0f * (qy * qz - qw * qx) * fc_m;
-    dv[2] = (1.0f - 2.0f * (qx * qx + qy * qy)) * fc_m - P.g;
-    dq[0] = -0.5f * (qx * ox + qy * oy + qz * oz);
-    dq[1] = 0.5f * (qw * ox + qy * oz - qz * oy);
-    dq[2] = 0.5f * (qw * oy + qz * ox - qx * oz);
-    dq[3] = 0.5f * (qw * oz + qx * oy - qy * ox);
-    // I^-1 (tau - w x (I w)), diagonal inertia
-    dw[0] = (tau[0] - (oy * (P.izz * oz) - oz * (P.iyy * oy))) * P.inv_ixx;
-    dw[1] = (tau[1] - (oz * (P.ixx * ox) - ox * (P.izz * oz))) * P.inv_iyy;
-    dw[2] = (tau[2] - (ox * (P.iyy * oy) - oy * (P.ixx * ox))) * P.inv_izz;
+    const float hx = 0.5f * w[0], hy = 0.5f * w[1], hz = 0.5f * w[2];
+    dv[0] = fc2 * fmaf(qx, qz, qw * qy);
+    dv[1] = fc2 * fmaf(qy, qz, -qw * qx);
+    dv[2] = fmaf(-fc2, fmaf(qx, qx, qy * qy), fcg);
+    dq[0] = -fmaf(qx, hx, fmaf(qy, hy, qz * hz));
+    dq[1] = fmaf(qw, hx, fmaf(qy, hz, -qz * hy));
+    dq[2] = fmaf(qw, hy, fmaf(qz, hx, -qx * hz));
+    dq[3] = fmaf(qw, hz, fmaf(qx, hy, -qy * hx));
+    dw[0] = fmaf(-D.gx, w[1] * w[2], tI[0]);
+    dw[1] = fmaf(-D.gy, w[2] * w[0], tI[1]);
+    dw[2] = fmaf(-D.gz, w[0] * w[1], tI[2]);
 }
 
 __device__ __forceinline__ void two_sum(float a, float b, float &s, float &e)
 {
     s = a + b;
-    float bb = s - a;
+    const float bb = s - a;
     e = (a - (s - bb)) + (b - bb);
 }
 
 // One classical RK4 step with the wrench held (quad.py:350-437).  Writes the
 // candidate state into the *_n arrays and returns true when the row stays
-// finite (the reference's fault predicate, quad.py:404-430).
+// finite (the reference's fault predicate, quad.py:404-430).  Position does
+// not feed any derivative, so only its final combination is formed.
 __device__ __forceinline__ bool rk4_row(const float p_hi[3], const float p_lo[3], const float v[3],
                                         const float q[4], const float w[3], float f_c,
                                         const float tau[3], const swarmstep_quad_params &P,
-                                        float dt, bool compensated,
+                                        const Derived &D, float dt, bool compensated,
                                         float p_hi_n[3], float p_lo_n[3], float v_n[3],
                                         float q_n[4], float w_n[3])
 {
     const float half = 0.5f * dt;
     const float h6 = dt * (1.0f / 6.0f);
-    const float fc_m = f_c * P.inv_m;
+    const float fcm = f_c * P.inv_m;
+    const float fc2 = 2.0f * fcm;
+    const float fcg = fcm - D.g;
+    const float tI[3] = {tau[0] * P.inv_ixx, tau[1] * P.inv_iyy, tau[2] * P.inv_izz};
     float kv[3], kq[4], kw[3];
     float av[3], aq[4], aw[3], ap[3];
     float sv[3], sq[4], sw[3];
 
-    // k1
-    deriv(q, w, fc_m, tau, P, kv, kq, kw);
+    deriv(q, w, fc2, fcg, tI, D, kv, kq, kw);                       // k1
 #pragma unroll
     for (int i = 0; i < 3; i++) { av[i] = kv[i]; aw[i] = kw[i]; ap[i] = v[i]; }
 #pragma unroll
     for (int i = 0; i < 4; i++) aq[i] = kq[i];
-    // k2 at y + h/2 k1
 #pragma unroll
-    for (int i = 0; i < 3; i++) { sv[i] = fmaf(half, kv[i], v[i]); sw[i] = fmaf(half, kw[i], w[i]); }
+    for (int s = 0; s < 2; s++) {                                   // k2, k3 at y + h/2 k
 #pragma unroll
-    for (int i = 0; i < 4; i++) sq[i] = fmaf(half, kq[i], q[i]);
+        for (int i = 0; i < 3; i++) { sv[i] = fmaf(half, kv[i], v[i]); sw[i] = fmaf(half, kw[i], w[i]); }
 #pragma unroll
-    for (int i = 0; i < 3; i++) ap[i] = fmaf(2.0f, sv[i], ap[i]);
-    deriv(sq, sw, fc_m, tau, P, kv, kq, kw);
+        for (int i = 0; i < 4; i++) sq[i] = fmaf(half, kq[i], q[i]);
 #pragma unroll
-    for (int i = 0; i < 3; i++) { av[i] = fmaf(2.0f, kv[i], av[i]); aw[i] = fmaf(2.0f, kw[i], aw[i]); }
+        for (int i = 0; i < 3; i++) ap[i] = fmaf(2.0f, sv[i], ap[i]);
+        deriv(sq, sw, fc2, fcg, tI, D, kv, kq, kw);
 #pragma unroll
-    for (int i = 0; i < 4; i++) aq[i] = fmaf(2.0f, kq[i], aq[i]);
-    // k3 at y + h/2 k2
+        for (int i = 0; i < 3; i++) { av[i] = fmaf(2.0f, kv[i], av[i]); aw[i] = fmaf(2.0f, kw[i], aw[i]); }
 #pragma unroll
-    for (int i = 0; i < 3; i++) { sv[i] = fmaf(half, kv[i], v[i]); sw[i] = fmaf(half, kw[i], w[i]); }
-#pragma unroll
-    for (int i = 0; i < 4; i++) sq[i] = fmaf(half, kq[i], q[i]);
-#pragma unroll
-    for (int i = 0; i < 3; i++) ap[i] = fmaf(2.0f, sv[i], ap[i]);
-    deriv(sq, sw, fc_m, tau, P, kv, kq, kw);
-#pragma unroll
-    for (int i = 0; i < 3; i++) { av[i] = fmaf(2.0f, kv[i], av[i]); aw[i] = fmaf(2.0f, kw[i], aw[i]); }
-#pragma unroll
-    for (int i = 0; i < 4; i++) aq[i] = fmaf(2.0f, kq[i], aq[i]);
-    // k4 at y + h k3
+        for (int i = 0; i < 4; i++) aq[i] = fmaf(2.0f, kq[i], aq[i]);
+    }
 #pragma unroll
     for (int i = 0; i < 3; i++) { sv[i] = fmaf(dt, kv[i], v[i]); sw[i] = fmaf(dt, kw[i], w[i]); }
 #pragma unroll
     for (int i = 0; i < 4; i++) sq[i] = fmaf(dt, kq[i], q[i]);
 #pragma unroll
     for (int i = 0; i < 3; i++) ap[i] += sv[i];
-    deriv(sq, sw, fc_m, tau, P, kv, kq, kw);
+    deriv(sq, sw, fc2, fcg, tI, D, kv, kq, kw);                     // k4
 #pragma unroll
     for (int i = 0; i < 3; i++) { av[i] += kv[i]; aw[i] += kw[i]; }
 #pragma unroll
     for (int i = 0; i < 4; i++) aq[i] += kq[i];
 
-    // combine: y' = y + dt/6 (k1 + 2k2 + 2k3 + k4)
+    // y' = y + dt/6 (k1 + 2 k2 + 2 k3 + k4)
 #pragma unroll
     for (int i = 0; i < 3; i++) {
         v_n[i] = fmaf(h6, av[i], v[i]);
@@ -128,8 +163,7 @@ __device__ __forceinline__ bool rk4_row(const float p_hi[3], const float p_lo[3]
         if (compensated) {
             float s, e;
             two_sum(p_hi[i], dp + p_lo[i], s, e);
-            // renormalise so |lo| <= ulp(hi)/2
-            float hi2 = s + e;
+            const float hi2 = s + e;          // renormalise: |lo| <= ulp(hi)/2
             p_lo_n[i] = e - (hi2 - s);
             p_hi_n[i] = hi2;
         } else {
@@ -141,15 +175,17 @@ __device__ __forceinline__ bool rk4_row(const float p_hi[3], const float p_lo[3]
     for (int i = 0; i < 4; i++) q_n[i] = fmaf(h6, aq[i], q[i]);
 
     // single post-step renormalisation; zero / non-finite norm is a fault
-    const float nsq = q_n[0] * q_n[0] + q_n[1] * q_n[1] + q_n[2] * q_n[2] + q_n[3] * q_n[3];
-    const float nrm = sqrtf(nsq);
-    bool ok = isfinite(nrm) && nrm > 0.0f;
-    const float inv = 1.0f / nrm;
+    const float nsq = fmaf(q_n[0], q_n[0], fmaf(q_n[1], q_n[1], fmaf(q_n[2], q_n[2], q_n[3] * q_n[3])));
+    const float inv = rsqrt_a(nsq);
+    bool ok = isfinite(nsq) && nsq > 0.0f;
 #pragma unroll
     for (int i = 0; i < 4; i++) q_n[i] *= inv;
-#pragma unroll
-    for (int i = 0; i < 3; i++)
-        ok = ok && isfinite(p_hi_n[i] + p_lo_n[i]) && isfinite(v_n[i]) && isfinite(w_n[i]);
+    // 0 * x is NaN exactly when x is inf / NaN (IEEE; no fast-math here), so
+    // one compare covers every position / velocity / rate component
+    const float chk = 0.0f * (((p_hi_n[0] + p_hi_n[1]) + (p_hi_n[2] + p_lo_n[0])) +
+                              ((p_lo_n[1] + p_lo_n[2]) + (v_n[0] + v_n[1])) +
+                              ((v_n[2] + w_n[0]) + (w_n[1] + w_n[2])));
+    ok = ok && (chk == 0.0f);
     return ok;
 }
 
@@ -161,18 +197,18 @@ __device__ __forceinline__ void mix_row(float &f_c, float tau[3], const swarmste
     bool sat = false;
 #pragma unroll
     for (int i = 0; i < 4; i++) {
-        m[i] = P.G_inv[i * 4 + 0] * w4[0] + P.G_inv[i * 4 + 1] * w4[1] +
-               P.G_inv[i * 4 + 2] * w4[2] + P.G_inv[i * 4 + 3] * w4[3];
+        m[i] = fmaf(P.G_inv[i * 4 + 0], w4[0], fmaf(P.G_inv[i * 4 + 1], w4[1],
+               fmaf(P.G_inv[i * 4 + 2], w4[2], P.G_inv[i * 4 + 3] * w4[3])));
         sat = sat || (m[i] < 0.0f) || (m[i] > P.f_max);
     }
     if (sat) {
 #pragma unroll
         for (int i = 0; i < 4; i++) m[i] = clip(m[i], 0.0f, P.f_max);
-        f_c = P.G[0] * m[0] + P.G[1] * m[1] + P.G[2] * m[2] + P.G[3] * m[3];
+        f_c = (m[0] + m[1]) + (m[2] + m[3]);
 #pragma unroll
         for (int i = 0; i < 3; i++)
-            tau[i] = P.G[(i + 1) * 4 + 0] * m[0] + P.G[(i + 1) * 4 + 1] * m[1] +
-                     P.G[(i + 1) * 4 + 2] * m[2] + P.G[(i + 1) * 4 + 3] * m[3];
+            tau[i] = fmaf(P.G[(i + 1) * 4 + 0], m[0], fmaf(P.G[(i + 1) * 4 + 1], m[1],
+                     fmaf(P.G[(i + 1) * 4 + 2], m[2], P.G[(i + 1) * 4 + 3] * m[3])));
     }
 }
 
@@ -196,32 +232,49 @@ __device__ __forceinline__ void motor_wrench(const float rpm[4], const swarmstep
 // rate_pid_step for one alive row (control.py:136-187).  Dead rows never
 // reach this (they are frozen: tau = 0, f_c = 0, state untouched).
 __device__ __forceinline__ void pid_row(const float w[3], const float w_sp[3],
-                                        const swarmstep_quad_params &P, float dt, float inv_dt,
+                                        const swarmstep_quad_params &P, const Derived &D, float dt,
                                         float integ[3], float prev[3], bool &has_prev, float tau[3])
 {
 #pragma unroll
     for (int a = 0; a < 3; a++) {
         const float e = w_sp[a] - w[a];
-        integ[a] = clip(integ[a] + e * dt, -P.i_limit[a], P.i_limit[a]);
+        integ[a] = clip(fmaf(e, dt, integ[a]), -P.i_limit[a], P.i_limit[a]);
         float t = fmaf(P.kp[a], e, P.ki[a] * integ[a]);
-        if (has_prev) t -= ((w[a] - prev[a]) * inv_dt) * P.kd[a];
+        if (has_prev) t = fmaf(-D.kd_dt[a], w[a] - prev[a], t);
         tau[a] = t;
         prev[a] = w[a];
     }
     has_prev = true;
 }
 
-__device__ __forceinline__ void cross3(const float a[3], const float b[3], float c[3])
+// 2 atan2(s, c) / s for s, c >= 0 (the axis-angle factor of control.py:283-285),
+// finite at s = 0 (-> 2/c): atan(t) = t P(t^2) on [0, 1], degree-8 minimax.
+__device__ __forceinline__ float axis_angle_factor(float s, float c)
 {
-    c[0] = a[1] * b[2] - a[2] * b[1];
-    c[1] = a[2] * b[0] - a[0] * b[2];
-    c[2] = a[0] * b[1] - a[1] * b[0];
+    const bool small = s <= c;
+    const float num = small ? s : c, den = small ? c : s;
+    const float r = rcp_a(den);
+    const float t = num * r;
+    const float u = t * t;
+    float p = 0.002846542978659272f;
+    p = fmaf(p, u, -0.01605575904250145f);
+    p = fmaf(p, u, 0.04267148673534393f);
+    p = fmaf(p, u, -0.07502678036689758f);
+    p = fmaf(p, u, 0.10640215128660202f);
+    p = fmaf(p, u, -0.14203472435474396f);
+    p = fmaf(p, u, 0.1999259889125824f);
+    p = fmaf(p, u, -0.3333307206630707f);
+    p = fmaf(p, u, 1.0f);
+    // small: atan2 = t p, factor = 2 t p / s = 2 p / c
+    // large: atan2 = pi/2 - t p, factor = 2 (pi/2 - t p) / s
+    return small ? 2.0f * p * r : 2.0f * fmaf(-t, p, 1.5707963267948966f) * r;
 }
 
-// position_outer_loop for one alive row (control.py:222-294) with the
-// desired-attitude quaternion from the one selected branch of
-// _rotmats_to_quats (control.py:190-213).  cy/sy = cos/sin(yaw_sp) are
-// hoisted by the caller (constant over fused substeps).
+// position_outer_loop for one alive row (control.py:222-294): PD position
+// loop -> desired frame (z_des, yaw) with the degenerate-heading fallback ->
+// desired quaternion from the one selected branch of _rotmats_to_quats
+// (control.py:190-213) -> axis-angle attitude error -> clipped rate setpoint.
+// cy / sy = cos / sin(yaw_sp) are hoisted by the caller.
 __device__ __forceinline__ void outer_row(const float p_err[3], const float v[3], const float q[4],
                                           const float v_sp[3], float cy, float sy,
                                           const swarmstep_quad_params &P,
@@ -231,75 +284,83 @@ __device__ __forceinline__ void outer_row(const float p_err[3], const float v[3]
 #pragma unroll
     for (int i = 0; i < 3; i++) a[i] = fmaf(P.kp_pos[i], p_err[i], P.kv[i] * (v_sp[i] - v[i]));
     a[2] += P.g;
-    const float an = sqrtf(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
-    const bool low = an < P.a_cmd_min;
-    const float eff = low ? P.a_cmd_min : an;   // np.maximum; NaN stays NaN
-    if (low) {
-        z[0] = 0.0f; z[1] = 0.0f; z[2] = 1.0f;
-    } else {
-        const float ie = 1.0f / eff;
-        z[0] = a[0] * ie; z[1] = a[1] * ie; z[2] = a[2] * ie;
-    }
+    const float asq = fmaf(a[0], a[0], fmaf(a[1], a[1], a[2] * a[2]));
     const float qw = q[0], qx = q[1], qy = q[2], qz = q[3];
-    const float zb0 = 2.0f * (qx * qz + qw * qy);
-    const float zb1 = 2.0f * (qy * qz - qw * qx);
-    const float zb2 = 1.0f - 2.0f * (qx * qx + qy * qy);
-    f_c_sp = clip(P.m * eff * (zb0 * z[0] + zb1 * z[1] + zb2 * z[2]), 0.0f, P.fc_max);
+    const float zb0 = 2.0f * fmaf(qx, qz, qw * qy);
+    const float zb1 = 2.0f * fmaf(qy, qz, -qw * qx);
+    const float zb2 = fmaf(-2.0f, fmaf(qx, qx, qy * qy), 1.0f);
+    const float amin = P.a_cmd_min;
+    float fc;
+    if (asq < amin * amin) {            // free-fall floor: z_des = e_z, |a| := a_min
+        z[0] = 0.0f; z[1] = 0.0f; z[2] = 1.0f;
+        fc = P.m * amin * zb2;
+    } else {                            // m |a| (z_body . a/|a|) = m (z_body . a)
+        const float ia = rsqrt_a(asq);
+        z[0] = a[0] * ia; z[1] = a[1] * ia; z[2] = a[2] * ia;
+        fc = P.m * fmaf(zb0, a[0], fmaf(zb1, a[1], zb2 * a[2]));
+    }
+    f_c_sp = clip(fc, 0.0f, P.fc_max);
 
-    // desired frame: y = z x x_c / |.|, degenerate fallback from y_c
-    float yd[3], xd[3];
-    const float xc[3] = {cy, sy, 0.0f};
-    float yr[3];
-    cross3(z, xc, yr);
-    const float ny = sqrtf(yr[0] * yr[0] + yr[1] * yr[1] + yr[2] * yr[2]);
-    if (!(ny < 1e-6f)) {
-        const float iy = 1.0f / ny;
-        yd[0] = yr[0] * iy; yd[1] = yr[1] * iy; yd[2] = yr[2] * iy;
+    // y = z x x_c / |z x x_c| with x_c = (cy, sy, 0); degenerate fallback from y_c
+    float yd[3];
+    const float yr0 = -z[2] * sy, yr1 = z[2] * cy, yr2 = fmaf(z[0], sy, -z[1] * cy);
+    const float nysq = fmaf(yr0, yr0, fmaf(yr1, yr1, yr2 * yr2));
+    if (nysq >= 1e-12f) {
+        const float iy = rsqrt_a(nysq);
+        yd[0] = yr0 * iy; yd[1] = yr1 * iy; yd[2] = yr2 * iy;
     } else {
-        const float yc[3] = {-sy, cy, 0.0f};
-        float xa[3];
-        cross3(yc, z, xa);
-        const float ix = 1.0f / sqrtf(xa[0] * xa[0] + xa[1] * xa[1] + xa[2] * xa[2]);
-        xa[0] *= ix; xa[1] *= ix; xa[2] *= ix;
-        cross3(z, xa, yd);
+        // x_alt = y_c x z, y_c = (-sy, cy, 0); y = z x x_alt / |x_alt|
+        const float xa0 = cy * z[2], xa1 = sy * z[2], xa2 = fmaf(-sy, z[1], -cy * z[0]);
+        const float ix = rsqrt_a(fmaf(xa0, xa0, fmaf(xa1, xa1, xa2 * xa2)));
+        const float x0 = xa0 * ix, x1 = xa1 * ix, x2 = xa2 * ix;
+        yd[0] = fmaf(z[1], x2, -z[2] * x1);
+        yd[1] = fmaf(z[2], x0, -z[0] * x2);
+        yd[2] = fmaf(z[0], x1, -z[1] * x0);
     }
-    cross3(yd, z, xd);
-    // R = [xd yd z] (columns); rotmat -> quaternion, one branch
-    const float m00 = xd[0], m01 = yd[0], m02 = z[0];
-    const float m10 = xd[1], m11 = yd[1], m12 = z[1];
-    const float m20 = xd[2], m21 = yd[2], m22 = z[2];
+    // x = y x z ;  R = [x y z] (columns)
+    const float m00 = fmaf(yd[1], z[2], -yd[2] * z[1]);
+    const float m10 = fmaf(yd[2], z[0], -yd[0] * z[2]);
+    const float m20 = fmaf(yd[0], z[1], -yd[1] * z[0]);
+    const float m01 = yd[0], m11 = yd[1], m21 = yd[2];
+    const float m02 = z[0], m12 = z[1], m22 = z[2];
     const float tr = m00 + m11 + m22;
+    // _rotmats_to_quats selects branch 0 (tr > 0), 1 (m00 largest), 2 (m11 >=
+    // m22) or 3; branch k has t = 1 + (+-m00 +- m11 +- m22), s = 2 sqrt(t), its
+    // own component s/4 = sqrt(t)/2 and the others (m_ij +- m_ji)/s.  Evaluated
+    // branch-free with selects (agents in a warp pick different branches).
+    const bool b0 = tr > 0.0f;
+    const bool b1 = !b0 && (m00 >= m11 && m00 >= m22);
+    const bool b2 = !b0 && !b1 && (m11 >= m22);
+    const bool b3 = !b0 && !b1 && !b2;
+    const float s00 = (b0 || b1) ? m00 : -m00;
+    const float s11 = (b0 || b2) ? m11 : -m11;
+    const float s22 = (b0 || b3) ? m22 : -m22;
+    const float t = fmaxf(1.0f + s00 + s11 + s22, 1e-30f);
+    const float rt = rsqrt_a(t);
+    const float big = 0.5f * (t * rt), hr = 0.5f * rt;
+    const float d21 = m21 - m12, d02 = m02 - m20, d10 = m10 - m01;
+    const float a01 = m01 + m10, a02 = m02 + m20, a12 = m12 + m21;
     float qd[4];
-    if (tr > 0.0f) {
-        const float s = sqrtf(fmaxf(tr + 1.0f, 1e-30f)) * 2.0f, is = 1.0f / s;
-        qd[0] = 0.25f * s; qd[1] = (m21 - m12) * is; qd[2] = (m02 - m20) * is; qd[3] = (m10 - m01) * is;
-    } else if (m00 >= m11 && m00 >= m22) {
-        const float s = sqrtf(fmaxf(1.0f + m00 - m11 - m22, 1e-30f)) * 2.0f, is = 1.0f / s;
-        qd[0] = (m21 - m12) * is; qd[1] = 0.25f * s; qd[2] = (m01 + m10) * is; qd[3] = (m02 + m20) * is;
-    } else if (m11 >= m22) {
-        const float s = sqrtf(fmaxf(1.0f + m11 - m00 - m22, 1e-30f)) * 2.0f, is = 1.0f / s;
-        qd[0] = (m02 - m20) * is; qd[1] = (m01 + m10) * is; qd[2] = 0.25f * s; qd[3] = (m12 + m21) * is;
-    } else {
-        const float s = sqrtf(fmaxf(1.0f + m22 - m00 - m11, 1e-30f)) * 2.0f, is = 1.0f / s;
-        qd[0] = (m10 - m01) * is; qd[1] = (m02 + m20) * is; qd[2] = (m12 + m21) * is; qd[3] = 0.25f * s;
-    }
+    qd[0] = b0 ? big : hr * (b1 ? d21 : (b2 ? d02 : d10));
+    qd[1] = b1 ? big : hr * (b0 ? d21 : (b2 ? a01 : a02));
+    qd[2] = b2 ? big : hr * (b0 ? d02 : (b1 ? a01 : a12));
+    qd[3] = b3 ? big : hr * (b0 ? d10 : (b1 ? a02 : a12));
     {
-        const float in = 1.0f / sqrtf(qd[0] * qd[0] + qd[1] * qd[1] + qd[2] * qd[2] + qd[3] * qd[3]);
+        const float in = rsqrt_a(fmaf(qd[0], qd[0], fmaf(qd[1], qd[1], fmaf(qd[2], qd[2], qd[3] * qd[3]))));
         qd[0] *= in; qd[1] *= in; qd[2] *= in; qd[3] *= in;
     }
-    // q_err = conj(q) * q_des, renormalised (quat.py:75-92), w >= 0
-    float e0 = qw * qd[0] + qx * qd[1] + qy * qd[2] + qz * qd[3];
-    float e1 = qw * qd[1] - qx * qd[0] - qy * qd[3] + qz * qd[2];
-    float e2 = qw * qd[2] + qx * qd[3] - qy * qd[0] - qz * qd[1];
-    float e3 = qw * qd[3] - qx * qd[2] + qy * qd[1] - qz * qd[0];
+    // q_err = conj(q) (x) q_des, renormalised (quat.py:75-92), sign so w >= 0
+    float e0 = fmaf(qw, qd[0], fmaf(qx, qd[1], fmaf(qy, qd[2], qz * qd[3])));
+    float e1 = fmaf(qw, qd[1], fmaf(-qx, qd[0], fmaf(-qy, qd[3], qz * qd[2])));
+    float e2 = fmaf(qw, qd[2], fmaf(qx, qd[3], fmaf(-qy, qd[0], -qz * qd[1])));
+    float e3 = fmaf(qw, qd[3], fmaf(-qx, qd[2], fmaf(qy, qd[1], -qz * qd[0])));
     {
-        float in = 1.0f / sqrtf(e0 * e0 + e1 * e1 + e2 * e2 + e3 * e3);
-        if (e0 < 0.0f) in = -in;
+        float in = rsqrt_a(fmaf(e0, e0, fmaf(e1, e1, fmaf(e2, e2, e3 * e3))));
+        in = e0 < 0.0f ? -in : in;
         e0 *= in; e1 *= in; e2 *= in; e3 *= in;
     }
-    const float s = sqrtf(e1 * e1 + e2 * e2 + e3 * e3);
-    const float angle = 2.0f * atan2f(s, e0);
-    const float factor = s > 1e-12f ? angle / s : 2.0f;
+    const float ssq = fmaf(e1, e1, fmaf(e2, e2, e3 * e3));
+    const float factor = axis_angle_factor(sqrt_a(ssq), e0);
     w_sp[0] = clip(P.k_att[0] * (e1 * factor), -P.omega_sp_max, P.omega_sp_max);
     w_sp[1] = clip(P.k_att[1] * (e2 * factor), -P.omega_sp_max, P.omega_sp_max);
     w_sp[2] = clip(P.k_att[2] * (e3 * factor), -P.omega_sp_max, P.omega_sp_max);

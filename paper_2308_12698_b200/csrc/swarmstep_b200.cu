@@ -43,7 +43,15 @@ int check_view(const swarmstep_group_view *g)
     return SWARMSTEP_OK;
 }
 
-constexpr int kBlock = 256;
+#ifndef SSB_STEP_BLOCK
+#define SSB_STEP_BLOCK 128
+#endif
+#ifndef SSB_STEP_MINB
+#define SSB_STEP_MINB 5
+#endif
+// 128-thread CTAs, >= 5 resident per SM: caps the step kernel at 102
+// registers (no spills) for 20 warps per SM.
+constexpr int kBlock = SSB_STEP_BLOCK;
 
 struct Cols {
     float *c;
@@ -54,20 +62,19 @@ struct Cols {
 // ---------------------------------------------------------------------------
 // The fused step kernel.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kBlock)
+template <bool COMP>
+__global__ void __launch_bounds__(kBlock, SSB_STEP_MINB)
 quad_step_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t n, int64_t stride,
                  uint32_t *__restrict__ counters, uint64_t *__restrict__ fault_log,
-                 int64_t fault_cap, int compensated, int overlay_active, uint32_t tick_base,
+                 int64_t fault_cap, int overlay_active, uint32_t tick_base,
                  const swarmstep_quad_params P, float dt, int K)
 {
     const int64_t r = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     if (r >= n) return;
-    uint8_t fl = flags[r];
-    if (!(fl & SWARMSTEP_FLAG_ALIVE)) return;  // dead rows are frozen (quad.py:395-437)
-    const int level = (fl & SWARMSTEP_LEVEL_MASK) >> SWARMSTEP_LEVEL_SHIFT;
     const Cols C{cols, stride};
-
-    // ---- load state (register-resident for all K substeps) ----
+    // Issue every state load before the flag test so one memory round trip
+    // covers the whole row (dead rows are rare; their loads are discarded).
+    const uint8_t fl = flags[r];
     float p_hi[3], p_lo[3], v[3], q[4], w[3], integ[3], prev[3];
 #pragma unroll
     for (int i = 0; i < 3; i++) {
@@ -76,63 +83,68 @@ quad_step_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t 
         w[i] = __ldcs(C.col(SWARMSTEP_COL_OMEGA + i) + r);
         integ[i] = __ldcs(C.col(SWARMSTEP_COL_INTEGRAL + i) + r);
         prev[i] = __ldcs(C.col(SWARMSTEP_COL_PREV + i) + r);
-        p_lo[i] = compensated ? __ldcs(C.col(SWARMSTEP_COL_POS_LO + i) + r) : 0.0f;
+        p_lo[i] = COMP ? __ldcs(C.col(SWARMSTEP_COL_POS_LO + i) + r) : 0.0f;
     }
 #pragma unroll
     for (int i = 0; i < 4; i++) q[i] = __ldcs(C.col(SWARMSTEP_COL_QUAT + i) + r);
+    // u[]: per-launch setpoint registers, shared by the three levels
+    //   POS:   p_sp xyz, v_sp xyz, cos(yaw), sin(yaw)
+    //   MOTOR: rotor-model wrench f_c, tau xyz (core.py:189-197)
+    float u[8];
+#pragma unroll
+    for (int i = 0; i < 7; i++) u[i] = __ldcs(C.col(SWARMSTEP_COL_CMD + i) + r);
+    u[7] = 0.0f;
+    if (!(fl & SWARMSTEP_FLAG_ALIVE)) return;  // dead rows are frozen (quad.py:395-437)
+    const int level = (fl & SWARMSTEP_LEVEL_MASK) >> SWARMSTEP_LEVEL_SHIFT;
     bool has_prev = (fl & SWARMSTEP_FLAG_HAS_PREV) != 0;
 
-    // ---- per-launch setpoint inputs (commands are fixed across substeps) ----
-    float cmd[7];
-    float w_sp[3], f_sp;
-    float mot_fc = 0.0f, mot_tau[3] = {0.0f, 0.0f, 0.0f};
-    float cy = 1.0f, sy = 0.0f, ov[3] = {0.0f, 0.0f, 0.0f};
+    float w_sp[3] = {0.0f, 0.0f, 0.0f}, f_sp = 0.0f;
     if (level == SWARMSTEP_LEVEL_POS) {
-#pragma unroll
-        for (int i = 0; i < 7; i++) cmd[i] = __ldg(C.col(SWARMSTEP_COL_CMD + i) + r);
-        sincosf(cmd[6], &sy, &cy);
+        float s, c;
+        sincosf(u[6], &s, &c);
+        u[6] = c;
+        u[7] = s;
         if (overlay_active) {
 #pragma unroll
-            for (int i = 0; i < 3; i++) ov[i] = __ldg(C.col(SWARMSTEP_COL_OVERLAY + i) + r);
+            for (int i = 0; i < 3; i++) u[3 + i] += __ldg(C.col(SWARMSTEP_COL_OVERLAY + i) + r);
         }
-        w_sp[0] = w_sp[1] = w_sp[2] = f_sp = 0.0f;
     } else if (level == SWARMSTEP_LEVEL_RATE) {
-#pragma unroll
-        for (int i = 0; i < 4; i++) cmd[i] = __ldg(C.col(SWARMSTEP_COL_CMD + i) + r);
-        w_sp[0] = cmd[0]; w_sp[1] = cmd[1]; w_sp[2] = cmd[2]; f_sp = cmd[3];
+        w_sp[0] = u[0]; w_sp[1] = u[1]; w_sp[2] = u[2]; f_sp = u[3];
     } else {
-        // MOTOR: PID runs on the stale setpoints (core.py:109-110, 184-186);
-        // the rk4 wrench comes from the rotor model.
-#pragma unroll
-        for (int i = 0; i < 4; i++) cmd[i] = __ldg(C.col(SWARMSTEP_COL_CMD + i) + r);
+        // MOTOR: the PID still runs on the stale setpoints (core.py:109-110,
+        // 184-186); the integrated wrench comes from the rotor model
         w_sp[0] = __ldg(C.col(SWARMSTEP_COL_SP + 0) + r);
         w_sp[1] = __ldg(C.col(SWARMSTEP_COL_SP + 1) + r);
         w_sp[2] = __ldg(C.col(SWARMSTEP_COL_SP + 2) + r);
         f_sp = __ldg(C.col(SWARMSTEP_COL_SP + 3) + r);
-        ssb::motor_wrench(cmd, P, mot_fc, mot_tau);
+        float mt[3], mf;
+        ssb::motor_wrench(u, P, mf, mt);
+        u[0] = mf; u[1] = mt[0]; u[2] = mt[1]; u[3] = mt[2];
     }
 
-    const float inv_dt = 1.0f / dt;
+    const ssb::Derived D = ssb::derive(P, 1.0f / dt);
     bool alive = true;
     for (int k = 0; k < K; k++) {
         if (level == SWARMSTEP_LEVEL_POS) {
-            float p_err[3], v_sp[3];
+            float p_err[3];
 #pragma unroll
-            for (int i = 0; i < 3; i++) {
-                p_err[i] = (cmd[i] - p_hi[i]) - p_lo[i];
-                v_sp[i] = (k == 0) ? cmd[3 + i] + ov[i] : cmd[3 + i];
+            for (int i = 0; i < 3; i++) p_err[i] = (u[i] - p_hi[i]) - p_lo[i];
+            ssb::outer_row(p_err, v, q, u + 3, u[6], u[7], P, w_sp, f_sp);
+            if (k == 0 && overlay_active) {
+                // the overlay lasts one tick (core.py:199-201)
+#pragma unroll
+                for (int i = 0; i < 3; i++) u[3 + i] = __ldg(C.col(SWARMSTEP_COL_CMD + 3 + i) + r);
             }
-            ssb::outer_row(p_err, v, q, v_sp, cy, sy, P, w_sp, f_sp);
         }
         float tau[3], f_c = f_sp;
-        ssb::pid_row(w, w_sp, P, dt, inv_dt, integ, prev, has_prev, tau);
-        ssb::mix_row(f_c, tau, P);
+        ssb::pid_row(w, w_sp, P, D, dt, integ, prev, has_prev, tau);
         if (level == SWARMSTEP_LEVEL_MOTOR) {
-            f_c = mot_fc;
-            tau[0] = mot_tau[0]; tau[1] = mot_tau[1]; tau[2] = mot_tau[2];
+            f_c = u[0]; tau[0] = u[1]; tau[1] = u[2]; tau[2] = u[3];
+        } else {
+            ssb::mix_row(f_c, tau, P);
         }
         float p_hi_n[3], p_lo_n[3], v_n[3], q_n[4], w_n[3];
-        const bool ok = ssb::rk4_row(p_hi, p_lo, v, q, w, f_c, tau, P, dt, compensated != 0,
+        const bool ok = ssb::rk4_row(p_hi, p_lo, v, q, w, f_c, tau, P, D, dt, COMP,
                                      p_hi_n, p_lo_n, v_n, q_n, w_n);
         if (!ok) {
             // fault: revert to pre-step values, kill, report (quad.py:425-436)
@@ -156,7 +168,7 @@ quad_step_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t 
         __stcs(C.col(SWARMSTEP_COL_OMEGA + i) + r, w[i]);
         __stcs(C.col(SWARMSTEP_COL_INTEGRAL + i) + r, integ[i]);
         __stcs(C.col(SWARMSTEP_COL_PREV + i) + r, prev[i]);
-        if (compensated) __stcs(C.col(SWARMSTEP_COL_POS_LO + i) + r, p_lo[i]);
+        if (COMP) __stcs(C.col(SWARMSTEP_COL_POS_LO + i) + r, p_lo[i]);
     }
 #pragma unroll
     for (int i = 0; i < 4; i++) __stcs(C.col(SWARMSTEP_COL_QUAT + i) + r, q[i]);
@@ -168,8 +180,8 @@ quad_step_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t 
         __stcs(C.col(SWARMSTEP_COL_SP + 2) + r, w_sp[2]);
         __stcs(C.col(SWARMSTEP_COL_SP + 3) + r, f_sp);
     }
-    uint8_t nfl = (uint8_t)((fl & SWARMSTEP_LEVEL_MASK) | (alive ? SWARMSTEP_FLAG_ALIVE : 0u) |
-                            (has_prev ? SWARMSTEP_FLAG_HAS_PREV : 0u));
+    const uint8_t nfl = (uint8_t)((fl & SWARMSTEP_LEVEL_MASK) | (alive ? SWARMSTEP_FLAG_ALIVE : 0u) |
+                                  (has_prev ? SWARMSTEP_FLAG_HAS_PREV : 0u));
     if (nfl != fl) flags[r] = nfl;
 }
 
@@ -321,9 +333,10 @@ int swarmstep_quad_step(const swarmstep_group_view *g, const swarmstep_quad_para
     if (k_substeps < 1) return set_err(SWARMSTEP_EINVAL, "k_substeps must be >= 1");
     if (!g->counters) return set_err(SWARMSTEP_EINVAL, "null counters");
     if (g->n == 0) return SWARMSTEP_OK;
-    quad_step_kernel<<<grid_for(g->n, kBlock), kBlock, 0, (cudaStream_t)stream>>>(
+    auto kern = g->compensated ? quad_step_kernel<true> : quad_step_kernel<false>;
+    kern<<<grid_for(g->n, kBlock), kBlock, 0, (cudaStream_t)stream>>>(
         g->cols, g->flags, g->n, g->stride, g->counters, g->fault_log, g->fault_log ? g->fault_cap : 0,
-        g->compensated, overlay_active, tick_base, *p, dt, k_substeps);
+        overlay_active, tick_base, *p, dt, k_substeps);
     return cuda_status("quad_step_kernel");
 }
 

@@ -1,0 +1,65 @@
+"""Summarise an ncu report (.ncu-rep) into a small JSON for profiles/.
+
+python tools/ncu_summary.py <report.ncu-rep> <out.json> [agents]
+"""
+
+import csv
+import io
+import json
+import subprocess
+import sys
+
+KEYS = [
+    "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "dram__throughput.avg.pct_of_peak_sustained_elapsed", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+    "launch__registers_per_thread", "launch__block_size", "launch__grid_size", "launch__occupancy_limit_registers",
+    "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+    "smsp__inst_executed.sum", "smsp__thread_inst_executed_per_inst_executed.ratio",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm__cycles_elapsed.avg.per_second",
+    "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_not_selected_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_branch_resolving_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_no_instruction_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_lg_throttle_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_drain_per_issue_active.ratio",
+    "lts__t_bytes.sum", "l1tex__t_bytes.sum",
+]
+
+
+def main():
+    rep, out = sys.argv[1], sys.argv[2]
+    agents = int(sys.argv[3]) if len(sys.argv) > 3 else None
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    kernels = []
+    for r in rows[2:]:
+        d = {"kernel": r[hdr.index("Kernel Name")][:80]}
+        for k in KEYS:
+            if k in hdr:
+                i = hdr.index(k)
+                d[k] = f"{r[i]} {units[i]}".strip()
+        if agents:
+            def num(k, scale):
+                try:
+                    return float(r[hdr.index(k)].replace(",", "")) * scale
+                except (ValueError, IndexError):
+                    return None
+            unit = units[hdr.index("dram__bytes_read.sum")]
+            sc = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+            rd, wr = num("dram__bytes_read.sum", sc), num("dram__bytes_write.sum", sc)
+            if rd is not None and wr is not None:
+                d["dram_bytes_per_agent"] = (rd + wr) / agents
+        kernels.append(d)
+    json.dump({"report": rep, "agents": agents, "kernels": kernels}, open(out, "w"), indent=1)
+    print(json.dumps(kernels, indent=1))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,70 @@
+"""Kernel-variant sweep on a B200 (tuning aid, not part of the product).
+
+Builds variants of libswarmstep_b200.so with different -D macros into /tmp,
+then times the fused step (K=10 and K=1) for each in a fresh subprocess.
+Usage: python tools/tune.py [agents]
+"""
+
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+VARIANTS = {
+    "b256m2": ["-DSSB_STEP_BLOCK=256", "-DSSB_STEP_MINB=2"],
+    "b128m5": ["-DSSB_STEP_BLOCK=128", "-DSSB_STEP_MINB=5"],
+    "b128m6": ["-DSSB_STEP_BLOCK=128", "-DSSB_STEP_MINB=6"],
+    "b64m10": ["-DSSB_STEP_BLOCK=64", "-DSSB_STEP_MINB=10"],
+}
+
+CHILD = r'''
+import json, sys, torch, numpy as np
+sys.path.insert(0, "%(root)s")
+from bench import workload, _Batch
+from paper_2308_12698_b200 import B200QuadGroup
+n = %(n)d
+pos, sp = workload(n, 0)
+g = B200QuadGroup(0, _Batch(n, pos, 0), device="cuda:0")
+g.set_setpoints(torch.from_numpy(sp).cuda(), columns=True)
+out = {}
+for k in (10, 1):
+    for _ in range(5): g.step_async(1e-3, k)
+    g.collect_faults(); torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = 20
+    e0.record(g.stream)
+    for _ in range(steps): g.step_async(1e-3, k)
+    e1.record(g.stream); torch.cuda.synchronize(); g.collect_faults()
+    ms = e0.elapsed_time(e1) / steps
+    out[f"K{k}_ms"] = ms
+    out[f"K{k}_agent_steps_per_s"] = n * k / ms * 1e3
+out["K1_GBps"] = 221 * n / out["K1_ms"] / 1e6
+print("RESULT " + json.dumps(out))
+'''
+
+
+def main():
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 4_000_000
+    from paper_2308_12698_b200._build import NVCC_FLAGS, _nvcc, sources, INCLUDE, CSRC
+    res = {}
+    for name, defs in VARIANTS.items():
+        so = f"/tmp/ssb_{name}.so"
+        cmd = [_nvcc(), *NVCC_FLAGS, *defs, f"-I{INCLUDE}", f"-I{CSRC}", "-o", so, *map(str, sources())]
+        b = subprocess.run(cmd, capture_output=True, text=True)
+        regs = [l for l in b.stderr.splitlines() if "registers" in l]
+        env = dict(os.environ, SWARMSTEP_B200_LIB_OVERRIDE=so)
+        p = subprocess.run([sys.executable, "-c", CHILD % dict(root=ROOT, n=n)], env=env, capture_output=True, text=True)
+        line = [l for l in p.stdout.splitlines() if l.startswith("RESULT ")]
+        res[name] = json.loads(line[0][7:]) if line else {"error": p.stderr[-800:]}
+        res[name]["ptxas"] = regs[-2:]
+        print(name, json.dumps(res[name]), flush=True)
+    Path(ROOT / "gpurun_out").mkdir(exist_ok=True)
+    (ROOT / "gpurun_out" / "tune.json").write_text(json.dumps(res, indent=1))
+
+
+if __name__ == "__main__":
+    main()
