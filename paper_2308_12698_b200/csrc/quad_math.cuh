@@ -65,9 +65,9 @@ __device__ __forceinline__ Derived derive(const swarmstep_quad_params &P, float 
 {
     Derived d;
     d.g = P.g;
-    d.gx = (P.izz - P.iyy) * P.inv_ixx;
-    d.gy = (P.ixx - P.izz) * P.inv_iyy;
-    d.gz = (P.iyy - P.ixx) * P.inv_izz;
+    d.gx = 4.0f * (P.izz - P.iyy) * P.inv_ixx;   // x4: products of half rates
+    d.gy = 4.0f * (P.ixx - P.izz) * P.inv_iyy;
+    d.gz = 4.0f * (P.iyy - P.ixx) * P.inv_izz;
 #pragma unroll
     for (int i = 0; i < 3; i++) d.kd_dt[i] = P.kd[i] * inv_dt;
     return d;
@@ -77,12 +77,14 @@ __device__ __forceinline__ Derived derive(const swarmstep_quad_params &P, float 
 //   vdot = (f_c/m) R(q) e_z - g e_z ; qdot = q (x) (0, w) / 2 ;
 //   wdot = I^-1 (tau - w x (I w)) = tau/I - (gyro coefficient) w_j w_k.
 // fc2 = 2 f_c / m, fcg = f_c / m - g, tI = tau / I (per axis).
-__device__ __forceinline__ void deriv(const float q[4], const float w[3], float fc2, float fcg,
+// h = w / 2 is carried instead of w (saves the halving per stage); the
+// gyroscopic coefficients are pre-multiplied by 4 accordingly.
+__device__ __forceinline__ void deriv(const float q[4], const float h[3], float fc2, float fcg,
                                       const float tI[3], const Derived &D,
                                       float dv[3], float dq[4], float dw[3])
 {
     const float qw = q[0], qx = q[1], qy = q[2], qz = q[3];
-    const float hx = 0.5f * w[0], hy = 0.5f * w[1], hz = 0.5f * w[2];
+    const float hx = h[0], hy = h[1], hz = h[2];
     dv[0] = fc2 * fmaf(qx, qz, qw * qy);
     dv[1] = fc2 * fmaf(qy, qz, -qw * qx);
     dv[2] = fmaf(-fc2, fmaf(qx, qx, qy * qy), fcg);
@@ -90,28 +92,21 @@ __device__ __forceinline__ void deriv(const float q[4], const float w[3], float 
     dq[1] = fmaf(qw, hx, fmaf(qy, hz, -qz * hy));
     dq[2] = fmaf(qw, hy, fmaf(qz, hx, -qx * hz));
     dq[3] = fmaf(qw, hz, fmaf(qx, hy, -qy * hx));
-    dw[0] = fmaf(-D.gx, w[1] * w[2], tI[0]);
-    dw[1] = fmaf(-D.gy, w[2] * w[0], tI[1]);
-    dw[2] = fmaf(-D.gz, w[0] * w[1], tI[2]);
+    dw[0] = fmaf(-D.gx, hy * hz, tI[0]);
+    dw[1] = fmaf(-D.gy, hz * hx, tI[1]);
+    dw[2] = fmaf(-D.gz, hx * hy, tI[2]);
 }
 
-__device__ __forceinline__ void two_sum(float a, float b, float &s, float &e)
-{
-    s = a + b;
-    const float bb = s - a;
-    e = (a - (s - bb)) + (b - bb);
-}
-
-// One classical RK4 step with the wrench held (quad.py:350-437).  Writes the
-// candidate state into the *_n arrays and returns true when the row stays
-// finite (the reference's fault predicate, quad.py:404-430).  Position does
-// not feed any derivative, so only its final combination is formed.
-__device__ __forceinline__ bool rk4_row(const float p_hi[3], const float p_lo[3], const float v[3],
-                                        const float q[4], const float w[3], float f_c,
-                                        const float tau[3], const swarmstep_quad_params &P,
-                                        const Derived &D, float dt, bool compensated,
-                                        float p_hi_n[3], float p_lo_n[3], float v_n[3],
-                                        float q_n[4], float w_n[3])
+// One classical RK4 step with the wrench held (quad.py:350-437), in place.
+// Returns false when the row turns non-finite (the reference's fault
+// predicate, quad.py:404-430); the state is then garbage and the caller
+// restores the pre-step values (by deterministic re-execution, see
+// swarmstep_b200.cu).  Position feeds no derivative, so only its final
+// combination is formed: dp = dt/6 (v + 2 v2 + 2 v3 + v4).
+template <bool COMP>
+__device__ __forceinline__ bool rk4_inplace(float p_hi[3], float p_lo[3], float v[3], float q[4],
+                                            float w[3], float f_c, const float tau[3],
+                                            const swarmstep_quad_params &P, const Derived &D, float dt)
 {
     const float half = 0.5f * dt;
     const float h6 = dt * (1.0f / 6.0f);
@@ -122,8 +117,10 @@ __device__ __forceinline__ bool rk4_row(const float p_hi[3], const float p_lo[3]
     float kv[3], kq[4], kw[3];
     float av[3], aq[4], aw[3], ap[3];
     float sv[3], sq[4], sw[3];
+    const float hw[3] = {0.5f * w[0], 0.5f * w[1], 0.5f * w[2]};
+    const float qtr = 0.5f * half, hdt = 0.5f * dt;  // stage steps on half rates
 
-    deriv(q, w, fc2, fcg, tI, D, kv, kq, kw);                       // k1
+    deriv(q, hw, fc2, fcg, tI, D, kv, kq, kw);                      // k1
 #pragma unroll
     for (int i = 0; i < 3; i++) { av[i] = kv[i]; aw[i] = kw[i]; ap[i] = v[i]; }
 #pragma unroll
@@ -131,7 +128,7 @@ __device__ __forceinline__ bool rk4_row(const float p_hi[3], const float p_lo[3]
 #pragma unroll
     for (int s = 0; s < 2; s++) {                                   // k2, k3 at y + h/2 k
 #pragma unroll
-        for (int i = 0; i < 3; i++) { sv[i] = fmaf(half, kv[i], v[i]); sw[i] = fmaf(half, kw[i], w[i]); }
+        for (int i = 0; i < 3; i++) { sv[i] = fmaf(half, kv[i], v[i]); sw[i] = fmaf(qtr, kw[i], hw[i]); }
 #pragma unroll
         for (int i = 0; i < 4; i++) sq[i] = fmaf(half, kq[i], q[i]);
 #pragma unroll
@@ -143,7 +140,7 @@ __device__ __forceinline__ bool rk4_row(const float p_hi[3], const float p_lo[3]
         for (int i = 0; i < 4; i++) aq[i] = fmaf(2.0f, kq[i], aq[i]);
     }
 #pragma unroll
-    for (int i = 0; i < 3; i++) { sv[i] = fmaf(dt, kv[i], v[i]); sw[i] = fmaf(dt, kw[i], w[i]); }
+    for (int i = 0; i < 3; i++) { sv[i] = fmaf(dt, kv[i], v[i]); sw[i] = fmaf(hdt, kw[i], hw[i]); }
 #pragma unroll
     for (int i = 0; i < 4; i++) sq[i] = fmaf(dt, kq[i], q[i]);
 #pragma unroll
@@ -157,51 +154,49 @@ __device__ __forceinline__ bool rk4_row(const float p_hi[3], const float p_lo[3]
     // y' = y + dt/6 (k1 + 2 k2 + 2 k3 + k4)
 #pragma unroll
     for (int i = 0; i < 3; i++) {
-        v_n[i] = fmaf(h6, av[i], v[i]);
-        w_n[i] = fmaf(h6, aw[i], w[i]);
+        v[i] = fmaf(h6, av[i], v[i]);
+        w[i] = fmaf(h6, aw[i], w[i]);
         const float dp = h6 * ap[i];
-        if (compensated) {
-            float s, e;
-            two_sum(p_hi[i], dp + p_lo[i], s, e);
-            const float hi2 = s + e;          // renormalise: |lo| <= ulp(hi)/2
-            p_lo_n[i] = e - (hi2 - s);
-            p_hi_n[i] = hi2;
+        if (COMP) {
+            // Fast2Sum: exact when |hi| >= |dp + lo| (a position against one
+            // tick's displacement); keeps |lo| <= ulp(hi)/2
+            const float b = dp + p_lo[i];
+            const float sum = p_hi[i] + b;
+            p_lo[i] = b - (sum - p_hi[i]);
+            p_hi[i] = sum;
         } else {
-            p_hi_n[i] = p_hi[i] + dp;
-            p_lo_n[i] = 0.0f;
+            p_hi[i] += dp;
         }
     }
 #pragma unroll
-    for (int i = 0; i < 4; i++) q_n[i] = fmaf(h6, aq[i], q[i]);
+    for (int i = 0; i < 4; i++) q[i] = fmaf(h6, aq[i], q[i]);
 
     // single post-step renormalisation; zero / non-finite norm is a fault
-    const float nsq = fmaf(q_n[0], q_n[0], fmaf(q_n[1], q_n[1], fmaf(q_n[2], q_n[2], q_n[3] * q_n[3])));
+    const float nsq = fmaf(q[0], q[0], fmaf(q[1], q[1], fmaf(q[2], q[2], q[3] * q[3])));
     const float inv = rsqrt_a(nsq);
-    bool ok = isfinite(nsq) && nsq > 0.0f;
 #pragma unroll
-    for (int i = 0; i < 4; i++) q_n[i] *= inv;
+    for (int i = 0; i < 4; i++) q[i] *= inv;
     // 0 * x is NaN exactly when x is inf / NaN (IEEE; no fast-math here), so
     // one compare covers every position / velocity / rate component
-    const float chk = 0.0f * (((p_hi_n[0] + p_hi_n[1]) + (p_hi_n[2] + p_lo_n[0])) +
-                              ((p_lo_n[1] + p_lo_n[2]) + (v_n[0] + v_n[1])) +
-                              ((v_n[2] + w_n[0]) + (w_n[1] + w_n[2])));
-    ok = ok && (chk == 0.0f);
-    return ok;
+    const float chk = 0.0f * (((p_hi[0] + p_hi[1]) + (p_hi[2] + v[0])) + ((v[1] + v[2]) + (w[0] + w[1])) +
+                              (w[2] + (COMP ? (p_lo[0] + p_lo[1]) + p_lo[2] : 0.0f)));
+    return isfinite(nsq) && nsq > 0.0f && chk == 0.0f;
 }
 
 // mix_to_motors (quad.py:143-168): realized wrench after per-motor clamp.
+// G (quad.py:106-122) has mutually orthogonal rows, so G^-1 = G^T diag(c):
+// motor i = c0 f + s_i1 c1 tau_x + s_i2 c2 tau_y + s_i3 c3 tau_z with the
+// sign pattern of G's columns.  P.G_inv carries the exact inverse; the host
+// checks the pattern (params.py) and the kernel uses c = |G_inv[0][:]|.
 __device__ __forceinline__ void mix_row(float &f_c, float tau[3], const swarmstep_quad_params &P)
 {
-    const float w4[4] = {f_c, tau[0], tau[1], tau[2]};
-    float m[4];
-    bool sat = false;
-#pragma unroll
-    for (int i = 0; i < 4; i++) {
-        m[i] = fmaf(P.G_inv[i * 4 + 0], w4[0], fmaf(P.G_inv[i * 4 + 1], w4[1],
-               fmaf(P.G_inv[i * 4 + 2], w4[2], P.G_inv[i * 4 + 3] * w4[3])));
-        sat = sat || (m[i] < 0.0f) || (m[i] > P.f_max);
-    }
-    if (sat) {
+    const float F = P.G_inv[0] * f_c, A = P.G_inv[1] * tau[0];
+    const float B = fabsf(P.G_inv[2]) * tau[1], C = P.G_inv[3] * tau[2];
+    const float FpA = F + A, FmA = F - A, BmC = B - C, BpC = B + C;
+    float m[4] = {FpA - BmC, FmA - BpC, FmA + BpC, FpA + BmC};
+    const float lo = fminf(fminf(m[0], m[1]), fminf(m[2], m[3]));
+    const float hi = fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3]));
+    if (lo < 0.0f || hi > P.f_max) {
 #pragma unroll
         for (int i = 0; i < 4; i++) m[i] = clip(m[i], 0.0f, P.f_max);
         f_c = (m[0] + m[1]) + (m[2] + m[3]);
@@ -233,18 +228,21 @@ __device__ __forceinline__ void motor_wrench(const float rpm[4], const swarmstep
 // reach this (they are frozen: tau = 0, f_c = 0, state untouched).
 __device__ __forceinline__ void pid_row(const float w[3], const float w_sp[3],
                                         const swarmstep_quad_params &P, const Derived &D, float dt,
-                                        float integ[3], float prev[3], bool &has_prev, float tau[3])
+                                        float integ[3], float prev[3], float tau[3])
 {
+    // (no previous sample -> no D term, control.py:175-177: the caller sets
+    // prev := w for such rows before the first tick, making the difference 0)
 #pragma unroll
     for (int a = 0; a < 3; a++) {
+        const float pv = prev[a];
         const float e = w_sp[a] - w[a];
-        integ[a] = clip(fmaf(e, dt, integ[a]), -P.i_limit[a], P.i_limit[a]);
-        float t = fmaf(P.kp[a], e, P.ki[a] * integ[a]);
-        if (has_prev) t = fmaf(-D.kd_dt[a], w[a] - prev[a], t);
-        tau[a] = t;
+        // min/max clamp: a NaN error (NaN rate command) faults the row this
+        // tick regardless (tau is NaN), so NaN need not be kept in the state
+        integ[a] = fminf(fmaxf(fmaf(e, dt, integ[a]), -P.i_limit[a]), P.i_limit[a]);
+        const float t = fmaf(P.kp[a], e, P.ki[a] * integ[a]);
+        tau[a] = fmaf(-D.kd_dt[a], w[a] - pv, t);
         prev[a] = w[a];
     }
-    has_prev = true;
 }
 
 // 2 atan2(s, c) / s for s, c >= 0 (the axis-angle factor of control.py:283-285),
@@ -299,7 +297,7 @@ __device__ __forceinline__ void outer_row(const float p_err[3], const float v[3]
         z[0] = a[0] * ia; z[1] = a[1] * ia; z[2] = a[2] * ia;
         fc = P.m * fmaf(zb0, a[0], fmaf(zb1, a[1], zb2 * a[2]));
     }
-    f_c_sp = clip(fc, 0.0f, P.fc_max);
+    f_c_sp = fminf(fmaxf(fc, 0.0f), P.fc_max);
 
     // y = z x x_c / |z x x_c| with x_c = (cy, sy, 0); degenerate fallback from y_c
     float yd[3];
@@ -335,35 +333,35 @@ __device__ __forceinline__ void outer_row(const float p_err[3], const float v[3]
     const float s00 = (b0 || b1) ? m00 : -m00;
     const float s11 = (b0 || b2) ? m11 : -m11;
     const float s22 = (b0 || b3) ? m22 : -m22;
+    // Any positive scale of q_des leaves the result unchanged: q_err is
+    // linear in q_des, and the axis-angle vector e_xyz * 2 atan2(|e_xyz|,
+    // e_w) / |e_xyz| is invariant to a positive scale of q_err.  So the
+    // branch quaternion is formed scaled by s = 2 sqrt(t) -- (t, m_ij +- m_ji)
+    // -- with no square root, and neither q_des nor q_err is renormalised
+    // (the reference renormalises both; identical in R).
     const float t = fmaxf(1.0f + s00 + s11 + s22, 1e-30f);
-    const float rt = rsqrt_a(t);
-    const float big = 0.5f * (t * rt), hr = 0.5f * rt;
     const float d21 = m21 - m12, d02 = m02 - m20, d10 = m10 - m01;
     const float a01 = m01 + m10, a02 = m02 + m20, a12 = m12 + m21;
     float qd[4];
-    qd[0] = b0 ? big : hr * (b1 ? d21 : (b2 ? d02 : d10));
-    qd[1] = b1 ? big : hr * (b0 ? d21 : (b2 ? a01 : a02));
-    qd[2] = b2 ? big : hr * (b0 ? d02 : (b1 ? a01 : a12));
-    qd[3] = b3 ? big : hr * (b0 ? d10 : (b1 ? a02 : a12));
-    {
-        const float in = rsqrt_a(fmaf(qd[0], qd[0], fmaf(qd[1], qd[1], fmaf(qd[2], qd[2], qd[3] * qd[3]))));
-        qd[0] *= in; qd[1] *= in; qd[2] *= in; qd[3] *= in;
-    }
-    // q_err = conj(q) (x) q_des, renormalised (quat.py:75-92), sign so w >= 0
-    float e0 = fmaf(qw, qd[0], fmaf(qx, qd[1], fmaf(qy, qd[2], qz * qd[3])));
-    float e1 = fmaf(qw, qd[1], fmaf(-qx, qd[0], fmaf(-qy, qd[3], qz * qd[2])));
-    float e2 = fmaf(qw, qd[2], fmaf(qx, qd[3], fmaf(-qy, qd[0], -qz * qd[1])));
-    float e3 = fmaf(qw, qd[3], fmaf(-qx, qd[2], fmaf(qy, qd[1], -qz * qd[0])));
-    {
-        float in = rsqrt_a(fmaf(e0, e0, fmaf(e1, e1, fmaf(e2, e2, e3 * e3))));
-        in = e0 < 0.0f ? -in : in;
-        e0 *= in; e1 *= in; e2 *= in; e3 *= in;
-    }
+    qd[0] = b0 ? t : (b1 ? d21 : (b2 ? d02 : d10));
+    qd[1] = b1 ? t : (b0 ? d21 : (b2 ? a01 : a02));
+    qd[2] = b2 ? t : (b0 ? d02 : (b1 ? a01 : a12));
+    qd[3] = b3 ? t : (b0 ? d10 : (b1 ? a02 : a12));
+    // q_err = conj(q) (x) q_des (quat.py:75-92); the w >= 0 flip becomes |e_w|
+    // and a sign on the rate setpoint
+    const float e0 = fmaf(qw, qd[0], fmaf(qx, qd[1], fmaf(qy, qd[2], qz * qd[3])));
+    const float e1 = fmaf(qw, qd[1], fmaf(-qx, qd[0], fmaf(-qy, qd[3], qz * qd[2])));
+    const float e2 = fmaf(qw, qd[2], fmaf(qx, qd[3], fmaf(-qy, qd[0], -qz * qd[1])));
+    const float e3 = fmaf(qw, qd[3], fmaf(-qx, qd[2], fmaf(qy, qd[1], -qz * qd[0])));
     const float ssq = fmaf(e1, e1, fmaf(e2, e2, e3 * e3));
-    const float factor = axis_angle_factor(sqrt_a(ssq), e0);
-    w_sp[0] = clip(P.k_att[0] * (e1 * factor), -P.omega_sp_max, P.omega_sp_max);
-    w_sp[1] = clip(P.k_att[1] * (e2 * factor), -P.omega_sp_max, P.omega_sp_max);
-    w_sp[2] = clip(P.k_att[2] * (e3 * factor), -P.omega_sp_max, P.omega_sp_max);
+    float factor = axis_angle_factor(sqrt_a(ssq), fabsf(e0));
+    factor = e0 < 0.0f ? -factor : factor;
+    // |w_sp| <= omega_sp_max.  min/max (not NaN-propagating) is safe here:
+    // non-finite outer-loop inputs are rejected before launch (InvalidState).
+    const float wm = P.omega_sp_max;
+    w_sp[0] = fminf(fmaxf(P.k_att[0] * (e1 * factor), -wm), wm);
+    w_sp[1] = fminf(fmaxf(P.k_att[1] * (e2 * factor), -wm), wm);
+    w_sp[2] = fminf(fmaxf(P.k_att[2] * (e3 * factor), -wm), wm);
 }
 
 }  // namespace ssb

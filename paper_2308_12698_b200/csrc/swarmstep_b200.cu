@@ -62,6 +62,123 @@ struct Cols {
 // ---------------------------------------------------------------------------
 // The fused step kernel.
 // ---------------------------------------------------------------------------
+#ifndef SSB_TICK_UNROLL
+#define SSB_TICK_UNROLL 1
+#endif
+constexpr int kTickUnroll = SSB_TICK_UNROLL;
+
+// One agent's registers for a launch.
+struct Row {
+    float p_hi[3], p_lo[3], v[3], q[4], w[3], integ[3], prev[3];
+    // u[]: per-launch setpoint registers, shared by the three levels
+    //   POS:   p_sp xyz, v_sp xyz (+ overlay on tick 0), cos(yaw), sin(yaw)
+    //   MOTOR: rotor-model wrench f_c, tau xyz (core.py:189-197)
+    float u[8];
+    float w_sp[3], f_sp;   // inner-loop setpoints (stale ones for MOTOR rows)
+    bool has_prev;
+};
+
+template <bool COMP>
+__device__ __forceinline__ void load_state(const Cols &C, int64_t r, Row &R)
+{
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+        R.p_hi[i] = __ldcs(C.col(SWARMSTEP_COL_POS + i) + r);
+        R.v[i] = __ldcs(C.col(SWARMSTEP_COL_VEL + i) + r);
+        R.w[i] = __ldcs(C.col(SWARMSTEP_COL_OMEGA + i) + r);
+        R.integ[i] = __ldcs(C.col(SWARMSTEP_COL_INTEGRAL + i) + r);
+        R.prev[i] = __ldcs(C.col(SWARMSTEP_COL_PREV + i) + r);
+        R.p_lo[i] = COMP ? __ldcs(C.col(SWARMSTEP_COL_POS_LO + i) + r) : 0.0f;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; i++) R.q[i] = __ldcs(C.col(SWARMSTEP_COL_QUAT + i) + r);
+#pragma unroll
+    for (int i = 0; i < 7; i++) R.u[i] = __ldcs(C.col(SWARMSTEP_COL_CMD + i) + r);
+    R.u[7] = 0.0f;
+}
+
+// Per-launch setpoint preparation (commands are fixed across the K ticks).
+__device__ __forceinline__ void setup_level(const Cols &C, int64_t r, int level, int overlay_active,
+                                            const swarmstep_quad_params &P, Row &R)
+{
+    if (!R.has_prev) {
+        // first sample: no D term (control.py:175-177) <=> prev := w
+#pragma unroll
+        for (int i = 0; i < 3; i++) R.prev[i] = R.w[i];
+    }
+    R.w_sp[0] = R.w_sp[1] = R.w_sp[2] = R.f_sp = 0.0f;
+    if (level == SWARMSTEP_LEVEL_POS) {
+        float s, c;
+        sincosf(R.u[6], &s, &c);
+        R.u[6] = c;
+        R.u[7] = s;
+        if (overlay_active) {
+#pragma unroll
+            for (int i = 0; i < 3; i++) R.u[3 + i] += __ldg(C.col(SWARMSTEP_COL_OVERLAY + i) + r);
+        }
+    } else if (level == SWARMSTEP_LEVEL_RATE) {
+        R.w_sp[0] = R.u[0]; R.w_sp[1] = R.u[1]; R.w_sp[2] = R.u[2]; R.f_sp = R.u[3];
+    } else {
+        // MOTOR: the PID still runs on the stale setpoints (core.py:109-110,
+        // 184-186); the integrated wrench comes from the rotor model
+#pragma unroll
+        for (int i = 0; i < 3; i++) R.w_sp[i] = __ldg(C.col(SWARMSTEP_COL_SP + i) + r);
+        R.f_sp = __ldg(C.col(SWARMSTEP_COL_SP + 3) + r);
+        float mt[3], mf;
+        ssb::motor_wrench(R.u, P, mf, mt);
+        R.u[0] = mf; R.u[1] = mt[0]; R.u[2] = mt[1]; R.u[3] = mt[2];
+    }
+}
+
+// K ticks of one agent at a fixed command level (the body of QuadGroup.step,
+// core.py:166-202, repeated), state updated in place.  Returns the tick at
+// which the row faulted (its state registers are then garbage), or -1.
+// With pid_only_at >= 0 the loop stops after the controller part of that tick
+// (used to rebuild a faulted row's state, see the kernel).
+template <int LEVEL, bool COMP, bool RERUN>
+__device__ __forceinline__ int run_ticks(const Cols &C, int64_t r, int overlay_active,
+                                         const swarmstep_quad_params &P, const ssb::Derived &D,
+                                         float dt, int K, int pid_only_at, Row &R)
+{
+#pragma unroll kTickUnroll
+    for (int k = 0; k < K; k++) {
+        if (LEVEL == SWARMSTEP_LEVEL_POS) {
+            float p_err[3];
+#pragma unroll
+            for (int i = 0; i < 3; i++) p_err[i] = (R.u[i] - R.p_hi[i]) - R.p_lo[i];
+            ssb::outer_row(p_err, R.v, R.q, R.u + 3, R.u[6], R.u[7], P, R.w_sp, R.f_sp);
+            if (k == 0 && overlay_active) {
+                // the overlay lasts one tick (core.py:199-201)
+#pragma unroll
+                for (int i = 0; i < 3; i++) R.u[3 + i] = __ldg(C.col(SWARMSTEP_COL_CMD + 3 + i) + r);
+            }
+        }
+        float tau[3], f_c = R.f_sp;
+        ssb::pid_row(R.w, R.w_sp, P, D, dt, R.integ, R.prev, tau);
+        if (RERUN && k == pid_only_at) return -1;
+        if (LEVEL == SWARMSTEP_LEVEL_MOTOR) {
+            f_c = R.u[0]; tau[0] = R.u[1]; tau[1] = R.u[2]; tau[2] = R.u[3];
+        } else {
+            ssb::mix_row(f_c, tau, P);
+        }
+        if (!ssb::rk4_inplace<COMP>(R.p_hi, R.p_lo, R.v, R.q, R.w, f_c, tau, P, D, dt)) return k;
+    }
+    return -1;
+}
+
+template <bool COMP, bool RERUN>
+__device__ __forceinline__ int run_level(const Cols &C, int64_t r, int level, int overlay_active,
+                                         const swarmstep_quad_params &P, const ssb::Derived &D,
+                                         float dt, int K, int pid_only_at, Row &R)
+{
+    // level-specialised tick loops: no per-tick level branches
+    if (level == SWARMSTEP_LEVEL_POS)
+        return run_ticks<SWARMSTEP_LEVEL_POS, COMP, RERUN>(C, r, overlay_active, P, D, dt, K, pid_only_at, R);
+    if (level == SWARMSTEP_LEVEL_RATE)
+        return run_ticks<SWARMSTEP_LEVEL_RATE, COMP, RERUN>(C, r, 0, P, D, dt, K, pid_only_at, R);
+    return run_ticks<SWARMSTEP_LEVEL_MOTOR, COMP, RERUN>(C, r, 0, P, D, dt, K, pid_only_at, R);
+}
+
 template <bool COMP>
 __global__ void __launch_bounds__(kBlock, SSB_STEP_MINB)
 quad_step_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t n, int64_t stride,
@@ -72,116 +189,58 @@ quad_step_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t 
     const int64_t r = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     if (r >= n) return;
     const Cols C{cols, stride};
-    // Issue every state load before the flag test so one memory round trip
-    // covers the whole row (dead rows are rare; their loads are discarded).
+    // every state load is issued before the flag test: one memory round trip
+    // per row (dead rows are rare; their loads are discarded)
     const uint8_t fl = flags[r];
-    float p_hi[3], p_lo[3], v[3], q[4], w[3], integ[3], prev[3];
-#pragma unroll
-    for (int i = 0; i < 3; i++) {
-        p_hi[i] = __ldcs(C.col(SWARMSTEP_COL_POS + i) + r);
-        v[i] = __ldcs(C.col(SWARMSTEP_COL_VEL + i) + r);
-        w[i] = __ldcs(C.col(SWARMSTEP_COL_OMEGA + i) + r);
-        integ[i] = __ldcs(C.col(SWARMSTEP_COL_INTEGRAL + i) + r);
-        prev[i] = __ldcs(C.col(SWARMSTEP_COL_PREV + i) + r);
-        p_lo[i] = COMP ? __ldcs(C.col(SWARMSTEP_COL_POS_LO + i) + r) : 0.0f;
-    }
-#pragma unroll
-    for (int i = 0; i < 4; i++) q[i] = __ldcs(C.col(SWARMSTEP_COL_QUAT + i) + r);
-    // u[]: per-launch setpoint registers, shared by the three levels
-    //   POS:   p_sp xyz, v_sp xyz, cos(yaw), sin(yaw)
-    //   MOTOR: rotor-model wrench f_c, tau xyz (core.py:189-197)
-    float u[8];
-#pragma unroll
-    for (int i = 0; i < 7; i++) u[i] = __ldcs(C.col(SWARMSTEP_COL_CMD + i) + r);
-    u[7] = 0.0f;
+    Row R;
+    load_state<COMP>(C, r, R);
     if (!(fl & SWARMSTEP_FLAG_ALIVE)) return;  // dead rows are frozen (quad.py:395-437)
     const int level = (fl & SWARMSTEP_LEVEL_MASK) >> SWARMSTEP_LEVEL_SHIFT;
-    bool has_prev = (fl & SWARMSTEP_FLAG_HAS_PREV) != 0;
-
-    float w_sp[3] = {0.0f, 0.0f, 0.0f}, f_sp = 0.0f;
-    if (level == SWARMSTEP_LEVEL_POS) {
-        float s, c;
-        sincosf(u[6], &s, &c);
-        u[6] = c;
-        u[7] = s;
-        if (overlay_active) {
-#pragma unroll
-            for (int i = 0; i < 3; i++) u[3 + i] += __ldg(C.col(SWARMSTEP_COL_OVERLAY + i) + r);
-        }
-    } else if (level == SWARMSTEP_LEVEL_RATE) {
-        w_sp[0] = u[0]; w_sp[1] = u[1]; w_sp[2] = u[2]; f_sp = u[3];
-    } else {
-        // MOTOR: the PID still runs on the stale setpoints (core.py:109-110,
-        // 184-186); the integrated wrench comes from the rotor model
-        w_sp[0] = __ldg(C.col(SWARMSTEP_COL_SP + 0) + r);
-        w_sp[1] = __ldg(C.col(SWARMSTEP_COL_SP + 1) + r);
-        w_sp[2] = __ldg(C.col(SWARMSTEP_COL_SP + 2) + r);
-        f_sp = __ldg(C.col(SWARMSTEP_COL_SP + 3) + r);
-        float mt[3], mf;
-        ssb::motor_wrench(u, P, mf, mt);
-        u[0] = mf; u[1] = mt[0]; u[2] = mt[1]; u[3] = mt[2];
-    }
-
+    R.has_prev = (fl & SWARMSTEP_FLAG_HAS_PREV) != 0;
+    setup_level(C, r, level, overlay_active, P, R);
     const ssb::Derived D = ssb::derive(P, 1.0f / dt);
+
+    const int fault_k = run_level<COMP, false>(C, r, level, overlay_active, P, D, dt, K, -1, R);
     bool alive = true;
-    for (int k = 0; k < K; k++) {
-        if (level == SWARMSTEP_LEVEL_POS) {
-            float p_err[3];
-#pragma unroll
-            for (int i = 0; i < 3; i++) p_err[i] = (u[i] - p_hi[i]) - p_lo[i];
-            ssb::outer_row(p_err, v, q, u + 3, u[6], u[7], P, w_sp, f_sp);
-            if (k == 0 && overlay_active) {
-                // the overlay lasts one tick (core.py:199-201)
-#pragma unroll
-                for (int i = 0; i < 3; i++) u[3 + i] = __ldg(C.col(SWARMSTEP_COL_CMD + 3 + i) + r);
-            }
-        }
-        float tau[3], f_c = f_sp;
-        ssb::pid_row(w, w_sp, P, D, dt, integ, prev, has_prev, tau);
-        if (level == SWARMSTEP_LEVEL_MOTOR) {
-            f_c = u[0]; tau[0] = u[1]; tau[1] = u[2]; tau[2] = u[3];
-        } else {
-            ssb::mix_row(f_c, tau, P);
-        }
-        float p_hi_n[3], p_lo_n[3], v_n[3], q_n[4], w_n[3];
-        const bool ok = ssb::rk4_row(p_hi, p_lo, v, q, w, f_c, tau, P, D, dt, COMP,
-                                     p_hi_n, p_lo_n, v_n, q_n, w_n);
-        if (!ok) {
-            // fault: revert to pre-step values, kill, report (quad.py:425-436)
-            alive = false;
-            const uint32_t slot = atomicAdd(&counters[0], 1u);
-            if ((int64_t)slot < fault_cap)
-                fault_log[slot] = ((uint64_t)((tick_base + (uint32_t)k) & 0xFFFFFFu) << 40) | (uint64_t)r;
-            break;
-        }
-#pragma unroll
-        for (int i = 0; i < 3; i++) { p_hi[i] = p_hi_n[i]; p_lo[i] = p_lo_n[i]; v[i] = v_n[i]; w[i] = w_n[i]; }
-#pragma unroll
-        for (int i = 0; i < 4; i++) q[i] = q_n[i];
+    if (fault_k >= 0) {
+        // Fault at tick fault_k: the row keeps its pre-tick values, dies and is
+        // reported with its tick (quad.py:425-436).  The state was updated in
+        // place, so rebuild it by re-running ticks [0, fault_k) from the
+        // launch's inputs -- bit-identical by determinism -- plus the
+        // controller part of tick fault_k (the reference updates the PID state
+        // before rk4_step faults the row).
+        alive = false;
+        load_state<COMP>(C, r, R);
+        R.has_prev = (fl & SWARMSTEP_FLAG_HAS_PREV) != 0;
+        setup_level(C, r, level, overlay_active, P, R);
+        run_level<COMP, true>(C, r, level, overlay_active, P, D, dt, fault_k + 1, fault_k, R);
+        const uint32_t slot = atomicAdd(&counters[0], 1u);
+        if ((int64_t)slot < fault_cap)
+            fault_log[slot] = ((uint64_t)((tick_base + (uint32_t)fault_k) & 0xFFFFFFu) << 40) | (uint64_t)r;
     }
 
     // ---- store ----
 #pragma unroll
     for (int i = 0; i < 3; i++) {
-        __stcs(C.col(SWARMSTEP_COL_POS + i) + r, p_hi[i]);
-        __stcs(C.col(SWARMSTEP_COL_VEL + i) + r, v[i]);
-        __stcs(C.col(SWARMSTEP_COL_OMEGA + i) + r, w[i]);
-        __stcs(C.col(SWARMSTEP_COL_INTEGRAL + i) + r, integ[i]);
-        __stcs(C.col(SWARMSTEP_COL_PREV + i) + r, prev[i]);
-        if (COMP) __stcs(C.col(SWARMSTEP_COL_POS_LO + i) + r, p_lo[i]);
+        __stcs(C.col(SWARMSTEP_COL_POS + i) + r, R.p_hi[i]);
+        __stcs(C.col(SWARMSTEP_COL_VEL + i) + r, R.v[i]);
+        __stcs(C.col(SWARMSTEP_COL_OMEGA + i) + r, R.w[i]);
+        __stcs(C.col(SWARMSTEP_COL_INTEGRAL + i) + r, R.integ[i]);
+        __stcs(C.col(SWARMSTEP_COL_PREV + i) + r, R.prev[i]);
+        if (COMP) __stcs(C.col(SWARMSTEP_COL_POS_LO + i) + r, R.p_lo[i]);
     }
 #pragma unroll
-    for (int i = 0; i < 4; i++) __stcs(C.col(SWARMSTEP_COL_QUAT + i) + r, q[i]);
+    for (int i = 0; i < 4; i++) __stcs(C.col(SWARMSTEP_COL_QUAT + i) + r, R.q[i]);
     if (level != SWARMSTEP_LEVEL_MOTOR) {
-        // the last substep's setpoints become the stale setpoints a later
-        // MOTOR command runs the PID on (core.py:178-182)
-        __stcs(C.col(SWARMSTEP_COL_SP + 0) + r, w_sp[0]);
-        __stcs(C.col(SWARMSTEP_COL_SP + 1) + r, w_sp[1]);
-        __stcs(C.col(SWARMSTEP_COL_SP + 2) + r, w_sp[2]);
-        __stcs(C.col(SWARMSTEP_COL_SP + 3) + r, f_sp);
+        // the last tick's setpoints become the stale setpoints a later MOTOR
+        // command runs the PID on (core.py:178-182)
+#pragma unroll
+        for (int i = 0; i < 3; i++) __stcs(C.col(SWARMSTEP_COL_SP + i) + r, R.w_sp[i]);
+        __stcs(C.col(SWARMSTEP_COL_SP + 3) + r, R.f_sp);
     }
+    // has_prev |= alive (control.py:181): every row reaching here was alive
     const uint8_t nfl = (uint8_t)((fl & SWARMSTEP_LEVEL_MASK) | (alive ? SWARMSTEP_FLAG_ALIVE : 0u) |
-                                  (has_prev ? SWARMSTEP_FLAG_HAS_PREV : 0u));
+                                  SWARMSTEP_FLAG_HAS_PREV);
     if (nfl != fl) flags[r] = nfl;
 }
 

@@ -152,6 +152,11 @@ class DeviceParams(ctypes.Structure):
 def pack_device_params(params, rate_gains, outer_gains) -> DeviceParams:
     """Round the float64 per-type constants to the kernel's float32 struct."""
     g_mat, g_inv = allocation_matrices(params)
+    # the kernel's mixer uses G^-1 = sign(G^T) * c (csrc/quad_math.cuh mix_row)
+    c = np.abs(g_inv[0])
+    if not (g_mat[1, 0] > 0 and g_mat[2, 0] < 0 and g_mat[3, 0] > 0
+            and np.allclose(g_inv, np.sign(g_mat.T) * c, rtol=1e-9, atol=0.0)):
+        raise ValidationError("allocation matrix does not have the quadrotor X structure")
     ixx, iyy, izz = (float(v) for v in params.i_diag)
     f_max = float(params.k_t) * float(params.omega_max) ** 2
     dp = DeviceParams()

@@ -15,10 +15,12 @@ ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
 VARIANTS = {
-    "b256m2": ["-DSSB_STEP_BLOCK=256", "-DSSB_STEP_MINB=2"],
     "b128m5": ["-DSSB_STEP_BLOCK=128", "-DSSB_STEP_MINB=5"],
     "b128m6": ["-DSSB_STEP_BLOCK=128", "-DSSB_STEP_MINB=6"],
     "b64m10": ["-DSSB_STEP_BLOCK=64", "-DSSB_STEP_MINB=10"],
+    "b128m4u2": ["-DSSB_STEP_BLOCK=128", "-DSSB_STEP_MINB=4", "-DSSB_TICK_UNROLL=2"],
+    "b128m5u2": ["-DSSB_STEP_BLOCK=128", "-DSSB_STEP_MINB=5", "-DSSB_TICK_UNROLL=2"],
+    "b256m3": ["-DSSB_STEP_BLOCK=256", "-DSSB_STEP_MINB=3"],
 }
 
 CHILD = r'''
