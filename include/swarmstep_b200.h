@@ -154,6 +154,27 @@ int swarmstep_quad_unpack_f64(const swarmstep_group_view *g, const double *pos,
                               const double *vel, const double *quat, const double *omega,
                               const uint8_t *alive, void *stream);
 
+/* ---- neighbour-coupled swarm controller (config 5) --------- */
+
+/* Packs the alive rows' positions as float4 (x, y, z, 0) -- NaN for dead rows
+ * and for padding rows [n, n_out) -- into out_xyzw (device, n_out float4):
+ * the per-rank contribution to the NCCL all-gather. */
+int swarmstep_pack_positions(const swarmstep_group_view *g, float *out_xyzw, int64_t n_out,
+                             void *stream);
+
+/* Device workspace needed by swarmstep_neighbor_overlay for n_all agents. */
+int swarmstep_neighbor_workspace_bytes(int64_t n_all, uint64_t *bytes);
+
+/* Separation overlay for the local rows from all gathered positions:
+ *   v_i += sum_{j != i, alive, |p_i - p_j| < r_sense} k_sep (1 - d/r_sense) (p_i - p_j)/d
+ * (wire.py:320-340 repel field per neighbour, strict < as collision.py:166).
+ * Local row r is gathered row self_offset + r.  Spatial hash (cell >= r_sense)
+ * + CUB radix sort + 27-cell scan; writes (or adds, accumulate != 0) the
+ * overlay column block.  Deterministic summation order. */
+int swarmstep_neighbor_overlay(const swarmstep_group_view *g, const float *all_xyzw, int64_t n_all,
+                               int64_t self_offset, float r_sense, float k_sep, float cell,
+                               int accumulate, void *workspace, uint64_t ws_bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -295,6 +295,25 @@ class OracleGroup:
         return np.hstack([self.pos, self.vel, self.quat, self.omega])
 
 
+def neighbor_overlay(pos, alive, r_sense: float, k_sep: float, rows=None, chunk: int = 2048) -> np.ndarray:
+    """All-pairs float64 separation overlay (SURVEY 8(e) controller; the
+    wire.py:320-340 repel field applied per neighbour, strict < of
+    collision.py:166, zero-distance guard of wire.py:335).  Returns (len(rows), 3)."""
+    pos = np.asarray(pos, dtype=float)
+    alive = np.asarray(alive, dtype=bool)
+    rows = np.arange(pos.shape[0]) if rows is None else np.asarray(rows)
+    out = np.zeros((rows.shape[0], 3))
+    pa, ia = pos[alive], np.nonzero(alive)[0]
+    for s in range(0, rows.shape[0], chunk):
+        rr = rows[s:s + chunk]
+        diff = pos[rr][:, None, :] - pa[None, :, :]
+        d = np.sqrt(np.sum(diff * diff, axis=2))
+        m = (d < r_sense) & (d > 1e-12) & (ia[None, :] != rr[:, None]) & alive[rr][:, None]
+        w = np.where(m, k_sep * (1.0 - d / r_sense) / np.where(m, d, 1.0), 0.0)
+        out[s:s + chunk] = np.einsum("ij,ijk->ik", w, diff)
+    return out
+
+
 def cpu_count() -> int:
     try:
         return len(os.sched_getaffinity(0))

@@ -34,6 +34,7 @@ EXPORTS = (
     "swarmstep_quad_step", "swarmstep_quad_apply_commands", "swarmstep_quad_set_setpoints",
     "swarmstep_quad_mark_dead", "swarmstep_quad_retarget_waypoint",
     "swarmstep_quad_pack_f64", "swarmstep_quad_unpack_f64",
+    "swarmstep_pack_positions", "swarmstep_neighbor_workspace_bytes", "swarmstep_neighbor_overlay",
 )
 
 
@@ -76,6 +77,12 @@ def _declare(lib) -> None:
     lib.swarmstep_quad_pack_f64.argtypes = [view, vp, vp, vp, vp, vp, vp]
     lib.swarmstep_quad_unpack_f64.restype = i32
     lib.swarmstep_quad_unpack_f64.argtypes = [view, vp, vp, vp, vp, vp, vp]
+    lib.swarmstep_pack_positions.restype = i32
+    lib.swarmstep_pack_positions.argtypes = [view, vp, i64, vp]
+    lib.swarmstep_neighbor_workspace_bytes.restype = i32
+    lib.swarmstep_neighbor_workspace_bytes.argtypes = [i64, ctypes.POINTER(ctypes.c_uint64)]
+    lib.swarmstep_neighbor_overlay.restype = i32
+    lib.swarmstep_neighbor_overlay.argtypes = [view, vp, i64, i64, f32, f32, f32, i32, vp, ctypes.c_uint64, vp]
 
 
 def load():

@@ -11,27 +11,13 @@
 #include <string.h>
 
 #include "swarmstep_b200.h"
+#include "common.cuh"
 #include "quad_math.cuh"
 
 namespace {
 
-thread_local char g_err[512] = "";
-
-int set_err(int code, const char *msg)
-{
-    snprintf(g_err, sizeof(g_err), "%s", msg);
-    return code;
-}
-
-int cuda_status(const char *where)
-{
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) {
-        snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
-        return SWARMSTEP_ECUDA;
-    }
-    return SWARMSTEP_OK;
-}
+using ssb::cuda_status;
+using ssb::set_err;
 
 int check_view(const swarmstep_group_view *g)
 {
@@ -367,7 +353,7 @@ extern "C" {
 
 int swarmstep_abi_version(void) { return SWARMSTEP_ABI_VERSION; }
 
-const char *swarmstep_last_error(void) { return g_err; }
+const char *swarmstep_last_error(void) { return ssb::err_buf(); }
 
 int swarmstep_device_info(int *sm_count, int *cc_major, int *cc_minor)
 {

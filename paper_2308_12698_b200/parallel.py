@@ -1,0 +1,167 @@
+"""Agent sharding across GPUs and the neighbour-coupled swarm controller.
+
+One process per GPU (torchrun / torch.distributed).  Agents are independent
+in the reference (quad.py:6-7), so a swarm of N agents shards by
+contiguous agent index: rank r owns ids [lo_r, hi_r) in its own
+``B200QuadGroup`` and steps them with no data-path collective
+(``shard_range``, ``ShardedSwarm``).
+
+The only exchange is for the neighbour-coupled controller of config 5
+(``NeighborSeparation``): every tick each rank packs its alive positions
+(float4, NaN for dead rows), the ranks all-gather them over NCCL (NVLink /
+NVSwitch), and each rank computes the separation overlay of its own agents
+against the whole swarm on its GPU (csrc/neighbors.cu), which enters the
+next tick through the group's one-tick velocity overlay (core.py:137-139,
+172-175).  The reference defines no such controller; its form follows
+SURVEY.md 8(e) (the viewer repel field of wire.py:320-340 per neighbour,
+strict < of collision.py:166).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import ValidationError
+
+
+def shard_range(n_total: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous, balanced [lo, hi) agent-index range of ``rank`` (sizes differ by <= 1)."""
+    if world < 1 or not 0 <= rank < world or n_total < 0:
+        raise ValidationError("bad shard arguments")
+    base, extra = divmod(n_total, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def shard_sizes(n_total: int, world: int) -> list[int]:
+    return [hi - lo for lo, hi in (shard_range(n_total, r, world) for r in range(world))]
+
+
+@dataclass
+class ShardInfo:
+    rank: int
+    world: int
+    n_total: int
+    lo: int
+    hi: int
+    pad: int          # per-rank slot count in the all-gather (max shard size)
+
+    @property
+    def n_local(self) -> int:
+        return self.hi - self.lo
+
+    @property
+    def self_offset(self) -> int:
+        """Row of this rank's first agent in the gathered position buffer."""
+        return self.rank * self.pad
+
+    @property
+    def n_gathered(self) -> int:
+        return self.world * self.pad
+
+
+def make_shard(n_total: int, rank: int = 0, world: int = 1) -> ShardInfo:
+    lo, hi = shard_range(n_total, rank, world)
+    return ShardInfo(rank, world, n_total, lo, hi, max(shard_sizes(n_total, world)))
+
+
+class ShardedSwarm:
+    """This rank's shard of one homogeneous swarm: id routing and fault gathering.
+
+    ``group`` is the rank-local group (a ``B200QuadGroup`` holding ids
+    [lo, hi)); commands for ids outside the shard are ignored locally (every
+    rank sees the full command stream and applies its own), and fault ids of
+    a tick are all-gathered so every rank can emit the same FAULT_DEATH
+    event (core.py:460-465).
+    """
+
+    def __init__(self, group, shard: ShardInfo, process_group=None):
+        self.group = group
+        self.shard = shard
+        self.pg = process_group
+
+    def owns(self, agent_id: int) -> bool:
+        return self.shard.lo <= int(agent_id) < self.shard.hi
+
+    def apply_command(self, cmd) -> bool | None:
+        """True/False from the owning rank; None on ranks that do not own the id."""
+        if not self.owns(cmd.agent_id):
+            return None
+        return self.group.apply_command(cmd)
+
+    def mark_dead(self, agent_ids) -> list[int]:
+        return self.group.mark_dead([a for a in agent_ids if self.owns(a)])
+
+    def step(self, dt: float) -> np.ndarray:
+        """One tick; returns the fault ids of the whole swarm (sorted)."""
+        local = np.asarray(self.group.step(dt), dtype=np.int64)
+        return self.gather_ids(local)
+
+    def gather_ids(self, local: np.ndarray) -> np.ndarray:
+        if self.shard.world == 1:
+            return np.sort(local).astype(np.uint64)
+        import torch.distributed as dist
+        out = [None] * self.shard.world
+        dist.all_gather_object(out, local.tolist(), group=self.pg)
+        return np.sort(np.array([i for part in out for i in part], dtype=np.int64)).astype(np.uint64)
+
+
+class NeighborSeparation:
+    """Neighbour-coupled separation controller over a sharded swarm (config 5).
+
+    ``apply()`` performs one exchange + overlay computation; call it right
+    before ``group.step(dt)`` (``step()`` does both).  With world == 1 the
+    all-gather is skipped (the local buffer is the whole swarm).
+    """
+
+    def __init__(self, group, shard: ShardInfo, r_sense: float = 2.0, k_sep: float = 1.0,
+                 cell: float | None = None, process_group=None):
+        if not r_sense > 0.0:
+            raise ValidationError("r_sense must be positive")
+        self.group, self.shard = group, shard
+        self.r_sense, self.k_sep = float(r_sense), float(k_sep)
+        self.cell = float(cell) if cell is not None else float(r_sense)
+        if self.cell < self.r_sense:
+            raise ValidationError("cell must be >= r_sense")
+        self.pg = process_group
+        self._lib = _lib.load()
+        dev = group.device
+        n_all = shard.n_gathered
+        self.n_all = n_all
+        self.local = torch.empty((shard.pad, 4), dtype=torch.float32, device=dev)
+        self.all = self.local if shard.world == 1 else torch.empty((n_all, 4), dtype=torch.float32, device=dev)
+        nbytes = ctypes.c_uint64()
+        _lib.check(self._lib.swarmstep_neighbor_workspace_bytes(n_all, ctypes.byref(nbytes)))
+        self.workspace = torch.empty(int(nbytes.value), dtype=torch.uint8, device=dev)
+
+    def gather(self) -> torch.Tensor:
+        g = self.group
+        with torch.cuda.device(g.device), torch.cuda.stream(g.stream):
+            _lib.check(self._lib.swarmstep_pack_positions(g._view_ref, self.local.data_ptr(), self.shard.pad,
+                                                          ctypes.c_void_p(g.stream.cuda_stream)))
+            if self.shard.world > 1:
+                import torch.distributed as dist
+                dist.all_gather_into_tensor(self.all, self.local, group=self.pg)
+        return self.all
+
+    def apply(self) -> None:
+        g = self.group
+        self.gather()
+        # the overlay block is all-zero whenever no overlay is pending (the group
+        # clears it after every step), so the kernel always accumulates
+        with torch.cuda.device(g.device), torch.cuda.stream(g.stream):
+            _lib.check(self._lib.swarmstep_neighbor_overlay(
+                g._view_ref, self.all.data_ptr(), self.n_all, self.shard.self_offset,
+                ctypes.c_float(self.r_sense), ctypes.c_float(self.k_sep), ctypes.c_float(self.cell), 1,
+                self.workspace.data_ptr(), ctypes.c_uint64(self.workspace.numel()),
+                ctypes.c_void_p(g.stream.cuda_stream)))
+        g._overlay_active = True
+
+    def step(self, dt: float) -> np.ndarray:
+        self.apply()
+        return self.group.step(dt)

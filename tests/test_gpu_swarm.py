@@ -1,0 +1,91 @@
+"""GPU checks of the neighbour-coupled swarm controller (config 5): the device
+spatial-hash separation overlay against the float64 all-pairs oracle, at small
+size and at the config-5 size (100k agents, sampled rows)."""
+
+import numpy as np
+import pytest
+
+from conftest import cuda_ok
+from gpu_util import make_group
+from oracle import oracle as orc
+from scenarios import Scenario
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_ok(), reason="needs CUDA")]
+
+
+def _swarm(n, box, seed=0):
+    rng = np.random.default_rng(seed)
+    q = np.tile([1.0, 0, 0, 0], (n, 1))
+    return Scenario("swarm", n, 1e-3, 1, rng.uniform(0, box, (n, 3)) + [0, 0, 5], np.zeros((n, 3)), q,
+                    np.zeros((n, 3)), record=[])
+
+
+def _overlay(g):
+    return g.cols[33:36, :g.n].T.double().cpu().numpy()
+
+
+def _positions(g):
+    return g.batch.pos.copy(), g.batch.alive.copy()
+
+
+@pytest.mark.parametrize("n,box", [(3000, 15.0), (257, 4.0)])
+def test_overlay_matches_all_pairs_oracle(n, box):
+    from paper_2308_12698_b200.parallel import NeighborSeparation, make_shard
+    g = make_group(_swarm(n, box))
+    g.mark_dead([1, 7, n - 1])
+    ns = NeighborSeparation(g, make_shard(n), r_sense=2.0, k_sep=1.5)
+    ns.apply()
+    got = _overlay(g)
+    pos, alive = _positions(g)
+    want = orc.neighbor_overlay(pos, alive, 2.0, 1.5)
+    scale = np.max(np.abs(want))
+    assert scale > 0.1
+    np.testing.assert_allclose(got, want, rtol=1e-4, atol=1e-5 * scale)
+    assert np.all(got[~alive] == 0.0)
+
+
+def test_overlay_deterministic_and_one_tick():
+    from paper_2308_12698_b200.parallel import NeighborSeparation, make_shard
+    sc = _swarm(2000, 12.0, seed=3)
+    outs = []
+    for _ in range(2):
+        g = make_group(sc)
+        ns = NeighborSeparation(g, make_shard(sc.n), r_sense=2.0, k_sep=1.0)
+        ns.apply()
+        outs.append(_overlay(g).tobytes())
+        ns.group.step(1e-3)
+        assert np.all(_overlay(g) == 0.0)          # cleared after the tick (core.py:199-201)
+    assert outs[0] == outs[1]
+
+
+def test_coupled_steps_push_neighbours_apart():
+    from paper_2308_12698_b200.parallel import NeighborSeparation, make_shard
+    sc = _swarm(500, 3.0, seed=4)
+    g = make_group(sc)
+    ns = NeighborSeparation(g, make_shard(sc.n), r_sense=2.0, k_sep=2.0)
+
+    def mean_nn(pos):
+        d = np.linalg.norm(pos[:, None] - pos[None], axis=2) + np.eye(len(pos)) * 1e9
+        return d.min(axis=1).mean()
+
+    d0 = mean_nn(g.batch.pos)
+    for _ in range(300):
+        ns.step(2e-3)
+    assert mean_nn(g.batch.pos) > d0
+    assert g.batch.alive.all()
+
+
+def test_config5_size_sampled_rows():
+    """100k agents (config 5), r_sense 2 m: sampled rows vs the all-pairs oracle."""
+    from paper_2308_12698_b200.parallel import NeighborSeparation, make_shard
+    n = 100_000
+    sc = _swarm(n, 60.0, seed=5)
+    g = make_group(sc)
+    ns = NeighborSeparation(g, make_shard(n), r_sense=2.0, k_sep=1.0)
+    ns.apply()
+    got = _overlay(g)
+    pos, alive = _positions(g)
+    rows = np.random.default_rng(6).choice(n, 1024, replace=False)
+    want = orc.neighbor_overlay(pos, alive, 2.0, 1.0, rows=rows)
+    scale = np.max(np.abs(want))
+    np.testing.assert_allclose(got[rows], want, rtol=1e-4, atol=1e-5 * scale)
