@@ -94,6 +94,9 @@ typedef struct swarmstep_group_view {
 /* Library / device info.  Returns SWARMSTEP_ABI_VERSION. */
 int swarmstep_abi_version(void);
 const char *swarmstep_last_error(void);
+/* Loads every kernel of the library on the current device (no side effects);
+ * call before capturing launches into a CUDA graph. */
+int swarmstep_preload(void);
 /* Fills sm count and compute capability of the current device. */
 int swarmstep_device_info(int *sm_count, int *cc_major, int *cc_minor);
 
@@ -112,7 +115,7 @@ int swarmstep_device_info(int *sm_count, int *cc_major, int *cc_minor);
  * SWARMSTEP_EINVAL (quad.py:359-360, control.py:154-155). */
 int swarmstep_quad_step(const swarmstep_group_view *g, const swarmstep_quad_params *p,
                         float dt, int k_substeps, int overlay_active, uint32_t tick_base,
-                        void *stream);
+                        const int64_t *tick_dev, void *stream);
 
 /* Latest-wins command scatter (QuadGroup.apply_command, core.py:117-135).
  * rows[i] (int64), levels[i] (uint8, SWARMSTEP_LEVEL_*), values[i*7..]
@@ -174,6 +177,22 @@ int swarmstep_neighbor_workspace_bytes(int64_t n_all, uint64_t *bytes);
 int swarmstep_neighbor_overlay(const swarmstep_group_view *g, const float *all_xyzw, int64_t n_all,
                                int64_t self_offset, float r_sense, float k_sep, float cell,
                                int accumulate, void *workspace, uint64_t ws_bytes, void *stream);
+
+/* ---- device-resident setpoint feed ---------------------- */
+
+/* circle_swarm_strategy (client.py:55-73) + circle_reference (control.py:
+ * 297-315) on the device: every alive row r gets POS level and
+ *   th = omega t + phase0 + r dphase,  t = (*tick_dev + tick_offset) dt,
+ *   p_sp = (R cos th, R sin th, z), v_sp = (-R omega sin th, R omega cos th, 0),
+ *   yaw_sp = th + copysign(pi/2, omega)   (angles reduced mod 2 pi).
+ * The reference layout uses phase0 = 0, dphase = 2 pi / n (client.py:43-52).
+ * Reading the tick from device memory lets a run of ticks be one CUDA graph. */
+int swarmstep_quad_circle_setpoints(const swarmstep_group_view *g, const int64_t *tick_dev,
+                                    int64_t tick_offset, double dt, double radius, double omega,
+                                    double z, double phase0, double dphase, void *stream);
+
+/* *tick_dev += delta (one thread; graph-capturable tick counter). */
+int swarmstep_tick_add(int64_t *tick_dev, int64_t delta, void *stream);
 
 #ifdef __cplusplus
 }

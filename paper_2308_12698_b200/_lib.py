@@ -30,11 +30,12 @@ FLAG_ALIVE, FLAG_HAS_PREV, LEVEL_SHIFT, LEVEL_MASK = 0x01, 0x02, 2, 0x0C
 
 # every symbol include/swarmstep_b200.h declares
 EXPORTS = (
-    "swarmstep_abi_version", "swarmstep_last_error", "swarmstep_device_info",
+    "swarmstep_abi_version", "swarmstep_last_error", "swarmstep_device_info", "swarmstep_preload",
     "swarmstep_quad_step", "swarmstep_quad_apply_commands", "swarmstep_quad_set_setpoints",
     "swarmstep_quad_mark_dead", "swarmstep_quad_retarget_waypoint",
     "swarmstep_quad_pack_f64", "swarmstep_quad_unpack_f64",
     "swarmstep_pack_positions", "swarmstep_neighbor_workspace_bytes", "swarmstep_neighbor_overlay",
+    "swarmstep_quad_circle_setpoints", "swarmstep_tick_add",
 )
 
 
@@ -61,10 +62,12 @@ def _declare(lib) -> None:
     lib.swarmstep_abi_version.argtypes = []
     lib.swarmstep_last_error.restype = ctypes.c_char_p
     lib.swarmstep_last_error.argtypes = []
+    lib.swarmstep_preload.restype = i32
+    lib.swarmstep_preload.argtypes = []
     lib.swarmstep_device_info.restype = i32
     lib.swarmstep_device_info.argtypes = [ctypes.POINTER(i32)] * 3
     lib.swarmstep_quad_step.restype = i32
-    lib.swarmstep_quad_step.argtypes = [view, vp, f32, i32, i32, ctypes.c_uint32, vp]
+    lib.swarmstep_quad_step.argtypes = [view, vp, f32, i32, i32, ctypes.c_uint32, vp, vp]
     lib.swarmstep_quad_apply_commands.restype = i32
     lib.swarmstep_quad_apply_commands.argtypes = [view, vp, vp, vp, i64, vp]
     lib.swarmstep_quad_set_setpoints.restype = i32
@@ -83,6 +86,10 @@ def _declare(lib) -> None:
     lib.swarmstep_neighbor_workspace_bytes.argtypes = [i64, ctypes.POINTER(ctypes.c_uint64)]
     lib.swarmstep_neighbor_overlay.restype = i32
     lib.swarmstep_neighbor_overlay.argtypes = [view, vp, i64, i64, f32, f32, f32, i32, vp, ctypes.c_uint64, vp]
+    lib.swarmstep_quad_circle_setpoints.restype = i32
+    lib.swarmstep_quad_circle_setpoints.argtypes = [view, vp, i64, f64, f64, f64, f64, f64, f64, vp]
+    lib.swarmstep_tick_add.restype = i32
+    lib.swarmstep_tick_add.argtypes = [vp, i64, vp]
 
 
 def load():

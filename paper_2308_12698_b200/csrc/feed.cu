@@ -1,0 +1,81 @@
+// feed.cu -- device-resident setpoint feed.
+//
+// The reference's in-loop circle strategy builds one AgentCommand Python
+// object per alive agent per tick (client.py:55-73 circle_swarm_strategy ->
+// control.py:297-315 circle_reference -> core.py:117-135 apply_command),
+// which the survey measured at 80% of a 5k-agent tick.  Here the same
+// setpoints are written straight into the command columns by one kernel that
+// reads the simulation tick from device memory, so a whole run of ticks --
+// feed + fused step per tick -- can be captured in one CUDA graph.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace {
+
+// circle_reference (control.py:297-315) for row r with phase phase0 + r*dphase
+// (make_circle_layout, client.py:43-52): p = (R cos th, R sin th, z),
+// v = (-R w sin th, R w cos th, 0), yaw = th + copysign(pi/2, w), th = w t + phase.
+__global__ void circle_kernel(float *cols, uint8_t *flags, int64_t n, int64_t stride, const int64_t *tick_dev,
+                              int64_t tick_offset, double dt, double radius, double omega, double z,
+                              double phase0, double dphase)
+{
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const uint8_t fl = flags[r];
+    if (!(fl & SWARMSTEP_FLAG_ALIVE)) return;       // the strategy skips dead agents (client.py:66-67)
+    const double t = (double)(*tick_dev + tick_offset) * dt;
+    // the angle in double (|w t| grows without bound), reduced mod 2 pi
+    double th = omega * t + (phase0 + dphase * (double)r);
+    // heading reduced mod 2 pi as well: only cos / sin of yaw_sp are used
+    // (control.py:259-260), and float32 cannot hold an unreduced angle
+    const double yaw = fmod(th + copysign(1.5707963267948966, omega), 6.283185307179586);
+    th = fmod(th, 6.283185307179586);
+    float s, c;
+    sincosf((float)th, &s, &c);
+    const float R = (float)radius, W = (float)omega;
+    const float vals[7] = {R * c, R * s, (float)z, -R * W * s, R * W * c, 0.0f, (float)yaw};
+#pragma unroll
+    for (int i = 0; i < 7; i++) cols[(int64_t)(SWARMSTEP_COL_CMD + i) * stride + r] = vals[i];
+    const uint8_t nfl = (uint8_t)(fl & ~SWARMSTEP_LEVEL_MASK);  // POS level
+    if (nfl != fl) flags[r] = nfl;
+}
+
+__global__ void tick_add_kernel(int64_t *tick_dev, int64_t delta) { *tick_dev += delta; }
+
+}  // namespace
+
+extern "C" {
+
+int swarmstep_quad_circle_setpoints(const swarmstep_group_view *g, const int64_t *tick_dev, int64_t tick_offset,
+                                    double dt, double radius, double omega, double z, double phase0,
+                                    double dphase, void *stream)
+{
+    if (!g || !g->cols || !g->flags || !tick_dev) return ssb::set_err(SWARMSTEP_EINVAL, "null argument");
+    if (!(radius > 0.0)) return ssb::set_err(SWARMSTEP_EINVAL, "circle radius must be positive");  // control.py:305-306
+    if (!(dt > 0.0)) return ssb::set_err(SWARMSTEP_EINVAL, "dt must be positive");
+    if (g->n == 0) return SWARMSTEP_OK;
+    circle_kernel<<<(unsigned)((g->n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        g->cols, g->flags, g->n, g->stride, tick_dev, tick_offset, dt, radius, omega, z, phase0, dphase);
+    return ssb::cuda_status("circle_kernel");
+}
+
+int swarmstep_feed_preload(void)
+{
+    cudaFuncAttributes a;
+    if (cudaFuncGetAttributes(&a, (const void *)circle_kernel) != cudaSuccess ||
+        cudaFuncGetAttributes(&a, (const void *)tick_add_kernel) != cudaSuccess)
+        return ssb::cuda_status("cudaFuncGetAttributes");
+    return SWARMSTEP_OK;
+}
+
+int swarmstep_tick_add(int64_t *tick_dev, int64_t delta, void *stream)
+{
+    if (!tick_dev) return ssb::set_err(SWARMSTEP_EINVAL, "null tick");
+    tick_add_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(tick_dev, delta);
+    return ssb::cuda_status("tick_add_kernel");
+}
+
+}  // extern "C"

@@ -169,7 +169,7 @@ template <bool COMP>
 __global__ void __launch_bounds__(kBlock, SSB_STEP_MINB)
 quad_step_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t n, int64_t stride,
                  uint32_t *__restrict__ counters, uint64_t *__restrict__ fault_log,
-                 int64_t fault_cap, int overlay_active, uint32_t tick_base,
+                 int64_t fault_cap, int overlay_active, uint32_t tick_base, const int64_t *tick_dev,
                  const swarmstep_quad_params P, float dt, int K)
 {
     const int64_t r = (int64_t)blockIdx.x * kBlock + threadIdx.x;
@@ -201,8 +201,9 @@ quad_step_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t 
         setup_level(C, r, level, overlay_active, P, R);
         run_level<COMP, true>(C, r, level, overlay_active, P, D, dt, fault_k + 1, fault_k, R);
         const uint32_t slot = atomicAdd(&counters[0], 1u);
+        const uint32_t tick = (tick_dev ? (uint32_t)*tick_dev : 0u) + tick_base + (uint32_t)fault_k;
         if ((int64_t)slot < fault_cap)
-            fault_log[slot] = ((uint64_t)((tick_base + (uint32_t)fault_k) & 0xFFFFFFu) << 40) | (uint64_t)r;
+            fault_log[slot] = ((uint64_t)(tick & 0xFFFFFFu) << 40) | (uint64_t)r;
     }
 
     // ---- store ----
@@ -349,6 +350,8 @@ inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 
 // ---------------------------------------------------------------------------
 // C ABI
 // ---------------------------------------------------------------------------
+extern "C" int swarmstep_feed_preload(void);
+
 extern "C" {
 
 int swarmstep_abi_version(void) { return SWARMSTEP_ABI_VERSION; }
@@ -368,8 +371,23 @@ int swarmstep_device_info(int *sm_count, int *cc_major, int *cc_minor)
     return SWARMSTEP_OK;
 }
 
+int swarmstep_preload(void)
+{
+    // force-load every kernel of this translation unit (lazy module loading
+    // must not happen inside a CUDA graph capture)
+    cudaFuncAttributes a;
+    const void *fns[] = {(const void *)quad_step_kernel<true>, (const void *)quad_step_kernel<false>,
+                         (const void *)apply_commands_kernel, (const void *)set_setpoints_kernel,
+                         (const void *)mark_dead_kernel, (const void *)retarget_kernel,
+                         (const void *)pack_f64_kernel, (const void *)unpack_f64_kernel};
+    for (const void *f : fns)
+        if (cudaFuncGetAttributes(&a, f) != cudaSuccess) return cuda_status("cudaFuncGetAttributes");
+    return swarmstep_feed_preload();
+}
+
 int swarmstep_quad_step(const swarmstep_group_view *g, const swarmstep_quad_params *p, float dt,
-                        int k_substeps, int overlay_active, uint32_t tick_base, void *stream)
+                        int k_substeps, int overlay_active, uint32_t tick_base, const int64_t *tick_dev,
+                        void *stream)
 {
     int st = check_view(g);
     if (st) return st;
@@ -381,7 +399,7 @@ int swarmstep_quad_step(const swarmstep_group_view *g, const swarmstep_quad_para
     auto kern = g->compensated ? quad_step_kernel<true> : quad_step_kernel<false>;
     kern<<<grid_for(g->n, kBlock), kBlock, 0, (cudaStream_t)stream>>>(
         g->cols, g->flags, g->n, g->stride, g->counters, g->fault_log, g->fault_log ? g->fault_cap : 0,
-        overlay_active, tick_base, *p, dt, k_substeps);
+        overlay_active, tick_base, tick_dev, *p, dt, k_substeps);
     return cuda_status("quad_step_kernel");
 }
 

@@ -1,0 +1,112 @@
+"""Device-resident setpoint feed and CUDA-graph tick loops.
+
+``CircleFeed`` is the reference's in-loop circle strategy (client.py:43-73,
+control.py:297-315) as one kernel writing the command columns of every alive
+row from a device tick counter -- the reference builds one Python
+``AgentCommand`` per agent per tick instead (80% of a 5k-agent tick,
+SURVEY.md 3.5).
+
+``TickGraph`` captures ``ticks`` World-style ticks -- [feed ->] fused step --
+of one group into a single CUDA graph, so a tick costs one graph node pair
+instead of a Python call, a ctypes call and a launch.  Fault ids keep their
+exact tick (the step kernel reads the tick from the device counter) and are
+gathered by the group's own ``collect_faults()``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import ValidationError
+
+
+class CircleFeed:
+    """circle_swarm_strategy on the device for one group (all alive rows, POS level).
+
+    Phases follow make_circle_layout (client.py:43-52): phase_r = 2 pi r / n
+    over the group's rows, unless ``phase0`` / ``dphase`` are given.
+    """
+
+    def __init__(self, group, dt: float, radius: float = 5.0, omega: float = 0.3, z: float = 10.0,
+                 phase0: float = 0.0, dphase: float | None = None):
+        if not radius > 0.0:
+            raise ValidationError("circle radius must be positive")  # control.py:305-306
+        self.group, self.dt = group, float(dt)
+        self.radius, self.omega, self.z = float(radius), float(omega), float(z)
+        self.phase0 = float(phase0)
+        self.dphase = float(dphase) if dphase is not None else 2.0 * math.pi / max(group.n, 1)
+        self._lib = _lib.load()
+        with torch.cuda.device(group.device):
+            self.tick = torch.full((1,), group._tick, dtype=torch.int64, device=group.device)
+
+    def apply(self, tick_offset: int = 0, sync_tick: bool = True) -> None:
+        """Write the setpoints of tick (*tick + tick_offset); by default the device
+        tick is first set to the group's current tick (the next one to step)."""
+        g = self.group
+        with torch.cuda.device(g.device):
+            if sync_tick:
+                with torch.cuda.stream(g.stream):
+                    self.tick.fill_(g._tick)
+            _lib.check(self._lib.swarmstep_quad_circle_setpoints(
+                g._view_ref, self.tick.data_ptr(), int(tick_offset), self.dt, self.radius, self.omega,
+                self.z, self.phase0, self.dphase, ctypes.c_void_p(g.stream.cuda_stream)))
+        g._cmd_stale = True
+
+    def advance(self, k: int) -> None:
+        g = self.group
+        with torch.cuda.device(g.device):
+            _lib.check(self._lib.swarmstep_tick_add(self.tick.data_ptr(), int(k),
+                                                    ctypes.c_void_p(g.stream.cuda_stream)))
+
+
+class TickGraph:
+    """``ticks`` ticks of [feed ->] fused step (K=1 each) as one CUDA graph."""
+
+    def __init__(self, group, dt: float, ticks: int, feed: CircleFeed | None = None):
+        if ticks < 1:
+            raise ValidationError("ticks must be >= 1")
+        if group._pending or group._overlay_active:
+            group._flush_commands()
+        self.group, self.dt, self.ticks = group, float(dt), int(ticks)
+        self.feed = feed
+        self._lib = _lib.load()
+        with torch.cuda.device(group.device):
+            self.tick = feed.tick if feed is not None else torch.full(
+                (1,), group._tick, dtype=torch.int64, device=group.device)
+        _lib.check(self._lib.swarmstep_preload())   # no lazy module loads inside the capture
+        torch.cuda.synchronize(group.device)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.device(group.device):
+            with torch.cuda.graph(self.graph, stream=group.stream):
+                self._body()
+        torch.cuda.synchronize(group.device)
+
+    def _body(self) -> None:
+        g = self.group
+        s = ctypes.c_void_p(g.stream.cuda_stream)
+        for j in range(self.ticks):
+            if self.feed is not None:
+                self.feed.apply(j, sync_tick=False)
+            _lib.check(self._lib.swarmstep_quad_step(g._view_ref, g._params_ref, ctypes.c_float(self.dt), 1, 0,
+                                                     ctypes.c_uint32(j), self.tick.data_ptr(), s))
+        _lib.check(self._lib.swarmstep_tick_add(self.tick.data_ptr(), self.ticks, s))
+
+    def replay(self) -> None:
+        """Run the captured ticks (asynchronously on the group's stream)."""
+        g = self.group
+        if g._pending:
+            g._flush_commands()
+        with torch.cuda.device(g.device), torch.cuda.stream(g.stream):
+            self.tick.fill_(g._tick)       # the graph's tick counter follows the group's
+            self.graph.replay()
+            g._counters_host.copy_(g._counters, non_blocking=True)
+        g._launched.append((g._tick, self.ticks))
+        g._tick += self.ticks
+        g._state_stale = True
+        if self.feed is not None:
+            g._cmd_stale = True

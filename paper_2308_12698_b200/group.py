@@ -388,7 +388,7 @@ class B200QuadGroup:
         self._flush_commands()
         with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
             self._call(self._lib.swarmstep_quad_step, self._params_ref, ctypes.c_float(dt), int(k),
-                       int(self._overlay_active), ctypes.c_uint32(self._tick & 0xFFFFFF),
+                       int(self._overlay_active), ctypes.c_uint32(self._tick & 0xFFFFFF), None,
                        ctypes.c_void_p(self.stream.cuda_stream))
             self._overlay_reset()
             self._counters_host.copy_(self._counters, non_blocking=True)

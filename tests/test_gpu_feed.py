@@ -1,0 +1,121 @@
+"""GPU checks of the device setpoint feed (f1) and CUDA-graph tick loops:
+circle setpoints equal circle_reference (control.py:297-315), graph replays are
+bit-identical to eager ticks, faults inside a graph keep their tick, and the
+closed-loop circle demo meets the reference's acceptance bound
+(test_acceptance.py:187-224: RMS < 0.3 m after the 10 s transient)."""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import cuda_ok
+from gpu_util import gpu_state, make_group
+from oracle import oracle as orc
+from scenarios import Scenario
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_ok(), reason="needs CUDA")]
+
+
+def circle_reference(t, radius, omega, z, phase):
+    """control.py:297-315 in float64 (numpy restatement for the check)."""
+    th = omega * t + phase
+    p = np.stack([radius * np.cos(th), radius * np.sin(th), np.full_like(th, z)], axis=-1)
+    v = np.stack([-radius * omega * np.sin(th), radius * omega * np.cos(th), np.zeros_like(th)], axis=-1)
+    return p, v, th + math.copysign(math.pi / 2, omega)
+
+
+def _circle_group(n, radius=5.0, z=10.0):
+    ph = 2 * np.pi * np.arange(n) / n
+    pos = np.stack([radius * np.cos(ph), radius * np.sin(ph), np.full(n, z)], axis=1)   # config.py:159-168
+    yaw = ph + np.pi / 2
+    q = np.stack([np.cos(yaw / 2), np.zeros(n), np.zeros(n), np.sin(yaw / 2)], axis=1)
+    return make_group(Scenario("circle", n, 2e-3, 1, pos, np.zeros((n, 3)), q, np.zeros((n, 3)), record=[]))
+
+
+def test_circle_feed_setpoints():
+    from paper_2308_12698_b200.feed import CircleFeed
+    n, dt = 1000, 2e-3
+    g = _circle_group(n)
+    feed = CircleFeed(g, dt, radius=5.0, omega=0.3, z=10.0)
+    g._tick = 12345
+    feed.apply()
+    cv = g.cmd_values
+    p, v, yaw = circle_reference(12345 * dt, 5.0, 0.3, 10.0, 2 * np.pi * np.arange(n) / n)
+    np.testing.assert_allclose(cv[:, :3], p, atol=2e-6)
+    np.testing.assert_allclose(cv[:, 3:6], v, atol=2e-6)
+    np.testing.assert_allclose(np.cos(cv[:, 6]), np.cos(yaw), atol=1e-6)
+    np.testing.assert_allclose(np.sin(cv[:, 6]), np.sin(yaw), atol=1e-6)
+    assert np.all(g.cmd_level == 0)
+
+
+def test_graph_replay_bit_identical_to_eager_ticks():
+    from paper_2308_12698_b200.feed import CircleFeed, TickGraph
+    n, dt, T = 777, 2e-3, 25
+    ga, gb = _circle_group(n), _circle_group(n)
+    fa, fb = CircleFeed(ga, dt), CircleFeed(gb, dt)
+    graph = TickGraph(ga, dt, T, feed=fa)
+    for _ in range(4):
+        graph.replay()
+    ga.collect_faults()
+    for _ in range(4 * T):
+        fb.apply()
+        gb.step(dt)
+    sa, sb = gpu_state(ga), gpu_state(gb)
+    for k in ("pos", "vel", "quat", "omega", "integral", "prev_omega"):
+        np.testing.assert_array_equal(sa[k], sb[k], err_msg=k)
+    assert ga._tick == gb._tick == 4 * T
+
+
+def test_graph_fault_keeps_its_tick():
+    from paper_2308_12698_b200 import AgentCommand, CommandLevel
+    from paper_2308_12698_b200.feed import TickGraph
+    n, dt, T = 64, 1e-3, 10
+    g = _circle_group(n)
+    g.set_setpoints(np.tile([0.0, 0.0, 0.0, 9.81], (n, 1)), level="rate")
+    graph = TickGraph(g, dt, T)
+    graph.replay()
+    assert all(f.size == 0 for f in g.collect_faults())
+    assert g.apply_command(AgentCommand(5, CommandLevel.RATE, (0.0, 0.0, 0.0, float("nan"))))
+    graph.replay()
+    per_tick = g.collect_faults()
+    assert len(per_tick) == T and per_tick[0].tolist() == [5]
+    assert not g.batch.alive[5] and g.batch.alive.sum() == n - 1
+
+
+def test_closed_loop_circle_demo_shape():
+    """100 quads on 5 m circles (test_acceptance.py:187-224), device feed + graphs,
+    and the same run on the float64 oracle with per-tick commands."""
+    from paper_2308_12698_b200.feed import CircleFeed, TickGraph
+    n, dt, radius, omega, z = 100, 2e-3, 5.0, 0.3, 10.0
+    g = _circle_group(n)
+    feed = CircleFeed(g, dt, radius=radius, omega=omega, z=z)
+    T = 500
+    graph = TickGraph(g, dt, T, feed=feed)
+    n_ticks = round(40.0 / dt)
+    phases = 2 * np.pi * np.arange(n) / n
+    st0 = gpu_state(g)
+    og = orc.OracleGroup(0, type("B", (), dict(agent_ids=np.arange(n, dtype=np.uint64), pos=st0["pos"],
+                                                vel=st0["vel"], quat=st0["quat"], omega=st0["omega"],
+                                                alive=np.ones(n, bool)))())
+    sq, samples, worst_div = np.zeros(n), 0, 0.0
+    for rep in range(n_ticks // T):
+        graph.replay()
+        for j in range(T):
+            k = rep * T + j
+            p, v, yaw = circle_reference(k * dt, radius, omega, z, phases)
+            og.cmd_level[:] = 0
+            og.cmd_values[:, :3], og.cmd_values[:, 3:6], og.cmd_values[:, 6] = p, v, yaw
+            og.step(float(np.float32(dt)))
+        assert all(f.size == 0 for f in g.collect_faults())
+        t = (rep + 1) * T * dt
+        pos = g.batch.pos
+        worst_div = max(worst_div, float(np.max(np.abs(pos - og.pos))))
+        if t > 10.0:
+            ref, _, _ = circle_reference(t, radius, omega, z, phases)
+            err = np.linalg.norm(pos - ref, axis=1)
+            sq += err * err
+            samples += 1
+    rms = float(np.max(np.sqrt(sq / samples)))
+    assert rms < 0.3, rms
+    assert worst_div < 1e-3, worst_div     # bounded divergence from the float64 oracle over 40 s

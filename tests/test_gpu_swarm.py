@@ -21,6 +21,7 @@ def _swarm(n, box, seed=0):
 
 
 def _overlay(g):
+    g.stream.synchronize()   # the overlay was written on the group's stream
     return g.cols[33:36, :g.n].T.double().cpu().numpy()
 
 
@@ -52,7 +53,9 @@ def test_overlay_deterministic_and_one_tick():
         g = make_group(sc)
         ns = NeighborSeparation(g, make_shard(sc.n), r_sense=2.0, k_sep=1.0)
         ns.apply()
-        outs.append(_overlay(g).tobytes())
+        ov = _overlay(g)
+        assert np.abs(ov).sum() > 0
+        outs.append(ov.tobytes())
         ns.group.step(1e-3)
         assert np.all(_overlay(g) == 0.0)          # cleared after the tick (core.py:199-201)
     assert outs[0] == outs[1]
