@@ -17,9 +17,16 @@
  *    across the ABI.
  *  - `stream` is a cudaStream_t passed as void*; every launch is async on it.
  *    Calls on distinct streams over distinct groups are thread-safe.
- *  - State is structure-of-arrays float32, one column per scalar component,
- *    each column `stride` floats long (stride >= n, multiple of 32, 16-byte
- *    aligned).  Rows in [n, stride) must have flags == 0 (dead padding).
+ *  - State is a tiled structure of arrays ("AoSoA") of float32: one column
+ *    per scalar component, agents grouped in tiles of SWARMSTEP_TILE = 128;
+ *    a tile stores its SWARMSTEP_NCOL columns contiguously (18,432 bytes),
+ *    so element (column c, row r) is
+ *        cols[(r / 128) * (NCOL * 128) + c * 128 + r % 128].
+ *    A warp's access to one component is one 128-byte line, every column
+ *    offset inside a tile is a compile-time constant, and a tile's inputs
+ *    (or outputs) are one contiguous block for a single TMA bulk copy.
+ *    `stride` is the row capacity (>= n, multiple of 128); rows in
+ *    [n, stride) must have flags == 0 (dead padding).
  */
 #ifndef SWARMSTEP_B200_H
 #define SWARMSTEP_B200_H
@@ -63,7 +70,10 @@ typedef struct swarmstep_quad_params {
     float _pad[2];
 } swarmstep_quad_params;
 
-/* Column block offsets inside `cols` (each block is k columns of `stride`). */
+/* Column offsets inside a tile (each block is k consecutive columns).  The
+ * order puts everything the step kernel reads first (cols [0, 29)) and keeps
+ * the columns it writes in two runs ([0, 22) and [29, 33)). */
+#define SWARMSTEP_TILE 128
 enum {
     SWARMSTEP_COL_POS = 0,      /* px py pz          (state.py:57)          */
     SWARMSTEP_COL_VEL = 3,      /* vx vy vz                                 */
@@ -72,8 +82,8 @@ enum {
     SWARMSTEP_COL_POS_LO = 13,  /* compensated-position low words           */
     SWARMSTEP_COL_INTEGRAL = 16,/* RatePidState.integral (control.py:103)   */
     SWARMSTEP_COL_PREV = 19,    /* RatePidState.prev_omega                  */
-    SWARMSTEP_COL_SP = 22,      /* QuadGroup.omega_sp xyz, f_c_sp (core.py:109-110) */
-    SWARMSTEP_COL_CMD = 26,     /* QuadGroup.cmd_values[0..6] (core.py:99)  */
+    SWARMSTEP_COL_CMD = 22,     /* QuadGroup.cmd_values[0..6] (core.py:99)  */
+    SWARMSTEP_COL_SP = 29,      /* QuadGroup.omega_sp xyz, f_c_sp (core.py:109-110) */
     SWARMSTEP_COL_OVERLAY = 33, /* QuadGroup.v_overlay (core.py:106)        */
     SWARMSTEP_NCOL = 36
 };
@@ -81,8 +91,8 @@ enum {
 /* A borrowed view of one group's device columns. */
 typedef struct swarmstep_group_view {
     int64_t n;              /* live rows                                    */
-    int64_t stride;         /* floats per column (>= n, multiple of 32)     */
-    float *cols;            /* [SWARMSTEP_NCOL][stride] float32             */
+    int64_t stride;         /* row capacity (>= n, multiple of 128)         */
+    float *cols;            /* [stride/128][SWARMSTEP_NCOL][128] float32    */
     uint8_t *flags;         /* [stride]                                     */
     uint32_t *counters;     /* device [4]: 0 faults logged (monotonic), 1 scratch count */
     uint64_t *fault_log;    /* device [fault_cap]: (tick << 40) | row       */
@@ -105,16 +115,24 @@ int swarmstep_device_info(int *sm_count, int *cc_major, int *cc_minor);
  * position_outer_loop (control.py:222-294), rate_pid_step (control.py:136-187),
  * mix_to_motors (quad.py:143-168), raw-motor override (core.py:189-197) and
  * rk4_step (quad.py:350-437) including fault revert + kill.  The overlay
- * column block is added to v_sp on substep 0 only when overlay_active != 0
- * (core.py:172-175, 199-201); the caller clears it afterwards.
+ * column block is added to v_sp on substep 0 only with SWARMSTEP_STEP_OVERLAY
+ * (core.py:172-175, 199-201); the caller clears it afterwards.  Without
+ * SWARMSTEP_STEP_MOTOR no row may be at MOTOR level (the stale-setpoint
+ * columns are then not read).  Few-tick launches run the TMA-staged kernel
+ * (HBM-bound regime), many-tick launches the direct kernel.
  * Faulted rows are appended to fault_log as ((tick_base + substep) mod 2^24)
  * << 40 | row and counted in counters[0], which only ever grows: a row can
  * fault at most once (dead rows never revive), so fault_cap >= n never
  * overflows and no per-launch reset is needed.
  * Replaces: QuadGroup.step (core.py:166).  Errors: dt <= 0 or k < 1 ->
  * SWARMSTEP_EINVAL (quad.py:359-360, control.py:154-155). */
+/* launch_flags for swarmstep_quad_step */
+#define SWARMSTEP_STEP_OVERLAY       0x1  /* add the overlay block to v_sp on tick 0      */
+#define SWARMSTEP_STEP_MOTOR         0x2  /* some row may be at MOTOR level               */
+#define SWARMSTEP_STEP_FORCE_DIRECT  0x4  /* tuning: force the direct-load kernel         */
+#define SWARMSTEP_STEP_FORCE_TMA     0x8  /* tuning: force the TMA-staged kernel          */
 int swarmstep_quad_step(const swarmstep_group_view *g, const swarmstep_quad_params *p,
-                        float dt, int k_substeps, int overlay_active, uint32_t tick_base,
+                        float dt, int k_substeps, int launch_flags, uint32_t tick_base,
                         const int64_t *tick_dev, void *stream);
 
 /* Latest-wins command scatter (QuadGroup.apply_command, core.py:117-135).
@@ -126,7 +144,7 @@ int swarmstep_quad_apply_commands(const swarmstep_group_view *g, const int64_t *
                                   int64_t count, void *stream);
 
 /* Bulk device setpoints: every row in [row0, row0+count) gets `level` and
- * values from the column block `values` ([7][ld] float32, device), alive
+ * values from the plain column block `values` ([7][ld] float32, device), alive
  * rows only.  The device-resident setpoint feed. */
 int swarmstep_quad_set_setpoints(const swarmstep_group_view *g, int64_t row0, int64_t count,
                                  int level, const float *values, int64_t ld, void *stream);

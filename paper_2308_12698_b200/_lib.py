@@ -24,9 +24,12 @@ ABI_VERSION = 1
 
 # column block offsets (SWARMSTEP_COL_*)
 COL_POS, COL_VEL, COL_QUAT, COL_OMEGA = 0, 3, 6, 10
-COL_POS_LO, COL_INTEGRAL, COL_PREV, COL_SP, COL_CMD, COL_OVERLAY = 13, 16, 19, 22, 26, 33
+COL_POS_LO, COL_INTEGRAL, COL_PREV, COL_CMD, COL_SP, COL_OVERLAY = 13, 16, 19, 22, 29, 33
 NCOL = 36
+TILE = 128   # agents per tile of the tiled SoA layout (SWARMSTEP_TILE)
 FLAG_ALIVE, FLAG_HAS_PREV, LEVEL_SHIFT, LEVEL_MASK = 0x01, 0x02, 2, 0x0C
+# swarmstep_quad_step launch flags (SWARMSTEP_STEP_*)
+STEP_OVERLAY, STEP_MOTOR, STEP_FORCE_DIRECT, STEP_FORCE_TMA = 0x1, 0x2, 0x4, 0x8
 
 # every symbol include/swarmstep_b200.h declares
 EXPORTS = (

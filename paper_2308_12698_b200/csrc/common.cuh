@@ -7,6 +7,18 @@
 
 namespace ssb {
 
+// tiled SoA addressing (include/swarmstep_b200.h): element (c, r) lives at
+// tile_base(r) + c * SWARMSTEP_TILE
+__host__ __device__ __forceinline__ int64_t tile_base(int64_t r)
+{
+    return (r >> 7) * (int64_t)(SWARMSTEP_NCOL * SWARMSTEP_TILE) + (r & (SWARMSTEP_TILE - 1));
+}
+
+__host__ __device__ __forceinline__ int64_t at(int c, int64_t r)
+{
+    return tile_base(r) + (int64_t)c * SWARMSTEP_TILE;
+}
+
 // one thread-local message buffer for the whole library (C++17 inline)
 inline char *err_buf()
 {

@@ -38,7 +38,7 @@ __global__ void circle_kernel(float *cols, uint8_t *flags, int64_t n, int64_t st
     const float R = (float)radius, W = (float)omega;
     const float vals[7] = {R * c, R * s, (float)z, -R * W * s, R * W * c, 0.0f, (float)yaw};
 #pragma unroll
-    for (int i = 0; i < 7; i++) cols[(int64_t)(SWARMSTEP_COL_CMD + i) * stride + r] = vals[i];
+    for (int i = 0; i < 7; i++) cols[ssb::at(SWARMSTEP_COL_CMD + i, r)] = vals[i];
     const uint8_t nfl = (uint8_t)(fl & ~SWARMSTEP_LEVEL_MASK);  // POS level
     if (nfl != fl) flags[r] = nfl;
 }

@@ -87,13 +87,13 @@ __global__ void pack_positions_kernel(const float *cols, const uint8_t *flags, i
     if (r >= n_out) return;
     float4 p = make_float4(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000), __int_as_float(0x7fc00000), 0.0f);
     if (r < n && (flags[r] & SWARMSTEP_FLAG_ALIVE)) {
-        float x = cols[(int64_t)(SWARMSTEP_COL_POS + 0) * stride + r];
-        float y = cols[(int64_t)(SWARMSTEP_COL_POS + 1) * stride + r];
-        float z = cols[(int64_t)(SWARMSTEP_COL_POS + 2) * stride + r];
+        float x = cols[ssb::at(SWARMSTEP_COL_POS + 0, r)];
+        float y = cols[ssb::at(SWARMSTEP_COL_POS + 1, r)];
+        float z = cols[ssb::at(SWARMSTEP_COL_POS + 2, r)];
         if (compensated) {
-            x += cols[(int64_t)(SWARMSTEP_COL_POS_LO + 0) * stride + r];
-            y += cols[(int64_t)(SWARMSTEP_COL_POS_LO + 1) * stride + r];
-            z += cols[(int64_t)(SWARMSTEP_COL_POS_LO + 2) * stride + r];
+            x += cols[ssb::at(SWARMSTEP_COL_POS_LO + 0, r)];
+            y += cols[ssb::at(SWARMSTEP_COL_POS_LO + 1, r)];
+            z += cols[ssb::at(SWARMSTEP_COL_POS_LO + 2, r)];
         }
         p = make_float4(x, y, z, 0.0f);
     }
@@ -162,9 +162,9 @@ __global__ void query_kernel(const float4 *pos, const uint32_t *vals_sorted, con
                     }
                 }
     }
-    float *ox = cols + (int64_t)(SWARMSTEP_COL_OVERLAY + 0) * stride + r;
-    float *oy = cols + (int64_t)(SWARMSTEP_COL_OVERLAY + 1) * stride + r;
-    float *oz = cols + (int64_t)(SWARMSTEP_COL_OVERLAY + 2) * stride + r;
+    float *ox = cols + ssb::at(SWARMSTEP_COL_OVERLAY + 0, r);
+    float *oy = cols + ssb::at(SWARMSTEP_COL_OVERLAY + 1, r);
+    float *oz = cols + ssb::at(SWARMSTEP_COL_OVERLAY + 2, r);
     if (accumulate) {
         *ox += ax; *oy += ay; *oz += az;
     } else {

@@ -22,8 +22,8 @@ using ssb::set_err;
 int check_view(const swarmstep_group_view *g)
 {
     if (!g || !g->cols || !g->flags) return set_err(SWARMSTEP_EINVAL, "null group view");
-    if (g->n < 0 || g->stride < g->n || (g->stride % 32) != 0)
-        return set_err(SWARMSTEP_EINVAL, "bad n/stride (stride must be >= n and a multiple of 32)");
+    if (g->n < 0 || g->stride < g->n || (g->stride % SWARMSTEP_TILE) != 0)
+        return set_err(SWARMSTEP_EINVAL, "bad n/stride (stride must be >= n and a multiple of 128)");
     if ((reinterpret_cast<uintptr_t>(g->cols) & 15u) != 0)
         return set_err(SWARMSTEP_EINVAL, "cols must be 16-byte aligned");
     return SWARMSTEP_OK;
@@ -39,10 +39,10 @@ int check_view(const swarmstep_group_view *g)
 // registers (no spills) for 20 warps per SM.
 constexpr int kBlock = SSB_STEP_BLOCK;
 
+// one agent's row inside its tile: column k at p + k * 128 (constant offsets)
 struct Cols {
-    float *c;
-    int64_t s;
-    __device__ __forceinline__ float *col(int k) const { return c + (int64_t)k * s; }
+    float *p;
+    __device__ __forceinline__ float *col(int k) const { return p + k * SWARMSTEP_TILE; }
 };
 
 // ---------------------------------------------------------------------------
@@ -52,6 +52,9 @@ struct Cols {
 #define SSB_TICK_UNROLL 1
 #endif
 constexpr int kTickUnroll = SSB_TICK_UNROLL;
+#ifndef SSB_TMA_MAX_K
+#define SSB_TMA_MAX_K 4   // TMA-staged kernel for the memory-bound (few-tick) regime
+#endif
 
 // One agent's registers for a launch.
 struct Row {
@@ -64,27 +67,66 @@ struct Row {
     bool has_prev;
 };
 
-template <bool COMP>
-__device__ __forceinline__ void load_state(const Cols &C, int64_t r, Row &R)
+// Row accessors: the same step code reads a row from global memory (direct
+// kernel, streaming loads) or from a shared-memory tile staged by TMA.
+struct GlobalRow {
+    float *p;
+    __device__ __forceinline__ float ld(int c) const { return __ldcs(p + c * SWARMSTEP_TILE); }
+    __device__ __forceinline__ float ldc(int c) const { return __ldg(p + c * SWARMSTEP_TILE); }
+    __device__ __forceinline__ void st(int c, float v) const { __stcs(p + c * SWARMSTEP_TILE, v); }
+};
+struct SmemRow {
+    float *p;
+    __device__ __forceinline__ float ld(int c) const { return p[c * SWARMSTEP_TILE]; }
+    __device__ __forceinline__ float ldc(int c) const { return p[c * SWARMSTEP_TILE]; }
+    __device__ __forceinline__ void st(int c, float v) const { p[c * SWARMSTEP_TILE] = v; }
+};
+
+template <bool COMP, class A>
+__device__ __forceinline__ void load_state(const A &C, Row &R)
 {
 #pragma unroll
     for (int i = 0; i < 3; i++) {
-        R.p_hi[i] = __ldcs(C.col(SWARMSTEP_COL_POS + i) + r);
-        R.v[i] = __ldcs(C.col(SWARMSTEP_COL_VEL + i) + r);
-        R.w[i] = __ldcs(C.col(SWARMSTEP_COL_OMEGA + i) + r);
-        R.integ[i] = __ldcs(C.col(SWARMSTEP_COL_INTEGRAL + i) + r);
-        R.prev[i] = __ldcs(C.col(SWARMSTEP_COL_PREV + i) + r);
-        R.p_lo[i] = COMP ? __ldcs(C.col(SWARMSTEP_COL_POS_LO + i) + r) : 0.0f;
+        R.p_hi[i] = C.ld(SWARMSTEP_COL_POS + i);
+        R.v[i] = C.ld(SWARMSTEP_COL_VEL + i);
+        R.w[i] = C.ld(SWARMSTEP_COL_OMEGA + i);
+        R.integ[i] = C.ld(SWARMSTEP_COL_INTEGRAL + i);
+        R.prev[i] = C.ld(SWARMSTEP_COL_PREV + i);
+        R.p_lo[i] = COMP ? C.ld(SWARMSTEP_COL_POS_LO + i) : 0.0f;
     }
 #pragma unroll
-    for (int i = 0; i < 4; i++) R.q[i] = __ldcs(C.col(SWARMSTEP_COL_QUAT + i) + r);
+    for (int i = 0; i < 4; i++) R.q[i] = C.ld(SWARMSTEP_COL_QUAT + i);
 #pragma unroll
-    for (int i = 0; i < 7; i++) R.u[i] = __ldcs(C.col(SWARMSTEP_COL_CMD + i) + r);
+    for (int i = 0; i < 7; i++) R.u[i] = C.ld(SWARMSTEP_COL_CMD + i);
     R.u[7] = 0.0f;
 }
 
+template <bool COMP, class A>
+__device__ __forceinline__ void store_state(const A &C, int level, const Row &R)
+{
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+        C.st(SWARMSTEP_COL_POS + i, R.p_hi[i]);
+        C.st(SWARMSTEP_COL_VEL + i, R.v[i]);
+        C.st(SWARMSTEP_COL_OMEGA + i, R.w[i]);
+        C.st(SWARMSTEP_COL_INTEGRAL + i, R.integ[i]);
+        C.st(SWARMSTEP_COL_PREV + i, R.prev[i]);
+        if (COMP) C.st(SWARMSTEP_COL_POS_LO + i, R.p_lo[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; i++) C.st(SWARMSTEP_COL_QUAT + i, R.q[i]);
+    if (level != SWARMSTEP_LEVEL_MOTOR) {
+        // the last tick's setpoints become the stale setpoints a later MOTOR
+        // command runs the PID on (core.py:178-182)
+#pragma unroll
+        for (int i = 0; i < 3; i++) C.st(SWARMSTEP_COL_SP + i, R.w_sp[i]);
+        C.st(SWARMSTEP_COL_SP + 3, R.f_sp);
+    }
+}
+
 // Per-launch setpoint preparation (commands are fixed across the K ticks).
-__device__ __forceinline__ void setup_level(const Cols &C, int64_t r, int level, int overlay_active,
+template <class A>
+__device__ __forceinline__ void setup_level(const A &C, int level, int overlay_active,
                                             const swarmstep_quad_params &P, Row &R)
 {
     if (!R.has_prev) {
@@ -100,7 +142,7 @@ __device__ __forceinline__ void setup_level(const Cols &C, int64_t r, int level,
         R.u[7] = s;
         if (overlay_active) {
 #pragma unroll
-            for (int i = 0; i < 3; i++) R.u[3 + i] += __ldg(C.col(SWARMSTEP_COL_OVERLAY + i) + r);
+            for (int i = 0; i < 3; i++) R.u[3 + i] += C.ldc(SWARMSTEP_COL_OVERLAY + i);
         }
     } else if (level == SWARMSTEP_LEVEL_RATE) {
         R.w_sp[0] = R.u[0]; R.w_sp[1] = R.u[1]; R.w_sp[2] = R.u[2]; R.f_sp = R.u[3];
@@ -108,8 +150,8 @@ __device__ __forceinline__ void setup_level(const Cols &C, int64_t r, int level,
         // MOTOR: the PID still runs on the stale setpoints (core.py:109-110,
         // 184-186); the integrated wrench comes from the rotor model
 #pragma unroll
-        for (int i = 0; i < 3; i++) R.w_sp[i] = __ldg(C.col(SWARMSTEP_COL_SP + i) + r);
-        R.f_sp = __ldg(C.col(SWARMSTEP_COL_SP + 3) + r);
+        for (int i = 0; i < 3; i++) R.w_sp[i] = C.ldc(SWARMSTEP_COL_SP + i);
+        R.f_sp = C.ldc(SWARMSTEP_COL_SP + 3);
         float mt[3], mf;
         ssb::motor_wrench(R.u, P, mf, mt);
         R.u[0] = mf; R.u[1] = mt[0]; R.u[2] = mt[1]; R.u[3] = mt[2];
@@ -119,11 +161,10 @@ __device__ __forceinline__ void setup_level(const Cols &C, int64_t r, int level,
 // K ticks of one agent at a fixed command level (the body of QuadGroup.step,
 // core.py:166-202, repeated), state updated in place.  Returns the tick at
 // which the row faulted (its state registers are then garbage), or -1.
-// With pid_only_at >= 0 the loop stops after the controller part of that tick
-// (used to rebuild a faulted row's state, see the kernel).
+// With RERUN the loop stops after the controller part of tick pid_only_at
+// (used to rebuild a faulted row's state, see the kernels).
 template <int LEVEL, bool COMP, bool RERUN>
-__device__ __forceinline__ int run_ticks(const Cols &C, int64_t r, int overlay_active,
-                                         const swarmstep_quad_params &P, const ssb::Derived &D,
+__device__ __forceinline__ int run_ticks(const swarmstep_quad_params &P, const ssb::Derived &D,
                                          float dt, int K, int pid_only_at, Row &R)
 {
 #pragma unroll kTickUnroll
@@ -133,11 +174,6 @@ __device__ __forceinline__ int run_ticks(const Cols &C, int64_t r, int overlay_a
 #pragma unroll
             for (int i = 0; i < 3; i++) p_err[i] = (R.u[i] - R.p_hi[i]) - R.p_lo[i];
             ssb::outer_row(p_err, R.v, R.q, R.u + 3, R.u[6], R.u[7], P, R.w_sp, R.f_sp);
-            if (k == 0 && overlay_active) {
-                // the overlay lasts one tick (core.py:199-201)
-#pragma unroll
-                for (int i = 0; i < 3; i++) R.u[3 + i] = __ldg(C.col(SWARMSTEP_COL_CMD + 3 + i) + r);
-            }
         }
         float tau[3], f_c = R.f_sp;
         ssb::pid_row(R.w, R.w_sp, P, D, dt, R.integ, R.prev, tau);
@@ -152,83 +188,209 @@ __device__ __forceinline__ int run_ticks(const Cols &C, int64_t r, int overlay_a
     return -1;
 }
 
-template <bool COMP, bool RERUN>
-__device__ __forceinline__ int run_level(const Cols &C, int64_t r, int level, int overlay_active,
+template <bool COMP, bool RERUN, class A>
+__device__ __forceinline__ int run_level(const A &C, int level, int overlay_active,
                                          const swarmstep_quad_params &P, const ssb::Derived &D,
                                          float dt, int K, int pid_only_at, Row &R)
 {
     // level-specialised tick loops: no per-tick level branches
-    if (level == SWARMSTEP_LEVEL_POS)
-        return run_ticks<SWARMSTEP_LEVEL_POS, COMP, RERUN>(C, r, overlay_active, P, D, dt, K, pid_only_at, R);
+    if (level == SWARMSTEP_LEVEL_POS) {
+        if (!overlay_active)
+            return run_ticks<SWARMSTEP_LEVEL_POS, COMP, RERUN>(P, D, dt, K, pid_only_at, R);
+        // tick 0 sees v_sp + overlay (setup_level added it); the overlay lasts
+        // one tick (core.py:172-175, 199-201), so tick 0 is peeled off
+        int f = run_ticks<SWARMSTEP_LEVEL_POS, COMP, RERUN>(P, D, dt, 1, pid_only_at, R);
+        if (f >= 0 || K == 1 || (RERUN && pid_only_at == 0)) return f;
+#pragma unroll
+        for (int i = 0; i < 3; i++) R.u[3 + i] = C.ldc(SWARMSTEP_COL_CMD + 3 + i);
+        f = run_ticks<SWARMSTEP_LEVEL_POS, COMP, RERUN>(P, D, dt, K - 1, pid_only_at - 1, R);
+        return f >= 0 ? f + 1 : -1;
+    }
     if (level == SWARMSTEP_LEVEL_RATE)
-        return run_ticks<SWARMSTEP_LEVEL_RATE, COMP, RERUN>(C, r, 0, P, D, dt, K, pid_only_at, R);
-    return run_ticks<SWARMSTEP_LEVEL_MOTOR, COMP, RERUN>(C, r, 0, P, D, dt, K, pid_only_at, R);
+        return run_ticks<SWARMSTEP_LEVEL_RATE, COMP, RERUN>(P, D, dt, K, pid_only_at, R);
+    return run_ticks<SWARMSTEP_LEVEL_MOTOR, COMP, RERUN>(P, D, dt, K, pid_only_at, R);
 }
 
+// The whole per-row launch: K ticks from the row's inputs behind accessor C,
+// outputs back through C; returns the new flag byte.  A fault at tick f
+// leaves the row at its pre-tick values, dead, and logged with its tick
+// (quad.py:425-436).  State is updated in place, so a faulted row is rebuilt
+// by re-running ticks [0, f) from the launch's inputs -- bit-identical by
+// determinism -- plus the controller part of tick f (the reference updates
+// the PID state before rk4_step faults the row).  Inputs must still be
+// readable through C at that point (global memory, or the staged tile).
+template <bool COMP, class A>
+__device__ __forceinline__ uint8_t step_row(const A &C, uint8_t fl, int64_t r, int overlay_active,
+                                            const swarmstep_quad_params &P, float dt, int K,
+                                            uint32_t tick_base, const int64_t *tick_dev,
+                                            uint32_t *counters, uint64_t *fault_log, int64_t fault_cap)
+{
+    Row R;
+    load_state<COMP>(C, R);
+    const int level = (fl & SWARMSTEP_LEVEL_MASK) >> SWARMSTEP_LEVEL_SHIFT;
+    R.has_prev = (fl & SWARMSTEP_FLAG_HAS_PREV) != 0;
+    setup_level(C, level, overlay_active, P, R);
+    const ssb::Derived D = ssb::derive(P, 1.0f / dt);
+    const int fault_k = run_level<COMP, false>(C, level, overlay_active, P, D, dt, K, -1, R);
+    bool alive = true;
+    if (fault_k >= 0) {
+        alive = false;
+        load_state<COMP>(C, R);
+        R.has_prev = (fl & SWARMSTEP_FLAG_HAS_PREV) != 0;
+        setup_level(C, level, overlay_active, P, R);
+        run_level<COMP, true>(C, level, overlay_active, P, D, dt, fault_k + 1, fault_k, R);
+        const uint32_t slot = atomicAdd(&counters[0], 1u);
+        const uint32_t tick = (tick_dev ? (uint32_t)*tick_dev : 0u) + tick_base + (uint32_t)fault_k;
+        if ((int64_t)slot < fault_cap)
+            fault_log[slot] = ((uint64_t)(tick & 0xFFFFFFu) << 40) | (uint64_t)r;
+    }
+    store_state<COMP>(C, level, R);
+    // has_prev |= alive (control.py:181): every row reaching here was alive
+    return (uint8_t)((fl & SWARMSTEP_LEVEL_MASK) | (alive ? SWARMSTEP_FLAG_ALIVE : 0u) | SWARMSTEP_FLAG_HAS_PREV);
+}
+
+// ---- direct kernel: one row per thread, loads/stores straight to HBM -------
 template <bool COMP>
 __global__ void __launch_bounds__(kBlock, SSB_STEP_MINB)
-quad_step_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t n, int64_t stride,
+quad_step_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t n,
                  uint32_t *__restrict__ counters, uint64_t *__restrict__ fault_log,
                  int64_t fault_cap, int overlay_active, uint32_t tick_base, const int64_t *tick_dev,
                  const swarmstep_quad_params P, float dt, int K)
 {
     const int64_t r = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     if (r >= n) return;
-    const Cols C{cols, stride};
-    // every state load is issued before the flag test: one memory round trip
-    // per row (dead rows are rare; their loads are discarded)
     const uint8_t fl = flags[r];
-    Row R;
-    load_state<COMP>(C, r, R);
     if (!(fl & SWARMSTEP_FLAG_ALIVE)) return;  // dead rows are frozen (quad.py:395-437)
-    const int level = (fl & SWARMSTEP_LEVEL_MASK) >> SWARMSTEP_LEVEL_SHIFT;
-    R.has_prev = (fl & SWARMSTEP_FLAG_HAS_PREV) != 0;
-    setup_level(C, r, level, overlay_active, P, R);
-    const ssb::Derived D = ssb::derive(P, 1.0f / dt);
-
-    const int fault_k = run_level<COMP, false>(C, r, level, overlay_active, P, D, dt, K, -1, R);
-    bool alive = true;
-    if (fault_k >= 0) {
-        // Fault at tick fault_k: the row keeps its pre-tick values, dies and is
-        // reported with its tick (quad.py:425-436).  The state was updated in
-        // place, so rebuild it by re-running ticks [0, fault_k) from the
-        // launch's inputs -- bit-identical by determinism -- plus the
-        // controller part of tick fault_k (the reference updates the PID state
-        // before rk4_step faults the row).
-        alive = false;
-        load_state<COMP>(C, r, R);
-        R.has_prev = (fl & SWARMSTEP_FLAG_HAS_PREV) != 0;
-        setup_level(C, r, level, overlay_active, P, R);
-        run_level<COMP, true>(C, r, level, overlay_active, P, D, dt, fault_k + 1, fault_k, R);
-        const uint32_t slot = atomicAdd(&counters[0], 1u);
-        const uint32_t tick = (tick_dev ? (uint32_t)*tick_dev : 0u) + tick_base + (uint32_t)fault_k;
-        if ((int64_t)slot < fault_cap)
-            fault_log[slot] = ((uint64_t)(tick & 0xFFFFFFu) << 40) | (uint64_t)r;
-    }
-
-    // ---- store ----
-#pragma unroll
-    for (int i = 0; i < 3; i++) {
-        __stcs(C.col(SWARMSTEP_COL_POS + i) + r, R.p_hi[i]);
-        __stcs(C.col(SWARMSTEP_COL_VEL + i) + r, R.v[i]);
-        __stcs(C.col(SWARMSTEP_COL_OMEGA + i) + r, R.w[i]);
-        __stcs(C.col(SWARMSTEP_COL_INTEGRAL + i) + r, R.integ[i]);
-        __stcs(C.col(SWARMSTEP_COL_PREV + i) + r, R.prev[i]);
-        if (COMP) __stcs(C.col(SWARMSTEP_COL_POS_LO + i) + r, R.p_lo[i]);
-    }
-#pragma unroll
-    for (int i = 0; i < 4; i++) __stcs(C.col(SWARMSTEP_COL_QUAT + i) + r, R.q[i]);
-    if (level != SWARMSTEP_LEVEL_MOTOR) {
-        // the last tick's setpoints become the stale setpoints a later MOTOR
-        // command runs the PID on (core.py:178-182)
-#pragma unroll
-        for (int i = 0; i < 3; i++) __stcs(C.col(SWARMSTEP_COL_SP + i) + r, R.w_sp[i]);
-        __stcs(C.col(SWARMSTEP_COL_SP + 3) + r, R.f_sp);
-    }
-    // has_prev |= alive (control.py:181): every row reaching here was alive
-    const uint8_t nfl = (uint8_t)((fl & SWARMSTEP_LEVEL_MASK) | (alive ? SWARMSTEP_FLAG_ALIVE : 0u) |
-                                  SWARMSTEP_FLAG_HAS_PREV);
+    const GlobalRow C{cols + ssb::tile_base(r)};
+    const uint8_t nfl = step_row<COMP>(C, fl, r, overlay_active, P, dt, K, tick_base, tick_dev,
+                                       counters, fault_log, fault_cap);
     if (nfl != fl) flags[r] = nfl;
+}
+
+// ---- TMA kernel: persistent CTAs, tiles staged through shared memory --------
+// Each CTA walks tiles blockIdx.x, +gridDim.x, ...  One elected thread moves a
+// tile's input columns HBM -> shared memory with one cp.async.bulk (TMA) per
+// tile into a kStages-deep ring (mbarrier completion), so the next tiles'
+// loads are in flight while this one is computed; results are written back
+// into the same shared tile and leave with two bulk stores (cols [0, 22) and
+// the stale setpoints [29, 33)).  No register holds an in-flight load.
+#ifndef SSB_TMA_STAGES
+#define SSB_TMA_STAGES 2
+#endif
+constexpr int kStages = SSB_TMA_STAGES;
+constexpr int kTileFloats = SWARMSTEP_NCOL * SWARMSTEP_TILE;
+
+struct TmaSmem {
+    float tile[kStages][kTileFloats];
+    uint8_t flags[kStages][SWARMSTEP_TILE];
+    unsigned long long full[kStages];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "SSB_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra SSB_WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, unsigned long long *bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t bytes)
+{
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+template <bool COMP>
+__global__ void __launch_bounds__(SWARMSTEP_TILE, SSB_STEP_MINB)
+quad_step_tma_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t ntiles,
+                     uint32_t *__restrict__ counters, uint64_t *__restrict__ fault_log, int64_t fault_cap,
+                     int overlay_active, int motor_possible, uint32_t tick_base, const int64_t *tick_dev,
+                     const swarmstep_quad_params P, float dt, int K)
+{
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    TmaSmem &S = *reinterpret_cast<TmaSmem *>(smem_raw);
+    const int tid = threadIdx.x;
+    // input columns: [0, 29) always; the stale setpoints [29, 33) only if a
+    // MOTOR row may exist; the overlay [33, 36) only on overlay ticks
+    const int in_cols = overlay_active ? SWARMSTEP_NCOL : (motor_possible ? SWARMSTEP_COL_OVERLAY : SWARMSTEP_COL_SP);
+    const uint32_t in_bytes = (uint32_t)in_cols * SWARMSTEP_TILE * 4u;
+    if (tid == 0) {
+        for (int s = 0; s < kStages; s++) mbar_init(&S.full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int64_t t0 = blockIdx.x, tstep = gridDim.x;
+    auto issue = [&](int s, int64_t t) {
+        mbar_expect_tx(&S.full[s], in_bytes + SWARMSTEP_TILE);
+        bulk_g2s(S.tile[s], cols + t * kTileFloats, in_bytes, &S.full[s]);
+        bulk_g2s(S.flags[s], flags + t * SWARMSTEP_TILE, SWARMSTEP_TILE, &S.full[s]);
+    };
+    if (tid == 0)
+        for (int s = 0; s < kStages; s++)
+            if (t0 + s * tstep < ntiles) issue(s, t0 + s * tstep);
+
+    int64_t j = 0;
+    for (int64_t t = t0; t < ntiles; t += tstep, j++) {
+        const int s = (int)(j % kStages);
+        mbar_wait(&S.full[s], (uint32_t)((j / kStages) & 1));
+        float *T = S.tile[s];
+        const uint8_t fl = S.flags[s][tid];
+        const int64_t r = t * SWARMSTEP_TILE + tid;
+        const SmemRow C{T + tid};
+        if (fl & SWARMSTEP_FLAG_ALIVE) {
+            const uint8_t nfl = step_row<COMP>(C, fl, r, overlay_active, P, dt, K, tick_base, tick_dev,
+                                               counters, fault_log, fault_cap);
+            if (nfl != fl) flags[r] = nfl;
+        } else if (!motor_possible && !overlay_active) {
+            // dead row, stale setpoints not staged: store zeros, not stale smem
+#pragma unroll
+            for (int i = 0; i < 4; i++) C.st(SWARMSTEP_COL_SP + i, 0.0f);
+        }
+        // make the generic-proxy smem writes visible to the bulk-copy engine
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (tid == 0) {
+            float *g = cols + t * kTileFloats;
+            bulk_s2g(g, T, SWARMSTEP_COL_CMD * SWARMSTEP_TILE * 4u);
+            bulk_s2g(g + SWARMSTEP_COL_SP * SWARMSTEP_TILE, T + SWARMSTEP_COL_SP * SWARMSTEP_TILE,
+                     4u * SWARMSTEP_TILE * 4u);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            const int64_t tn = t + kStages * tstep;
+            if (tn < ntiles) {
+                // the stage may be refilled once the stores have read it
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                issue(s, tn);
+            }
+        }
+    }
+    if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -245,7 +407,7 @@ __global__ void apply_commands_kernel(float *cols, uint8_t *flags, int64_t strid
     if (!(fl & SWARMSTEP_FLAG_ALIVE)) return;
     flags[r] = (uint8_t)((fl & ~SWARMSTEP_LEVEL_MASK) | ((levels[i] & 3u) << SWARMSTEP_LEVEL_SHIFT));
 #pragma unroll
-    for (int c = 0; c < 7; c++) cols[(int64_t)(SWARMSTEP_COL_CMD + c) * stride + r] = values[i * 7 + c];
+    for (int c = 0; c < 7; c++) cols[ssb::at(SWARMSTEP_COL_CMD + c, r)] = values[i * 7 + c];
 }
 
 __global__ void set_setpoints_kernel(float *cols, uint8_t *flags, int64_t stride, int64_t row0,
@@ -260,7 +422,7 @@ __global__ void set_setpoints_kernel(float *cols, uint8_t *flags, int64_t stride
     if (nfl != fl) flags[r] = nfl;
     const int nv = level == SWARMSTEP_LEVEL_POS ? 7 : 4;
     for (int c = 0; c < 7; c++)
-        cols[(int64_t)(SWARMSTEP_COL_CMD + c) * stride + r] = c < nv ? values[(int64_t)c * ld + i] : 0.0f;
+        cols[ssb::at(SWARMSTEP_COL_CMD + c, r)] = c < nv ? values[(int64_t)c * ld + i] : 0.0f;
 }
 
 __global__ void mark_dead_kernel(uint8_t *flags, const int64_t *rows, uint8_t *was_alive, int64_t count)
@@ -282,20 +444,20 @@ __global__ void retarget_kernel(float *cols, uint8_t *flags, int64_t n, int64_t 
     if (!(fl & SWARMSTEP_FLAG_ALIVE)) return;
     double p[3];
     for (int i = 0; i < 3; i++) {
-        p[i] = (double)cols[(int64_t)(SWARMSTEP_COL_POS + i) * stride + r];
-        if (compensated) p[i] += (double)cols[(int64_t)(SWARMSTEP_COL_POS_LO + i) * stride + r];
+        p[i] = (double)cols[ssb::at(SWARMSTEP_COL_POS + i, r)];
+        if (compensated) p[i] += (double)cols[ssb::at(SWARMSTEP_COL_POS_LO + i, r)];
     }
     const double dx = p[0] - px, dy = p[1] - py, dz = p[2] - pz;
     const double d = sqrt(dx * dx + dy * dy + dz * dz);
     if (!(d < radius)) return;
-    const double w = cols[(int64_t)(SWARMSTEP_COL_QUAT + 0) * stride + r];
-    const double x = cols[(int64_t)(SWARMSTEP_COL_QUAT + 1) * stride + r];
-    const double y = cols[(int64_t)(SWARMSTEP_COL_QUAT + 2) * stride + r];
-    const double z = cols[(int64_t)(SWARMSTEP_COL_QUAT + 3) * stride + r];
+    const double w = cols[ssb::at(SWARMSTEP_COL_QUAT + 0, r)];
+    const double x = cols[ssb::at(SWARMSTEP_COL_QUAT + 1, r)];
+    const double y = cols[ssb::at(SWARMSTEP_COL_QUAT + 2, r)];
+    const double z = cols[ssb::at(SWARMSTEP_COL_QUAT + 3, r)];
     const double yaw = atan2(2.0 * (w * z + x * y), 1.0 - 2.0 * (y * y + z * z));  // quat.py:139-143
     flags[r] = (uint8_t)(fl & ~SWARMSTEP_LEVEL_MASK);  // POS level
     const float vals[7] = {(float)px, (float)py, (float)pz, 0.0f, 0.0f, 0.0f, (float)yaw};
-    for (int c = 0; c < 7; c++) cols[(int64_t)(SWARMSTEP_COL_CMD + c) * stride + r] = vals[c];
+    for (int c = 0; c < 7; c++) cols[ssb::at(SWARMSTEP_COL_CMD + c, r)] = vals[c];
     atomicAdd(&counters[1], 1u);
 }
 
@@ -307,15 +469,15 @@ __global__ void pack_f64_kernel(const float *cols, const uint8_t *flags, int64_t
     if (r >= n) return;
     for (int i = 0; i < 3; i++) {
         if (pos) {
-            double p = cols[(int64_t)(SWARMSTEP_COL_POS + i) * stride + r];
-            if (compensated) p += (double)cols[(int64_t)(SWARMSTEP_COL_POS_LO + i) * stride + r];
+            double p = cols[ssb::at(SWARMSTEP_COL_POS + i, r)];
+            if (compensated) p += (double)cols[ssb::at(SWARMSTEP_COL_POS_LO + i, r)];
             pos[r * 3 + i] = p;
         }
-        if (vel) vel[r * 3 + i] = cols[(int64_t)(SWARMSTEP_COL_VEL + i) * stride + r];
-        if (omega) omega[r * 3 + i] = cols[(int64_t)(SWARMSTEP_COL_OMEGA + i) * stride + r];
+        if (vel) vel[r * 3 + i] = cols[ssb::at(SWARMSTEP_COL_VEL + i, r)];
+        if (omega) omega[r * 3 + i] = cols[ssb::at(SWARMSTEP_COL_OMEGA + i, r)];
     }
     if (quat)
-        for (int i = 0; i < 4; i++) quat[r * 4 + i] = cols[(int64_t)(SWARMSTEP_COL_QUAT + i) * stride + r];
+        for (int i = 0; i < 4; i++) quat[r * 4 + i] = cols[ssb::at(SWARMSTEP_COL_QUAT + i, r)];
     if (alive) alive[r] = (flags[r] & SWARMSTEP_FLAG_ALIVE) ? 1 : 0;
 }
 
@@ -329,14 +491,14 @@ __global__ void unpack_f64_kernel(float *cols, uint8_t *flags, int64_t n, int64_
         if (pos) {
             const double p = pos[r * 3 + i];
             const float hi = (float)p;
-            cols[(int64_t)(SWARMSTEP_COL_POS + i) * stride + r] = hi;
-            cols[(int64_t)(SWARMSTEP_COL_POS_LO + i) * stride + r] = compensated ? (float)(p - (double)hi) : 0.0f;
+            cols[ssb::at(SWARMSTEP_COL_POS + i, r)] = hi;
+            cols[ssb::at(SWARMSTEP_COL_POS_LO + i, r)] = compensated ? (float)(p - (double)hi) : 0.0f;
         }
-        if (vel) cols[(int64_t)(SWARMSTEP_COL_VEL + i) * stride + r] = (float)vel[r * 3 + i];
-        if (omega) cols[(int64_t)(SWARMSTEP_COL_OMEGA + i) * stride + r] = (float)omega[r * 3 + i];
+        if (vel) cols[ssb::at(SWARMSTEP_COL_VEL + i, r)] = (float)vel[r * 3 + i];
+        if (omega) cols[ssb::at(SWARMSTEP_COL_OMEGA + i, r)] = (float)omega[r * 3 + i];
     }
     if (quat)
-        for (int i = 0; i < 4; i++) cols[(int64_t)(SWARMSTEP_COL_QUAT + i) * stride + r] = (float)quat[r * 4 + i];
+        for (int i = 0; i < 4; i++) cols[ssb::at(SWARMSTEP_COL_QUAT + i, r)] = (float)quat[r * 4 + i];
     if (alive) {
         const uint8_t fl = flags[r];
         flags[r] = (uint8_t)((fl & SWARMSTEP_LEVEL_MASK) | (alive[r] ? SWARMSTEP_FLAG_ALIVE : 0u));
@@ -377,6 +539,7 @@ int swarmstep_preload(void)
     // must not happen inside a CUDA graph capture)
     cudaFuncAttributes a;
     const void *fns[] = {(const void *)quad_step_kernel<true>, (const void *)quad_step_kernel<false>,
+                         (const void *)quad_step_tma_kernel<true>, (const void *)quad_step_tma_kernel<false>,
                          (const void *)apply_commands_kernel, (const void *)set_setpoints_kernel,
                          (const void *)mark_dead_kernel, (const void *)retarget_kernel,
                          (const void *)pack_f64_kernel, (const void *)unpack_f64_kernel};
@@ -386,7 +549,7 @@ int swarmstep_preload(void)
 }
 
 int swarmstep_quad_step(const swarmstep_group_view *g, const swarmstep_quad_params *p, float dt,
-                        int k_substeps, int overlay_active, uint32_t tick_base, const int64_t *tick_dev,
+                        int k_substeps, int launch_flags, uint32_t tick_base, const int64_t *tick_dev,
                         void *stream)
 {
     int st = check_view(g);
@@ -396,10 +559,38 @@ int swarmstep_quad_step(const swarmstep_group_view *g, const swarmstep_quad_para
     if (k_substeps < 1) return set_err(SWARMSTEP_EINVAL, "k_substeps must be >= 1");
     if (!g->counters) return set_err(SWARMSTEP_EINVAL, "null counters");
     if (g->n == 0) return SWARMSTEP_OK;
+    const int overlay = launch_flags & SWARMSTEP_STEP_OVERLAY;
+    const int motor = (launch_flags & SWARMSTEP_STEP_MOTOR) ? 1 : 0;
+    const bool use_tma = (launch_flags & SWARMSTEP_STEP_FORCE_DIRECT) ? false
+                       : (launch_flags & SWARMSTEP_STEP_FORCE_TMA) ? true
+                       : k_substeps <= SSB_TMA_MAX_K;
+    const int64_t fcap = g->fault_log ? g->fault_cap : 0;
+    if (use_tma) {
+        static int blocks_per_sm[2] = {0, 0};
+        static int sm_count = 0;
+        const size_t smem = sizeof(TmaSmem);
+        auto kern = g->compensated ? quad_step_tma_kernel<true> : quad_step_tma_kernel<false>;
+        const int ci = g->compensated ? 1 : 0;
+        if (!blocks_per_sm[ci]) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm[ci], kern, SWARMSTEP_TILE, smem);
+            if (blocks_per_sm[ci] < 1) blocks_per_sm[ci] = 1;
+        }
+        const int64_t ntiles = (g->n + SWARMSTEP_TILE - 1) / SWARMSTEP_TILE;
+        int64_t grid = (int64_t)sm_count * blocks_per_sm[ci];
+        if (grid > ntiles) grid = ntiles;
+        kern<<<(unsigned)grid, SWARMSTEP_TILE, smem, (cudaStream_t)stream>>>(
+            g->cols, g->flags, ntiles, g->counters, g->fault_log, fcap, overlay, motor, tick_base, tick_dev,
+            *p, dt, k_substeps);
+        return cuda_status("quad_step_tma_kernel");
+    }
     auto kern = g->compensated ? quad_step_kernel<true> : quad_step_kernel<false>;
     kern<<<grid_for(g->n, kBlock), kBlock, 0, (cudaStream_t)stream>>>(
-        g->cols, g->flags, g->n, g->stride, g->counters, g->fault_log, g->fault_log ? g->fault_cap : 0,
-        overlay_active, tick_base, tick_dev, *p, dt, k_substeps);
+        g->cols, g->flags, g->n, g->counters, g->fault_log, fcap, overlay, tick_base, tick_dev, *p, dt,
+        k_substeps);
     return cuda_status("quad_step_kernel");
 }
 

@@ -70,8 +70,9 @@ class TickGraph:
     def __init__(self, group, dt: float, ticks: int, feed: CircleFeed | None = None):
         if ticks < 1:
             raise ValidationError("ticks must be >= 1")
-        if group._pending or group._overlay_active:
-            group._flush_commands()
+        if group._overlay_active:
+            raise ValidationError("apply or clear the pending overlay before capturing a graph")
+        group._flush_commands()
         self.group, self.dt, self.ticks = group, float(dt), int(ticks)
         self.feed = feed
         self._lib = _lib.load()
@@ -92,8 +93,8 @@ class TickGraph:
         for j in range(self.ticks):
             if self.feed is not None:
                 self.feed.apply(j, sync_tick=False)
-            _lib.check(self._lib.swarmstep_quad_step(g._view_ref, g._params_ref, ctypes.c_float(self.dt), 1, 0,
-                                                     ctypes.c_uint32(j), self.tick.data_ptr(), s))
+            _lib.check(self._lib.swarmstep_quad_step(g._view_ref, g._params_ref, ctypes.c_float(self.dt), 1,
+                                                     g._launch_flags(), ctypes.c_uint32(j), self.tick.data_ptr(), s))
         _lib.check(self._lib.swarmstep_tick_add(self.tick.data_ptr(), self.ticks, s))
 
     def replay(self) -> None:

@@ -9,9 +9,9 @@ duck-typed group protocol the reference ``World`` calls (core.py:308-505) --
 built for: ``step_k(dt, k)`` (k fused ticks per launch), ``set_setpoints``
 (device-resident setpoint feed) and ``step_async`` / ``collect_faults``.
 
-Device layout: one float32 buffer of ``NCOL`` columns x
-``stride`` rows (structure of arrays, one column per scalar component) plus a
-uint8 flag column (alive | has_prev | level).  The float64 host views the
+Device layout: one float32 buffer in tiled structure-of-arrays
+form -- tiles of 128 agents, each tile holding its ``NCOL`` component columns
+contiguously -- plus a uint8 flag column (alive | has_prev | level).  The float64 host views the
 reference exposes (``batch.pos`` ...) are mirrors synchronised lazily: a
 read after a step packs the device columns to float64 on the device and
 copies them down once.  Writes into those mirror arrays do not reach the
@@ -27,14 +27,16 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import (COL_CMD, COL_OVERLAY, FLAG_ALIVE, LEVEL_MASK, LEVEL_SHIFT, NCOL, GroupView)
+from ._lib import (COL_CMD, COL_INTEGRAL, COL_OVERLAY, COL_PREV, COL_SP, FLAG_ALIVE, FLAG_HAS_PREV,
+                   LEVEL_MASK, LEVEL_SHIFT, NCOL, STEP_FORCE_DIRECT, STEP_FORCE_TMA, STEP_MOTOR,
+                   STEP_OVERLAY, TILE, GroupView)
 from .commands import LEVEL_MOTOR, LEVEL_POS, LEVEL_RATE, level_code
 from .errors import InvalidStateError, NativeLibraryError, ValidationError
 from .params import (default_outer_gains, default_quad_params, default_rate_gains,
                      pack_device_params)
 from .state import AgentBatch, batch_snapshot, quat_yaw
 
-_ROW_ALIGN = 128  # stride multiple: whole 512-byte column tiles, 16-byte aligned
+_ROW_ALIGN = TILE  # row capacity is a whole number of 128-agent tiles
 
 
 def _round_up(x: int, m: int) -> int:
@@ -73,7 +75,8 @@ class B200QuadGroup:
         with torch.cuda.device(self.device):
             self.stream = torch.cuda.Stream(self.device)
             with torch.cuda.stream(self.stream):
-                self._cols = torch.zeros((NCOL, self.stride), dtype=torch.float32, device=self.device)
+                self.ntiles = self.stride // TILE
+                self._cols = torch.zeros((self.ntiles, NCOL, TILE), dtype=torch.float32, device=self.device)
                 self._flags = torch.zeros(self.stride, dtype=torch.uint8, device=self.device)
                 self._counters = torch.zeros(4, dtype=torch.int32, device=self.device)
                 cap = int(fault_capacity) if fault_capacity is not None else n
@@ -109,6 +112,7 @@ class B200QuadGroup:
         self._nonfinite_rows: set[int] = set()
         self._overlay_active = False
         self._overlay_poison = False
+        self._motor_possible = False     # sticky: a MOTOR-level row may exist
         self._tick = 0                   # ticks launched so far (fault-log tags)
         self._launched: list[tuple[int, int]] = []  # (first tick, k) not yet collected
         self._fault_seen = 0             # fault-log entries already returned
@@ -130,8 +134,28 @@ class B200QuadGroup:
 
     @property
     def cols(self) -> torch.Tensor:
-        """The device SoA buffer [NCOL, stride] (float32)."""
+        """The device tiled-SoA buffer [stride/128, NCOL, 128] (float32)."""
         return self._cols
+
+    def column_block(self, c0: int, c1: int) -> torch.Tensor:
+        """Columns [c0, c1) of rows [0, n) as an (n, c1-c0) device tensor (a copy);
+        stream-ordered after this group's work."""
+        with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
+            out = self._cols[:, c0:c1, :].permute(0, 2, 1).reshape(-1, c1 - c0)[:self.n].clone()
+        self.stream.synchronize()
+        return out
+
+    def _cols_write(self, c0: int, data: torch.Tensor, add: bool = False) -> None:
+        """Write (n, k) rows into columns [c0, c0+k) (on the current stream)."""
+        k = data.shape[1]
+        buf = torch.zeros((self.stride, k), dtype=torch.float32, device=self.device)
+        buf[:self.n] = data
+        view = self._cols[:, c0:c0 + k, :]
+        src = buf.view(self.ntiles, TILE, k).permute(0, 2, 1)
+        if add:
+            view += src
+        else:
+            view.copy_(src)
 
     @property
     def flags(self) -> torch.Tensor:
@@ -150,8 +174,10 @@ class B200QuadGroup:
             self._call(self._lib.swarmstep_quad_unpack_f64, _ptr(pos), _ptr(vel), _ptr(quat),
                        _ptr(omega), _ptr(alive), ctypes.c_void_p(self.stream.cuda_stream))
             if upload_commands:
-                vals = torch.from_numpy(self._cmd_values.T.astype(np.float32).copy()).to(self.device)
-                self._cols[COL_CMD:COL_CMD + 7, :self.n].copy_(vals)
+                if np.any(self._cmd_level == LEVEL_MOTOR):
+                    self._motor_possible = True
+                vals = torch.from_numpy(self._cmd_values.astype(np.float32)).to(self.device)
+                self._cols_write(COL_CMD, vals)
                 lv = torch.from_numpy(self._cmd_level.astype(np.uint8)).to(self.device)
                 fl = self._flags[:self.n]
                 fl.copy_((fl & (0xFF ^ LEVEL_MASK)) | (lv << LEVEL_SHIFT))
@@ -185,7 +211,7 @@ class B200QuadGroup:
         if not self._cmd_stale:
             return
         with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
-            vals = self._cols[COL_CMD:COL_CMD + 7, :self.n].T.double().cpu().numpy()
+            vals = self._cols[:, COL_CMD:COL_CMD + 7, :].permute(0, 2, 1).reshape(-1, 7)[:self.n].double().cpu().numpy()
             lv = ((self._flags[:self.n] & LEVEL_MASK) >> LEVEL_SHIFT).cpu().numpy()
         self._cmd_values[:] = vals
         self._cmd_level[:] = lv
@@ -247,6 +273,8 @@ class B200QuadGroup:
         full[:want] = vals
         self._cmd_level[row] = lvl
         self._cmd_values[row] = full
+        if lvl == LEVEL_MOTOR:
+            self._motor_possible = True
         if np.all(np.isfinite(full)):
             self._nonfinite_rows.discard(row)
         else:
@@ -319,6 +347,8 @@ class B200QuadGroup:
                 self._sp_src[slot] = t
         if self._nonfinite_rows:
             self._nonfinite_rows = {r for r in self._nonfinite_rows if not (row0 <= r < row0 + count)}
+        if lvl == LEVEL_MOTOR:
+            self._motor_possible = True
         self._cmd_stale = True
 
     def add_velocity_overlay(self, offsets) -> None:
@@ -329,8 +359,8 @@ class B200QuadGroup:
             if not bool(torch.isfinite(t).all()):
                 self._overlay_poison = True
             if not self._overlay_active:
-                self._cols[COL_OVERLAY:COL_OVERLAY + 3].zero_()
-            self._cols[COL_OVERLAY:COL_OVERLAY + 3, :self.n] += t.T
+                self._cols[:, COL_OVERLAY:COL_OVERLAY + 3, :].zero_()
+            self._cols_write(COL_OVERLAY, t, add=True)
         self._overlay_active = True
 
     def retarget_waypoint(self, point, radius: float) -> None:
@@ -388,7 +418,7 @@ class B200QuadGroup:
         self._flush_commands()
         with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
             self._call(self._lib.swarmstep_quad_step, self._params_ref, ctypes.c_float(dt), int(k),
-                       int(self._overlay_active), ctypes.c_uint32(self._tick & 0xFFFFFF), None,
+                       self._launch_flags(), ctypes.c_uint32(self._tick & 0xFFFFFF), None,
                        ctypes.c_void_p(self.stream.cuda_stream))
             self._overlay_reset()
             self._counters_host.copy_(self._counters, non_blocking=True)
@@ -396,10 +426,24 @@ class B200QuadGroup:
         self._tick += k
         self._state_stale = True
 
+    # kernel selection for tuning: "auto" (TMA-staged for few ticks per launch,
+    # direct for many), "direct" or "tma"
+    kernel = "auto"
+
+    def _launch_flags(self) -> int:
+        f = STEP_OVERLAY if self._overlay_active else 0
+        if self._motor_possible:
+            f |= STEP_MOTOR
+        if self.kernel == "direct":
+            f |= STEP_FORCE_DIRECT
+        elif self.kernel == "tma":
+            f |= STEP_FORCE_TMA
+        return f
+
     def _overlay_reset(self) -> None:
         if self._overlay_active:
             with torch.cuda.stream(self.stream):
-                self._cols[COL_OVERLAY:COL_OVERLAY + 3].zero_()
+                self._cols[:, COL_OVERLAY:COL_OVERLAY + 3, :].zero_()
         self._overlay_active = False
         self._overlay_poison = False
 
@@ -439,24 +483,21 @@ class B200QuadGroup:
         return int(self._alive.sum())
 
     def pid_state(self) -> dict:
-        """Host float64 copy of the PID columns (RatePidState, control.py:100-114)."""
-        from ._lib import COL_INTEGRAL, COL_PREV, COL_SP, FLAG_HAS_PREV
+        """Host float64 copy of the PID columns (RatePidState, control.py:100-114)
+        and the stale inner-loop setpoints (QuadGroup.omega_sp / f_c_sp)."""
+        blk = self.column_block(COL_INTEGRAL, COL_PREV + 3).double().cpu().numpy()
+        sp = self.column_block(COL_SP, COL_SP + 4).double().cpu().numpy()
         with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
-            integ = self._cols[COL_INTEGRAL:COL_INTEGRAL + 3, :self.n].T.double().cpu().numpy()
-            prev = self._cols[COL_PREV:COL_PREV + 3, :self.n].T.double().cpu().numpy()
-            sp = self._cols[COL_SP:COL_SP + 4, :self.n].T.double().cpu().numpy()
             hp = ((self._flags[:self.n] & FLAG_HAS_PREV) != 0).cpu().numpy()
-        return {"integral": integ, "prev_omega": prev, "has_prev": hp,
+        return {"integral": blk[:, :3].copy(), "prev_omega": blk[:, 3:6].copy(), "has_prev": hp,
                 "omega_sp": sp[:, :3].copy(), "f_c_sp": sp[:, 3].copy()}
 
     def set_pid_state(self, integral=None, prev_omega=None, has_prev=None, omega_sp=None, f_c_sp=None) -> None:
         """Load PID / stale-setpoint columns (test and resume support)."""
-        from ._lib import COL_INTEGRAL, COL_PREV, COL_SP, FLAG_HAS_PREV
         n = self.n
         with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
             def put(c0, arr, k):
-                t = torch.from_numpy(np.asarray(arr, dtype=np.float32).reshape(n, k).T.copy()).to(self.device)
-                self._cols[c0:c0 + k, :n].copy_(t)
+                self._cols_write(c0, torch.from_numpy(np.asarray(arr, dtype=np.float32).reshape(n, k)).to(self.device))
             if integral is not None:
                 put(COL_INTEGRAL, integral, 3)
             if prev_omega is not None:

@@ -15,12 +15,9 @@ ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
 VARIANTS = {
-    "b128m5": ["-DSSB_STEP_BLOCK=128", "-DSSB_STEP_MINB=5"],
-    "b128m6": ["-DSSB_STEP_BLOCK=128", "-DSSB_STEP_MINB=6"],
-    "b64m10": ["-DSSB_STEP_BLOCK=64", "-DSSB_STEP_MINB=10"],
-    "b128m4u2": ["-DSSB_STEP_BLOCK=128", "-DSSB_STEP_MINB=4", "-DSSB_TICK_UNROLL=2"],
-    "b128m5u2": ["-DSSB_STEP_BLOCK=128", "-DSSB_STEP_MINB=5", "-DSSB_TICK_UNROLL=2"],
-    "b256m3": ["-DSSB_STEP_BLOCK=256", "-DSSB_STEP_MINB=3"],
+    "default": [],
+    "m6": ["-DSSB_STEP_MINB=6"],
+    "m4st3": ["-DSSB_STEP_MINB=4", "-DSSB_TMA_STAGES=3"],
 }
 
 CHILD = r'''
@@ -33,7 +30,9 @@ pos, sp = workload(n, 0)
 g = B200QuadGroup(0, _Batch(n, pos, 0), device="cuda:0")
 g.set_setpoints(torch.from_numpy(sp).cuda(), columns=True)
 out = {}
-for k in (10, 1):
+import os
+g.kernel = os.environ.get("TUNE_KERNEL", "auto")
+for k in (10, 4, 2, 1):
     for _ in range(5): g.step_async(1e-3, k)
     g.collect_faults(); torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -45,6 +44,7 @@ for k in (10, 1):
     out[f"K{k}_ms"] = ms
     out[f"K{k}_agent_steps_per_s"] = n * k / ms * 1e3
 out["K1_GBps"] = 221 * n / out["K1_ms"] / 1e6
+out["kernel"] = g.kernel
 print("RESULT " + json.dumps(out))
 '''
 
@@ -53,17 +53,18 @@ def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 4_000_000
     from paper_2308_12698_b200._build import NVCC_FLAGS, _nvcc, sources, INCLUDE, CSRC
     res = {}
-    for name, defs in VARIANTS.items():
+    runs = [(name, defs, kern) for name, defs in VARIANTS.items() for kern in ("direct", "tma")]
+    for name, defs, kern in runs:
         so = f"/tmp/ssb_{name}.so"
         cmd = [_nvcc(), *NVCC_FLAGS, *defs, f"-I{INCLUDE}", f"-I{CSRC}", "-o", so, *map(str, sources())]
         b = subprocess.run(cmd, capture_output=True, text=True)
         regs = [l for l in b.stderr.splitlines() if "registers" in l]
-        env = dict(os.environ, SWARMSTEP_B200_LIB_OVERRIDE=so)
+        env = dict(os.environ, SWARMSTEP_B200_LIB_OVERRIDE=so, TUNE_KERNEL=kern)
         p = subprocess.run([sys.executable, "-c", CHILD % dict(root=ROOT, n=n)], env=env, capture_output=True, text=True)
         line = [l for l in p.stdout.splitlines() if l.startswith("RESULT ")]
-        res[name] = json.loads(line[0][7:]) if line else {"error": p.stderr[-800:]}
-        res[name]["ptxas"] = regs[-2:]
-        print(name, json.dumps(res[name]), flush=True)
+        key = f"{name}/{kern}"
+        res[key] = json.loads(line[0][7:]) if line else {"error": p.stderr[-800:]}
+        print(key, json.dumps(res[key]), flush=True)
     Path(ROOT / "gpurun_out").mkdir(exist_ok=True)
     (ROOT / "gpurun_out" / "tune.json").write_text(json.dumps(res, indent=1))
 
