@@ -238,7 +238,17 @@ def run_b200(args, rank: int, world: int) -> None:
     achieved_tf = n * k * ALG_FLOPS_PER_AGENT_TICK / launch_s / 1e12
     sm_mhz = clk.get("sm_max_mhz") or 1965.0
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    fp32_peak_tf = sms * 128 * 2 * sm_mhz * 1e6 / 1e12
+    fp32_nominal_tf = sms * 128 * 2 * sm_mhz * 1e6 / 1e12
+    fp32_meas = _fp32_peak()
+    if fp32_meas:
+        fp32_peak_tf = fp32_meas["tflops"]
+        peak_source = (f"measured: FFMA microbenchmark tools/fp32_peak.cu ({fp32_meas['form']} form, best of "
+                       f"register/immediate operand) on this GPU; nominal {fp32_nominal_tf:.1f} TFLOP/s = "
+                       f"{sms} SMs x 128 lanes x 2 x {sm_mhz:.0f} MHz")
+    else:
+        fp32_peak_tf = fp32_nominal_tf
+        peak_source = (f"derived: {sms} SMs x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz "
+                       "(MEASURED_PEAKS.json has no FP32 SIMT figure)")
 
     # ---- K=1 leg: the same kernel in its HBM-bound regime
     k1 = None
@@ -308,9 +318,8 @@ def run_b200(args, rank: int, world: int) -> None:
                        "parallelism": f"agent-index shards x{world}, no collective"},
             "roofline": {"bound": "fp32", "achieved": achieved_tf, "peak": fp32_peak_tf, "unit": "TFLOP/s",
                          "frac": achieved_tf / fp32_peak_tf, "traffic": _traffic("k10", n),
-                         "flops_per_agent_tick": ALG_FLOPS_PER_AGENT_TICK,
-                         "peak_source": f"derived: {sms} SMs x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz "
-                                        "(MEASURED_PEAKS.json has no FP32 SIMT figure)"},
+                         "flops_per_agent_tick": ALG_FLOPS_PER_AGENT_TICK, "peak_source": peak_source,
+                         "fp32_peak_measurements": fp32_meas},
             "roofline_k1": k1,
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -320,6 +329,25 @@ def run_b200(args, rank: int, world: int) -> None:
             "setup_s": setup_s,
         }
         print(json.dumps(line), flush=True)
+
+
+def _fp32_peak():
+    """FP32 SIMT peak measured on this GPU (tools/fp32_peak.cu), or None."""
+    import ctypes
+    so = ROOT / "tools" / "libfp32peak.so"
+    if not so.exists():
+        return None
+    lib = ctypes.CDLL(str(so))
+    lib.fp32_peak_tflops.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
+    res = {}
+    for imm in (0, 1):
+        tf, ms = ctypes.c_double(), ctypes.c_double()
+        if lib.fp32_peak_tflops(imm, ctypes.byref(tf), ctypes.byref(ms)) == 0:
+            res["imm" if imm else "reg"] = tf.value
+    if not res:
+        return None
+    form = max(res, key=res.get)
+    return {"tflops": res[form], "form": "immediate" if form == "imm" else "register", **res}
 
 
 def _peaks() -> dict:

@@ -33,10 +33,10 @@ int check_view(const swarmstep_group_view *g)
 #define SSB_STEP_BLOCK 128
 #endif
 #ifndef SSB_STEP_MINB
-#define SSB_STEP_MINB 5
+#define SSB_STEP_MINB 6
 #endif
-// 128-thread CTAs, >= 5 resident per SM: caps the step kernel at 102
-// registers (no spills) for 20 warps per SM.
+// 128-thread CTAs, >= 6 resident per SM: caps the step kernel at 85
+// registers (no spills with the tiled layout) for 24 warps per SM.
 constexpr int kBlock = SSB_STEP_BLOCK;
 
 // one agent's row inside its tile: column k at p + k * 128 (constant offsets)
@@ -53,7 +53,7 @@ struct Cols {
 #endif
 constexpr int kTickUnroll = SSB_TICK_UNROLL;
 #ifndef SSB_TMA_MAX_K
-#define SSB_TMA_MAX_K 4   // TMA-staged kernel for the memory-bound (few-tick) regime
+#define SSB_TMA_MAX_K 0   // auto never picks the TMA-staged kernel (measured slower)
 #endif
 
 // One agent's registers for a launch.
@@ -275,7 +275,7 @@ quad_step_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t 
 // into the same shared tile and leave with two bulk stores (cols [0, 22) and
 // the stale setpoints [29, 33)).  No register holds an in-flight load.
 #ifndef SSB_TMA_STAGES
-#define SSB_TMA_STAGES 2
+#define SSB_TMA_STAGES 3
 #endif
 constexpr int kStages = SSB_TMA_STAGES;
 constexpr int kTileFloats = SWARMSTEP_NCOL * SWARMSTEP_TILE;
@@ -327,8 +327,11 @@ __device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t by
                  : "memory");
 }
 
+#ifndef SSB_TMA_MINB
+#define SSB_TMA_MINB 4   // 3 x 18.6 KB stages per CTA: 4 CTAs fill the 228 KB of shared memory
+#endif
 template <bool COMP>
-__global__ void __launch_bounds__(SWARMSTEP_TILE, SSB_STEP_MINB)
+__global__ void __launch_bounds__(SWARMSTEP_TILE, SSB_TMA_MINB)
 quad_step_tma_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t ntiles,
                      uint32_t *__restrict__ counters, uint64_t *__restrict__ fault_log, int64_t fault_cap,
                      int overlay_active, int motor_possible, uint32_t tick_base, const int64_t *tick_dev,
@@ -382,11 +385,13 @@ quad_step_tma_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int6
             bulk_s2g(g + SWARMSTEP_COL_SP * SWARMSTEP_TILE, T + SWARMSTEP_COL_SP * SWARMSTEP_TILE,
                      4u * SWARMSTEP_TILE * 4u);
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            const int64_t tn = t + kStages * tstep;
-            if (tn < ntiles) {
-                // the stage may be refilled once the stores have read it
-                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-                issue(s, tn);
+            // Refill the stage of the PREVIOUS tile (its stores were issued one
+            // iteration ago, so waiting until all but the newest store group
+            // have read shared memory rarely blocks): tile (j-1) + kStages.
+            const int64_t tn = t + (kStages - 1) * tstep;
+            if (j >= 1 && tn < ntiles) {
+                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                issue((int)((j - 1) % kStages), tn);
             }
         }
     }

@@ -1,0 +1,65 @@
+// fp32_peak.cu -- FP32 SIMT peak microbenchmark (tuning/measurement aid, not product).
+//
+// MEASURED_PEAKS.json carries HBM and tensor-core peaks only; the fused step at
+// K >= 4 is bound by the FP32 SIMT pipes, so bench.py measures their peak here:
+// 8 independent FFMA chains per thread, 256 threads x (#SM x 8) CTAs, both the
+// register-operand and the immediate-operand FFMA forms.
+//   build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -Xcompiler -fPIC -shared
+//          -o tools/libfp32peak.so tools/fp32_peak.cu
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+template <bool IMM>
+__global__ void __launch_bounds__(256) ffma_kernel(float *out, float a, float b, int iters)
+{
+    float x[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) x[i] = threadIdx.x * 1e-3f + i;
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int r = 0; r < 16; r++) {
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                if (IMM)
+                    x[i] = fmaf(x[i], 0.9999f, 0.0001f);
+                else
+                    x[i] = fmaf(x[i], a, b);
+            }
+        }
+    }
+    float s = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 8; i++) s += x[i];
+    if (s == 12345.678f) out[0] = s;  // keep the chains alive
+}
+
+extern "C" int fp32_peak_tflops(int imm, double *tflops, double *ms)
+{
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    float *out = nullptr;
+    cudaMalloc(&out, sizeof(float));
+    const int iters = 2048, blocks = sms * 8, threads = 256;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    for (int rep = 0; rep < 2; rep++) {  // rep 0 warms up
+        cudaEventRecord(e0);
+        if (imm)
+            ffma_kernel<true><<<blocks, threads>>>(out, 0.9999f, 0.0001f, iters);
+        else
+            ffma_kernel<false><<<blocks, threads>>>(out, 0.9999f, 0.0001f, iters);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+    }
+    float t = 0.0f;
+    cudaEventElapsedTime(&t, e0, e1);
+    const double ffma = (double)blocks * threads * iters * 16 * 8;
+    *ms = t;
+    *tflops = 2.0 * ffma / (t * 1e-3) / 1e12;
+    cudaFree(out);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}

@@ -16,8 +16,9 @@ sys.path.insert(0, str(ROOT))
 
 VARIANTS = {
     "default": [],
-    "m6": ["-DSSB_STEP_MINB=6"],
-    "m4st3": ["-DSSB_STEP_MINB=4", "-DSSB_TMA_STAGES=3"],
+    "m5": ["-DSSB_STEP_MINB=5"],
+    "tst4": ["-DSSB_TMA_MINB=3", "-DSSB_TMA_STAGES=4"],
+    "tst2m5": ["-DSSB_TMA_MINB=5", "-DSSB_TMA_STAGES=2"],
 }
 
 CHILD = r'''
