@@ -242,8 +242,8 @@ def run_b200(args, rank: int, world: int) -> None:
     fp32_meas = _fp32_peak()
     if fp32_meas:
         fp32_peak_tf = fp32_meas["tflops"]
-        peak_source = (f"measured: FFMA microbenchmark tools/fp32_peak.cu ({fp32_meas['form']} form, best of "
-                       f"register/immediate operand) on this GPU; nominal {fp32_nominal_tf:.1f} TFLOP/s = "
+        peak_source = (f"measured: FP32 microbenchmark tools/fp32_peak.cu (best of FFMA register / immediate / "
+                       f"packed FFMA2: {fp32_meas['form']}) on this GPU; nominal {fp32_nominal_tf:.1f} TFLOP/s = "
                        f"{sms} SMs x 128 lanes x 2 x {sm_mhz:.0f} MHz")
     else:
         fp32_peak_tf = fp32_nominal_tf
@@ -340,14 +340,15 @@ def _fp32_peak():
     lib = ctypes.CDLL(str(so))
     lib.fp32_peak_tflops.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
     res = {}
-    for imm in (0, 1):
+    for imm, key in ((0, "reg"), (1, "imm"), (2, "ffma2")):
         tf, ms = ctypes.c_double(), ctypes.c_double()
         if lib.fp32_peak_tflops(imm, ctypes.byref(tf), ctypes.byref(ms)) == 0:
-            res["imm" if imm else "reg"] = tf.value
+            res[key] = tf.value
     if not res:
         return None
     form = max(res, key=res.get)
-    return {"tflops": res[form], "form": "immediate" if form == "imm" else "register", **res}
+    names = {"reg": "register-operand FFMA", "imm": "immediate-operand FFMA", "ffma2": "packed FFMA2"}
+    return {"tflops": res[form], "form": names[form], **res}
 
 
 def _peaks() -> dict:

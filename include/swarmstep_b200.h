@@ -212,6 +212,16 @@ int swarmstep_quad_circle_setpoints(const swarmstep_group_view *g, const int64_t
 /* *tick_dev += delta (one thread; graph-capturable tick counter). */
 int swarmstep_tick_add(int64_t *tick_dev, int64_t delta, void *stream);
 
+/* ---- device snapshot packing ----------------------------- */
+
+/* One group's SnapshotMsg section body (wire.py:162-178, PROTOCOL.md
+ * "Snapshot (0x01)"): u64*n agent_ids | u8*n alive | f32*3n pos | f32*3n vel |
+ * f32*4n quat (canonical, w >= 0) | f32*3n omega, little-endian, into `out`
+ * (device, 8-byte aligned, 61*n bytes).  agent_ids: device uint64[n].
+ * Bytes equal encode_snapshot of the group's float64 host mirror. */
+int swarmstep_quad_pack_wire(const swarmstep_group_view *g, const uint64_t *agent_ids, uint8_t *out,
+                             void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -38,7 +38,7 @@ EXPORTS = (
     "swarmstep_quad_mark_dead", "swarmstep_quad_retarget_waypoint",
     "swarmstep_quad_pack_f64", "swarmstep_quad_unpack_f64",
     "swarmstep_pack_positions", "swarmstep_neighbor_workspace_bytes", "swarmstep_neighbor_overlay",
-    "swarmstep_quad_circle_setpoints", "swarmstep_tick_add",
+    "swarmstep_quad_circle_setpoints", "swarmstep_tick_add", "swarmstep_quad_pack_wire",
 )
 
 
@@ -91,6 +91,8 @@ def _declare(lib) -> None:
     lib.swarmstep_neighbor_overlay.argtypes = [view, vp, i64, i64, f32, f32, f32, i32, vp, ctypes.c_uint64, vp]
     lib.swarmstep_quad_circle_setpoints.restype = i32
     lib.swarmstep_quad_circle_setpoints.argtypes = [view, vp, i64, f64, f64, f64, f64, f64, f64, vp]
+    lib.swarmstep_quad_pack_wire.restype = i32
+    lib.swarmstep_quad_pack_wire.argtypes = [view, vp, vp, vp]
     lib.swarmstep_tick_add.restype = i32
     lib.swarmstep_tick_add.argtypes = [vp, i64, vp]
 

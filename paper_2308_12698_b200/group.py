@@ -100,6 +100,7 @@ class B200QuadGroup:
             alive=np.array(batch.alive, dtype=bool).reshape(n),
         )
         self._row = {int(a): i for i, a in enumerate(self._batch.agent_ids)}
+        self._ids_dev = None             # device copy of agent_ids (wire packing), on demand
         self._alive = self._batch.alive  # exact: changes only via mark_dead / faults
         self._state_stale = False        # device state newer than the host mirror
         # command store (core.py:98-104): position hold at the initial pose
@@ -397,6 +398,20 @@ class B200QuadGroup:
 
     def snapshot(self, tick: int):
         return batch_snapshot(self.batch, tick)
+
+    def wire_section(self) -> bytes:
+        """This group's SnapshotMsg section (wire.py:162-178), packed on the device:
+        u16 type_id, u32 n, then 61*n bytes of columns."""
+        import struct
+        n = self.n
+        with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
+            if self._ids_dev is None:
+                self._ids_dev = torch.from_numpy(self._batch.agent_ids.view(np.int64).copy()).to(self.device)
+            buf = torch.empty(61 * n + 8, dtype=torch.uint8, device=self.device)
+            self._call(self._lib.swarmstep_quad_pack_wire, _ptr(self._ids_dev), _ptr(buf),
+                       ctypes.c_void_p(self.stream.cuda_stream))
+            host = buf[:61 * n].cpu().numpy().tobytes()
+        return struct.pack("<HI", self._batch.type_id, n) + host
 
     # ------------------------------------------------------------ stepping
     def _any_pos_rows(self) -> bool:
