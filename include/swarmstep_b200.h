@@ -222,6 +222,40 @@ int swarmstep_tick_add(int64_t *tick_dev, int64_t delta, void *stream);
 int swarmstep_quad_pack_wire(const swarmstep_group_view *g, const uint64_t *agent_ids, uint8_t *out,
                              void *stream);
 
+/* ---- GPU collision / neighbour detection ----------------- */
+
+/* Gathers a group's rows as float64 (x, y, z, r) into xyzr[offset + row]
+ * (r = NaN for dead rows, which the detector skips); position is hi + lo. */
+int swarmstep_pack_collision(const swarmstep_group_view *g, double radius, double *xyzr, int64_t offset,
+                             void *stream);
+
+/* Device workspace for swarmstep_collision_pairs over m gathered agents. */
+int swarmstep_collision_workspace_bytes(int64_t m, uint64_t *bytes);
+
+/* detect() (collision.py:110-176) over m gathered agents: grid cells of size
+ * `cell`, candidate pairs = same-cell pairs (i < j) + the half-space cell
+ * offsets given (int[3 * n_off], device; collision.py:86-95), narrow phase in
+ * float64 with the reference's operation order.  Colliding pairs
+ * (d2 < (r_i + r_j)^2) go to coll[2k], coll[2k+1] and neighbour pairs
+ * (d2 < r_sense^2) to near[...] as gathered indices (i, j); counts_dev[0],
+ * counts_dev[1] receive the pair counts (all pairs are counted, only the
+ * first *_cap stored; with fill == 0 nothing is stored) and counts_dev[2] is
+ * non-zero if a cell coordinate left (-2^20, 2^20). */
+int swarmstep_collision_pairs(const double *xyzr, int64_t m, double cell, const int *offsets_dev, int n_off,
+                              double r_sense, uint32_t *coll, uint64_t coll_cap, uint32_t *near,
+                              uint64_t near_cap, uint64_t *counts_dev, void *workspace, uint64_t ws_bytes,
+                              int fill, void *stream);
+
+/* ---- unicycle group -------------------------------------- */
+
+/* k_substeps ticks of unicycle_step (core.py:221-246) for every alive row:
+ * (v, w) = clip(cmd cols 0, 1) (+ overlay projected on the heading on tick 0
+ * with SWARMSTEP_STEP_OVERLAY, core.py:277-283); exact-arc xy update, yaw
+ * quaternion, vel = v (cos th1, sin th1, 0), omega_z = w.  Layout as the quad
+ * group (tiled SoA, COL_CMD + 0 / + 1 hold v / w). */
+int swarmstep_unicycle_step(const swarmstep_group_view *g, float v_max, float omega_max, float dt,
+                            int k_substeps, int launch_flags, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

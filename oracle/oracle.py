@@ -295,6 +295,109 @@ class OracleGroup:
         return np.hstack([self.pos, self.vel, self.quat, self.omega])
 
 
+def unicycle_step(pos, vel, quat, omega, alive, cmd, v_max, omega_max, dt):
+    """float64 restatement of unicycle_step (core.py:221-246), in place."""
+    alive = np.asarray(alive, dtype=bool)
+    v = np.clip(cmd[:, 0], -v_max, v_max)
+    w = np.clip(cmd[:, 1], -omega_max, omega_max)
+    theta0 = quat_yaw(quat)
+    theta1 = theta0 + w * dt
+    straight = np.abs(w) <= 1e-9
+    w_safe = np.where(straight, 1.0, w)
+    dx = np.where(straight, v * np.cos(theta0) * dt, v / w_safe * (np.sin(theta1) - np.sin(theta0)))
+    dy = np.where(straight, v * np.sin(theta0) * dt, -v / w_safe * (np.cos(theta1) - np.cos(theta0)))
+    pos[alive, 0] += dx[alive]
+    pos[alive, 1] += dy[alive]
+    yq = np.zeros((theta1.shape[0], 4))
+    yq[:, 0], yq[:, 3] = np.cos(0.5 * theta1), np.sin(0.5 * theta1)
+    quat[alive] = yq[alive]
+    vel[alive, 0] = (v * np.cos(theta1))[alive]
+    vel[alive, 1] = (v * np.sin(theta1))[alive]
+    vel[alive, 2] = 0.0
+    omega[alive, 2] = w[alive]
+
+
+class OracleUnicycleGroup:
+    """float64 twin of UnicycleGroup (core.py:249-289)."""
+
+    kind = "unicycle"
+
+    def __init__(self, type_id, batch, v_max=5.0, omega_max=3.0):
+        n = int(np.asarray(batch.agent_ids).shape[0])
+        self.type_id, self.n = type_id, n
+        self.v_max, self.omega_max = v_max, omega_max
+        self.agent_ids = np.array(batch.agent_ids, dtype=np.uint64)
+        self.pos = np.array(batch.pos, dtype=float).reshape(n, 3).copy()
+        self.vel = np.array(batch.vel, dtype=float).reshape(n, 3).copy()
+        self.quat = np.array(batch.quat, dtype=float).reshape(n, 4).copy()
+        self.omega = np.array(batch.omega, dtype=float).reshape(n, 3).copy()
+        self.alive = np.array(batch.alive, dtype=bool).reshape(n).copy()
+        self.cmd = np.zeros((n, 2))
+        self.v_overlay = np.zeros((n, 3))
+        self.overlay_active = False
+        self._row = {int(a): i for i, a in enumerate(self.agent_ids)}
+
+    def apply_command(self, cmd) -> bool:
+        row = self._row.get(int(cmd.agent_id))
+        if row is None or not self.alive[row] or getattr(cmd.level, "value", cmd.level) != "unicycle":
+            return False
+        self.cmd[row] = cmd.values
+        return True
+
+    def add_velocity_overlay(self, offsets):
+        self.v_overlay += offsets
+        self.overlay_active = True
+
+    def retarget_waypoint(self, point, radius):
+        pass
+
+    def mark_dead(self, agent_ids):
+        killed = []
+        for aid in agent_ids:
+            row = self._row.get(int(aid))
+            if row is not None and self.alive[row]:
+                self.alive[row] = False
+                killed.append(int(aid))
+        return killed
+
+    def step(self, dt):
+        cmd = self.cmd
+        if self.overlay_active:
+            heading = quat_yaw(self.quat)
+            along = self.v_overlay[:, 0] * np.cos(heading) + self.v_overlay[:, 1] * np.sin(heading)
+            cmd = cmd.copy()
+            cmd[:, 0] += along
+            self.v_overlay[:] = 0.0
+            self.overlay_active = False
+        unicycle_step(self.pos, self.vel, self.quat, self.omega, self.alive, cmd, self.v_max, self.omega_max, dt)
+        return np.empty(0, dtype=np.uint64)
+
+
+def collide_all_pairs(ids, pos, radii, alive, r_sense: float):
+    """All-pairs float64 collision / neighbour oracle (tests/oracles.py:79-102 and
+    test_acceptance.py:141-156 restated): (sorted colliding id pairs, dict id ->
+    sorted tuple of neighbour ids) over alive agents, strict inequalities."""
+    ids, pos, radii, alive = (np.asarray(ids, dtype=np.int64), np.asarray(pos, dtype=float),
+                              np.asarray(radii, dtype=float), np.asarray(alive, dtype=bool))
+    ids, pos, radii = ids[alive], pos[alive], radii[alive]
+    n = ids.shape[0]
+    nbrs = {int(i): [] for i in ids}
+    pairs = []
+    if n >= 2:
+        diff = pos[:, None, :] - pos[None, :, :]
+        d2 = np.sum(diff * diff, axis=2)
+        iu, ju = np.triu_indices(n, k=1)
+        rsum = radii[iu] + radii[ju]
+        hit = d2[iu, ju] < rsum * rsum
+        for a, b in zip(iu[hit], ju[hit]):
+            pairs.append((min(int(ids[a]), int(ids[b])), max(int(ids[a]), int(ids[b]))))
+        near = d2[iu, ju] < r_sense * r_sense
+        for a, b in zip(iu[near], ju[near]):
+            nbrs[int(ids[a])].append(int(ids[b]))
+            nbrs[int(ids[b])].append(int(ids[a]))
+    return sorted(pairs), {k: tuple(sorted(v)) for k, v in nbrs.items()}
+
+
 def neighbor_overlay(pos, alive, r_sense: float, k_sep: float, rows=None, chunk: int = 2048) -> np.ndarray:
     """All-pairs float64 separation overlay (SURVEY 8(e) controller; the
     wire.py:320-340 repel field applied per neighbour, strict < of

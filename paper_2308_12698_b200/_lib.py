@@ -39,6 +39,8 @@ EXPORTS = (
     "swarmstep_quad_pack_f64", "swarmstep_quad_unpack_f64",
     "swarmstep_pack_positions", "swarmstep_neighbor_workspace_bytes", "swarmstep_neighbor_overlay",
     "swarmstep_quad_circle_setpoints", "swarmstep_tick_add", "swarmstep_quad_pack_wire",
+    "swarmstep_pack_collision", "swarmstep_collision_workspace_bytes", "swarmstep_collision_pairs",
+    "swarmstep_unicycle_step",
 )
 
 
@@ -93,6 +95,15 @@ def _declare(lib) -> None:
     lib.swarmstep_quad_circle_setpoints.argtypes = [view, vp, i64, f64, f64, f64, f64, f64, f64, vp]
     lib.swarmstep_quad_pack_wire.restype = i32
     lib.swarmstep_quad_pack_wire.argtypes = [view, vp, vp, vp]
+    lib.swarmstep_pack_collision.restype = i32
+    lib.swarmstep_pack_collision.argtypes = [view, f64, vp, i64, vp]
+    lib.swarmstep_collision_workspace_bytes.restype = i32
+    lib.swarmstep_collision_workspace_bytes.argtypes = [i64, ctypes.POINTER(ctypes.c_uint64)]
+    lib.swarmstep_collision_pairs.restype = i32
+    lib.swarmstep_collision_pairs.argtypes = [vp, i64, f64, vp, i32, f64, vp, ctypes.c_uint64, vp, ctypes.c_uint64,
+                                              vp, vp, ctypes.c_uint64, i32, vp]
+    lib.swarmstep_unicycle_step.restype = i32
+    lib.swarmstep_unicycle_step.argtypes = [view, f32, f32, f32, i32, i32, vp]
     lib.swarmstep_tick_add.restype = i32
     lib.swarmstep_tick_add.argtypes = [vp, i64, vp]
 

@@ -1,0 +1,149 @@
+"""GPU sphere-collision and neighbour detection over device-resident groups
+(the reference's collision.py).
+
+``detect(groups, config, tick)`` returns the reference's ``CollisionReport``
+(collision.py:49-56) for the alive agents of the given B200 groups: all
+colliding pairs (``|p_a - p_b| < r_a + r_b``, strict, cross-type included)
+and per-agent neighbour sets (strictly within ``r_sense``).  The grid broad
+phase and the float64 narrow phase run on the GPU (csrc/collision.cu) with
+the reference's arithmetic, so on the same float64 positions the report is
+identical to ``swarmstep.collision.detect``; the host only sorts the pair
+lists as collision.py:160-175 does.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+from typing import Mapping
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import ValidationError
+
+
+@dataclass(frozen=True)
+class CollisionConfig:
+    """Per-type collision radii, one sensing radius, and the grid cell size (collision.py:30-46)."""
+
+    r_collide: Mapping[int, float]
+    r_sense: float
+    cell: float
+
+    def __post_init__(self):
+        if not self.r_collide:
+            raise ValidationError("r_collide must name at least one agent type")
+        rmax = max(self.r_collide.values())
+        for tid, r in self.r_collide.items():
+            if not 0.0 < r <= self.r_sense:
+                raise ValidationError(f"type {tid}: need 0 < r_collide <= r_sense, got {r}")
+        if self.cell < 2.0 * rmax:
+            raise ValidationError(f"cell size {self.cell} must be >= 2 * max collision radius {2 * rmax}")
+
+
+@dataclass(frozen=True)
+class CollisionReport:
+    """Tick-tagged collision pairs and neighbour sets over alive agents (collision.py:49-56)."""
+
+    tick: int
+    collisions: tuple = ()
+    neighbor_sets: dict = field(default_factory=dict)
+    dropped: int = 0
+
+
+def half_space_offsets(d_max: int, reach: float, cell: float) -> np.ndarray:
+    """Cell offsets o > (0,0,0) lexicographically whose closest corners can be
+    within ``reach`` (collision.py:86-95)."""
+    rng = np.arange(-d_max, d_max + 1)
+    grid = np.stack(np.meshgrid(rng, rng, rng, indexing="ij"), axis=-1).reshape(-1, 3)
+    k0, k1, k2 = grid[:, 0], grid[:, 1], grid[:, 2]
+    lex_positive = (k0 > 0) | ((k0 == 0) & ((k1 > 0) | ((k1 == 0) & (k2 > 0))))
+    min_sep = np.maximum(np.abs(grid) - 1, 0) * cell
+    reachable = np.sum(min_sep * min_sep, axis=1) < reach * reach
+    return grid[lex_positive & reachable]
+
+
+class GpuDetector:
+    """Reusable device buffers for ``detect`` on one device."""
+
+    def __init__(self, config: CollisionConfig, device=None):
+        self.config = config
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self._lib = _lib.load()
+        self._counts = torch.zeros(4, dtype=torch.int64, device=self.device)
+
+    def detect(self, groups, tick: int, dropped: int = 0) -> CollisionReport:
+        cfg = self.config
+        groups = sorted(groups, key=lambda g: g.type_id)
+        for g in groups:
+            if g.type_id not in cfg.r_collide:
+                raise ValidationError(f"no collision radius configured for type {g.type_id}")
+            if g.device != self.device:
+                raise ValidationError("all groups must live on the detector's device")
+        alive = [g.batch.alive for g in groups]
+        ids_all = np.concatenate([g.batch.agent_ids.astype(np.int64) for g in groups]) if groups else np.empty(0, np.int64)
+        alive_all = np.concatenate(alive) if groups else np.empty(0, bool)
+        neighbor_sets = {int(i): () for i in ids_all[alive_all]}
+        if int(alive_all.sum()) < 2:
+            return CollisionReport(tick=tick, collisions=(), neighbor_sets=neighbor_sets, dropped=dropped)
+        rmax = max(cfg.r_collide[g.type_id] for g, a in zip(groups, alive) if a.any())
+        reach = max(cfg.r_sense, 2.0 * float(rmax))
+        d_max = int(math.ceil(reach / cfg.cell))
+        offs = half_space_offsets(d_max, reach, cfg.cell).astype(np.int32)
+        m = int(ids_all.shape[0])
+        stream = torch.cuda.current_stream(self.device)
+        with torch.cuda.device(self.device):
+            xyzr = torch.empty((m, 4), dtype=torch.float64, device=self.device)
+            off = 0
+            for g in groups:
+                g.stream.synchronize()   # positions of the group's last step
+                _lib.check(self._lib.swarmstep_pack_collision(g._view_ref, float(cfg.r_collide[g.type_id]),
+                                                              xyzr.data_ptr(), off, ctypes.c_void_p(stream.cuda_stream)))
+                off += g.n
+            nbytes = ctypes.c_uint64()
+            _lib.check(self._lib.swarmstep_collision_workspace_bytes(m, ctypes.byref(nbytes)))
+            ws = torch.empty(int(nbytes.value), dtype=torch.uint8, device=self.device)
+            offs_d = torch.from_numpy(offs.reshape(-1)).to(self.device) if offs.size else torch.zeros(3, dtype=torch.int32, device=self.device)
+
+            def run(coll, cc, near, nc, fill):
+                _lib.check(self._lib.swarmstep_collision_pairs(
+                    xyzr.data_ptr(), m, float(cfg.cell), offs_d.data_ptr(), int(offs.shape[0]), float(cfg.r_sense),
+                    coll, cc, near, nc, self._counts.data_ptr(), ws.data_ptr(), nbytes.value, fill,
+                    ctypes.c_void_p(stream.cuda_stream)))
+                return self._counts.cpu().numpy()
+
+            counts = run(None, 0, None, 0, 0)
+            if counts[2]:
+                raise ValidationError("world extent exceeds the supported grid range")
+            n_coll, n_near = int(counts[0]), int(counts[1])
+            coll = torch.empty(max(2 * n_coll, 2), dtype=torch.int32, device=self.device)
+            near = torch.empty(max(2 * n_near, 2), dtype=torch.int32, device=self.device)
+            if n_coll or n_near:
+                run(coll.data_ptr(), n_coll, near.data_ptr(), n_near, 1)
+            coll_h = coll[:2 * n_coll].cpu().numpy().astype(np.int64).reshape(-1, 2)
+            near_h = near[:2 * n_near].cpu().numpy().astype(np.int64).reshape(-1, 2)
+        # host post-processing exactly as collision.py:160-175
+        src, dst = coll_h[:, 0], coll_h[:, 1]
+        ids_a = np.minimum(ids_all[src], ids_all[dst])
+        ids_b = np.maximum(ids_all[src], ids_all[dst])
+        order = np.lexsort((ids_b, ids_a))
+        collisions = tuple(zip(ids_a[order].tolist(), ids_b[order].tolist()))
+        na = np.concatenate([near_h[:, 0], near_h[:, 1]])
+        nb = np.concatenate([near_h[:, 1], near_h[:, 0]])
+        if na.size:
+            order = np.lexsort((ids_all[nb], ids_all[na]))
+            na, nb = na[order], nb[order]
+            bounds = np.nonzero(np.diff(na))[0] + 1
+            for chunk_a, chunk_b in zip(np.split(na, bounds), np.split(nb, bounds)):
+                neighbor_sets[int(ids_all[chunk_a[0]])] = tuple(ids_all[chunk_b].tolist())
+        return CollisionReport(tick=tick, collisions=collisions, neighbor_sets=neighbor_sets, dropped=dropped)
+
+
+def detect(groups, config: CollisionConfig, tick: int, dropped: int = 0) -> CollisionReport:
+    """One-shot detection over B200 groups (see GpuDetector)."""
+    groups = list(groups)
+    dev = groups[0].device if groups else None
+    return GpuDetector(config, dev).detect(groups, tick, dropped)

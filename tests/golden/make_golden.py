@@ -177,7 +177,74 @@ def gen_functions() -> None:
     print("functions: deriv/rk4/mix/pid/outer written")
 
 
+def gen_collision() -> None:
+    """detect() (collision.py:110-176) on random two-type worlds; positions are
+    multiples of 2^-10 so they are exact in float32 (the B200 groups hold them
+    bit-exactly and the comparison can be exact)."""
+    from swarmstep.collision import CollisionConfig, detect
+    from swarmstep.state import WorldSnapshot, batch_snapshot
+    rng = np.random.default_rng(77)
+    out = {}
+    worlds = 24
+    for w in range(worlds):
+        n0, n1 = int(rng.integers(1, 300)), int(rng.integers(0, 60))
+        box = float(rng.uniform(3, 15))
+        r0, r1 = float(rng.uniform(0.05, 0.4)), float(rng.uniform(0.05, 0.4))
+        r_sense = float(rng.uniform(2 * max(r0, r1), 3.0))
+        cell = float(rng.uniform(2 * max(r0, r1), 2.5))
+        q = lambda a: np.round(a * 1024.0) / 1024.0
+        p0, p1 = q(rng.uniform(-box, box, (n0, 3))), q(rng.uniform(-box, box, (n1, 3)))
+        a0, a1 = rng.random(n0) > 0.1, rng.random(n1) > 0.1
+        batches = []
+        b0 = batch_create(0, n0, p0)
+        b0.alive[:] = a0
+        batches.append(batch_snapshot(b0, w))
+        if n1:
+            b1 = batch_create(1, n1, p1, id_base=n0)
+            b1.alive[:] = a1
+            batches.append(batch_snapshot(b1, w))
+        cfg = CollisionConfig(r_collide={0: r0, 1: r1}, r_sense=r_sense, cell=cell)
+        rep = detect(WorldSnapshot(tick=w, batches=tuple(batches)), cfg)
+        pre = f"w{w}_"
+        out[pre + "p0"], out[pre + "p1"], out[pre + "a0"], out[pre + "a1"] = p0, p1.reshape(-1, 3), a0, a1
+        out[pre + "cfg"] = np.array([r0, r1, r_sense, cell])
+        out[pre + "coll"] = np.array(rep.collisions, dtype=np.int64).reshape(-1, 2)
+        keys = sorted(rep.neighbor_sets)
+        out[pre + "nb_keys"] = np.array(keys, dtype=np.int64)
+        out[pre + "nb_len"] = np.array([len(rep.neighbor_sets[k]) for k in keys], dtype=np.int64)
+        out[pre + "nb_ids"] = np.array([i for k in keys for i in rep.neighbor_sets[k]], dtype=np.int64)
+    out["worlds"] = np.array(worlds)
+    np.savez_compressed(HERE / "collision.npz", **out)
+    print(f"collision: {worlds} worlds")
+
+
+def gen_unicycle() -> None:
+    from swarmstep.core import UnicycleGroup, UnicycleParams
+    sc = scenarios.unicycles()
+    batch = batch_create(1, sc.n, sc.pos, quat=sc.quat, vel=sc.vel, omega=sc.omega)
+    init = dict(pos=batch.pos.copy(), vel=batch.vel.copy(), quat=batch.quat.copy(), omega=batch.omega.copy())
+    group = UnicycleGroup(1, batch, UnicycleParams())
+
+    def state(g):
+        b = g.batch
+        return dict(pos=b.pos.copy(), vel=b.vel.copy(), quat=b.quat.copy(), omega=b.omega.copy(),
+                    alive=b.alive.copy(), cmd=g.cmd.copy())
+
+    records, cmd_ok, faults = scenarios.run_script(group, sc, make_cmd, state)
+    out = sc.to_arrays()
+    out.update(init)
+    ticks = sorted(records)
+    out["rec_ticks"] = np.array(ticks, dtype=np.int64)
+    for key in records[ticks[0]]:
+        out[f"rec_{key}"] = np.stack([records[t][key] for t in ticks])
+    out["cmd_ok"] = cmd_ok
+    np.savez_compressed(HERE / "scenario_unicycles.npz", **out)
+    print(f"unicycles: n={sc.n} ticks={sc.ticks}")
+
+
 if __name__ == "__main__":
+    gen_unicycle()
+    gen_collision()
     gen_functions()
     for name in scenarios.ALL:
         gen_scenario(name)

@@ -231,5 +231,35 @@ def crash_nan(n=8, ticks=10):
     return sc
 
 
+def unicycles(n=40, ticks=150, seed=9):
+    """UnicycleGroup (core.py:249-289): commands incl. clamped speeds / turn
+    rates and straight lines, a death, an overlay tick."""
+    rng = np.random.default_rng(seed)
+    yaw = rng.uniform(-np.pi, np.pi, n)
+    q = np.stack([np.cos(yaw / 2), np.zeros(n), np.zeros(n), np.sin(yaw / 2)], axis=1)
+    sc = Scenario("unicycles", n, 0.01, ticks, _grid(n, 2.0, (0, 0, 0)), np.zeros((n, 3)), q, np.zeros((n, 3)),
+                  record=[0, 1, 10, 49, 50, 51, 100, ticks - 1])
+    cmds = []
+    for i in range(n):
+        k = i % 4
+        if k == 0:
+            cmds.append((0, i, 3, (float(rng.uniform(0, 3)), float(rng.uniform(-1, 1)))))
+        elif k == 1:
+            cmds.append((0, i, 3, (9.0, -7.0)))                    # both clamped
+        elif k == 2:
+            cmds.append((0, i, 3, (1.5, 0.0)))                     # straight line
+        else:
+            cmds.append((0, i, 3, (-0.7, 2.0)))
+            cmds.append((60, i, 3, (0.4, -0.3)))
+    cmds.append((5, 2, 0, (0.0,) * 7))                              # non-unicycle level -> rejected
+    cmds.sort(key=lambda c: c[0])
+    sc.cmds = cmds
+    sc.deaths = [(30, [5])]
+    ov = np.zeros((n, 3))
+    ov[::3] = rng.uniform(-1, 1, (len(ov[::3]), 3))
+    sc.overlays = [(50, ov)]
+    return sc
+
+
 ALL = {"hover_rate": hover_rate, "pos_random": pos_random, "mixed": mixed,
        "fault_nan": fault_nan, "crash_nan": crash_nan}
