@@ -131,6 +131,7 @@ int swarmstep_device_info(int *sm_count, int *cc_major, int *cc_minor);
 #define SWARMSTEP_STEP_MOTOR         0x2  /* some row may be at MOTOR level               */
 #define SWARMSTEP_STEP_FORCE_DIRECT  0x4  /* tuning: force the direct-load kernel         */
 #define SWARMSTEP_STEP_FORCE_TMA     0x8  /* tuning: force the TMA-staged kernel          */
+#define SWARMSTEP_STEP_FORCE_PAIR    0x10 /* tuning: force the paired FFMA2 kernel        */
 int swarmstep_quad_step(const swarmstep_group_view *g, const swarmstep_quad_params *p,
                         float dt, int k_substeps, int launch_flags, uint32_t tick_base,
                         const int64_t *tick_dev, void *stream);

@@ -29,7 +29,7 @@ NCOL = 36
 TILE = 128   # agents per tile of the tiled SoA layout (SWARMSTEP_TILE)
 FLAG_ALIVE, FLAG_HAS_PREV, LEVEL_SHIFT, LEVEL_MASK = 0x01, 0x02, 2, 0x0C
 # swarmstep_quad_step launch flags (SWARMSTEP_STEP_*)
-STEP_OVERLAY, STEP_MOTOR, STEP_FORCE_DIRECT, STEP_FORCE_TMA = 0x1, 0x2, 0x4, 0x8
+STEP_OVERLAY, STEP_MOTOR, STEP_FORCE_DIRECT, STEP_FORCE_TMA, STEP_FORCE_PAIR = 0x1, 0x2, 0x4, 0x8, 0x10
 
 # every symbol include/swarmstep_b200.h declares
 EXPORTS = (

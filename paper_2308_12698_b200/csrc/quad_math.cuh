@@ -1,24 +1,30 @@
 // quad_math.cuh -- per-agent float32 device math for the quadrotor hot path.
 //
 // Each function restates one piece of the reference's batched numpy path for
-// a single agent held in registers:
-//   deriv / rk4_row  quad.py:222-310, 350-437  (_deriv_kernel, rk4_step)
-//   mix_row          quad.py:143-168           (mix_to_motors)
-//   motor_wrench     quad.py:130-140 + core.py:189-197
-//   pid_row          control.py:136-187        (rate_pid_step)
-//   outer_row        control.py:190-294        (position_outer_loop, _rotmats_to_quats)
+// agents held in registers:
+//   deriv / rk4_inplace  quad.py:222-310, 350-437  (_deriv_kernel, rk4_step)
+//   mix_row              quad.py:143-168           (mix_to_motors)
+//   motor_wrench         quad.py:130-140 + core.py:189-197
+//   pid_row              control.py:136-187        (rate_pid_step)
+//   outer_row            control.py:190-294        (position_outer_loop, _rotmats_to_quats)
+//
+// Every function is a template over the lane type T: `float` (one agent) or
+// `f2` (two agents in the two halves of Blackwell's packed FP32x2 registers,
+// so FFMA2 / FADD2 / FMUL2 do two agents' arithmetic per issued instruction).
+// All arithmetic goes through explicitly rounded operations (no compiler
+// contraction), so an agent's result is bit-identical whichever lane type
+// computed it -- rows stay independent of their neighbours.
 //
 // Numerics (float32 against the float64 reference, target <= 1e-5 relative
 // per step):
-//  * clamps are compare-selects so NaN propagates like np.clip;
 //  * the mixer returns the requested wrench unchanged for unsaturated rows
 //    (G G^-1 w == w in R; a float32 round trip would inject |f_c| eps32 of
 //    torque error -- SURVEY.md Appendix B);
-//  * position can be carried as an unevaluated sum hi + lo (TwoSum update) so
-//    the reference's sub-ulp increments at |p| ~ 100 m are kept;
+//  * position can be carried as an unevaluated sum hi + lo (Fast2Sum) so the
+//    reference's sub-ulp increments at |p| ~ 100 m are kept;
 //  * sqrt / 1/x / 1/sqrt use the SFU (MUFU) approximations (<= 2 ulp) and
 //    atan2 a degree-8 minimax polynomial (9e-8 relative): all well inside the
-//    1e-5 budget, and branch-free of the IEEE slow paths.
+//    1e-5 budget, and free of the IEEE slow paths.
 #pragma once
 #include <cuda_runtime.h>
 #include <math.h>
@@ -26,38 +32,110 @@
 
 namespace ssb {
 
-__device__ __forceinline__ float clip(float x, float lo, float hi)
-{
-    // np.clip semantics: NaN passes through
-    return x < lo ? lo : (x > hi ? hi : x);
-}
+// ---------------------------------------------------------------------------
+// lane types
+// ---------------------------------------------------------------------------
+struct f2 {
+    float2 v;
+};
+struct m2 {
+    bool x, y;
+};
 
-__device__ __forceinline__ float rsqrt_a(float x)
+template <class T> struct LaneMask;
+template <> struct LaneMask<float> { using type = bool; };
+template <> struct LaneMask<f2> { using type = m2; };
+template <class T> using mask_t = typename LaneMask<T>::type;
+
+template <class T> __device__ __forceinline__ T bc(float a);
+template <> __device__ __forceinline__ float bc<float>(float a) { return a; }
+template <> __device__ __forceinline__ f2 bc<f2>(float a) { return f2{make_float2(a, a)}; }
+
+__device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float fma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ float fnma(float a, float b, float c) { return __fmaf_rn(-a, b, c); }  // c - a b
+__device__ __forceinline__ float neg(float a) { return -a; }
+
+__device__ __forceinline__ f2 add(f2 a, f2 b) { return f2{__fadd2_rn(a.v, b.v)}; }
+__device__ __forceinline__ f2 sub(f2 a, f2 b) { return f2{__fadd2_rn(a.v, make_float2(-b.v.x, -b.v.y))}; }
+__device__ __forceinline__ f2 mul(f2 a, f2 b) { return f2{__fmul2_rn(a.v, b.v)}; }
+__device__ __forceinline__ f2 fma(f2 a, f2 b, f2 c) { return f2{__ffma2_rn(a.v, b.v, c.v)}; }
+__device__ __forceinline__ f2 fnma(f2 a, f2 b, f2 c) { return f2{__ffma2_rn(make_float2(-a.v.x, -a.v.y), b.v, c.v)}; }
+__device__ __forceinline__ f2 neg(f2 a) { return f2{make_float2(-a.v.x, -a.v.y)}; }
+
+// per-lane helpers
+template <class F> __device__ __forceinline__ float lane1(float a, F f) { return f(a); }
+template <class F> __device__ __forceinline__ f2 lane1(f2 a, F f) { return f2{make_float2(f(a.v.x), f(a.v.y))}; }
+
+__device__ __forceinline__ float rsqrt1(float x)
 {
     float y;
     asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
-
-__device__ __forceinline__ float sqrt_a(float x)
+__device__ __forceinline__ float sqrt1(float x)
 {
     float y;
     asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
-
-__device__ __forceinline__ float rcp_a(float x)
+__device__ __forceinline__ float rcp1(float x)
 {
     float y;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+template <class T> __device__ __forceinline__ T rsqrt_a(T x) { return lane1(x, rsqrt1); }
+template <class T> __device__ __forceinline__ T sqrt_a(T x) { return lane1(x, sqrt1); }
+template <class T> __device__ __forceinline__ T rcp_a(T x) { return lane1(x, rcp1); }
 
-// Per-tick constants derived from the per-type struct (hoisted out of the
-// substep loop by the caller).
+__device__ __forceinline__ float vmin(float a, float b) { return fminf(a, b); }
+__device__ __forceinline__ float vmax(float a, float b) { return fmaxf(a, b); }
+__device__ __forceinline__ float vabs(float a) { return fabsf(a); }
+__device__ __forceinline__ f2 vmin(f2 a, f2 b) { return f2{make_float2(fminf(a.v.x, b.v.x), fminf(a.v.y, b.v.y))}; }
+__device__ __forceinline__ f2 vmax(f2 a, f2 b) { return f2{make_float2(fmaxf(a.v.x, b.v.x), fmaxf(a.v.y, b.v.y))}; }
+__device__ __forceinline__ f2 vabs(f2 a) { return f2{make_float2(fabsf(a.v.x), fabsf(a.v.y))}; }
+
+__device__ __forceinline__ bool lt(float a, float b) { return a < b; }
+__device__ __forceinline__ bool gt(float a, float b) { return a > b; }
+__device__ __forceinline__ bool ge(float a, float b) { return a >= b; }
+__device__ __forceinline__ bool le(float a, float b) { return a <= b; }
+__device__ __forceinline__ bool eq(float a, float b) { return a == b; }
+__device__ __forceinline__ m2 lt(f2 a, f2 b) { return m2{a.v.x < b.v.x, a.v.y < b.v.y}; }
+__device__ __forceinline__ m2 gt(f2 a, f2 b) { return m2{a.v.x > b.v.x, a.v.y > b.v.y}; }
+__device__ __forceinline__ m2 ge(f2 a, f2 b) { return m2{a.v.x >= b.v.x, a.v.y >= b.v.y}; }
+__device__ __forceinline__ m2 le(f2 a, f2 b) { return m2{a.v.x <= b.v.x, a.v.y <= b.v.y}; }
+__device__ __forceinline__ m2 eq(f2 a, f2 b) { return m2{a.v.x == b.v.x, a.v.y == b.v.y}; }
+
+__device__ __forceinline__ bool mand(bool a, bool b) { return a && b; }
+__device__ __forceinline__ bool mor(bool a, bool b) { return a || b; }
+__device__ __forceinline__ bool mnot(bool a) { return !a; }
+__device__ __forceinline__ bool any(bool a) { return a; }
+__device__ __forceinline__ m2 mand(m2 a, m2 b) { return m2{a.x && b.x, a.y && b.y}; }
+__device__ __forceinline__ m2 mor(m2 a, m2 b) { return m2{a.x || b.x, a.y || b.y}; }
+__device__ __forceinline__ m2 mnot(m2 a) { return m2{!a.x, !a.y}; }
+__device__ __forceinline__ bool any(m2 a) { return a.x || a.y; }
+
+__device__ __forceinline__ float sel(bool m, float a, float b) { return m ? a : b; }
+__device__ __forceinline__ f2 sel(m2 m, f2 a, f2 b) { return f2{make_float2(m.x ? a.v.x : b.v.x, m.y ? a.v.y : b.v.y)}; }
+
+__device__ __forceinline__ float lane(float a, int) { return a; }
+__device__ __forceinline__ float lane(f2 a, int i) { return i ? a.v.y : a.v.x; }
+
+// np.clip semantics: NaN passes through
+template <class T> __device__ __forceinline__ T clip(T x, T lo, T hi)
+{
+    return sel(lt(x, lo), lo, sel(gt(x, hi), hi, x));
+}
+
+// ---------------------------------------------------------------------------
+// Per-tick constants derived from the per-type struct (hoisted by the caller)
+// ---------------------------------------------------------------------------
 struct Derived {
     float g;
-    float gx, gy, gz;        // gyroscopic coefficients (I_zz-I_yy)/I_xx, ...
+    float gx, gy, gz;        // 4 (I_zz - I_yy) / I_xx, ... (products of half rates)
     float kd_dt[3];          // kd / dt
 };
 
@@ -65,7 +143,7 @@ __device__ __forceinline__ Derived derive(const swarmstep_quad_params &P, float 
 {
     Derived d;
     d.g = P.g;
-    d.gx = 4.0f * (P.izz - P.iyy) * P.inv_ixx;   // x4: products of half rates
+    d.gx = 4.0f * (P.izz - P.iyy) * P.inv_ixx;
     d.gy = 4.0f * (P.ixx - P.izz) * P.inv_iyy;
     d.gz = 4.0f * (P.iyy - P.ixx) * P.inv_izz;
 #pragma unroll
@@ -73,52 +151,49 @@ __device__ __forceinline__ Derived derive(const swarmstep_quad_params &P, float 
     return d;
 }
 
-// d/dt of (v, q, w) at (q, w) for a held wrench (quad.py:222-310):
-//   vdot = (f_c/m) R(q) e_z - g e_z ; qdot = q (x) (0, w) / 2 ;
-//   wdot = I^-1 (tau - w x (I w)) = tau/I - (gyro coefficient) w_j w_k.
-// fc2 = 2 f_c / m, fcg = f_c / m - g, tI = tau / I (per axis).
-// h = w / 2 is carried instead of w (saves the halving per stage); the
-// gyroscopic coefficients are pre-multiplied by 4 accordingly.
-__device__ __forceinline__ void deriv(const float q[4], const float h[3], float fc2, float fcg,
-                                      const float tI[3], const Derived &D,
-                                      float dv[3], float dq[4], float dw[3])
+// d/dt of (v, q, w) at (q, h = w/2) for a held wrench (quad.py:222-310):
+//   vdot = (f_c/m) R(q) e_z - g e_z ; qdot = q (x) (0, h) ;
+//   wdot = tau/I - 4 c (h_j h_k)  (gyroscopic term, diagonal inertia).
+// fc2 = 2 f_c / m, fcg = f_c / m - g, tI = tau / I.
+template <class T>
+__device__ __forceinline__ void deriv(const T q[4], const T h[3], T fc2, T fcg, const T tI[3], const Derived &D,
+                                      T dv[3], T dq[4], T dw[3])
 {
-    const float qw = q[0], qx = q[1], qy = q[2], qz = q[3];
-    const float hx = h[0], hy = h[1], hz = h[2];
-    dv[0] = fc2 * fmaf(qx, qz, qw * qy);
-    dv[1] = fc2 * fmaf(qy, qz, -qw * qx);
-    dv[2] = fmaf(-fc2, fmaf(qx, qx, qy * qy), fcg);
-    dq[0] = -fmaf(qx, hx, fmaf(qy, hy, qz * hz));
-    dq[1] = fmaf(qw, hx, fmaf(qy, hz, -qz * hy));
-    dq[2] = fmaf(qw, hy, fmaf(qz, hx, -qx * hz));
-    dq[3] = fmaf(qw, hz, fmaf(qx, hy, -qy * hx));
-    dw[0] = fmaf(-D.gx, hy * hz, tI[0]);
-    dw[1] = fmaf(-D.gy, hz * hx, tI[1]);
-    dw[2] = fmaf(-D.gz, hx * hy, tI[2]);
+    const T qw = q[0], qx = q[1], qy = q[2], qz = q[3];
+    const T hx = h[0], hy = h[1], hz = h[2];
+    dv[0] = mul(fc2, fma(qx, qz, mul(qw, qy)));
+    dv[1] = mul(fc2, fnma(qw, qx, mul(qy, qz)));
+    dv[2] = fnma(fc2, fma(qx, qx, mul(qy, qy)), fcg);
+    dq[0] = neg(fma(qx, hx, fma(qy, hy, mul(qz, hz))));
+    dq[1] = fma(qw, hx, fnma(qz, hy, mul(qy, hz)));
+    dq[2] = fma(qw, hy, fnma(qx, hz, mul(qz, hx)));
+    dq[3] = fma(qw, hz, fnma(qy, hx, mul(qx, hy)));
+    dw[0] = fnma(bc<T>(D.gx), mul(hy, hz), tI[0]);
+    dw[1] = fnma(bc<T>(D.gy), mul(hz, hx), tI[1]);
+    dw[2] = fnma(bc<T>(D.gz), mul(hx, hy), tI[2]);
 }
 
 // One classical RK4 step with the wrench held (quad.py:350-437), in place.
-// Returns false when the row turns non-finite (the reference's fault
-// predicate, quad.py:404-430); the state is then garbage and the caller
-// restores the pre-step values (by deterministic re-execution, see
-// swarmstep_b200.cu).  Position feeds no derivative, so only its final
-// combination is formed: dp = dt/6 (v + 2 v2 + 2 v3 + v4).
-template <bool COMP>
-__device__ __forceinline__ bool rk4_inplace(float p_hi[3], float p_lo[3], float v[3], float q[4],
-                                            float w[3], float f_c, const float tau[3],
-                                            const swarmstep_quad_params &P, const Derived &D, float dt)
+// Returns, per lane, whether the row stays finite (the reference's fault
+// predicate, quad.py:404-430); a faulted lane's state is garbage and the
+// caller restores its pre-step values.  Position feeds no derivative, so only
+// its final combination is formed: dp = dt/6 (v + 2 v2 + 2 v3 + v4).
+template <class T, bool COMP>
+__device__ __forceinline__ mask_t<T> rk4_inplace(T p_hi[3], T p_lo[3], T v[3], T q[4], T w[3], T f_c,
+                                                 const T tau[3], const swarmstep_quad_params &P,
+                                                 const Derived &D, float dt)
 {
-    const float half = 0.5f * dt;
-    const float h6 = dt * (1.0f / 6.0f);
-    const float fcm = f_c * P.inv_m;
-    const float fc2 = 2.0f * fcm;
-    const float fcg = fcm - D.g;
-    const float tI[3] = {tau[0] * P.inv_ixx, tau[1] * P.inv_iyy, tau[2] * P.inv_izz};
-    float kv[3], kq[4], kw[3];
-    float av[3], aq[4], aw[3], ap[3];
-    float sv[3], sq[4], sw[3];
-    const float hw[3] = {0.5f * w[0], 0.5f * w[1], 0.5f * w[2]};
-    const float qtr = 0.5f * half, hdt = 0.5f * dt;  // stage steps on half rates
+    const T half = bc<T>(0.5f * dt), h6 = bc<T>(dt * (1.0f / 6.0f)), dtv = bc<T>(dt);
+    const T qtr = bc<T>(0.25f * dt), hdt = bc<T>(0.5f * dt);  // stage steps on half rates
+    const T two = bc<T>(2.0f);
+    const T fcm = mul(f_c, bc<T>(P.inv_m));
+    const T fc2 = add(fcm, fcm);
+    const T fcg = sub(fcm, bc<T>(D.g));
+    const T tI[3] = {mul(tau[0], bc<T>(P.inv_ixx)), mul(tau[1], bc<T>(P.inv_iyy)), mul(tau[2], bc<T>(P.inv_izz))};
+    T kv[3], kq[4], kw[3];
+    T av[3], aq[4], aw[3], ap[3];
+    T sv[3], sq[4], sw[3];
+    const T hw[3] = {mul(bc<T>(0.5f), w[0]), mul(bc<T>(0.5f), w[1]), mul(bc<T>(0.5f), w[2])};
 
     deriv(q, hw, fc2, fcg, tI, D, kv, kq, kw);                      // k1
 #pragma unroll
@@ -128,59 +203,61 @@ __device__ __forceinline__ bool rk4_inplace(float p_hi[3], float p_lo[3], float 
 #pragma unroll
     for (int s = 0; s < 2; s++) {                                   // k2, k3 at y + h/2 k
 #pragma unroll
-        for (int i = 0; i < 3; i++) { sv[i] = fmaf(half, kv[i], v[i]); sw[i] = fmaf(qtr, kw[i], hw[i]); }
+        for (int i = 0; i < 3; i++) { sv[i] = fma(half, kv[i], v[i]); sw[i] = fma(qtr, kw[i], hw[i]); }
 #pragma unroll
-        for (int i = 0; i < 4; i++) sq[i] = fmaf(half, kq[i], q[i]);
+        for (int i = 0; i < 4; i++) sq[i] = fma(half, kq[i], q[i]);
 #pragma unroll
-        for (int i = 0; i < 3; i++) ap[i] = fmaf(2.0f, sv[i], ap[i]);
+        for (int i = 0; i < 3; i++) ap[i] = fma(two, sv[i], ap[i]);
         deriv(sq, sw, fc2, fcg, tI, D, kv, kq, kw);
 #pragma unroll
-        for (int i = 0; i < 3; i++) { av[i] = fmaf(2.0f, kv[i], av[i]); aw[i] = fmaf(2.0f, kw[i], aw[i]); }
+        for (int i = 0; i < 3; i++) { av[i] = fma(two, kv[i], av[i]); aw[i] = fma(two, kw[i], aw[i]); }
 #pragma unroll
-        for (int i = 0; i < 4; i++) aq[i] = fmaf(2.0f, kq[i], aq[i]);
+        for (int i = 0; i < 4; i++) aq[i] = fma(two, kq[i], aq[i]);
     }
 #pragma unroll
-    for (int i = 0; i < 3; i++) { sv[i] = fmaf(dt, kv[i], v[i]); sw[i] = fmaf(hdt, kw[i], hw[i]); }
+    for (int i = 0; i < 3; i++) { sv[i] = fma(dtv, kv[i], v[i]); sw[i] = fma(hdt, kw[i], hw[i]); }
 #pragma unroll
-    for (int i = 0; i < 4; i++) sq[i] = fmaf(dt, kq[i], q[i]);
+    for (int i = 0; i < 4; i++) sq[i] = fma(dtv, kq[i], q[i]);
 #pragma unroll
-    for (int i = 0; i < 3; i++) ap[i] += sv[i];
+    for (int i = 0; i < 3; i++) ap[i] = add(ap[i], sv[i]);
     deriv(sq, sw, fc2, fcg, tI, D, kv, kq, kw);                     // k4
 #pragma unroll
-    for (int i = 0; i < 3; i++) { av[i] += kv[i]; aw[i] += kw[i]; }
+    for (int i = 0; i < 3; i++) { av[i] = add(av[i], kv[i]); aw[i] = add(aw[i], kw[i]); }
 #pragma unroll
-    for (int i = 0; i < 4; i++) aq[i] += kq[i];
+    for (int i = 0; i < 4; i++) aq[i] = add(aq[i], kq[i]);
 
     // y' = y + dt/6 (k1 + 2 k2 + 2 k3 + k4)
 #pragma unroll
     for (int i = 0; i < 3; i++) {
-        v[i] = fmaf(h6, av[i], v[i]);
-        w[i] = fmaf(h6, aw[i], w[i]);
-        const float dp = h6 * ap[i];
+        v[i] = fma(h6, av[i], v[i]);
+        w[i] = fma(h6, aw[i], w[i]);
+        const T dp = mul(h6, ap[i]);
         if (COMP) {
             // Fast2Sum: exact when |hi| >= |dp + lo| (a position against one
             // tick's displacement); keeps |lo| <= ulp(hi)/2
-            const float b = dp + p_lo[i];
-            const float sum = p_hi[i] + b;
-            p_lo[i] = b - (sum - p_hi[i]);
+            const T b = add(dp, p_lo[i]);
+            const T sum = add(p_hi[i], b);
+            p_lo[i] = sub(b, sub(sum, p_hi[i]));
             p_hi[i] = sum;
         } else {
-            p_hi[i] += dp;
+            p_hi[i] = add(p_hi[i], dp);
         }
     }
 #pragma unroll
-    for (int i = 0; i < 4; i++) q[i] = fmaf(h6, aq[i], q[i]);
+    for (int i = 0; i < 4; i++) q[i] = fma(h6, aq[i], q[i]);
 
     // single post-step renormalisation; zero / non-finite norm is a fault
-    const float nsq = fmaf(q[0], q[0], fmaf(q[1], q[1], fmaf(q[2], q[2], q[3] * q[3])));
-    const float inv = rsqrt_a(nsq);
+    const T nsq = fma(q[0], q[0], fma(q[1], q[1], fma(q[2], q[2], mul(q[3], q[3]))));
+    const T inv = rsqrt_a(nsq);
 #pragma unroll
-    for (int i = 0; i < 4; i++) q[i] *= inv;
-    // 0 * x is NaN exactly when x is inf / NaN (IEEE; no fast-math here), so
-    // one compare covers every position / velocity / rate component
-    const float chk = 0.0f * (((p_hi[0] + p_hi[1]) + (p_hi[2] + v[0])) + ((v[1] + v[2]) + (w[0] + w[1])) +
-                              (w[2] + (COMP ? (p_lo[0] + p_lo[1]) + p_lo[2] : 0.0f)));
-    return isfinite(nsq) && nsq > 0.0f && chk == 0.0f;
+    for (int i = 0; i < 4; i++) q[i] = mul(q[i], inv);
+    // 0 * x is NaN exactly when x is inf / NaN, so one compare covers every
+    // position / velocity / rate component (and nsq)
+    T s = add(add(add(p_hi[0], p_hi[1]), add(p_hi[2], v[0])), add(add(v[1], v[2]), add(w[0], w[1])));
+    s = add(s, add(w[2], nsq));
+    if (COMP) s = add(s, add(add(p_lo[0], p_lo[1]), p_lo[2]));
+    const T chk = mul(bc<T>(0.0f), s);
+    return mand(gt(nsq, bc<T>(0.0f)), eq(chk, bc<T>(0.0f)));
 }
 
 // mix_to_motors (quad.py:143-168): realized wrench after per-motor clamp.
@@ -188,22 +265,27 @@ __device__ __forceinline__ bool rk4_inplace(float p_hi[3], float p_lo[3], float 
 // motor i = c0 f + s_i1 c1 tau_x + s_i2 c2 tau_y + s_i3 c3 tau_z with the
 // sign pattern of G's columns.  P.G_inv carries the exact inverse; the host
 // checks the pattern (params.py) and the kernel uses c = |G_inv[0][:]|.
-__device__ __forceinline__ void mix_row(float &f_c, float tau[3], const swarmstep_quad_params &P)
+template <class T>
+__device__ __forceinline__ void mix_row(T &f_c, T tau[3], const swarmstep_quad_params &P)
 {
-    const float F = P.G_inv[0] * f_c, A = P.G_inv[1] * tau[0];
-    const float B = fabsf(P.G_inv[2]) * tau[1], C = P.G_inv[3] * tau[2];
-    const float FpA = F + A, FmA = F - A, BmC = B - C, BpC = B + C;
-    float m[4] = {FpA - BmC, FmA - BpC, FmA + BpC, FpA + BmC};
-    const float lo = fminf(fminf(m[0], m[1]), fminf(m[2], m[3]));
-    const float hi = fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3]));
-    if (lo < 0.0f || hi > P.f_max) {
+    const T F = mul(bc<T>(P.G_inv[0]), f_c), A = mul(bc<T>(P.G_inv[1]), tau[0]);
+    const T B = mul(bc<T>(fabsf(P.G_inv[2])), tau[1]), C = mul(bc<T>(P.G_inv[3]), tau[2]);
+    const T FpA = add(F, A), FmA = sub(F, A), BmC = sub(B, C), BpC = add(B, C);
+    T m[4] = {sub(FpA, BmC), sub(FmA, BpC), add(FmA, BpC), add(FpA, BmC)};
+    const T lo = vmin(vmin(m[0], m[1]), vmin(m[2], m[3]));
+    const T hi = vmax(vmax(m[0], m[1]), vmax(m[2], m[3]));
+    const mask_t<T> sat = mor(lt(lo, bc<T>(0.0f)), gt(hi, bc<T>(P.f_max)));
+    if (any(sat)) {
 #pragma unroll
-        for (int i = 0; i < 4; i++) m[i] = clip(m[i], 0.0f, P.f_max);
-        f_c = (m[0] + m[1]) + (m[2] + m[3]);
+        for (int i = 0; i < 4; i++) m[i] = clip(m[i], bc<T>(0.0f), bc<T>(P.f_max));
+        const T fc_s = add(add(m[0], m[1]), add(m[2], m[3]));
+        f_c = sel(sat, fc_s, f_c);
 #pragma unroll
-        for (int i = 0; i < 3; i++)
-            tau[i] = fmaf(P.G[(i + 1) * 4 + 0], m[0], fmaf(P.G[(i + 1) * 4 + 1], m[1],
-                     fmaf(P.G[(i + 1) * 4 + 2], m[2], P.G[(i + 1) * 4 + 3] * m[3])));
+        for (int i = 0; i < 3; i++) {
+            const T t = fma(bc<T>(P.G[(i + 1) * 4 + 0]), m[0], fma(bc<T>(P.G[(i + 1) * 4 + 1]), m[1],
+                        fma(bc<T>(P.G[(i + 1) * 4 + 2]), m[2], mul(bc<T>(P.G[(i + 1) * 4 + 3]), m[3]))));
+            tau[i] = sel(sat, t, tau[i]);
+        }
     }
 }
 
@@ -224,144 +306,141 @@ __device__ __forceinline__ void motor_wrench(const float rpm[4], const swarmstep
                  P.G[(i + 1) * 4 + 2] * f[2] + P.G[(i + 1) * 4 + 3] * f[3];
 }
 
-// rate_pid_step for one alive row (control.py:136-187).  Dead rows never
-// reach this (they are frozen: tau = 0, f_c = 0, state untouched).
-__device__ __forceinline__ void pid_row(const float w[3], const float w_sp[3],
-                                        const swarmstep_quad_params &P, const Derived &D, float dt,
-                                        float integ[3], float prev[3], float tau[3])
+// rate_pid_step for alive rows (control.py:136-187).  Dead rows never reach
+// this (they are frozen: tau = 0, f_c = 0, state untouched).  A row without a
+// previous sample has no D term (control.py:175-177): the caller sets
+// prev := w for it before the first tick, making the difference exactly 0.
+template <class T>
+__device__ __forceinline__ void pid_row(const T w[3], const T w_sp[3], const swarmstep_quad_params &P,
+                                        const Derived &D, float dt, T integ[3], T prev[3], T tau[3])
 {
-    // (no previous sample -> no D term, control.py:175-177: the caller sets
-    // prev := w for such rows before the first tick, making the difference 0)
 #pragma unroll
     for (int a = 0; a < 3; a++) {
-        const float pv = prev[a];
-        const float e = w_sp[a] - w[a];
+        const T e = sub(w_sp[a], w[a]);
         // min/max clamp: a NaN error (NaN rate command) faults the row this
         // tick regardless (tau is NaN), so NaN need not be kept in the state
-        integ[a] = fminf(fmaxf(fmaf(e, dt, integ[a]), -P.i_limit[a]), P.i_limit[a]);
-        const float t = fmaf(P.kp[a], e, P.ki[a] * integ[a]);
-        tau[a] = fmaf(-D.kd_dt[a], w[a] - pv, t);
+        integ[a] = vmin(vmax(fma(e, bc<T>(dt), integ[a]), bc<T>(-P.i_limit[a])), bc<T>(P.i_limit[a]));
+        const T t = fma(bc<T>(P.kp[a]), e, mul(bc<T>(P.ki[a]), integ[a]));
+        tau[a] = fnma(bc<T>(D.kd_dt[a]), sub(w[a], prev[a]), t);
         prev[a] = w[a];
     }
 }
 
 // 2 atan2(s, c) / s for s, c >= 0 (the axis-angle factor of control.py:283-285),
 // finite at s = 0 (-> 2/c): atan(t) = t P(t^2) on [0, 1], degree-8 minimax.
-__device__ __forceinline__ float axis_angle_factor(float s, float c)
+template <class T>
+__device__ __forceinline__ T axis_angle_factor(T s, T c)
 {
-    const bool small = s <= c;
-    const float num = small ? s : c, den = small ? c : s;
-    const float r = rcp_a(den);
-    const float t = num * r;
-    const float u = t * t;
-    float p = 0.002846542978659272f;
-    p = fmaf(p, u, -0.01605575904250145f);
-    p = fmaf(p, u, 0.04267148673534393f);
-    p = fmaf(p, u, -0.07502678036689758f);
-    p = fmaf(p, u, 0.10640215128660202f);
-    p = fmaf(p, u, -0.14203472435474396f);
-    p = fmaf(p, u, 0.1999259889125824f);
-    p = fmaf(p, u, -0.3333307206630707f);
-    p = fmaf(p, u, 1.0f);
+    const mask_t<T> small = le(s, c);
+    const T num = sel(small, s, c), den = sel(small, c, s);
+    const T r = rcp_a(den);
+    const T t = mul(num, r);
+    const T u = mul(t, t);
+    T p = bc<T>(0.002846542978659272f);
+    p = fma(p, u, bc<T>(-0.01605575904250145f));
+    p = fma(p, u, bc<T>(0.04267148673534393f));
+    p = fma(p, u, bc<T>(-0.07502678036689758f));
+    p = fma(p, u, bc<T>(0.10640215128660202f));
+    p = fma(p, u, bc<T>(-0.14203472435474396f));
+    p = fma(p, u, bc<T>(0.1999259889125824f));
+    p = fma(p, u, bc<T>(-0.3333307206630707f));
+    p = fma(p, u, bc<T>(1.0f));
     // small: atan2 = t p, factor = 2 t p / s = 2 p / c
     // large: atan2 = pi/2 - t p, factor = 2 (pi/2 - t p) / s
-    return small ? 2.0f * p * r : 2.0f * fmaf(-t, p, 1.5707963267948966f) * r;
+    const T big = fnma(t, p, bc<T>(1.5707963267948966f));
+    return mul(mul(bc<T>(2.0f), sel(small, p, big)), r);
 }
 
-// position_outer_loop for one alive row (control.py:222-294): PD position
-// loop -> desired frame (z_des, yaw) with the degenerate-heading fallback ->
-// desired quaternion from the one selected branch of _rotmats_to_quats
+// position_outer_loop for alive rows (control.py:222-294): PD position loop
+// -> desired frame (z_des, yaw) with the degenerate-heading fallback ->
+// desired quaternion from the selected branch of _rotmats_to_quats
 // (control.py:190-213) -> axis-angle attitude error -> clipped rate setpoint.
 // cy / sy = cos / sin(yaw_sp) are hoisted by the caller.
-__device__ __forceinline__ void outer_row(const float p_err[3], const float v[3], const float q[4],
-                                          const float v_sp[3], float cy, float sy,
-                                          const swarmstep_quad_params &P,
-                                          float w_sp[3], float &f_c_sp)
+template <class T>
+__device__ __forceinline__ void outer_row(const T p_err[3], const T v[3], const T q[4], const T v_sp[3],
+                                          T cy, T sy, const swarmstep_quad_params &P, T w_sp[3], T &f_c_sp)
 {
-    float a[3], z[3];
+    const T zero = bc<T>(0.0f), one = bc<T>(1.0f);
+    T a[3], z[3];
 #pragma unroll
-    for (int i = 0; i < 3; i++) a[i] = fmaf(P.kp_pos[i], p_err[i], P.kv[i] * (v_sp[i] - v[i]));
-    a[2] += P.g;
-    const float asq = fmaf(a[0], a[0], fmaf(a[1], a[1], a[2] * a[2]));
-    const float qw = q[0], qx = q[1], qy = q[2], qz = q[3];
-    const float zb0 = 2.0f * fmaf(qx, qz, qw * qy);
-    const float zb1 = 2.0f * fmaf(qy, qz, -qw * qx);
-    const float zb2 = fmaf(-2.0f, fmaf(qx, qx, qy * qy), 1.0f);
+    for (int i = 0; i < 3; i++) a[i] = fma(bc<T>(P.kp_pos[i]), p_err[i], mul(bc<T>(P.kv[i]), sub(v_sp[i], v[i])));
+    a[2] = add(a[2], bc<T>(P.g));
+    const T asq = fma(a[0], a[0], fma(a[1], a[1], mul(a[2], a[2])));
+    const T qw = q[0], qx = q[1], qy = q[2], qz = q[3];
+    const T zb0 = mul(bc<T>(2.0f), fma(qx, qz, mul(qw, qy)));
+    const T zb1 = mul(bc<T>(2.0f), fnma(qw, qx, mul(qy, qz)));
+    const T zb2 = fnma(bc<T>(2.0f), fma(qx, qx, mul(qy, qy)), one);
     const float amin = P.a_cmd_min;
-    float fc;
-    if (asq < amin * amin) {            // free-fall floor: z_des = e_z, |a| := a_min
-        z[0] = 0.0f; z[1] = 0.0f; z[2] = 1.0f;
-        fc = P.m * amin * zb2;
-    } else {                            // m |a| (z_body . a/|a|) = m (z_body . a)
-        const float ia = rsqrt_a(asq);
-        z[0] = a[0] * ia; z[1] = a[1] * ia; z[2] = a[2] * ia;
-        fc = P.m * fmaf(zb0, a[0], fmaf(zb1, a[1], zb2 * a[2]));
-    }
-    f_c_sp = fminf(fmaxf(fc, 0.0f), P.fc_max);
+    // free-fall floor (control.py:243-247): |a| < a_min -> z_des = e_z, |a| := a_min;
+    // else m |a| (z_body . a/|a|) = m (z_body . a)
+    const mask_t<T> low = lt(asq, bc<T>(amin * amin));
+    const T ia = rsqrt_a(asq);
+    z[0] = sel(low, zero, mul(a[0], ia));
+    z[1] = sel(low, zero, mul(a[1], ia));
+    z[2] = sel(low, one, mul(a[2], ia));
+    const T fc = sel(low, mul(bc<T>(P.m * amin), zb2), mul(bc<T>(P.m), fma(zb0, a[0], fma(zb1, a[1], mul(zb2, a[2])))));
+    f_c_sp = vmin(vmax(fc, zero), bc<T>(P.fc_max));
 
     // y = z x x_c / |z x x_c| with x_c = (cy, sy, 0); degenerate fallback from y_c
-    float yd[3];
-    const float yr0 = -z[2] * sy, yr1 = z[2] * cy, yr2 = fmaf(z[0], sy, -z[1] * cy);
-    const float nysq = fmaf(yr0, yr0, fmaf(yr1, yr1, yr2 * yr2));
-    if (nysq >= 1e-12f) {
-        const float iy = rsqrt_a(nysq);
-        yd[0] = yr0 * iy; yd[1] = yr1 * iy; yd[2] = yr2 * iy;
-    } else {
+    T yd[3];
+    const T yr0 = neg(mul(z[2], sy)), yr1 = mul(z[2], cy), yr2 = fnma(z[1], cy, mul(z[0], sy));
+    const T nysq = fma(yr0, yr0, fma(yr1, yr1, mul(yr2, yr2)));
+    const T iy = rsqrt_a(nysq);
+    yd[0] = mul(yr0, iy); yd[1] = mul(yr1, iy); yd[2] = mul(yr2, iy);
+    const mask_t<T> degen = mnot(ge(nysq, bc<T>(1e-12f)));
+    if (any(degen)) {
         // x_alt = y_c x z, y_c = (-sy, cy, 0); y = z x x_alt / |x_alt|
-        const float xa0 = cy * z[2], xa1 = sy * z[2], xa2 = fmaf(-sy, z[1], -cy * z[0]);
-        const float ix = rsqrt_a(fmaf(xa0, xa0, fmaf(xa1, xa1, xa2 * xa2)));
-        const float x0 = xa0 * ix, x1 = xa1 * ix, x2 = xa2 * ix;
-        yd[0] = fmaf(z[1], x2, -z[2] * x1);
-        yd[1] = fmaf(z[2], x0, -z[0] * x2);
-        yd[2] = fmaf(z[0], x1, -z[1] * x0);
+        const T xa0 = mul(cy, z[2]), xa1 = mul(sy, z[2]), xa2 = fnma(sy, z[1], neg(mul(cy, z[0])));
+        const T ix = rsqrt_a(fma(xa0, xa0, fma(xa1, xa1, mul(xa2, xa2))));
+        const T x0 = mul(xa0, ix), x1 = mul(xa1, ix), x2 = mul(xa2, ix);
+        yd[0] = sel(degen, fnma(z[2], x1, mul(z[1], x2)), yd[0]);
+        yd[1] = sel(degen, fnma(z[0], x2, mul(z[2], x0)), yd[1]);
+        yd[2] = sel(degen, fnma(z[1], x0, mul(z[0], x1)), yd[2]);
     }
     // x = y x z ;  R = [x y z] (columns)
-    const float m00 = fmaf(yd[1], z[2], -yd[2] * z[1]);
-    const float m10 = fmaf(yd[2], z[0], -yd[0] * z[2]);
-    const float m20 = fmaf(yd[0], z[1], -yd[1] * z[0]);
-    const float m01 = yd[0], m11 = yd[1], m21 = yd[2];
-    const float m02 = z[0], m12 = z[1], m22 = z[2];
-    const float tr = m00 + m11 + m22;
+    const T m00 = fnma(yd[2], z[1], mul(yd[1], z[2]));
+    const T m10 = fnma(yd[0], z[2], mul(yd[2], z[0]));
+    const T m20 = fnma(yd[1], z[0], mul(yd[0], z[1]));
+    const T m01 = yd[0], m11 = yd[1], m21 = yd[2];
+    const T m02 = z[0], m12 = z[1], m22 = z[2];
+    const T tr = add(add(m00, m11), m22);
     // _rotmats_to_quats selects branch 0 (tr > 0), 1 (m00 largest), 2 (m11 >=
     // m22) or 3; branch k has t = 1 + (+-m00 +- m11 +- m22), s = 2 sqrt(t), its
-    // own component s/4 = sqrt(t)/2 and the others (m_ij +- m_ji)/s.  Evaluated
-    // branch-free with selects (agents in a warp pick different branches).
-    const bool b0 = tr > 0.0f;
-    const bool b1 = !b0 && (m00 >= m11 && m00 >= m22);
-    const bool b2 = !b0 && !b1 && (m11 >= m22);
-    const bool b3 = !b0 && !b1 && !b2;
-    const float s00 = (b0 || b1) ? m00 : -m00;
-    const float s11 = (b0 || b2) ? m11 : -m11;
-    const float s22 = (b0 || b3) ? m22 : -m22;
-    // Any positive scale of q_des leaves the result unchanged: q_err is
-    // linear in q_des, and the axis-angle vector e_xyz * 2 atan2(|e_xyz|,
-    // e_w) / |e_xyz| is invariant to a positive scale of q_err.  So the
-    // branch quaternion is formed scaled by s = 2 sqrt(t) -- (t, m_ij +- m_ji)
-    // -- with no square root, and neither q_des nor q_err is renormalised
-    // (the reference renormalises both; identical in R).
-    const float t = fmaxf(1.0f + s00 + s11 + s22, 1e-30f);
-    const float d21 = m21 - m12, d02 = m02 - m20, d10 = m10 - m01;
-    const float a01 = m01 + m10, a02 = m02 + m20, a12 = m12 + m21;
-    float qd[4];
-    qd[0] = b0 ? t : (b1 ? d21 : (b2 ? d02 : d10));
-    qd[1] = b1 ? t : (b0 ? d21 : (b2 ? a01 : a02));
-    qd[2] = b2 ? t : (b0 ? d02 : (b1 ? a01 : a12));
-    qd[3] = b3 ? t : (b0 ? d10 : (b1 ? a02 : a12));
+    // own component s/4 and the others (m_ij +- m_ji)/s.  Any positive scale
+    // of q_des leaves the result unchanged (q_err is linear in q_des and the
+    // axis-angle vector is scale invariant), so the branch quaternion is
+    // formed scaled by s -- (t, m_ij +- m_ji) -- with no square root, and
+    // neither q_des nor q_err is renormalised (identical in R).
+    const mask_t<T> b0 = gt(tr, zero);
+    const mask_t<T> b1 = mand(mnot(b0), mand(ge(m00, m11), ge(m00, m22)));
+    const mask_t<T> b2 = mand(mand(mnot(b0), mnot(b1)), ge(m11, m22));
+    const mask_t<T> b3 = mand(mand(mnot(b0), mnot(b1)), mnot(b2));
+    const T s00 = sel(mor(b0, b1), m00, neg(m00));
+    const T s11 = sel(mor(b0, b2), m11, neg(m11));
+    const T s22 = sel(mor(b0, b3), m22, neg(m22));
+    const T t = vmax(add(add(add(one, s00), s11), s22), bc<T>(1e-30f));
+    const T d21 = sub(m21, m12), d02 = sub(m02, m20), d10 = sub(m10, m01);
+    const T a01 = add(m01, m10), a02 = add(m02, m20), a12 = add(m12, m21);
+    T qd[4];
+    qd[0] = sel(b0, t, sel(b1, d21, sel(b2, d02, d10)));
+    qd[1] = sel(b1, t, sel(b0, d21, sel(b2, a01, a02)));
+    qd[2] = sel(b2, t, sel(b0, d02, sel(b1, a01, a12)));
+    qd[3] = sel(b3, t, sel(b0, d10, sel(b1, a02, a12)));
     // q_err = conj(q) (x) q_des (quat.py:75-92); the w >= 0 flip becomes |e_w|
     // and a sign on the rate setpoint
-    const float e0 = fmaf(qw, qd[0], fmaf(qx, qd[1], fmaf(qy, qd[2], qz * qd[3])));
-    const float e1 = fmaf(qw, qd[1], fmaf(-qx, qd[0], fmaf(-qy, qd[3], qz * qd[2])));
-    const float e2 = fmaf(qw, qd[2], fmaf(qx, qd[3], fmaf(-qy, qd[0], -qz * qd[1])));
-    const float e3 = fmaf(qw, qd[3], fmaf(-qx, qd[2], fmaf(qy, qd[1], -qz * qd[0])));
-    const float ssq = fmaf(e1, e1, fmaf(e2, e2, e3 * e3));
-    float factor = axis_angle_factor(sqrt_a(ssq), fabsf(e0));
-    factor = e0 < 0.0f ? -factor : factor;
+    const T e0 = fma(qw, qd[0], fma(qx, qd[1], fma(qy, qd[2], mul(qz, qd[3]))));
+    const T e1 = fma(qw, qd[1], fnma(qx, qd[0], fnma(qy, qd[3], mul(qz, qd[2]))));
+    const T e2 = fma(qw, qd[2], fma(qx, qd[3], fnma(qy, qd[0], neg(mul(qz, qd[1])))));
+    const T e3 = fma(qw, qd[3], fnma(qx, qd[2], fnma(qz, qd[0], mul(qy, qd[1]))));
+    const T ssq = fma(e1, e1, fma(e2, e2, mul(e3, e3)));
+    T factor = axis_angle_factor(sqrt_a(ssq), vabs(e0));
+    factor = sel(lt(e0, zero), neg(factor), factor);
     // |w_sp| <= omega_sp_max.  min/max (not NaN-propagating) is safe here:
     // non-finite outer-loop inputs are rejected before launch (InvalidState).
-    const float wm = P.omega_sp_max;
-    w_sp[0] = fminf(fmaxf(P.k_att[0] * (e1 * factor), -wm), wm);
-    w_sp[1] = fminf(fmaxf(P.k_att[1] * (e2 * factor), -wm), wm);
-    w_sp[2] = fminf(fmaxf(P.k_att[2] * (e3 * factor), -wm), wm);
+    const T wm = bc<T>(P.omega_sp_max), nwm = bc<T>(-P.omega_sp_max);
+    w_sp[0] = vmin(vmax(mul(bc<T>(P.k_att[0]), mul(e1, factor)), nwm), wm);
+    w_sp[1] = vmin(vmax(mul(bc<T>(P.k_att[1]), mul(e2, factor)), nwm), wm);
+    w_sp[2] = vmin(vmax(mul(bc<T>(P.k_att[2]), mul(e3, factor)), nwm), wm);
 }
 
 }  // namespace ssb

@@ -52,23 +52,27 @@ struct Cols {
 #define SSB_TICK_UNROLL 1
 #endif
 constexpr int kTickUnroll = SSB_TICK_UNROLL;
+#ifndef SSB_PAIR_MIN_K
+#define SSB_PAIR_MIN_K 1000000   // auto picks the paired (FFMA2) kernel from this many ticks per launch
+#endif
 #ifndef SSB_TMA_MAX_K
 #define SSB_TMA_MAX_K 0   // auto never picks the TMA-staged kernel (measured slower)
 #endif
 
-// One agent's registers for a launch.
-struct Row {
-    float p_hi[3], p_lo[3], v[3], q[4], w[3], integ[3], prev[3];
+// One or two agents' registers for a launch (T = float or ssb::f2).
+template <class T>
+struct RowT {
+    T p_hi[3], p_lo[3], v[3], q[4], w[3], integ[3], prev[3];
     // u[]: per-launch setpoint registers, shared by the three levels
     //   POS:   p_sp xyz, v_sp xyz (+ overlay on tick 0), cos(yaw), sin(yaw)
     //   MOTOR: rotor-model wrench f_c, tau xyz (core.py:189-197)
-    float u[8];
-    float w_sp[3], f_sp;   // inner-loop setpoints (stale ones for MOTOR rows)
-    bool has_prev;
+    T u[8];
+    T w_sp[3], f_sp;   // inner-loop setpoints (stale ones for MOTOR rows)
 };
+using Row = RowT<float>;
 
 // Row accessors: the same step code reads a row from global memory (direct
-// kernel, streaming loads) or from a shared-memory tile staged by TMA.
+// kernels, streaming loads) or from a shared-memory tile staged by TMA.
 struct GlobalRow {
     float *p;
     __device__ __forceinline__ float ld(int c) const { return __ldcs(p + c * SWARMSTEP_TILE); }
@@ -81,9 +85,19 @@ struct SmemRow {
     __device__ __forceinline__ float ldc(int c) const { return p[c * SWARMSTEP_TILE]; }
     __device__ __forceinline__ void st(int c, float v) const { p[c * SWARMSTEP_TILE] = v; }
 };
+// Two rows read / written as one f2 lane pair (the paired kernel).
+template <class A>
+struct PairRow {
+    A a, b;
+    __device__ __forceinline__ ssb::f2 ld(int c) const { return ssb::f2{make_float2(a.ld(c), b.ld(c))}; }
+    __device__ __forceinline__ ssb::f2 ldc(int c) const { return ssb::f2{make_float2(a.ldc(c), b.ldc(c))}; }
+    __device__ __forceinline__ void st(int c, ssb::f2 v) const { a.st(c, v.v.x); b.st(c, v.v.y); }
+};
 
-template <bool COMP, class A>
-__device__ __forceinline__ void load_state(const A &C, Row &R)
+template <class T> __device__ __forceinline__ T zero_t() { return ssb::bc<T>(0.0f); }
+
+template <bool COMP, class T, class A>
+__device__ __forceinline__ void load_state(const A &C, RowT<T> &R)
 {
 #pragma unroll
     for (int i = 0; i < 3; i++) {
@@ -92,17 +106,17 @@ __device__ __forceinline__ void load_state(const A &C, Row &R)
         R.w[i] = C.ld(SWARMSTEP_COL_OMEGA + i);
         R.integ[i] = C.ld(SWARMSTEP_COL_INTEGRAL + i);
         R.prev[i] = C.ld(SWARMSTEP_COL_PREV + i);
-        R.p_lo[i] = COMP ? C.ld(SWARMSTEP_COL_POS_LO + i) : 0.0f;
+        R.p_lo[i] = COMP ? C.ld(SWARMSTEP_COL_POS_LO + i) : zero_t<T>();
     }
 #pragma unroll
     for (int i = 0; i < 4; i++) R.q[i] = C.ld(SWARMSTEP_COL_QUAT + i);
 #pragma unroll
     for (int i = 0; i < 7; i++) R.u[i] = C.ld(SWARMSTEP_COL_CMD + i);
-    R.u[7] = 0.0f;
+    R.u[7] = zero_t<T>();
 }
 
-template <bool COMP, class A>
-__device__ __forceinline__ void store_state(const A &C, int level, const Row &R)
+template <bool COMP, class T, class A>
+__device__ __forceinline__ void store_state(const A &C, int level, const RowT<T> &R)
 {
 #pragma unroll
     for (int i = 0; i < 3; i++) {
@@ -124,31 +138,38 @@ __device__ __forceinline__ void store_state(const A &C, int level, const Row &R)
     }
 }
 
-// Per-launch setpoint preparation (commands are fixed across the K ticks).
-template <class A>
-__device__ __forceinline__ void setup_level(const A &C, int level, int overlay_active,
-                                            const swarmstep_quad_params &P, Row &R)
+__device__ __forceinline__ void sincos_lane(float x, float &s, float &c) { sincosf(x, &s, &c); }
+__device__ __forceinline__ void sincos_lane(ssb::f2 x, ssb::f2 &s, ssb::f2 &c)
 {
-    if (!R.has_prev) {
-        // first sample: no D term (control.py:175-177) <=> prev := w
+    sincosf(x.v.x, &s.v.x, &c.v.x);
+    sincosf(x.v.y, &s.v.y, &c.v.y);
+}
+
+// Per-launch setpoint preparation (commands are fixed across the K ticks).
+// has_prev: per-row "previous rate sample exists" (control.py:104).
+template <class T, class A, class M>
+__device__ __forceinline__ void setup_level(const A &C, int level, int overlay_active,
+                                            const swarmstep_quad_params &P, M has_prev, RowT<T> &R)
+{
+    // first sample: no D term (control.py:175-177) <=> prev := w
 #pragma unroll
-        for (int i = 0; i < 3; i++) R.prev[i] = R.w[i];
-    }
-    R.w_sp[0] = R.w_sp[1] = R.w_sp[2] = R.f_sp = 0.0f;
+    for (int i = 0; i < 3; i++) R.prev[i] = ssb::sel(has_prev, R.prev[i], R.w[i]);
+    R.w_sp[0] = R.w_sp[1] = R.w_sp[2] = R.f_sp = zero_t<T>();
     if (level == SWARMSTEP_LEVEL_POS) {
-        float s, c;
-        sincosf(R.u[6], &s, &c);
+        T s, c;
+        sincos_lane(R.u[6], s, c);
         R.u[6] = c;
         R.u[7] = s;
         if (overlay_active) {
 #pragma unroll
-            for (int i = 0; i < 3; i++) R.u[3 + i] += C.ldc(SWARMSTEP_COL_OVERLAY + i);
+            for (int i = 0; i < 3; i++) R.u[3 + i] = ssb::add(R.u[3 + i], C.ldc(SWARMSTEP_COL_OVERLAY + i));
         }
     } else if (level == SWARMSTEP_LEVEL_RATE) {
         R.w_sp[0] = R.u[0]; R.w_sp[1] = R.u[1]; R.w_sp[2] = R.u[2]; R.f_sp = R.u[3];
-    } else {
-        // MOTOR: the PID still runs on the stale setpoints (core.py:109-110,
-        // 184-186); the integrated wrench comes from the rotor model
+    } else if constexpr (sizeof(T) == sizeof(float)) {
+        // MOTOR (scalar rows only): the PID still runs on the stale setpoints
+        // (core.py:109-110, 184-186); the integrated wrench comes from the
+        // rotor model
 #pragma unroll
         for (int i = 0; i < 3; i++) R.w_sp[i] = C.ldc(SWARMSTEP_COL_SP + i);
         R.f_sp = C.ldc(SWARMSTEP_COL_SP + 3);
@@ -158,24 +179,24 @@ __device__ __forceinline__ void setup_level(const A &C, int level, int overlay_a
     }
 }
 
-// K ticks of one agent at a fixed command level (the body of QuadGroup.step,
-// core.py:166-202, repeated), state updated in place.  Returns the tick at
-// which the row faulted (its state registers are then garbage), or -1.
-// With RERUN the loop stops after the controller part of tick pid_only_at
-// (used to rebuild a faulted row's state, see the kernels).
-template <int LEVEL, bool COMP, bool RERUN>
+// K ticks at a fixed command level (the body of QuadGroup.step, core.py:
+// 166-202, repeated), state updated in place.  Returns the first tick at which
+// a lane faulted (the state registers are then garbage), or -1.  With RERUN
+// the loop stops after the controller part of tick pid_only_at (used to
+// rebuild a faulted row's state, see step_row).
+template <int LEVEL, bool COMP, bool RERUN, class T>
 __device__ __forceinline__ int run_ticks(const swarmstep_quad_params &P, const ssb::Derived &D,
-                                         float dt, int K, int pid_only_at, Row &R)
+                                         float dt, int K, int pid_only_at, RowT<T> &R)
 {
 #pragma unroll kTickUnroll
     for (int k = 0; k < K; k++) {
         if (LEVEL == SWARMSTEP_LEVEL_POS) {
-            float p_err[3];
+            T p_err[3];
 #pragma unroll
-            for (int i = 0; i < 3; i++) p_err[i] = (R.u[i] - R.p_hi[i]) - R.p_lo[i];
+            for (int i = 0; i < 3; i++) p_err[i] = ssb::sub(ssb::sub(R.u[i], R.p_hi[i]), R.p_lo[i]);
             ssb::outer_row(p_err, R.v, R.q, R.u + 3, R.u[6], R.u[7], P, R.w_sp, R.f_sp);
         }
-        float tau[3], f_c = R.f_sp;
+        T tau[3], f_c = R.f_sp;
         ssb::pid_row(R.w, R.w_sp, P, D, dt, R.integ, R.prev, tau);
         if (RERUN && k == pid_only_at) return -1;
         if (LEVEL == SWARMSTEP_LEVEL_MOTOR) {
@@ -183,15 +204,16 @@ __device__ __forceinline__ int run_ticks(const swarmstep_quad_params &P, const s
         } else {
             ssb::mix_row(f_c, tau, P);
         }
-        if (!ssb::rk4_inplace<COMP>(R.p_hi, R.p_lo, R.v, R.q, R.w, f_c, tau, P, D, dt)) return k;
+        const auto ok = ssb::rk4_inplace<T, COMP>(R.p_hi, R.p_lo, R.v, R.q, R.w, f_c, tau, P, D, dt);
+        if (ssb::any(ssb::mnot(ok))) return k;
     }
     return -1;
 }
 
-template <bool COMP, bool RERUN, class A>
+template <bool COMP, bool RERUN, class T, class A>
 __device__ __forceinline__ int run_level(const A &C, int level, int overlay_active,
                                          const swarmstep_quad_params &P, const ssb::Derived &D,
-                                         float dt, int K, int pid_only_at, Row &R)
+                                         float dt, int K, int pid_only_at, RowT<T> &R)
 {
     // level-specialised tick loops: no per-tick level branches
     if (level == SWARMSTEP_LEVEL_POS) {
@@ -208,7 +230,9 @@ __device__ __forceinline__ int run_level(const A &C, int level, int overlay_acti
     }
     if (level == SWARMSTEP_LEVEL_RATE)
         return run_ticks<SWARMSTEP_LEVEL_RATE, COMP, RERUN>(P, D, dt, K, pid_only_at, R);
-    return run_ticks<SWARMSTEP_LEVEL_MOTOR, COMP, RERUN>(P, D, dt, K, pid_only_at, R);
+    if constexpr (sizeof(T) == sizeof(float))
+        return run_ticks<SWARMSTEP_LEVEL_MOTOR, COMP, RERUN>(P, D, dt, K, pid_only_at, R);
+    return -1;
 }
 
 // The whole per-row launch: K ticks from the row's inputs behind accessor C,
@@ -228,16 +252,15 @@ __device__ __forceinline__ uint8_t step_row(const A &C, uint8_t fl, int64_t r, i
     Row R;
     load_state<COMP>(C, R);
     const int level = (fl & SWARMSTEP_LEVEL_MASK) >> SWARMSTEP_LEVEL_SHIFT;
-    R.has_prev = (fl & SWARMSTEP_FLAG_HAS_PREV) != 0;
-    setup_level(C, level, overlay_active, P, R);
+    const bool has_prev = (fl & SWARMSTEP_FLAG_HAS_PREV) != 0;
+    setup_level(C, level, overlay_active, P, has_prev, R);
     const ssb::Derived D = ssb::derive(P, 1.0f / dt);
     const int fault_k = run_level<COMP, false>(C, level, overlay_active, P, D, dt, K, -1, R);
     bool alive = true;
     if (fault_k >= 0) {
         alive = false;
         load_state<COMP>(C, R);
-        R.has_prev = (fl & SWARMSTEP_FLAG_HAS_PREV) != 0;
-        setup_level(C, level, overlay_active, P, R);
+        setup_level(C, level, overlay_active, P, has_prev, R);
         run_level<COMP, true>(C, level, overlay_active, P, D, dt, fault_k + 1, fault_k, R);
         const uint32_t slot = atomicAdd(&counters[0], 1u);
         const uint32_t tick = (tick_dev ? (uint32_t)*tick_dev : 0u) + tick_base + (uint32_t)fault_k;
@@ -265,6 +288,63 @@ quad_step_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t 
     const uint8_t nfl = step_row<COMP>(C, fl, r, overlay_active, P, dt, K, tick_base, tick_dev,
                                        counters, fault_log, fault_cap);
     if (nfl != fl) flags[r] = nfl;
+}
+
+// ---- paired kernel: two rows per thread on packed FP32x2 (FFMA2) -------------
+// Thread t of a 64-thread CTA owns rows t and t + 64 of one 128-agent tile.
+// When both rows are alive at the same POS or RATE level (the common case)
+// they run as one f2 lane pair: every FFMA / FADD / FMUL of the step becomes
+// one FFMA2 / FADD2 / FMUL2 for both agents, halving the issued FP
+// instructions of this issue-bound kernel.  Otherwise (a dead partner, mixed
+// or MOTOR levels) -- and whenever a lane faults -- each row runs the scalar
+// path.  Both paths are the same templates with explicitly rounded ops, so
+// every row's result is bit-identical to the direct kernel's.
+#ifndef SSB_PAIR_MINB
+#define SSB_PAIR_MINB 6
+#endif
+template <bool COMP>
+__global__ void __launch_bounds__(64, SSB_PAIR_MINB)
+quad_step_pair_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t n,
+                      uint32_t *__restrict__ counters, uint64_t *__restrict__ fault_log,
+                      int64_t fault_cap, int overlay_active, uint32_t tick_base, const int64_t *tick_dev,
+                      const swarmstep_quad_params P, float dt, int K)
+{
+    const int64_t r0 = (int64_t)blockIdx.x * SWARMSTEP_TILE + threadIdx.x, r1 = r0 + 64;
+    if (r0 >= n) return;
+    const uint8_t f0 = flags[r0], f1 = r1 < n ? flags[r1] : 0;
+    const bool a0 = f0 & SWARMSTEP_FLAG_ALIVE, a1 = f1 & SWARMSTEP_FLAG_ALIVE;
+    const int l0 = (f0 & SWARMSTEP_LEVEL_MASK) >> SWARMSTEP_LEVEL_SHIFT;
+    const int l1 = (f1 & SWARMSTEP_LEVEL_MASK) >> SWARMSTEP_LEVEL_SHIFT;
+    const GlobalRow C0{cols + ssb::tile_base(r0)}, C1{cols + ssb::tile_base(r1)};
+    bool scalar = !(a0 && a1 && l0 == l1 && l0 != SWARMSTEP_LEVEL_MOTOR);
+    if (!scalar) {
+        const PairRow<GlobalRow> C{C0, C1};
+        RowT<ssb::f2> R;
+        load_state<COMP>(C, R);
+        const ssb::m2 hp{(f0 & SWARMSTEP_FLAG_HAS_PREV) != 0, (f1 & SWARMSTEP_FLAG_HAS_PREV) != 0};
+        setup_level(C, l0, overlay_active, P, hp, R);
+        const ssb::Derived D = ssb::derive(P, 1.0f / dt);
+        if (run_level<COMP, false>(C, l0, overlay_active, P, D, dt, K, -1, R) >= 0) {
+            scalar = true;     // a lane faulted: redo both rows on the scalar path
+        } else {
+            store_state<COMP>(C, l0, R);
+            const uint8_t hpf = SWARMSTEP_FLAG_HAS_PREV;
+            if ((f0 | hpf) != f0) flags[r0] = f0 | hpf;
+            if ((f1 | hpf) != f1) flags[r1] = f1 | hpf;
+        }
+    }
+    if (scalar) {
+        if (a0) {
+            const uint8_t nf = step_row<COMP>(C0, f0, r0, overlay_active, P, dt, K, tick_base, tick_dev,
+                                              counters, fault_log, fault_cap);
+            if (nf != f0) flags[r0] = nf;
+        }
+        if (a1) {
+            const uint8_t nf = step_row<COMP>(C1, f1, r1, overlay_active, P, dt, K, tick_base, tick_dev,
+                                              counters, fault_log, fault_cap);
+            if (nf != f1) flags[r1] = nf;
+        }
+    }
 }
 
 // ---- TMA kernel: persistent CTAs, tiles staged through shared memory --------
@@ -544,6 +624,7 @@ int swarmstep_preload(void)
     // must not happen inside a CUDA graph capture)
     cudaFuncAttributes a;
     const void *fns[] = {(const void *)quad_step_kernel<true>, (const void *)quad_step_kernel<false>,
+                         (const void *)quad_step_pair_kernel<true>, (const void *)quad_step_pair_kernel<false>,
                          (const void *)quad_step_tma_kernel<true>, (const void *)quad_step_tma_kernel<false>,
                          (const void *)apply_commands_kernel, (const void *)set_setpoints_kernel,
                          (const void *)mark_dead_kernel, (const void *)retarget_kernel,
@@ -591,6 +672,14 @@ int swarmstep_quad_step(const swarmstep_group_view *g, const swarmstep_quad_para
             g->cols, g->flags, ntiles, g->counters, g->fault_log, fcap, overlay, motor, tick_base, tick_dev,
             *p, dt, k_substeps);
         return cuda_status("quad_step_tma_kernel");
+    }
+    if (!(launch_flags & SWARMSTEP_STEP_FORCE_DIRECT) &&
+        ((launch_flags & SWARMSTEP_STEP_FORCE_PAIR) || k_substeps >= SSB_PAIR_MIN_K)) {
+        auto kern = g->compensated ? quad_step_pair_kernel<true> : quad_step_pair_kernel<false>;
+        kern<<<(unsigned)((g->n + SWARMSTEP_TILE - 1) / SWARMSTEP_TILE), 64, 0, (cudaStream_t)stream>>>(
+            g->cols, g->flags, g->n, g->counters, g->fault_log, fcap, overlay, tick_base, tick_dev, *p, dt,
+            k_substeps);
+        return cuda_status("quad_step_pair_kernel");
     }
     auto kern = g->compensated ? quad_step_kernel<true> : quad_step_kernel<false>;
     kern<<<grid_for(g->n, kBlock), kBlock, 0, (cudaStream_t)stream>>>(

@@ -28,7 +28,7 @@ import torch
 
 from . import _lib
 from ._lib import (COL_CMD, COL_INTEGRAL, COL_OVERLAY, COL_PREV, COL_SP, FLAG_ALIVE, FLAG_HAS_PREV,
-                   LEVEL_MASK, LEVEL_SHIFT, NCOL, STEP_FORCE_DIRECT, STEP_FORCE_TMA, STEP_MOTOR,
+                   LEVEL_MASK, LEVEL_SHIFT, NCOL, STEP_FORCE_DIRECT, STEP_FORCE_PAIR, STEP_FORCE_TMA, STEP_MOTOR,
                    STEP_OVERLAY, TILE, GroupView)
 from .commands import LEVEL_MOTOR, LEVEL_POS, LEVEL_RATE, level_code
 from .errors import InvalidStateError, NativeLibraryError, ValidationError
@@ -441,8 +441,8 @@ class B200QuadGroup:
         self._tick += k
         self._state_stale = True
 
-    # kernel selection for tuning: "auto" (TMA-staged for few ticks per launch,
-    # direct for many), "direct" or "tma"
+    # kernel selection for tuning: "auto" (the library's choice), "direct",
+    # "pair" (two rows per thread on packed FP32x2) or "tma"
     kernel = "auto"
 
     def _launch_flags(self) -> int:
@@ -453,6 +453,8 @@ class B200QuadGroup:
             f |= STEP_FORCE_DIRECT
         elif self.kernel == "tma":
             f |= STEP_FORCE_TMA
+        elif self.kernel == "pair":
+            f |= STEP_FORCE_PAIR
         return f
 
     def _overlay_reset(self) -> None:

@@ -238,11 +238,13 @@ def test_large_n_sampled_rows_vs_oracle():
 
 
 @pytest.mark.parametrize("k", [1, 3, 10])
-def test_direct_and_tma_kernels_bit_identical(k):
-    """The TMA-staged and the direct-load kernel run the same per-row code."""
+@pytest.mark.parametrize("other", ["tma", "pair"])
+def test_kernel_variants_bit_identical(k, other):
+    """The TMA-staged, paired (FFMA2) and direct kernels run the same per-row
+    templates with explicitly rounded arithmetic: identical bits, all levels."""
     sc = ALL["mixed"]()
     outs = []
-    for kern in ("direct", "tma"):
+    for kern in ("direct", other):
         g = make_group(sc)
         g.kernel = kern
         run_script(g, Scenario(**{**sc.__dict__, "ticks": 30, "record": []}))
@@ -251,5 +253,24 @@ def test_direct_and_tma_kernels_bit_identical(k):
         st = gpu_state(g)
         outs.append({q: st[q].copy() for q in ("pos", "vel", "quat", "omega", "integral", "prev_omega",
                                                 "omega_sp", "f_c_sp", "alive")})
+    for q in outs[0]:
+        np.testing.assert_array_equal(outs[0][q], outs[1][q], err_msg=q)
+
+
+def test_pair_kernel_fault_fallback_bit_identical():
+    """A lane fault inside a pair falls back to the scalar path for both rows."""
+    from paper_2308_12698_b200 import AgentCommand, CommandLevel
+    sc = ALL["fault_nan"](n=256, ticks=3)
+    outs, faults = [], []
+    for kern in ("direct", "pair"):
+        g = make_group(sc)
+        g.kernel = kern
+        run_script(g, Scenario(**{**sc.__dict__, "record": []}))
+        g.apply_command(AgentCommand(70, CommandLevel.RATE, (0.0, 0.0, 0.0, float("nan"))))
+        g.step_async(sc.dt, 6)
+        faults.append([f.tolist() for f in g.collect_faults()])
+        st = gpu_state(g)
+        outs.append({q: st[q].copy() for q in ("pos", "vel", "quat", "omega", "integral", "alive")})
+    assert faults[0] == faults[1] and faults[0][0] == [70]
     for q in outs[0]:
         np.testing.assert_array_equal(outs[0][q], outs[1][q], err_msg=q)

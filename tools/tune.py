@@ -16,9 +16,8 @@ sys.path.insert(0, str(ROOT))
 
 VARIANTS = {
     "default": [],
-    "m5": ["-DSSB_STEP_MINB=5"],
-    "tst4": ["-DSSB_TMA_MINB=3", "-DSSB_TMA_STAGES=4"],
-    "tst2m5": ["-DSSB_TMA_MINB=5", "-DSSB_TMA_STAGES=2"],
+    "p5": ["-DSSB_PAIR_MINB=5"],
+    "p8": ["-DSSB_PAIR_MINB=8"],
 }
 
 CHILD = r'''
@@ -54,7 +53,7 @@ def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 4_000_000
     from paper_2308_12698_b200._build import NVCC_FLAGS, _nvcc, sources, INCLUDE, CSRC
     res = {}
-    runs = [(name, defs, kern) for name, defs in VARIANTS.items() for kern in ("direct", "tma")]
+    runs = [(name, defs, kern) for name, defs in VARIANTS.items() for kern in ("direct", "pair")]
     for name, defs, kern in runs:
         so = f"/tmp/ssb_{name}.so"
         cmd = [_nvcc(), *NVCC_FLAGS, *defs, f"-I{INCLUDE}", f"-I{CSRC}", "-o", so, *map(str, sources())]
