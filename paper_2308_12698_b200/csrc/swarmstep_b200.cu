@@ -53,7 +53,7 @@ struct Cols {
 #endif
 constexpr int kTickUnroll = SSB_TICK_UNROLL;
 #ifndef SSB_PAIR_MIN_K
-#define SSB_PAIR_MIN_K 1000000   // auto picks the paired (FFMA2) kernel from this many ticks per launch
+#define SSB_PAIR_MIN_K 2   // auto picks the paired (FFMA2) kernel from this many ticks per launch
 #endif
 #ifndef SSB_TMA_MAX_K
 #define SSB_TMA_MAX_K 0   // auto never picks the TMA-staged kernel (measured slower)
@@ -300,7 +300,7 @@ quad_step_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t 
 // path.  Both paths are the same templates with explicitly rounded ops, so
 // every row's result is bit-identical to the direct kernel's.
 #ifndef SSB_PAIR_MINB
-#define SSB_PAIR_MINB 6
+#define SSB_PAIR_MINB 8   // 128 regs: 16 warps per SM (measured best, profiles/tune_r01_v4.json)
 #endif
 template <bool COMP>
 __global__ void __launch_bounds__(64, SSB_PAIR_MINB)
