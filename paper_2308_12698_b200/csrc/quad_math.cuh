@@ -131,7 +131,8 @@ template <class T> __device__ __forceinline__ T clip(T x, T lo, T hi)
 }
 
 // ---------------------------------------------------------------------------
-// Per-tick constants derived from the per-type struct (hoisted by the caller)
+// Per-launch constants derived from the per-type struct on the host and passed
+// as a kernel parameter (constant bank: no per-thread registers)
 // ---------------------------------------------------------------------------
 struct Derived {
     float g;
@@ -139,7 +140,7 @@ struct Derived {
     float kd_dt[3];          // kd / dt
 };
 
-__device__ __forceinline__ Derived derive(const swarmstep_quad_params &P, float inv_dt)
+__host__ __device__ __forceinline__ Derived derive(const swarmstep_quad_params &P, float inv_dt)
 {
     Derived d;
     d.g = P.g;

@@ -245,7 +245,7 @@ __device__ __forceinline__ int run_level(const A &C, int level, int overlay_acti
 // readable through C at that point (global memory, or the staged tile).
 template <bool COMP, class A>
 __device__ __forceinline__ uint8_t step_row(const A &C, uint8_t fl, int64_t r, int overlay_active,
-                                            const swarmstep_quad_params &P, float dt, int K,
+                                            const swarmstep_quad_params &P, const ssb::Derived &D, float dt, int K,
                                             uint32_t tick_base, const int64_t *tick_dev,
                                             uint32_t *counters, uint64_t *fault_log, int64_t fault_cap)
 {
@@ -254,7 +254,6 @@ __device__ __forceinline__ uint8_t step_row(const A &C, uint8_t fl, int64_t r, i
     const int level = (fl & SWARMSTEP_LEVEL_MASK) >> SWARMSTEP_LEVEL_SHIFT;
     const bool has_prev = (fl & SWARMSTEP_FLAG_HAS_PREV) != 0;
     setup_level(C, level, overlay_active, P, has_prev, R);
-    const ssb::Derived D = ssb::derive(P, 1.0f / dt);
     const int fault_k = run_level<COMP, false>(C, level, overlay_active, P, D, dt, K, -1, R);
     bool alive = true;
     if (fault_k >= 0) {
@@ -278,14 +277,14 @@ __global__ void __launch_bounds__(kBlock, SSB_STEP_MINB)
 quad_step_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t n,
                  uint32_t *__restrict__ counters, uint64_t *__restrict__ fault_log,
                  int64_t fault_cap, int overlay_active, uint32_t tick_base, const int64_t *tick_dev,
-                 const swarmstep_quad_params P, float dt, int K)
+                 const swarmstep_quad_params P, const ssb::Derived D, float dt, int K)
 {
     const int64_t r = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     if (r >= n) return;
     const uint8_t fl = flags[r];
     if (!(fl & SWARMSTEP_FLAG_ALIVE)) return;  // dead rows are frozen (quad.py:395-437)
     const GlobalRow C{cols + ssb::tile_base(r)};
-    const uint8_t nfl = step_row<COMP>(C, fl, r, overlay_active, P, dt, K, tick_base, tick_dev,
+    const uint8_t nfl = step_row<COMP>(C, fl, r, overlay_active, P, D, dt, K, tick_base, tick_dev,
                                        counters, fault_log, fault_cap);
     if (nfl != fl) flags[r] = nfl;
 }
@@ -307,7 +306,7 @@ __global__ void __launch_bounds__(64, SSB_PAIR_MINB)
 quad_step_pair_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t n,
                       uint32_t *__restrict__ counters, uint64_t *__restrict__ fault_log,
                       int64_t fault_cap, int overlay_active, uint32_t tick_base, const int64_t *tick_dev,
-                      const swarmstep_quad_params P, float dt, int K)
+                      const swarmstep_quad_params P, const ssb::Derived D, float dt, int K)
 {
     const int64_t r0 = (int64_t)blockIdx.x * SWARMSTEP_TILE + threadIdx.x, r1 = r0 + 64;
     if (r0 >= n) return;
@@ -323,7 +322,6 @@ quad_step_pair_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int
         load_state<COMP>(C, R);
         const ssb::m2 hp{(f0 & SWARMSTEP_FLAG_HAS_PREV) != 0, (f1 & SWARMSTEP_FLAG_HAS_PREV) != 0};
         setup_level(C, l0, overlay_active, P, hp, R);
-        const ssb::Derived D = ssb::derive(P, 1.0f / dt);
         if (run_level<COMP, false>(C, l0, overlay_active, P, D, dt, K, -1, R) >= 0) {
             scalar = true;     // a lane faulted: redo both rows on the scalar path
         } else {
@@ -335,12 +333,12 @@ quad_step_pair_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int
     }
     if (scalar) {
         if (a0) {
-            const uint8_t nf = step_row<COMP>(C0, f0, r0, overlay_active, P, dt, K, tick_base, tick_dev,
+            const uint8_t nf = step_row<COMP>(C0, f0, r0, overlay_active, P, D, dt, K, tick_base, tick_dev,
                                               counters, fault_log, fault_cap);
             if (nf != f0) flags[r0] = nf;
         }
         if (a1) {
-            const uint8_t nf = step_row<COMP>(C1, f1, r1, overlay_active, P, dt, K, tick_base, tick_dev,
+            const uint8_t nf = step_row<COMP>(C1, f1, r1, overlay_active, P, D, dt, K, tick_base, tick_dev,
                                               counters, fault_log, fault_cap);
             if (nf != f1) flags[r1] = nf;
         }
@@ -415,7 +413,7 @@ __global__ void __launch_bounds__(SWARMSTEP_TILE, SSB_TMA_MINB)
 quad_step_tma_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t ntiles,
                      uint32_t *__restrict__ counters, uint64_t *__restrict__ fault_log, int64_t fault_cap,
                      int overlay_active, int motor_possible, uint32_t tick_base, const int64_t *tick_dev,
-                     const swarmstep_quad_params P, float dt, int K)
+                     const swarmstep_quad_params P, const ssb::Derived D, float dt, int K)
 {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     TmaSmem &S = *reinterpret_cast<TmaSmem *>(smem_raw);
@@ -448,7 +446,7 @@ quad_step_tma_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int6
         const int64_t r = t * SWARMSTEP_TILE + tid;
         const SmemRow C{T + tid};
         if (fl & SWARMSTEP_FLAG_ALIVE) {
-            const uint8_t nfl = step_row<COMP>(C, fl, r, overlay_active, P, dt, K, tick_base, tick_dev,
+            const uint8_t nfl = step_row<COMP>(C, fl, r, overlay_active, P, D, dt, K, tick_base, tick_dev,
                                                counters, fault_log, fault_cap);
             if (nfl != fl) flags[r] = nfl;
         } else if (!motor_possible && !overlay_active) {
@@ -645,6 +643,7 @@ int swarmstep_quad_step(const swarmstep_group_view *g, const swarmstep_quad_para
     if (k_substeps < 1) return set_err(SWARMSTEP_EINVAL, "k_substeps must be >= 1");
     if (!g->counters) return set_err(SWARMSTEP_EINVAL, "null counters");
     if (g->n == 0) return SWARMSTEP_OK;
+    const ssb::Derived D = ssb::derive(*p, 1.0f / dt);
     const int overlay = launch_flags & SWARMSTEP_STEP_OVERLAY;
     const int motor = (launch_flags & SWARMSTEP_STEP_MOTOR) ? 1 : 0;
     const bool use_tma = (launch_flags & SWARMSTEP_STEP_FORCE_DIRECT) ? false
@@ -670,20 +669,20 @@ int swarmstep_quad_step(const swarmstep_group_view *g, const swarmstep_quad_para
         if (grid > ntiles) grid = ntiles;
         kern<<<(unsigned)grid, SWARMSTEP_TILE, smem, (cudaStream_t)stream>>>(
             g->cols, g->flags, ntiles, g->counters, g->fault_log, fcap, overlay, motor, tick_base, tick_dev,
-            *p, dt, k_substeps);
+            *p, D, dt, k_substeps);
         return cuda_status("quad_step_tma_kernel");
     }
     if (!(launch_flags & SWARMSTEP_STEP_FORCE_DIRECT) &&
         ((launch_flags & SWARMSTEP_STEP_FORCE_PAIR) || k_substeps >= SSB_PAIR_MIN_K)) {
         auto kern = g->compensated ? quad_step_pair_kernel<true> : quad_step_pair_kernel<false>;
         kern<<<(unsigned)((g->n + SWARMSTEP_TILE - 1) / SWARMSTEP_TILE), 64, 0, (cudaStream_t)stream>>>(
-            g->cols, g->flags, g->n, g->counters, g->fault_log, fcap, overlay, tick_base, tick_dev, *p, dt,
+            g->cols, g->flags, g->n, g->counters, g->fault_log, fcap, overlay, tick_base, tick_dev, *p, D, dt,
             k_substeps);
         return cuda_status("quad_step_pair_kernel");
     }
     auto kern = g->compensated ? quad_step_kernel<true> : quad_step_kernel<false>;
     kern<<<grid_for(g->n, kBlock), kBlock, 0, (cudaStream_t)stream>>>(
-        g->cols, g->flags, g->n, g->counters, g->fault_log, fcap, overlay, tick_base, tick_dev, *p, dt,
+        g->cols, g->flags, g->n, g->counters, g->fault_log, fcap, overlay, tick_base, tick_dev, *p, D, dt,
         k_substeps);
     return cuda_status("quad_step_kernel");
 }

@@ -16,8 +16,8 @@ sys.path.insert(0, str(ROOT))
 
 VARIANTS = {
     "default": [],
-    "p5": ["-DSSB_PAIR_MINB=5"],
-    "p8": ["-DSSB_PAIR_MINB=8"],
+    "p6": ["-DSSB_PAIR_MINB=6"],
+    "p7": ["-DSSB_PAIR_MINB=7"],
 }
 
 CHILD = r'''
