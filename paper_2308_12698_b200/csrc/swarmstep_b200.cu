@@ -115,6 +115,24 @@ __device__ __forceinline__ void load_state(const A &C, RowT<T> &R)
     R.u[7] = zero_t<T>();
 }
 
+// Materialise the loaded row before a branch: ptxas would otherwise sink the
+// loads behind the kernel's alive test, serialising two memory round trips
+// (flags, then state) instead of overlapping them.
+__device__ __forceinline__ void pin(float v) { asm volatile("" ::"f"(v)); }
+template <bool COMP>
+__device__ __forceinline__ void pin_row(const Row &R)
+{
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+        pin(R.p_hi[i]); pin(R.v[i]); pin(R.w[i]); pin(R.integ[i]); pin(R.prev[i]);
+        if (COMP) pin(R.p_lo[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; i++) pin(R.q[i]);
+#pragma unroll
+    for (int i = 0; i < 7; i++) pin(R.u[i]);
+}
+
 template <bool COMP, class T, class A>
 __device__ __forceinline__ void store_state(const A &C, int level, const RowT<T> &R)
 {
@@ -247,10 +265,10 @@ template <bool COMP, class A>
 __device__ __forceinline__ uint8_t step_row(const A &C, uint8_t fl, int64_t r, int overlay_active,
                                             const swarmstep_quad_params &P, const ssb::Derived &D, float dt, int K,
                                             uint32_t tick_base, const int64_t *tick_dev,
-                                            uint32_t *counters, uint64_t *fault_log, int64_t fault_cap)
+                                            uint32_t *counters, uint64_t *fault_log, int64_t fault_cap,
+                                            Row &R, bool preloaded = false)
 {
-    Row R;
-    load_state<COMP>(C, R);
+    if (!preloaded) load_state<COMP>(C, R);
     const int level = (fl & SWARMSTEP_LEVEL_MASK) >> SWARMSTEP_LEVEL_SHIFT;
     const bool has_prev = (fl & SWARMSTEP_FLAG_HAS_PREV) != 0;
     setup_level(C, level, overlay_active, P, has_prev, R);
@@ -281,11 +299,16 @@ quad_step_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t 
 {
     const int64_t r = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     if (r >= n) return;
+    // every state load is issued before the flag test: one memory round trip
+    // per row (dead rows are rare; their loads are discarded)
     const uint8_t fl = flags[r];
-    if (!(fl & SWARMSTEP_FLAG_ALIVE)) return;  // dead rows are frozen (quad.py:395-437)
     const GlobalRow C{cols + ssb::tile_base(r)};
+    Row R;
+    load_state<COMP>(C, R);
+    pin_row<COMP>(R);
+    if (!(fl & SWARMSTEP_FLAG_ALIVE)) return;  // dead rows are frozen (quad.py:395-437)
     const uint8_t nfl = step_row<COMP>(C, fl, r, overlay_active, P, D, dt, K, tick_base, tick_dev,
-                                       counters, fault_log, fault_cap);
+                                       counters, fault_log, fault_cap, R, true);
     if (nfl != fl) flags[r] = nfl;
 }
 
@@ -332,14 +355,15 @@ quad_step_pair_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int
         }
     }
     if (scalar) {
+        Row Rs;
         if (a0) {
             const uint8_t nf = step_row<COMP>(C0, f0, r0, overlay_active, P, D, dt, K, tick_base, tick_dev,
-                                              counters, fault_log, fault_cap);
+                                              counters, fault_log, fault_cap, Rs);
             if (nf != f0) flags[r0] = nf;
         }
         if (a1) {
             const uint8_t nf = step_row<COMP>(C1, f1, r1, overlay_active, P, D, dt, K, tick_base, tick_dev,
-                                              counters, fault_log, fault_cap);
+                                              counters, fault_log, fault_cap, Rs);
             if (nf != f1) flags[r1] = nf;
         }
     }
@@ -446,8 +470,9 @@ quad_step_tma_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int6
         const int64_t r = t * SWARMSTEP_TILE + tid;
         const SmemRow C{T + tid};
         if (fl & SWARMSTEP_FLAG_ALIVE) {
+            Row Rs;
             const uint8_t nfl = step_row<COMP>(C, fl, r, overlay_active, P, D, dt, K, tick_base, tick_dev,
-                                               counters, fault_log, fault_cap);
+                                               counters, fault_log, fault_cap, Rs);
             if (nfl != fl) flags[r] = nfl;
         } else if (!motor_possible && !overlay_active) {
             // dead row, stale setpoints not staged: store zeros, not stale smem

@@ -49,8 +49,20 @@ print("RESULT " + json.dumps(out))
 '''
 
 
+def run_prebuilt(so, kern, n):
+    env = dict(os.environ, SWARMSTEP_B200_LIB_OVERRIDE=str(so), TUNE_KERNEL=kern)
+    p = subprocess.run([sys.executable, "-c", CHILD % dict(root=ROOT, n=n)], env=env, capture_output=True, text=True)
+    line = [l for l in p.stdout.splitlines() if l.startswith("RESULT ")]
+    return json.loads(line[0][7:]) if line else {"error": p.stderr[-800:]}
+
+
 def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 4_000_000
+    if len(sys.argv) > 2:   # compare prebuilt libraries: tune.py N a.so b.so ...
+        for so in sys.argv[2:]:
+            for kern in ("direct", "pair"):
+                print(so, kern, json.dumps(run_prebuilt(so, kern, n)), flush=True)
+        return
     from paper_2308_12698_b200._build import NVCC_FLAGS, _nvcc, sources, INCLUDE, CSRC
     res = {}
     runs = [(name, defs, kern) for name, defs in VARIANTS.items() for kern in ("direct", "pair")]
