@@ -71,6 +71,24 @@ struct RowT {
 };
 using Row = RowT<float>;
 
+// one lane of a paired row
+__device__ __forceinline__ Row lane_row(const RowT<ssb::f2> &R, int i)
+{
+    Row o;
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+        o.p_hi[k] = ssb::lane(R.p_hi[k], i); o.p_lo[k] = ssb::lane(R.p_lo[k], i); o.v[k] = ssb::lane(R.v[k], i);
+        o.w[k] = ssb::lane(R.w[k], i); o.integ[k] = ssb::lane(R.integ[k], i); o.prev[k] = ssb::lane(R.prev[k], i);
+        o.w_sp[k] = ssb::lane(R.w_sp[k], i);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; k++) o.q[k] = ssb::lane(R.q[k], i);
+#pragma unroll
+    for (int k = 0; k < 8; k++) o.u[k] = ssb::lane(R.u[k], i);
+    o.f_sp = ssb::lane(R.f_sp, i);
+    return o;
+}
+
 // Row accessors: the same step code reads a row from global memory (direct
 // kernels, streaming loads) or from a shared-memory tile staged by TMA.
 struct GlobalRow {
@@ -113,24 +131,6 @@ __device__ __forceinline__ void load_state(const A &C, RowT<T> &R)
 #pragma unroll
     for (int i = 0; i < 7; i++) R.u[i] = C.ld(SWARMSTEP_COL_CMD + i);
     R.u[7] = zero_t<T>();
-}
-
-// Materialise the loaded row before a branch: ptxas would otherwise sink the
-// loads behind the kernel's alive test, serialising two memory round trips
-// (flags, then state) instead of overlapping them.
-__device__ __forceinline__ void pin(float v) { asm volatile("" ::"f"(v)); }
-template <bool COMP>
-__device__ __forceinline__ void pin_row(const Row &R)
-{
-#pragma unroll
-    for (int i = 0; i < 3; i++) {
-        pin(R.p_hi[i]); pin(R.v[i]); pin(R.w[i]); pin(R.integ[i]); pin(R.prev[i]);
-        if (COMP) pin(R.p_lo[i]);
-    }
-#pragma unroll
-    for (int i = 0; i < 4; i++) pin(R.q[i]);
-#pragma unroll
-    for (int i = 0; i < 7; i++) pin(R.u[i]);
 }
 
 template <bool COMP, class T, class A>
@@ -305,7 +305,10 @@ quad_step_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t 
     const GlobalRow C{cols + ssb::tile_base(r)};
     Row R;
     load_state<COMP>(C, R);
-    pin_row<COMP>(R);
+    // Keep every load of the row ahead of the first use: without this fence
+    // ptxas sinks the level-specific command loads behind the level branch,
+    // adding a second dependent memory round trip to the HBM-bound K = 1 case.
+    __threadfence_block();
     if (!(fl & SWARMSTEP_FLAG_ALIVE)) return;  // dead rows are frozen (quad.py:395-437)
     const uint8_t nfl = step_row<COMP>(C, fl, r, overlay_active, P, D, dt, K, tick_base, tick_dev,
                                        counters, fault_log, fault_cap, R, true);
@@ -338,34 +341,41 @@ quad_step_pair_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int
     const int l0 = (f0 & SWARMSTEP_LEVEL_MASK) >> SWARMSTEP_LEVEL_SHIFT;
     const int l1 = (f1 & SWARMSTEP_LEVEL_MASK) >> SWARMSTEP_LEVEL_SHIFT;
     const GlobalRow C0{cols + ssb::tile_base(r0)}, C1{cols + ssb::tile_base(r1)};
-    bool scalar = !(a0 && a1 && l0 == l1 && l0 != SWARMSTEP_LEVEL_MOTOR);
-    if (!scalar) {
-        const PairRow<GlobalRow> C{C0, C1};
-        RowT<ssb::f2> R;
-        load_state<COMP>(C, R);
+    const PairRow<GlobalRow> C{C0, C1};
+    // both rows' loads in flight before any decision (see quad_step_kernel)
+    RowT<ssb::f2> R;
+    load_state<COMP>(C, R);
+    __threadfence_block();
+    const bool paired = a0 && a1 && l0 == l1 && l0 != SWARMSTEP_LEVEL_MOTOR;
+    bool reload = false;
+    if (paired) {
         const ssb::m2 hp{(f0 & SWARMSTEP_FLAG_HAS_PREV) != 0, (f1 & SWARMSTEP_FLAG_HAS_PREV) != 0};
         setup_level(C, l0, overlay_active, P, hp, R);
         if (run_level<COMP, false>(C, l0, overlay_active, P, D, dt, K, -1, R) >= 0) {
-            scalar = true;     // a lane faulted: redo both rows on the scalar path
+            // a lane faulted: redo both rows on the scalar path from the
+            // launch's inputs, still untouched in HBM
+            reload = true;
         } else {
             store_state<COMP>(C, l0, R);
             const uint8_t hpf = SWARMSTEP_FLAG_HAS_PREV;
             if ((f0 | hpf) != f0) flags[r0] = f0 | hpf;
             if ((f1 | hpf) != f1) flags[r1] = f1 | hpf;
+            return;
         }
     }
-    if (scalar) {
-        Row Rs;
-        if (a0) {
-            const uint8_t nf = step_row<COMP>(C0, f0, r0, overlay_active, P, D, dt, K, tick_base, tick_dev,
-                                              counters, fault_log, fault_cap, Rs);
-            if (nf != f0) flags[r0] = nf;
-        }
-        if (a1) {
-            const uint8_t nf = step_row<COMP>(C1, f1, r1, overlay_active, P, D, dt, K, tick_base, tick_dev,
-                                              counters, fault_log, fault_cap, Rs);
-            if (nf != f1) flags[r1] = nf;
-        }
+    // scalar path per row: the loaded lanes (dead partner, mixed or MOTOR
+    // levels) or a fresh load (after a fault in the pair)
+    if (a0) {
+        Row Rs = lane_row(R, 0);
+        const uint8_t nf = step_row<COMP>(C0, f0, r0, overlay_active, P, D, dt, K, tick_base, tick_dev,
+                                          counters, fault_log, fault_cap, Rs, !reload);
+        if (nf != f0) flags[r0] = nf;
+    }
+    if (a1) {
+        Row Rs = lane_row(R, 1);
+        const uint8_t nf = step_row<COMP>(C1, f1, r1, overlay_active, P, D, dt, K, tick_base, tick_dev,
+                                          counters, fault_log, fault_cap, Rs, !reload);
+        if (nf != f1) flags[r1] = nf;
     }
 }
 
