@@ -22,6 +22,7 @@ import numpy as np
 import torch
 
 from . import _lib
+from ._lib import COL_OVERLAY, STEP_OVERLAY
 from .errors import ValidationError
 
 
@@ -65,9 +66,11 @@ class CircleFeed:
 
 
 class TickGraph:
-    """``ticks`` ticks of [feed ->] fused step (K=1 each) as one CUDA graph."""
+    """``ticks`` ticks of [feed ->] [neighbour coupling ->] fused step (K=1 each)
+    as one CUDA graph.  ``coupling`` is a ``parallel.NeighborSeparation`` on a
+    single-rank shard (its exchange is then device-only)."""
 
-    def __init__(self, group, dt: float, ticks: int, feed: CircleFeed | None = None):
+    def __init__(self, group, dt: float, ticks: int, feed: CircleFeed | None = None, coupling=None):
         if ticks < 1:
             raise ValidationError("ticks must be >= 1")
         if group._overlay_active:
@@ -75,6 +78,9 @@ class TickGraph:
         group._flush_commands()
         self.group, self.dt, self.ticks = group, float(dt), int(ticks)
         self.feed = feed
+        if coupling is not None and coupling.shard.world != 1:
+            raise ValidationError("graph-captured coupling needs a single-rank shard (no NCCL in the graph)")
+        self.coupling = coupling
         self._lib = _lib.load()
         with torch.cuda.device(group.device):
             self.tick = feed.tick if feed is not None else torch.full(
@@ -90,11 +96,17 @@ class TickGraph:
     def _body(self) -> None:
         g = self.group
         s = ctypes.c_void_p(g.stream.cuda_stream)
+        flags = g._launch_flags() | (STEP_OVERLAY if self.coupling is not None else 0)
         for j in range(self.ticks):
             if self.feed is not None:
                 self.feed.apply(j, sync_tick=False)
+            if self.coupling is not None:
+                self.coupling.launch(accumulate=False)     # overwrites the overlay block
             _lib.check(self._lib.swarmstep_quad_step(g._view_ref, g._params_ref, ctypes.c_float(self.dt), 1,
-                                                     g._launch_flags(), ctypes.c_uint32(j), self.tick.data_ptr(), s))
+                                                     flags, ctypes.c_uint32(j), self.tick.data_ptr(), s))
+        if self.coupling is not None:
+            with torch.cuda.stream(g.stream):
+                g._cols[:, COL_OVERLAY:COL_OVERLAY + 3, :].zero_()   # one-tick overlay: leave it clear
         _lib.check(self._lib.swarmstep_tick_add(self.tick.data_ptr(), self.ticks, s))
 
     def replay(self) -> None:

@@ -149,18 +149,25 @@ class NeighborSeparation:
                 dist.all_gather_into_tensor(self.all, self.local, group=self.pg)
         return self.all
 
-    def apply(self) -> None:
+    def launch(self, accumulate: bool = True) -> None:
+        """Device work of one exchange: pack -> all-gather -> overlay kernel (no
+        host state change; graph-capturable when world == 1)."""
         g = self.group
         self.gather()
-        # the overlay block is all-zero whenever no overlay is pending (the group
-        # clears it after every step), so the kernel always accumulates
         with torch.cuda.device(g.device), torch.cuda.stream(g.stream):
             _lib.check(self._lib.swarmstep_neighbor_overlay(
                 g._view_ref, self.all.data_ptr(), self.n_all, self.shard.self_offset,
-                ctypes.c_float(self.r_sense), ctypes.c_float(self.k_sep), ctypes.c_float(self.cell), 1,
-                self.workspace.data_ptr(), ctypes.c_uint64(self.workspace.numel()),
+                ctypes.c_float(self.r_sense), ctypes.c_float(self.k_sep), ctypes.c_float(self.cell),
+                1 if accumulate else 0, self.workspace.data_ptr(), ctypes.c_uint64(self.workspace.numel()),
                 ctypes.c_void_p(g.stream.cuda_stream)))
-        g._overlay_active = True
+
+    def apply(self) -> None:
+        """Compute this tick's separation overlay into the group's one-tick
+        overlay input (added to any overlay already pending)."""
+        # the overlay block is all-zero whenever no overlay is pending (the
+        # group clears it after every step), so accumulating is always right
+        self.launch(accumulate=True)
+        self.group._overlay_active = True
 
     def step(self, dt: float) -> np.ndarray:
         self.apply()

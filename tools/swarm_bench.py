@@ -74,13 +74,29 @@ def main():
         ns.step(1e-3)
     torch.cuda.synchronize()
     wall_ms = (time.perf_counter() - t0) / ticks * 1e3
+    graph_ms = float("nan")
+    if world == 1:
+        # (c) the whole tick chain captured as CUDA graphs of 50 ticks
+        from paper_2308_12698_b200.feed import TickGraph
+        tg = TickGraph(g, 1e-3, 50, coupling=ns)
+        tg.replay()
+        g.collect_faults()
+        torch.cuda.synchronize()
+        e0.record(g.stream)
+        reps = max(1, ticks // 50)
+        for _ in range(reps):
+            tg.replay()
+        e1.record(g.stream)
+        torch.cuda.synchronize()
+        g.collect_faults()
+        graph_ms = e0.elapsed_time(e1) / (reps * 50)
     vals = torch.tensor([dev_ms, wall_ms], dtype=torch.float64, device=f"cuda:{local}")
     if world > 1:
         torch.distributed.all_reduce(vals, op=torch.distributed.ReduceOp.MAX)
     if rank == 0:
         print(json.dumps({"config": "cfg5 neighbour-coupled swarm", "agents_total": n_total, "world": world,
                           "r_sense": 2.0, "ticks": ticks, "device_ms_per_tick": float(vals[0]),
-                          "wall_ms_per_tick": float(vals[1]),
+                          "wall_ms_per_tick": float(vals[1]), "graph_ms_per_tick": graph_ms,
                           "agent_steps_per_s_device": n_total / (float(vals[0]) * 1e-3),
                           "alive": int(g.batch.alive.sum())}), flush=True)
     if world > 1:
