@@ -1,0 +1,151 @@
+"""CPU tests of the host-side pieces that need no GPU: parameter packing,
+command levels, layouts, wire framing, collision helpers, scenario fixtures,
+and property checks with hypothesis."""
+
+import math
+import struct
+
+import numpy as np
+import pytest
+from hypothesis import given, settings
+from hypothesis import strategies as st
+
+from paper_2308_12698_b200 import (AgentCommand, CommandLevel, OuterGains, PidGains, QuadParams,
+                                   ValidationError, batch_create, quat_yaw, yaw_quat)
+from paper_2308_12698_b200.collision import CollisionConfig, half_space_offsets
+from paper_2308_12698_b200.commands import LEVEL_MOTOR, LEVEL_POS, LEVEL_RATE, level_code
+from paper_2308_12698_b200.layout import layout_poses
+from paper_2308_12698_b200.params import allocation_matrices, pack_device_params
+from paper_2308_12698_b200.parallel import shard_range
+from paper_2308_12698_b200.wire import encode_frame, snapshot_frame
+
+
+def test_params_validation_mirrors_reference():
+    # quad.py:56-60, test_quad.py:67-69
+    with pytest.raises(ValidationError):
+        QuadParams(m=0.0)
+    with pytest.raises(ValidationError):
+        QuadParams(arm_angle=1e-300)
+    with pytest.raises(ValidationError):
+        PidGains(kp=-1.0, ki=0.0, kd=0.0, i_limit=1.0)
+    assert QuadParams().f_motor_max == pytest.approx(16.0)
+    assert QuadParams().hover_thrust == pytest.approx(9.81)
+
+
+@settings(max_examples=40, deadline=None)
+@given(st.floats(0.05, 1.0), st.floats(0.2, 1.3), st.floats(1e-9, 1e-7), st.floats(1e-11, 1e-9))
+def test_allocation_inverse_structure(arm, angle, k_t, k_q):
+    """G^-1 = sign(G^T) * c holds for every X-geometry the kernel's mixer accepts."""
+    p = QuadParams(arm_length=arm, arm_angle=angle, k_t=k_t, k_q=k_q)
+    g, gi = allocation_matrices(p)
+    np.testing.assert_allclose(gi @ g, np.eye(4), atol=1e-9)
+    np.testing.assert_allclose(gi, np.sign(g.T) * np.abs(gi[0]), rtol=1e-9)
+    pack_device_params(p, PidGains(kp=0.1, ki=0.1, kd=0.1, i_limit=0.1), OuterGains(kp_pos=1, kv=1, k_att=1))
+
+
+def test_level_codes():
+    assert level_code(CommandLevel.POS) == LEVEL_POS and level_code("rate") == LEVEL_RATE
+    assert level_code(CommandLevel.MOTOR) == LEVEL_MOTOR
+    assert level_code(CommandLevel.UNICYCLE) is None and level_code(7) is None
+    with pytest.raises(ValidationError):
+        AgentCommand(1, CommandLevel.POS, (1.0, 2.0))
+
+
+def test_layouts_match_reference_shapes():
+    pos, yaw = layout_poses({"kind": "grid", "spacing": 3.0, "origin": (0, 0, 10)}, 10)
+    assert pos.shape == (10, 3) and pos[5].tolist() == [3.0, 3.0, 10.0] and np.all(yaw == 0)
+    pos, yaw = layout_poses({"kind": "circle", "radius": 5.0, "z": 2.0}, 4)
+    np.testing.assert_allclose(pos[1], [0.0, 5.0, 2.0], atol=1e-12)
+    np.testing.assert_allclose(yaw[0], np.pi / 2)
+    with pytest.raises(ValidationError):
+        layout_poses({"kind": "spiral"}, 3)
+
+
+@settings(max_examples=50, deadline=None)
+@given(st.floats(-3.1, 3.1))
+def test_yaw_quat_roundtrip(theta):
+    assert quat_yaw(yaw_quat(theta)) == pytest.approx(theta, abs=1e-12)
+
+
+def test_batch_create_mirrors_reference():
+    b = batch_create(0, 3, np.zeros((3, 3)), id_base=100)
+    assert b.agent_ids.tolist() == [100, 101, 102] and b.alive.all()
+    with pytest.raises(ValidationError):
+        batch_create(0, 1, [[0, 0, 0]], quat=[[1.0, 1.0, 0, 0]])
+    with pytest.raises(ValidationError):
+        batch_create(0, 2, np.zeros((2, 3)), agent_ids=[7, 7])
+
+
+def test_encode_frame_and_snapshot_frame_layout():
+    # PROTOCOL.md framing example: {"op":"stop"} -> 0E 00 00 00 05 + payload
+    payload = b'{"op":"stop"}'
+    assert encode_frame(5, payload) == bytes.fromhex("0e00000005") + payload
+
+    class G:
+        def __init__(self, t, n):
+            self.type_id, self.n = t, n
+
+        def wire_section(self):
+            return struct.pack("<HI", self.type_id, self.n) + b"x" * (61 * self.n)
+
+    frame = snapshot_frame(9, [G(2, 1), G(0, 2)], empty_types=[1])
+    assert frame[4] == 1 and struct.unpack_from("<Q", frame, 5)[0] == 9
+    types = []
+    off = 13
+    while off < len(frame):
+        t, n = struct.unpack_from("<HI", frame, off)
+        types.append(t)
+        off += 6 + 61 * n
+    assert types == [0, 1, 2] and off == len(frame)
+
+
+def test_collision_config_and_offsets_mirror_reference():
+    with pytest.raises(ValidationError):
+        CollisionConfig(r_collide={0: 0.5}, r_sense=0.4, cell=1.0)    # r_collide > r_sense
+    with pytest.raises(ValidationError):
+        CollisionConfig(r_collide={0: 0.5}, r_sense=1.0, cell=0.9)    # cell < 2 r
+    offs = half_space_offsets(1, 1.0, 1.0)
+    assert len(offs) == 13                       # half of the 26 neighbours
+    keys = {tuple(o) for o in offs}
+    assert all((-a, -b, -c) not in keys for a, b, c in keys)
+    offs2 = half_space_offsets(2, 2.0, 1.0)
+    assert all(np.sum((np.maximum(np.abs(o) - 1, 0)) ** 2) < 4.0 for o in offs2)
+
+
+@settings(max_examples=60, deadline=None)
+@given(st.integers(0, 10**8), st.integers(1, 64))
+def test_shards_partition(n, world):
+    rs = [shard_range(n, r, world) for r in range(world)]
+    assert rs[0][0] == 0 and rs[-1][1] == n
+    assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
+    sizes = [hi - lo for lo, hi in rs]
+    assert max(sizes) - min(sizes) <= 1
+
+
+@settings(max_examples=25, deadline=None)
+@given(st.integers(1, 40), st.integers(0, 2**31))
+def test_oracle_rows_are_independent(n, seed):
+    """The float64 oracle's rows do not interact: stepping a subset equals the
+    same rows of the full batch (the property the GPU parity tests rely on)."""
+    from oracle import oracle as orc
+    rng = np.random.default_rng(seed)
+    q = rng.standard_normal((n, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+
+    class B:
+        agent_ids = np.arange(n, dtype=np.uint64)
+        pos, vel, quat = rng.uniform(-5, 5, (n, 3)), rng.uniform(-1, 1, (n, 3)), q
+        omega, alive = rng.uniform(-1, 1, (n, 3)), np.ones(n, bool)
+
+    full = orc.OracleGroup(0, B)
+    rows = np.sort(rng.choice(n, max(1, n // 2), replace=False))
+
+    class S:
+        agent_ids = B.agent_ids[rows]
+        pos, vel, quat, omega, alive = B.pos[rows], B.vel[rows], B.quat[rows], B.omega[rows], B.alive[rows]
+
+    sub = orc.OracleGroup(0, S)
+    for _ in range(5):
+        full.step(1e-3)
+        sub.step(1e-3)
+    np.testing.assert_array_equal(full.state13()[rows], sub.state13())
