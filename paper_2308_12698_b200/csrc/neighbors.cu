@@ -11,9 +11,9 @@
 // Pipeline per tick (one process per GPU): pack the local shard's positions
 // (float4, NaN for dead rows) -> NCCL all-gather across ranks (host side,
 // torch.distributed) -> spatial hash of every gathered agent -> radix sort
-// (CUB) -> bucket ranges -> per local agent, scan the 27 neighbouring cells.
-// Summation order is fixed (cell order, then agent index), so results are
-// bit-deterministic.
+// (CUB) -> bucket lower bounds + positions gathered into bucket order -> one
+// thread per local agent, in bucket order, scans the 9 x-rows of its 27
+// neighbouring cells.  Summation order is fixed: bit-deterministic results.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -27,9 +27,18 @@ namespace {
 int nb_err(int code, const char *msg) { return ssb::set_err(code, msg); }
 int nb_cuda(const char *where) { return ssb::cuda_status(where); }
 
+// Linear cell hash h = ix + HB*iy + HC*iz (mod m, m a power of two >= 64).
+// Being linear, the buckets of a cell's neighbours follow from its own bucket
+// (h + dx + HB*dy + HC*dz), x-neighbours are CONSECUTIVE buckets (so the three
+// cells of an x-row are one contiguous range of the sorted order), and with
+// HB = 3, HC = 9 (mod 32) the 27 neighbours of any cell land in 27 distinct
+// buckets for every m >= 32 (dx + 3dy + 9dz is injective on {-1,0,1}^3 with
+// span 26 < 32), so no bucket is ever scanned twice.
+constexpr uint32_t kHB = 0x8DA6B343u, kHC = 0xD8163849u;
+
 __device__ __forceinline__ uint32_t cell_hash(int ix, int iy, int iz, uint32_t mask)
 {
-    return (((uint32_t)ix * 73856093u) ^ ((uint32_t)iy * 19349663u) ^ ((uint32_t)iz * 83492791u)) & mask;
+    return ((uint32_t)ix + (uint32_t)iy * kHB + (uint32_t)iz * kHC) & mask;
 }
 
 __device__ __forceinline__ int cell_of(float x, float inv_cell)
@@ -39,13 +48,15 @@ __device__ __forceinline__ int cell_of(float x, float inv_cell)
 
 uint64_t next_pow2(uint64_t x)
 {
-    uint64_t p = 1;
+    uint64_t p = 64;
     while (p < x) p <<= 1;
     return p;
 }
 
 struct Workspace {
-    uint32_t *keys, *vals, *keys_sorted, *vals_sorted, *cell_start, *cell_end;
+    uint32_t *keys, *vals, *keys_sorted, *vals_sorted;
+    uint32_t *cell_start;   // m + 1 entries: lower bound of every bucket in the sorted keys
+    float4 *pos_sorted;     // alive positions in bucket order, .w = original index bits
     void *cub_tmp;
     size_t cub_bytes;
     uint32_t mask;
@@ -61,23 +72,23 @@ size_t layout(int64_t n_all, char *base, Workspace *w)
     size_t cub_bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (uint32_t *)nullptr, (uint32_t *)nullptr,
                                     (uint32_t *)nullptr, (uint32_t *)nullptr, (int)n_all);
-    size_t off = 0;
-    const size_t nb = align256(sizeof(uint32_t) * (size_t)n_all), mb = align256(sizeof(uint32_t) * m);
+    const size_t nb = align256(sizeof(uint32_t) * (size_t)n_all), mb = align256(sizeof(uint32_t) * (m + 1));
+    const size_t pb = align256(sizeof(float4) * (size_t)n_all);
     if (w) {
-        w->keys = (uint32_t *)(base + off);
-        w->vals = (uint32_t *)(base + off + nb);
-        w->keys_sorted = (uint32_t *)(base + off + 2 * nb);
-        w->vals_sorted = (uint32_t *)(base + off + 3 * nb);
-        w->cell_start = (uint32_t *)(base + off + 4 * nb);
-        w->cell_end = (uint32_t *)(base + off + 4 * nb + mb);
-        w->cub_tmp = base + off + 4 * nb + 2 * mb;
+        w->keys = (uint32_t *)base;
+        w->vals = (uint32_t *)(base + nb);
+        w->keys_sorted = (uint32_t *)(base + 2 * nb);
+        w->vals_sorted = (uint32_t *)(base + 3 * nb);
+        w->cell_start = (uint32_t *)(base + 4 * nb);
+        w->pos_sorted = (float4 *)(base + 4 * nb + mb);
+        w->cub_tmp = base + 4 * nb + mb + pb;
         w->cub_bytes = cub_bytes;
         w->mask = (uint32_t)(m - 1);
         int bits = 0;
         while ((1ull << bits) <= m) bits++;   // keys in [0, m], m = sentinel
         w->key_bits = bits;
     }
-    return 4 * nb + 2 * mb + align256(cub_bytes);
+    return 4 * nb + mb + pb + align256(cub_bytes);
 }
 
 __global__ void pack_positions_kernel(const float *cols, const uint8_t *flags, int64_t n, int64_t stride,
@@ -112,55 +123,91 @@ __global__ void hash_kernel(const float4 *pos, int64_t n_all, float inv_cell, ui
     vals[i] = (uint32_t)i;
 }
 
-__global__ void bucket_ranges_kernel(const uint32_t *keys_sorted, int64_t n_all, uint32_t mask,
-                                     uint32_t *cell_start, uint32_t *cell_end)
+// cell_start[k] = first sorted position whose key is >= k, for k in [0, m]
+// (empty buckets included, so bucket k is [start[k], start[k+1]) and a run of
+// consecutive buckets is [start[lo], start[hi+1])); and the alive positions
+// gathered into bucket order so each range is read contiguously.  Thread i
+// fills the keys in (key[i-1], key[i]]: every entry is written exactly once,
+// no memset needed.
+__global__ void bucket_ranges_kernel(const uint32_t *keys_sorted, const uint32_t *vals_sorted, const float4 *pos,
+                                     int64_t n_all, uint32_t mask, uint32_t *cell_start, float4 *pos_sorted)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n_all) return;
-    const uint32_t k = keys_sorted[i];
-    if (k > mask) return;
-    if (i == 0 || keys_sorted[i - 1] != k) cell_start[k] = (uint32_t)i;
-    if (i == n_all - 1 || keys_sorted[i + 1] != k) cell_end[k] = (uint32_t)(i + 1);
+    if (i > n_all) return;
+    const int64_t m = (int64_t)mask + 1;
+    const int64_t prev = i == 0 ? -1 : (int64_t)keys_sorted[i - 1];
+    const int64_t cur = i == n_all ? m : (int64_t)keys_sorted[i];
+    for (int64_t k = prev + 1; k <= cur; k++) cell_start[k] = (uint32_t)i;
+    if (i < n_all && cur <= (int64_t)mask) {
+        const uint32_t idx = vals_sorted[i];
+        float4 p = pos[idx];
+        p.w = __uint_as_float(idx);
+        pos_sorted[i] = p;
+    }
 }
 
-__global__ void query_kernel(const float4 *pos, const uint32_t *vals_sorted, const uint32_t *cell_start,
-                             const uint32_t *cell_end, uint32_t mask, float inv_cell, float r_sense,
-                             float k_sep, int64_t n_local, int64_t self_offset, int64_t stride,
-                             const uint8_t *flags, float *cols, int accumulate)
+__device__ __forceinline__ void sep_accumulate(const float4 &p, const float4 &q, bool take, float r2, float inv_r,
+                                               float k_sep, float &ax, float &ay, float &az)
 {
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n_local) return;
+    const float ddx = p.x - q.x, ddy = p.y - q.y, ddz = p.z - q.z;
+    const float d2 = fmaf(ddx, ddx, fmaf(ddy, ddy, ddz * ddz));
+    if (!take || !(d2 < r2) || !(d2 > 1e-24f)) return;   // strict <, d > 1e-12
+    const float d = sqrtf(d2);
+    const float s = k_sep * (1.0f - d * inv_r) / d;
+    ax = fmaf(s, ddx, ax);
+    ay = fmaf(s, ddy, ay);
+    az = fmaf(s, ddz, az);
+}
+
+// One thread per agent in BUCKET order (neighbouring threads are neighbouring
+// cells, so their candidate ranges overlap and hit L1).  An agent's 27
+// neighbour cells are 9 x-rows, each one contiguous range of pos_sorted
+// (split in two only where the row wraps the table end); each range is read
+// four candidates at a time with independent loads.  Summation order is
+// fixed (row order, then sorted order): bit-deterministic run to run.
+__global__ void __launch_bounds__(128) query_kernel(const float4 *pos_sorted, const uint32_t *keys_sorted,
+                                                    const uint32_t *vals_sorted, const uint32_t *cell_start,
+                                                    uint32_t mask, float r_sense, float k_sep, int64_t n_all,
+                                                    int64_t n_local, int64_t self_offset, const uint8_t *flags,
+                                                    float *cols, int accumulate)
+{
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n_all) return;
+    const int64_t r = (int64_t)vals_sorted[j] - self_offset;
+    if (r < 0 || r >= n_local) return;                       // another rank's agent
+    const uint32_t h = keys_sorted[j];
     float ax = 0.0f, ay = 0.0f, az = 0.0f;
-    const int64_t self = self_offset + r;
-    if (flags[r] & SWARMSTEP_FLAG_ALIVE) {
-        const float4 p = pos[self];
-        const int cx = cell_of(p.x, inv_cell), cy = cell_of(p.y, inv_cell), cz = cell_of(p.z, inv_cell);
-        uint32_t seen[27];
-        int nseen = 0;
-        const float inv_r = 1.0f / r_sense;
-        for (int dz = -1; dz <= 1; dz++)
-            for (int dy = -1; dy <= 1; dy++)
-                for (int dx = -1; dx <= 1; dx++) {
-                    const uint32_t b = cell_hash(cx + dx, cy + dy, cz + dz, mask);
-                    bool dup = false;
-                    for (int s = 0; s < nseen; s++) dup = dup || (seen[s] == b);
-                    if (dup) continue;          // two neighbour cells share a bucket
-                    seen[nseen++] = b;
-                    const uint32_t e = cell_end[b];
-                    for (uint32_t j = cell_start[b]; j < e; j++) {
-                        const uint32_t idx = vals_sorted[j];
-                        if ((int64_t)idx == self) continue;
-                        const float4 q = pos[idx];
-                        const float ddx = p.x - q.x, ddy = p.y - q.y, ddz = p.z - q.z;
-                        const float d2 = fmaf(ddx, ddx, fmaf(ddy, ddy, ddz * ddz));
-                        if (!(d2 < r_sense * r_sense) || !(d2 > 1e-24f)) continue;  // strict <, d > 1e-12
-                        const float d = sqrtf(d2);
-                        const float s = k_sep * (1.0f - d * inv_r) / d;
-                        ax = fmaf(s, ddx, ax);
-                        ay = fmaf(s, ddy, ay);
-                        az = fmaf(s, ddz, az);
-                    }
+    if (h <= mask && (flags[r] & SWARMSTEP_FLAG_ALIVE)) {
+        const float4 p = pos_sorted[j];
+        const float r2 = r_sense * r_sense, inv_r = 1.0f / r_sense;
+        const uint32_t end_all = cell_start[mask + 1];
+#pragma unroll 1
+        for (int row = 0; row < 9; row++) {
+            const int dy = row % 3 - 1, dz = row / 3 - 1;
+            const uint32_t hc = h + (uint32_t)dy * kHB + (uint32_t)dz * kHC;
+            const uint32_t lo = (hc - 1u) & mask, hi = (hc + 1u) & mask;
+            uint32_t s0 = cell_start[lo], e0, s1 = 0, e1 = 0;
+            if (lo <= hi) {
+                e0 = cell_start[hi + 1];
+            } else {                                         // row wraps the table end
+                e0 = end_all;
+                e1 = cell_start[hi + 1];
+            }
+#pragma unroll 1
+            for (int seg = 0; seg < 2; seg++) {
+                const uint32_t s = seg ? s1 : s0, e = seg ? e1 : e0;
+#pragma unroll 1
+                for (uint32_t c = s; c < e; c += 4) {
+                    float4 q[4];
+#pragma unroll
+                    for (int u = 0; u < 4; u++)
+                        q[u] = c + u < e ? pos_sorted[c + u] : p;
+#pragma unroll
+                    for (int u = 0; u < 4; u++)
+                        sep_accumulate(p, q[u], c + u < e && (int64_t)(c + u) != j, r2, inv_r, k_sep, ax, ay, az);
                 }
+            }
+        }
     }
     float *ox = cols + ssb::at(SWARMSTEP_COL_OVERLAY + 0, r);
     float *oy = cols + ssb::at(SWARMSTEP_COL_OVERLAY + 1, r);
@@ -214,12 +261,11 @@ int swarmstep_neighbor_overlay(const swarmstep_group_view *g, const float *all_x
     if (cub::DeviceRadixSort::SortPairs(w.cub_tmp, cb, w.keys, w.keys_sorted, w.vals, w.vals_sorted,
                                         (int)n_all, 0, w.key_bits, s) != cudaSuccess)
         return nb_cuda("cub::DeviceRadixSort");
-    cudaMemsetAsync(w.cell_start, 0, sizeof(uint32_t) * ((size_t)w.mask + 1), s);
-    cudaMemsetAsync(w.cell_end, 0, sizeof(uint32_t) * ((size_t)w.mask + 1), s);
-    bucket_ranges_kernel<<<grid_n(n_all, 256), 256, 0, s>>>(w.keys_sorted, n_all, w.mask, w.cell_start, w.cell_end);
-    query_kernel<<<grid_n(g->n, 128), 128, 0, s>>>(pos, w.vals_sorted, w.cell_start, w.cell_end, w.mask, inv_cell,
-                                                 r_sense, k_sep, g->n, self_offset, g->stride, g->flags, g->cols,
-                                                 accumulate);
+    bucket_ranges_kernel<<<grid_n(n_all + 1, 256), 256, 0, s>>>(w.keys_sorted, w.vals_sorted, pos, n_all, w.mask,
+                                                                w.cell_start, w.pos_sorted);
+    query_kernel<<<grid_n(n_all, 128), 128, 0, s>>>(w.pos_sorted, w.keys_sorted, w.vals_sorted, w.cell_start,
+                                                   w.mask, r_sense, k_sep, n_all, g->n, self_offset, g->flags,
+                                                   g->cols, accumulate);
     return nb_cuda("neighbor overlay");
 }
 
