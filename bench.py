@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-k1", action="store_true", help="skip the K=1 HBM-roofline leg")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--motor-tau", type=float, default=0.0,
+                    help="opt-in first-order rotor lag time constant (s); 0 = the reference's instantaneous mixer")
     return ap.parse_args()
 
 
@@ -128,12 +130,12 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------- CPU legs
-def cpu_leg(n_sample: int, k: int, dt: float, budget_s: float, min_reps: int = 1):
+def cpu_leg(n_sample: int, k: int, dt: float, budget_s: float, min_reps: int = 1, motor_tau: float = 0.0):
     """Time the float64 oracle (reference algorithm) on all host cores."""
     from oracle import oracle as orc
     threads = orc.cpu_count()
     pos, sp = workload(n_sample, seed=0)
-    g = orc.OracleGroup(0, _Batch(n_sample, pos, 0))
+    g = orc.OracleGroup(0, _Batch(n_sample, pos, 0), motor_tau=motor_tau)
     g.cmd_values[:] = sp.T.astype(np.float64)
     g.step(dt, nthreads=threads)  # warm
     reps, t0 = 0, time.perf_counter()
@@ -154,7 +156,7 @@ def run_reference(args, rank: int) -> None:
     threads = None
     vals = []
     for i in range(args.warmup + args.steps):
-        v, threads, reps, el = cpu_leg(n_sample, args.substeps, args.dt, 0.0, min_reps=1)
+        v, threads, reps, el = cpu_leg(n_sample, args.substeps, args.dt, 0.0, min_reps=1, motor_tau=args.motor_tau)
         if i >= args.warmup:
             vals.append(v)
     value = float(np.mean(vals))
@@ -191,7 +193,7 @@ def run_b200(args, rank: int, world: int) -> None:
 
     t_setup = time.perf_counter()
     pos, sp = workload(n, seed=rank, id_base=rank * n)
-    g = B200QuadGroup(0, _Batch(n, pos, rank * n), device=dev)
+    g = B200QuadGroup(0, _Batch(n, pos, rank * n), device=dev, motor_tau=args.motor_tau)
     sp_dev = torch.from_numpy(sp).to(dev)
     g.set_setpoints(sp_dev, columns=True)
     torch.cuda.synchronize(dev)
@@ -300,7 +302,7 @@ def run_b200(args, rank: int, world: int) -> None:
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         n_s = 262_144
-        v, threads, reps, el = cpu_leg(n_s, k, dt, args.cpu_seconds)
+        v, threads, reps, el = cpu_leg(n_s, k, dt, args.cpu_seconds, motor_tau=args.motor_tau)
         cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
                "sample": f"{n_s} agents x {k} ticks x {reps} reps ({el:.1f} s), same recipe, float64 C oracle "
                          f"(restatement of the reference QuadGroup.step), {threads} threads"}
@@ -313,7 +315,7 @@ def run_b200(args, rank: int, world: int) -> None:
             "config": {"workload": f"{n:,} quadrotors per GPU, POS level, random setpoints, "
                                    f"K={k} fused ticks per launch (cfg3 recipe at cfg4 size)",
                        "agents_per_gpu": n, "agents_total": n * world, "substeps": k, "dt": dt,
-                       "level": "pos", "compensated_position": True,
+                       "level": "pos", "compensated_position": True, "motor_tau": args.motor_tau,
                        "l2": f"inputs larger than L2 ({n * 221 / 1e9:.2f} GB touched per launch vs 0.126 GB L2)",
                        "parallelism": f"agent-index shards x{world}, no collective"},
             "roofline": {"bound": "fp32", "achieved": achieved_tf, "peak": fp32_peak_tf, "unit": "TFLOP/s",

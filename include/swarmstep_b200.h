@@ -136,6 +136,23 @@ int swarmstep_quad_step(const swarmstep_group_view *g, const swarmstep_quad_para
                         float dt, int k_substeps, int launch_flags, uint32_t tick_base,
                         const int64_t *tick_dev, void *stream);
 
+/* swarmstep_quad_step with the opt-in first-order rotor lag of the north star
+ * (absent in the reference; tau_m = 0 is swarmstep_quad_step
+ * itself).  Each rotor thrust f_i follows its commanded thrust u_i (the
+ * mixer's clamped motor thrust, or k_t clip(rpm)^2 for MOTOR rows), held over
+ * the tick: f(t + s) = u + (f(t) - u) exp(-s / tau_m); the rigid body
+ * integrates (wrench held, as QuadGroup.step) the wrench of the tick-mean
+ * thrust u + (f(t) - u)(tau_m/dt)(1 - exp(-dt/tau_m)): the thrust impulse is
+ * exact and tau_m -> 0 recovers the instantaneous mixer.  motor: device float32, tiled like
+ * the state -- 4 columns x 128 rows per tile, stride rows, 16-byte aligned;
+ * rotor i of row r at (r / 128) * 512 + i * 128 + r % 128 (newtons).  Dead
+ * and faulted rows keep their thrusts.  Errors: tau_m <= 0 or non-finite,
+ * dt <= 0, k < 1 -> SWARMSTEP_EINVAL.  No reference interface: this extends
+ * QuadGroup.step (core.py:166) behind the same group protocol. */
+int swarmstep_quad_step_lag(const swarmstep_group_view *g, const swarmstep_quad_params *p,
+                            float *motor, float tau_m, float dt, int k_substeps, int launch_flags,
+                            uint32_t tick_base, const int64_t *tick_dev, void *stream);
+
 /* Latest-wins command scatter (QuadGroup.apply_command, core.py:117-135).
  * rows[i] (int64), levels[i] (uint8, SWARMSTEP_LEVEL_*), values[i*7..]
  * (float32; RATE/MOTOR entries carry 4 values and zeros) are device arrays;

@@ -67,6 +67,10 @@ def load():
         lib.oracle_group_step.argtypes = [i64, ctypes.c_double, P, _f64p, _f64p, _f64p, _f64p, _u8p,
                                           _f64p, _f64p, _u8p, _f64p, _f64p, _u8p, _f64p, _f64p, _u8p,
                                           ctypes.c_int]
+        lib.oracle_group_step_lag.restype = i64
+        lib.oracle_group_step_lag.argtypes = [i64, ctypes.c_double, P, _f64p, _f64p, _f64p, _f64p, _u8p,
+                                              _f64p, _f64p, _u8p, _f64p, _f64p, _u8p, _f64p, _f64p, _u8p,
+                                              ctypes.c_int, _f64p, ctypes.c_double]
         lib.oracle_deriv_batch.restype = None
         lib.oracle_deriv_batch.argtypes = [i64, _f64p, _f64p, _f64p, P, _f64p]
         lib.oracle_rk4_batch.restype = i64
@@ -211,7 +215,7 @@ class OracleGroup:
 
     kind = "quadrotor"
 
-    def __init__(self, type_id, batch, quad=None, rate=None, outer=None):
+    def __init__(self, type_id, batch, quad=None, rate=None, outer=None, motor_tau: float = 0.0):
         n = int(np.asarray(batch.agent_ids).shape[0])
         self.type_id = type_id
         self.n = n
@@ -235,6 +239,10 @@ class OracleGroup:
         self.overlay_active = False
         self._row = {int(a): i for i, a in enumerate(self.agent_ids)}
         self.fault_mask = np.zeros(n, dtype=np.uint8)
+        # opt-in rotor lag (parity unpinned: absent in the reference); rotor
+        # thrusts start at the hover split m g / 4, like B200QuadGroup
+        self.motor_tau = float(motor_tau)
+        self.motor = np.full((n, 4), self.p.m * self.p.g / 4.0) if self.motor_tau > 0.0 else None
 
     def rows_for(self, agent_id):
         return self._row.get(int(agent_id))
@@ -277,11 +285,14 @@ class OracleGroup:
 
     def step(self, dt: float, nthreads: int = 1) -> np.ndarray:
         ov = self.v_overlay if self.overlay_active else None
-        nf = load().oracle_group_step(
-            self.n, dt, ctypes.byref(self.p), _d(self.pos), _d(self.vel), _d(self.quat), _d(self.omega),
-            _b(self.alive), _d(self.integral), _d(self.prev_omega), _b(self.has_prev), _d(self.omega_sp),
-            _d(self.f_c_sp), _b(self.cmd_level), _d(self.cmd_values),
-            _d(ov) if ov is not None else None, _b(self.fault_mask), int(nthreads))
+        args = (self.n, dt, ctypes.byref(self.p), _d(self.pos), _d(self.vel), _d(self.quat), _d(self.omega),
+                _b(self.alive), _d(self.integral), _d(self.prev_omega), _b(self.has_prev), _d(self.omega_sp),
+                _d(self.f_c_sp), _b(self.cmd_level), _d(self.cmd_values),
+                _d(ov) if ov is not None else None, _b(self.fault_mask), int(nthreads))
+        if self.motor is None:
+            nf = load().oracle_group_step(*args)
+        else:
+            nf = load().oracle_group_step_lag(*args, _d(self.motor), self.motor_tau)
         if self.overlay_active:
             self.v_overlay[:] = 0.0
             self.overlay_active = False

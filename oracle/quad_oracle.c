@@ -106,6 +106,26 @@ int oracle_rk4_row(const double *y, double f_c, const double *tau,
     }
 }
 
+/* ---- opt-in first-order rotor lag (north star; ABSENT in the reference) --
+ * Parity unpinned: the reference has no rotor dynamics, so this
+ * restates the model DESIGN.md defines, not reference code.  Rotor thrusts f
+ * follow the commanded thrusts u, held over the tick, exactly:
+ * f(t + s) = u + (f(t) - u) exp(-s / tau_m).  The rigid body integrates
+ * (quad.py:350-437, wrench held) the wrench of the tick-mean thrust
+ * fbar = u + (f(t) - u) phi, phi = (tau_m / dt)(1 - exp(-dt / tau_m)): the
+ * thrust impulse over the tick is exact, and tau_m -> 0 gives fbar = u, the
+ * reference's instantaneous mixer. */
+/* wrench of rotor thrusts f: G f (quad.py:138-140) */
+static void thrust_wrench(const double *f, const oracle_params *p, double *wrench)
+{
+    int i, j;
+    for (i = 0; i < 4; i++) {
+        double acc = 0.0;
+        for (j = 0; j < 4; j++) acc += f[j] * p->G[i * 4 + j];
+        wrench[i] = acc;
+    }
+}
+
 /* ---- mixer: quad.py:143-168 (mix_to_motors), one row ------------------ */
 int oracle_mix_row(double f_c, const double *tau, const oracle_params *p,
                    double *motors, double *realized)
@@ -302,6 +322,8 @@ typedef struct {
     const double *cmd_values;
     const double *v_overlay;
     uint8_t *fault;
+    double *motor;           /* (n,4) rotor thrusts, or NULL: no rotor lag */
+    double phi, e_full;      /* (tau_m / dt)(1 - exp(-dt / tau_m)), exp(-dt / tau_m) */
     int any_pos;
     int64_t n_fault;
     int bad;
@@ -354,7 +376,26 @@ static void step_rows(step_job *j)
         if (!alive) continue;
         for (i = 0; i < 3; i++) { y[i] = j->pos[r * 3 + i]; y[3 + i] = j->vel[r * 3 + i]; y[10 + i] = j->omega[r * 3 + i]; }
         for (i = 0; i < 4; i++) y[6 + i] = j->quat[r * 4 + i];
-        ok = oracle_rk4_row(y, f_c, tau, p, j->dt, out);
+        if (j->motor) {
+            /* rotor lag: commanded thrusts u = clamped mixer motors, or
+             * k_t clip(rpm)^2 for MOTOR rows (quad.py:134-137) */
+            double u[4], fbar[4], f1[4], wr[4], *f0 = j->motor + r * 4;
+            for (i = 0; i < 4; i++) {
+                if (lvl == LVL_MOTOR) {
+                    double c = cv[i] < 0.0 ? 0.0 : (cv[i] > p->omega_max ? p->omega_max : cv[i]);
+                    u[i] = p->k_t * (c * c);
+                } else {
+                    u[i] = motors[i];
+                }
+                fbar[i] = u[i] + (f0[i] - u[i]) * j->phi;
+                f1[i] = u[i] + (f0[i] - u[i]) * j->e_full;
+            }
+            thrust_wrench(fbar, p, wr);
+            ok = oracle_rk4_row(y, wr[0], wr + 1, p, j->dt, out);
+            if (ok) for (i = 0; i < 4; i++) f0[i] = f1[i];
+        } else {
+            ok = oracle_rk4_row(y, f_c, tau, p, j->dt, out);
+        }
         if (!ok) {
             j->alive[r] = 0;
             j->fault[r] = 1;
@@ -374,12 +415,13 @@ static void *step_thread(void *arg) { step_rows((step_job *)arg); return NULL; }
  * rows contiguously across POSIX threads; results are identical for any
  * thread count because rows are independent (core.py determinism,
  * test_core.py:314-339). */
-int64_t oracle_group_step(int64_t n, double dt, const oracle_params *p,
+static int64_t group_step(int64_t n, double dt, const oracle_params *p,
                           double *pos, double *vel, double *quat, double *omega, uint8_t *alive,
                           double *integral, double *prev_omega, uint8_t *has_prev,
                           double *omega_sp, double *f_c_sp,
                           const uint8_t *cmd_level, const double *cmd_values,
-                          const double *v_overlay, uint8_t *fault, int nthreads)
+                          const double *v_overlay, uint8_t *fault, int nthreads,
+                          double *motor, double tau_m)
 {
     step_job jobs[256];
     pthread_t th[256];
@@ -416,6 +458,9 @@ int64_t oracle_group_step(int64_t n, double dt, const oracle_params *p,
         j->omega_sp = omega_sp; j->f_c_sp = f_c_sp;
         j->cmd_level = cmd_level; j->cmd_values = cmd_values; j->v_overlay = v_overlay;
         j->fault = fault; j->any_pos = any_pos; j->n_fault = 0; j->bad = 0;
+        j->motor = motor;
+        j->phi = motor ? -(tau_m / dt) * expm1(-dt / tau_m) : 0.0;
+        j->e_full = motor ? exp(-dt / tau_m) : 0.0;
     }
     if (nthreads == 1) {
         step_rows(&jobs[0]);
@@ -425,6 +470,33 @@ int64_t oracle_group_step(int64_t n, double dt, const oracle_params *p,
     }
     for (t = 0; t < nthreads; t++) { total += jobs[t].n_fault; bad |= jobs[t].bad; }
     return bad ? -1 : total;
+}
+
+int64_t oracle_group_step(int64_t n, double dt, const oracle_params *p,
+                          double *pos, double *vel, double *quat, double *omega, uint8_t *alive,
+                          double *integral, double *prev_omega, uint8_t *has_prev,
+                          double *omega_sp, double *f_c_sp,
+                          const uint8_t *cmd_level, const double *cmd_values,
+                          const double *v_overlay, uint8_t *fault, int nthreads)
+{
+    return group_step(n, dt, p, pos, vel, quat, omega, alive, integral, prev_omega, has_prev, omega_sp,
+                      f_c_sp, cmd_level, cmd_values, v_overlay, fault, nthreads, NULL, 0.0);
+}
+
+/* QuadGroup.step with the opt-in rotor lag (parity unpinned, see above);
+ * motor (n,4) rotor thrusts are updated in place for rows that step without
+ * fault.  tau_m <= 0 -> -2. */
+int64_t oracle_group_step_lag(int64_t n, double dt, const oracle_params *p,
+                              double *pos, double *vel, double *quat, double *omega, uint8_t *alive,
+                              double *integral, double *prev_omega, uint8_t *has_prev,
+                              double *omega_sp, double *f_c_sp,
+                              const uint8_t *cmd_level, const double *cmd_values,
+                              const double *v_overlay, uint8_t *fault, int nthreads,
+                              double *motor, double tau_m)
+{
+    if (!(tau_m > 0.0) || !motor) return -2;
+    return group_step(n, dt, p, pos, vel, quat, omega, alive, integral, prev_omega, has_prev, omega_sp,
+                      f_c_sp, cmd_level, cmd_values, v_overlay, fault, nthreads, motor, tau_m);
 }
 
 /* ---- batched per-function entry points for golden pinning -------------- */

@@ -34,7 +34,7 @@ STEP_OVERLAY, STEP_MOTOR, STEP_FORCE_DIRECT, STEP_FORCE_TMA, STEP_FORCE_PAIR = 0
 # every symbol include/swarmstep_b200.h declares
 EXPORTS = (
     "swarmstep_abi_version", "swarmstep_last_error", "swarmstep_device_info", "swarmstep_preload",
-    "swarmstep_quad_step", "swarmstep_quad_apply_commands", "swarmstep_quad_set_setpoints",
+    "swarmstep_quad_step", "swarmstep_quad_step_lag", "swarmstep_quad_apply_commands", "swarmstep_quad_set_setpoints",
     "swarmstep_quad_mark_dead", "swarmstep_quad_retarget_waypoint",
     "swarmstep_quad_pack_f64", "swarmstep_quad_unpack_f64",
     "swarmstep_pack_positions", "swarmstep_neighbor_workspace_bytes", "swarmstep_neighbor_overlay",
@@ -73,6 +73,8 @@ def _declare(lib) -> None:
     lib.swarmstep_device_info.argtypes = [ctypes.POINTER(i32)] * 3
     lib.swarmstep_quad_step.restype = i32
     lib.swarmstep_quad_step.argtypes = [view, vp, f32, i32, i32, ctypes.c_uint32, vp, vp]
+    lib.swarmstep_quad_step_lag.restype = i32
+    lib.swarmstep_quad_step_lag.argtypes = [view, vp, vp, f32, f32, i32, i32, ctypes.c_uint32, vp, vp]
     lib.swarmstep_quad_apply_commands.restype = i32
     lib.swarmstep_quad_apply_commands.argtypes = [view, vp, vp, vp, i64, vp]
     lib.swarmstep_quad_set_setpoints.restype = i32

@@ -307,6 +307,45 @@ __device__ __forceinline__ void motor_wrench(const float rpm[4], const swarmstep
                  P.G[(i + 1) * 4 + 2] * f[2] + P.G[(i + 1) * 4 + 3] * f[3];
 }
 
+// ---- opt-in first-order motor lag (north_star; absent in the reference) ----
+// Rotor thrusts f_i follow the commanded thrusts u_i (held over the tick):
+// f' = (u - f) / tau_m, integrated exactly: f(t0 + s) = u + (f(t0) - u) e^(-s/tau_m).
+// u = the mixer's clamped motor thrusts (quad.py:143-168), or k_t clip(rpm)^2
+// for MOTOR rows (quad.py:130-140).  The rigid body integrates (rk4_inplace,
+// wrench held) G fbar, fbar = u + (f(t0) - u) phi the tick-mean thrust,
+// phi = (tau_m / dt)(1 - e^(-dt/tau_m)): exact thrust impulse per tick, and
+// tau_m -> 0 recovers the reference's instantaneous mixer.
+
+// clamped mixer motor thrusts m = clip(G^-1 [f_c, tau], 0, f_max) (quad.py:153-160)
+__device__ __forceinline__ void mix_motors(float f_c, const float tau[3], const swarmstep_quad_params &P, float m[4])
+{
+    const float F = mul(P.G_inv[0], f_c), A = mul(P.G_inv[1], tau[0]);
+    const float B = mul(fabsf(P.G_inv[2]), tau[1]), C = mul(P.G_inv[3], tau[2]);
+    const float FpA = add(F, A), FmA = sub(F, A), BmC = sub(B, C), BpC = add(B, C);
+    m[0] = sub(FpA, BmC); m[1] = sub(FmA, BpC); m[2] = add(FmA, BpC); m[3] = add(FpA, BmC);
+#pragma unroll
+    for (int i = 0; i < 4; i++) m[i] = clip(m[i], 0.0f, P.f_max);
+}
+
+// wrench of four rotor thrusts: (f_c, tau) = G f (quad.py:138-140)
+__device__ __forceinline__ void thrust_wrench(const float f[4], const swarmstep_quad_params &P, float &f_c,
+                                              float tau[3])
+{
+    f_c = add(add(f[0], f[1]), add(f[2], f[3]));
+#pragma unroll
+    for (int i = 0; i < 3; i++)
+        tau[i] = fma(P.G[(i + 1) * 4 + 0], f[0], fma(P.G[(i + 1) * 4 + 1], f[1],
+                 fma(P.G[(i + 1) * 4 + 2], f[2], mul(P.G[(i + 1) * 4 + 3], f[3]))));
+}
+
+// rotor thrusts lagging towards u: u + (f - u) e (e = e^(-dt/tau_m) for the
+// end of the tick, e = phi for the tick mean)
+__device__ __forceinline__ void lag_thrust(const float f[4], const float u[4], float e, float out[4])
+{
+#pragma unroll
+    for (int i = 0; i < 4; i++) out[i] = fma(sub(f[i], u[i]), e, u[i]);
+}
+
 // rate_pid_step for alive rows (control.py:136-187).  Dead rows never reach
 // this (they are frozen: tau = 0, f_c = 0, state untouched).  A row without a
 // previous sample has no D term (control.py:175-177): the caller sets

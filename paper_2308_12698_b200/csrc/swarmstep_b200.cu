@@ -6,6 +6,7 @@
 // component), so every warp-wide load/store of a component is one fully
 // coalesced 128-byte line.
 #include <cuda_runtime.h>
+#include <math.h>
 #include <stdint.h>
 #include <stdio.h>
 #include <string.h>
@@ -114,6 +115,32 @@ struct PairRow {
 
 template <class T> __device__ __forceinline__ T zero_t() { return ssb::bc<T>(0.0f); }
 
+// Motor-lag policy of a launch.  NoLag: the reference's instantaneous mixer
+// (every hot kernel).  MotorLag: the opt-in first-order rotor lag
+// (quad_math.cuh), scalar rows only; the four rotor thrusts live in their own
+// tiled array (4 columns x 128 rows per tile) next to the state.
+struct NoLag {
+    static constexpr bool on = false;
+    __device__ __forceinline__ void load() {}
+    __device__ __forceinline__ void store() const {}
+};
+struct MotorLag {
+    static constexpr bool on = true;
+    float *p;          // this row's rotor-thrust column 0 (column i at p + 128 i)
+    float phi, e_full;      // (tau_m / dt)(1 - e^(-dt / tau_m)), e^(-dt / tau_m)
+    float f[4];
+    __device__ __forceinline__ void load()
+    {
+#pragma unroll
+        for (int i = 0; i < 4; i++) f[i] = p[i * SWARMSTEP_TILE];
+    }
+    __device__ __forceinline__ void store() const
+    {
+#pragma unroll
+        for (int i = 0; i < 4; i++) p[i * SWARMSTEP_TILE] = f[i];
+    }
+};
+
 template <bool COMP, class T, class A>
 __device__ __forceinline__ void load_state(const A &C, RowT<T> &R)
 {
@@ -165,7 +192,7 @@ __device__ __forceinline__ void sincos_lane(ssb::f2 x, ssb::f2 &s, ssb::f2 &c)
 
 // Per-launch setpoint preparation (commands are fixed across the K ticks).
 // has_prev: per-row "previous rate sample exists" (control.py:104).
-template <class T, class A, class M>
+template <class L = NoLag, class T, class A, class M>
 __device__ __forceinline__ void setup_level(const A &C, int level, int overlay_active,
                                             const swarmstep_quad_params &P, M has_prev, RowT<T> &R)
 {
@@ -191,9 +218,18 @@ __device__ __forceinline__ void setup_level(const A &C, int level, int overlay_a
 #pragma unroll
         for (int i = 0; i < 3; i++) R.w_sp[i] = C.ldc(SWARMSTEP_COL_SP + i);
         R.f_sp = C.ldc(SWARMSTEP_COL_SP + 3);
-        float mt[3], mf;
-        ssb::motor_wrench(R.u, P, mf, mt);
-        R.u[0] = mf; R.u[1] = mt[0]; R.u[2] = mt[1]; R.u[3] = mt[2];
+        if constexpr (L::on) {
+            // lagged: the commanded rotor thrusts k_t clip(rpm)^2 (quad.py:134-137)
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                const float c = ssb::clip(R.u[i], 0.0f, P.omega_max);
+                R.u[i] = P.k_t * (c * c);
+            }
+        } else {
+            float mt[3], mf;
+            ssb::motor_wrench(R.u, P, mf, mt);
+            R.u[0] = mf; R.u[1] = mt[0]; R.u[2] = mt[1]; R.u[3] = mt[2];
+        }
     }
 }
 
@@ -202,9 +238,9 @@ __device__ __forceinline__ void setup_level(const A &C, int level, int overlay_a
 // a lane faulted (the state registers are then garbage), or -1.  With RERUN
 // the loop stops after the controller part of tick pid_only_at (used to
 // rebuild a faulted row's state, see step_row).
-template <int LEVEL, bool COMP, bool RERUN, class T>
+template <int LEVEL, bool COMP, bool RERUN, class T, class L>
 __device__ __forceinline__ int run_ticks(const swarmstep_quad_params &P, const ssb::Derived &D,
-                                         float dt, int K, int pid_only_at, RowT<T> &R)
+                                         float dt, int K, int pid_only_at, RowT<T> &R, L &lag)
 {
 #pragma unroll kTickUnroll
     for (int k = 0; k < K; k++) {
@@ -217,39 +253,56 @@ __device__ __forceinline__ int run_ticks(const swarmstep_quad_params &P, const s
         T tau[3], f_c = R.f_sp;
         ssb::pid_row(R.w, R.w_sp, P, D, dt, R.integ, R.prev, tau);
         if (RERUN && k == pid_only_at) return -1;
-        if (LEVEL == SWARMSTEP_LEVEL_MOTOR) {
-            f_c = R.u[0]; tau[0] = R.u[1]; tau[1] = R.u[2]; tau[2] = R.u[3];
+        if constexpr (L::on) {
+            // commanded rotor thrusts u; the body integrates the wrench of the
+            // tick-mean lagged thrust, the rotors end the tick lagged by e_full
+            float u[4], fbar[4];
+            if (LEVEL == SWARMSTEP_LEVEL_MOTOR) {
+#pragma unroll
+                for (int i = 0; i < 4; i++) u[i] = R.u[i];
+            } else {
+                ssb::mix_motors(f_c, tau, P, u);
+            }
+            ssb::lag_thrust(lag.f, u, lag.phi, fbar);
+            ssb::thrust_wrench(fbar, P, f_c, tau);
+            const bool ok = ssb::rk4_inplace<float, COMP>(R.p_hi, R.p_lo, R.v, R.q, R.w, f_c, tau, P, D, dt);
+            if (!ok) return k;
+            ssb::lag_thrust(lag.f, u, lag.e_full, lag.f);
         } else {
-            ssb::mix_row(f_c, tau, P);
+            if (LEVEL == SWARMSTEP_LEVEL_MOTOR) {
+                f_c = R.u[0]; tau[0] = R.u[1]; tau[1] = R.u[2]; tau[2] = R.u[3];
+            } else {
+                ssb::mix_row(f_c, tau, P);
+            }
+            const auto ok = ssb::rk4_inplace<T, COMP>(R.p_hi, R.p_lo, R.v, R.q, R.w, f_c, tau, P, D, dt);
+            if (ssb::any(ssb::mnot(ok))) return k;
         }
-        const auto ok = ssb::rk4_inplace<T, COMP>(R.p_hi, R.p_lo, R.v, R.q, R.w, f_c, tau, P, D, dt);
-        if (ssb::any(ssb::mnot(ok))) return k;
     }
     return -1;
 }
 
-template <bool COMP, bool RERUN, class T, class A>
+template <bool COMP, bool RERUN, class T, class A, class L>
 __device__ __forceinline__ int run_level(const A &C, int level, int overlay_active,
                                          const swarmstep_quad_params &P, const ssb::Derived &D,
-                                         float dt, int K, int pid_only_at, RowT<T> &R)
+                                         float dt, int K, int pid_only_at, RowT<T> &R, L &lag)
 {
     // level-specialised tick loops: no per-tick level branches
     if (level == SWARMSTEP_LEVEL_POS) {
         if (!overlay_active)
-            return run_ticks<SWARMSTEP_LEVEL_POS, COMP, RERUN>(P, D, dt, K, pid_only_at, R);
+            return run_ticks<SWARMSTEP_LEVEL_POS, COMP, RERUN>(P, D, dt, K, pid_only_at, R, lag);
         // tick 0 sees v_sp + overlay (setup_level added it); the overlay lasts
         // one tick (core.py:172-175, 199-201), so tick 0 is peeled off
-        int f = run_ticks<SWARMSTEP_LEVEL_POS, COMP, RERUN>(P, D, dt, 1, pid_only_at, R);
+        int f = run_ticks<SWARMSTEP_LEVEL_POS, COMP, RERUN>(P, D, dt, 1, pid_only_at, R, lag);
         if (f >= 0 || K == 1 || (RERUN && pid_only_at == 0)) return f;
 #pragma unroll
         for (int i = 0; i < 3; i++) R.u[3 + i] = C.ldc(SWARMSTEP_COL_CMD + 3 + i);
-        f = run_ticks<SWARMSTEP_LEVEL_POS, COMP, RERUN>(P, D, dt, K - 1, pid_only_at - 1, R);
+        f = run_ticks<SWARMSTEP_LEVEL_POS, COMP, RERUN>(P, D, dt, K - 1, pid_only_at - 1, R, lag);
         return f >= 0 ? f + 1 : -1;
     }
     if (level == SWARMSTEP_LEVEL_RATE)
-        return run_ticks<SWARMSTEP_LEVEL_RATE, COMP, RERUN>(P, D, dt, K, pid_only_at, R);
+        return run_ticks<SWARMSTEP_LEVEL_RATE, COMP, RERUN>(P, D, dt, K, pid_only_at, R, lag);
     if constexpr (sizeof(T) == sizeof(float))
-        return run_ticks<SWARMSTEP_LEVEL_MOTOR, COMP, RERUN>(P, D, dt, K, pid_only_at, R);
+        return run_ticks<SWARMSTEP_LEVEL_MOTOR, COMP, RERUN>(P, D, dt, K, pid_only_at, R, lag);
     return -1;
 }
 
@@ -261,30 +314,35 @@ __device__ __forceinline__ int run_level(const A &C, int level, int overlay_acti
 // determinism -- plus the controller part of tick f (the reference updates
 // the PID state before rk4_step faults the row).  Inputs must still be
 // readable through C at that point (global memory, or the staged tile).
-template <bool COMP, class A>
+template <bool COMP, class A, class L = NoLag>
 __device__ __forceinline__ uint8_t step_row(const A &C, uint8_t fl, int64_t r, int overlay_active,
                                             const swarmstep_quad_params &P, const ssb::Derived &D, float dt, int K,
                                             uint32_t tick_base, const int64_t *tick_dev,
                                             uint32_t *counters, uint64_t *fault_log, int64_t fault_cap,
-                                            Row &R, bool preloaded = false)
+                                            Row &R, bool preloaded = false, L lag = L())
 {
-    if (!preloaded) load_state<COMP>(C, R);
+    if (!preloaded) {
+        load_state<COMP>(C, R);
+        lag.load();
+    }
     const int level = (fl & SWARMSTEP_LEVEL_MASK) >> SWARMSTEP_LEVEL_SHIFT;
     const bool has_prev = (fl & SWARMSTEP_FLAG_HAS_PREV) != 0;
-    setup_level(C, level, overlay_active, P, has_prev, R);
-    const int fault_k = run_level<COMP, false>(C, level, overlay_active, P, D, dt, K, -1, R);
+    setup_level<L>(C, level, overlay_active, P, has_prev, R);
+    const int fault_k = run_level<COMP, false>(C, level, overlay_active, P, D, dt, K, -1, R, lag);
     bool alive = true;
     if (fault_k >= 0) {
         alive = false;
         load_state<COMP>(C, R);
-        setup_level(C, level, overlay_active, P, has_prev, R);
-        run_level<COMP, true>(C, level, overlay_active, P, D, dt, fault_k + 1, fault_k, R);
+        lag.load();
+        setup_level<L>(C, level, overlay_active, P, has_prev, R);
+        run_level<COMP, true>(C, level, overlay_active, P, D, dt, fault_k + 1, fault_k, R, lag);
         const uint32_t slot = atomicAdd(&counters[0], 1u);
         const uint32_t tick = (tick_dev ? (uint32_t)*tick_dev : 0u) + tick_base + (uint32_t)fault_k;
         if ((int64_t)slot < fault_cap)
             fault_log[slot] = ((uint64_t)(tick & 0xFFFFFFu) << 40) | (uint64_t)r;
     }
     store_state<COMP>(C, level, R);
+    lag.store();
     // has_prev |= alive (control.py:181): every row reaching here was alive
     return (uint8_t)((fl & SWARMSTEP_LEVEL_MASK) | (alive ? SWARMSTEP_FLAG_ALIVE : 0u) | SWARMSTEP_FLAG_HAS_PREV);
 }
@@ -312,6 +370,29 @@ quad_step_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t 
     if (!(fl & SWARMSTEP_FLAG_ALIVE)) return;  // dead rows are frozen (quad.py:395-437)
     const uint8_t nfl = step_row<COMP>(C, fl, r, overlay_active, P, D, dt, K, tick_base, tick_dev,
                                        counters, fault_log, fault_cap, R, true);
+    if (nfl != fl) flags[r] = nfl;
+}
+
+// ---- motor-lag kernel: the direct kernel with the opt-in rotor lag -----------
+// Off the reference path (tau_m = 0 launches the kernels above); one row per
+// thread, rotor thrusts in registers across the K ticks next to the state.
+template <bool COMP>
+__global__ void __launch_bounds__(kBlock, 4)
+quad_step_lag_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, float *__restrict__ motor, int64_t n,
+                     uint32_t *__restrict__ counters, uint64_t *__restrict__ fault_log,
+                     int64_t fault_cap, int overlay_active, uint32_t tick_base, const int64_t *tick_dev,
+                     const swarmstep_quad_params P, const ssb::Derived D, float phi, float e_full, float dt,
+                     int K)
+{
+    const int64_t r = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    if (r >= n) return;
+    const uint8_t fl = flags[r];
+    if (!(fl & SWARMSTEP_FLAG_ALIVE)) return;   // dead rows frozen, rotor thrusts included
+    const GlobalRow C{cols + ssb::tile_base(r)};
+    MotorLag lag{motor + (r >> 7) * (4 * SWARMSTEP_TILE) + (r & (SWARMSTEP_TILE - 1)), phi, e_full, {}};
+    Row R;
+    const uint8_t nfl = step_row<COMP>(C, fl, r, overlay_active, P, D, dt, K, tick_base, tick_dev,
+                                       counters, fault_log, fault_cap, R, false, lag);
     if (nfl != fl) flags[r] = nfl;
 }
 
@@ -351,7 +432,8 @@ quad_step_pair_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int
     if (paired) {
         const ssb::m2 hp{(f0 & SWARMSTEP_FLAG_HAS_PREV) != 0, (f1 & SWARMSTEP_FLAG_HAS_PREV) != 0};
         setup_level(C, l0, overlay_active, P, hp, R);
-        if (run_level<COMP, false>(C, l0, overlay_active, P, D, dt, K, -1, R) >= 0) {
+        NoLag nolag;
+        if (run_level<COMP, false>(C, l0, overlay_active, P, D, dt, K, -1, R, nolag) >= 0) {
             // a lane faulted: redo both rows on the scalar path from the
             // launch's inputs, still untouched in HBM
             reload = true;
@@ -659,6 +741,7 @@ int swarmstep_preload(void)
     const void *fns[] = {(const void *)quad_step_kernel<true>, (const void *)quad_step_kernel<false>,
                          (const void *)quad_step_pair_kernel<true>, (const void *)quad_step_pair_kernel<false>,
                          (const void *)quad_step_tma_kernel<true>, (const void *)quad_step_tma_kernel<false>,
+                         (const void *)quad_step_lag_kernel<true>, (const void *)quad_step_lag_kernel<false>,
                          (const void *)apply_commands_kernel, (const void *)set_setpoints_kernel,
                          (const void *)mark_dead_kernel, (const void *)retarget_kernel,
                          (const void *)pack_f64_kernel, (const void *)unpack_f64_kernel};
@@ -720,6 +803,32 @@ int swarmstep_quad_step(const swarmstep_group_view *g, const swarmstep_quad_para
         g->cols, g->flags, g->n, g->counters, g->fault_log, fcap, overlay, tick_base, tick_dev, *p, D, dt,
         k_substeps);
     return cuda_status("quad_step_kernel");
+}
+
+int swarmstep_quad_step_lag(const swarmstep_group_view *g, const swarmstep_quad_params *p, float *motor,
+                            float tau_m, float dt, int k_substeps, int launch_flags, uint32_t tick_base,
+                            const int64_t *tick_dev, void *stream)
+{
+    int st = check_view(g);
+    if (st) return st;
+    if (!p || !motor) return set_err(SWARMSTEP_EINVAL, "null params / motor");
+    if (!(dt > 0.0f)) return set_err(SWARMSTEP_EINVAL, "dt must be positive");
+    if (!(tau_m > 0.0f) || !isfinite(tau_m))
+        return set_err(SWARMSTEP_EINVAL, "tau_m must be positive and finite (tau_m = 0 is swarmstep_quad_step)");
+    if (k_substeps < 1) return set_err(SWARMSTEP_EINVAL, "k_substeps must be >= 1");
+    if (!g->counters) return set_err(SWARMSTEP_EINVAL, "null counters");
+    if ((reinterpret_cast<uintptr_t>(motor) & 15u) != 0) return set_err(SWARMSTEP_EINVAL, "motor must be 16-byte aligned");
+    if (g->n == 0) return SWARMSTEP_OK;
+    const ssb::Derived D = ssb::derive(*p, 1.0f / dt);
+    const float phi = (float)(-((double)tau_m / (double)dt) * expm1(-(double)dt / (double)tau_m));
+    const float e_full = (float)exp(-(double)dt / (double)tau_m);
+    const int overlay = launch_flags & SWARMSTEP_STEP_OVERLAY;
+    const int64_t fcap = g->fault_log ? g->fault_cap : 0;
+    auto kern = g->compensated ? quad_step_lag_kernel<true> : quad_step_lag_kernel<false>;
+    kern<<<grid_for(g->n, kBlock), kBlock, 0, (cudaStream_t)stream>>>(
+        g->cols, g->flags, motor, g->n, g->counters, g->fault_log, fcap, overlay, tick_base, tick_dev, *p, D,
+        phi, e_full, dt, k_substeps);
+    return cuda_status("quad_step_lag_kernel");
 }
 
 int swarmstep_quad_apply_commands(const swarmstep_group_view *g, const int64_t *rows, const uint8_t *levels,

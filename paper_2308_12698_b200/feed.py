@@ -102,8 +102,7 @@ class TickGraph:
                 self.feed.apply(j, sync_tick=False)
             if self.coupling is not None:
                 self.coupling.launch(accumulate=False)     # overwrites the overlay block
-            _lib.check(self._lib.swarmstep_quad_step(g._view_ref, g._params_ref, ctypes.c_float(self.dt), 1,
-                                                     flags, ctypes.c_uint32(j), self.tick.data_ptr(), s))
+            g._launch(self.dt, 1, flags, j, self.tick.data_ptr())
         if self.coupling is not None:
             with torch.cuda.stream(g.stream):
                 g._cols[:, COL_OVERLAY:COL_OVERLAY + 3, :].zero_()   # one-tick overlay: leave it clear

@@ -53,7 +53,8 @@ class B200QuadGroup:
     kind = "quadrotor"
 
     def __init__(self, type_id: int, batch, params=None, rate_gains=None, outer_gains=None, *,
-                 device=None, compensated: bool = True, fault_capacity: int | None = None):
+                 device=None, compensated: bool = True, fault_capacity: int | None = None,
+                 motor_tau: float = 0.0):
         lib = _lib.load()
         if not torch.cuda.is_available():
             raise NativeLibraryError("B200QuadGroup needs a CUDA device (there is no CPU fallback)")
@@ -67,6 +68,11 @@ class B200QuadGroup:
         self.outer_gains = outer_gains if outer_gains is not None else default_outer_gains()
         self._dparams = pack_device_params(self.params, self.rate_gains, self.outer_gains)
         self.compensated = bool(compensated)
+        # opt-in first-order rotor lag (north star; absent in the reference):
+        # 0 = the reference's instantaneous mixer
+        self.motor_tau = float(motor_tau)
+        if not (np.isfinite(self.motor_tau) and self.motor_tau >= 0.0):
+            raise ValidationError(f"motor_tau must be finite and >= 0, got {motor_tau}")
         self.n = n
         self.stride = _round_up(n, _ROW_ALIGN)
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -82,6 +88,11 @@ class B200QuadGroup:
                 cap = int(fault_capacity) if fault_capacity is not None else n
                 self._fault_cap = max(1, cap)
                 self._fault_log = torch.zeros(self._fault_cap, dtype=torch.int64, device=self.device)
+                self._motor = None
+                if self.motor_tau > 0.0:
+                    # rotor thrusts [tiles, 4, 128], starting at the hover split m g / 4
+                    self._motor = torch.full((self.ntiles, 4, TILE), self.params.hover_thrust / 4.0,
+                                             dtype=torch.float32, device=self.device)
             self._counters_host = torch.zeros(4, dtype=torch.int32, pin_memory=True)
         self._view = GroupView(n=n, stride=self.stride, cols=_ptr(self._cols), flags=_ptr(self._flags),
                                counters=_ptr(self._counters), fault_log=_ptr(self._fault_log),
@@ -432,14 +443,43 @@ class B200QuadGroup:
             raise InvalidStateError("non-finite quaternion input")
         self._flush_commands()
         with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
-            self._call(self._lib.swarmstep_quad_step, self._params_ref, ctypes.c_float(dt), int(k),
-                       self._launch_flags(), ctypes.c_uint32(self._tick & 0xFFFFFF), None,
-                       ctypes.c_void_p(self.stream.cuda_stream))
+            self._launch(dt, k, self._launch_flags(), self._tick & 0xFFFFFF, None)
             self._overlay_reset()
             self._counters_host.copy_(self._counters, non_blocking=True)
         self._launched.append((self._tick, k))
         self._tick += k
         self._state_stale = True
+
+    def _launch(self, dt: float, k: int, flags: int, tick_base: int, tick_dev) -> None:
+        """One step launch on the group's stream (no host bookkeeping)."""
+        s = ctypes.c_void_p(self.stream.cuda_stream)
+        if self._motor is None:
+            self._call(self._lib.swarmstep_quad_step, self._params_ref, ctypes.c_float(dt), int(k), flags,
+                       ctypes.c_uint32(tick_base), tick_dev, s)
+        else:
+            self._call(self._lib.swarmstep_quad_step_lag, self._params_ref, _ptr(self._motor),
+                       ctypes.c_float(self.motor_tau), ctypes.c_float(dt), int(k), flags,
+                       ctypes.c_uint32(tick_base), tick_dev, s)
+
+    def motor_thrusts(self) -> np.ndarray:
+        """Host float64 copy of the rotor thrusts (n, 4) in newtons (motor_tau > 0)."""
+        if self._motor is None:
+            raise ValidationError("no rotor state: the group runs the reference's instantaneous mixer (motor_tau = 0)")
+        with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
+            m = self._motor.permute(0, 2, 1).reshape(-1, 4)[:self.n].double().cpu().numpy()
+        return np.ascontiguousarray(m)
+
+    def set_motor_thrusts(self, thrusts) -> None:
+        """Load the rotor thrusts (n, 4) in newtons (motor_tau > 0)."""
+        if self._motor is None:
+            raise ValidationError("no rotor state: the group runs the reference's instantaneous mixer (motor_tau = 0)")
+        t = np.asarray(thrusts, dtype=np.float32).reshape(self.n, 4)
+        pad = np.zeros((self.stride, 4), dtype=np.float32)
+        pad[:self.n] = t
+        with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
+            src = torch.from_numpy(pad).to(self.device).reshape(self.ntiles, TILE, 4).permute(0, 2, 1)
+            self._motor.copy_(src)
+            self._sync()
 
     # kernel selection for tuning: "auto" (the library's choice), "direct",
     # "pair" (two rows per thread on packed FP32x2) or "tma"
