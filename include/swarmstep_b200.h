@@ -232,6 +232,19 @@ int swarmstep_tick_add(int64_t *tick_dev, int64_t delta, void *stream);
 
 /* ---- device snapshot packing ----------------------------- */
 
+/* Swarm-wide reductions over one group (World.alive_counts core.py:370,
+ * cli.py:161; the occupied extent of collision.py:124-128), one launch:
+ * out12 (device double[12]) = alive count, sum of alive positions (x, y, z),
+ * sum of |v|^2, max |v|^2, alive bounding box min (x, y, z), max (x, y, z)
+ * (+inf / -inf when no row is alive).  Warp-shuffle + shared-memory block
+ * reduction, last-block fold of the block partials in block order:
+ * deterministic.  workspace: >= swarmstep_swarm_stats_workspace_bytes()
+ * bytes, 16-byte aligned, ZEROED once at allocation (its ticket word is left
+ * at zero by every launch); one workspace per concurrent stream. */
+int swarmstep_swarm_stats_workspace_bytes(uint64_t *bytes);
+int swarmstep_quad_swarm_stats(const swarmstep_group_view *g, double *out12, void *workspace,
+                               uint64_t ws_bytes, void *stream);
+
 /* One group's SnapshotMsg section body (wire.py:162-178, PROTOCOL.md
  * "Snapshot (0x01)"): u64*n agent_ids | u8*n alive | f32*3n pos | f32*3n vel |
  * f32*4n quat (canonical, w >= 0) | f32*3n omega, little-endian, into `out`

@@ -40,7 +40,7 @@ EXPORTS = (
     "swarmstep_pack_positions", "swarmstep_neighbor_workspace_bytes", "swarmstep_neighbor_overlay",
     "swarmstep_quad_circle_setpoints", "swarmstep_tick_add", "swarmstep_quad_pack_wire",
     "swarmstep_pack_collision", "swarmstep_collision_workspace_bytes", "swarmstep_collision_pairs",
-    "swarmstep_unicycle_step",
+    "swarmstep_unicycle_step", "swarmstep_swarm_stats_workspace_bytes", "swarmstep_quad_swarm_stats",
 )
 
 
@@ -73,6 +73,10 @@ def _declare(lib) -> None:
     lib.swarmstep_device_info.argtypes = [ctypes.POINTER(i32)] * 3
     lib.swarmstep_quad_step.restype = i32
     lib.swarmstep_quad_step.argtypes = [view, vp, f32, i32, i32, ctypes.c_uint32, vp, vp]
+    lib.swarmstep_swarm_stats_workspace_bytes.restype = i32
+    lib.swarmstep_swarm_stats_workspace_bytes.argtypes = [vp]
+    lib.swarmstep_quad_swarm_stats.restype = i32
+    lib.swarmstep_quad_swarm_stats.argtypes = [view, vp, vp, ctypes.c_uint64, vp]
     lib.swarmstep_quad_step_lag.restype = i32
     lib.swarmstep_quad_step_lag.argtypes = [view, vp, vp, f32, f32, i32, i32, ctypes.c_uint32, vp, vp]
     lib.swarmstep_quad_apply_commands.restype = i32

@@ -461,6 +461,23 @@ class B200QuadGroup:
                        ctypes.c_float(self.motor_tau), ctypes.c_float(dt), int(k), flags,
                        ctypes.c_uint32(tick_base), tick_dev, s)
 
+    def swarm_stats(self) -> dict:
+        """Swarm-wide reductions on the device (one deterministic launch):
+        alive count, centroid, mean and max speed, alive bounding box."""
+        with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
+            if getattr(self, "_stats_ws", None) is None:
+                nb = ctypes.c_uint64(0)
+                _lib.check(self._lib.swarmstep_swarm_stats_workspace_bytes(ctypes.byref(nb)))
+                self._stats_ws = torch.zeros(int(nb.value), dtype=torch.uint8, device=self.device)
+                self._stats_out = torch.zeros(12, dtype=torch.float64, device=self.device)
+            self._call(self._lib.swarmstep_quad_swarm_stats, _ptr(self._stats_out), _ptr(self._stats_ws),
+                       ctypes.c_uint64(self._stats_ws.numel()), ctypes.c_void_p(self.stream.cuda_stream))
+            o = self._stats_out.cpu().numpy()
+        alive = int(o[0])
+        c = o[1:4] / alive if alive else np.full(3, np.nan)
+        return {"alive": alive, "centroid": c, "mean_speed_sq": o[4] / alive if alive else float("nan"),
+                "max_speed": float(np.sqrt(o[5])), "bbox_min": o[6:9].copy(), "bbox_max": o[9:12].copy()}
+
     def motor_thrusts(self) -> np.ndarray:
         """Host float64 copy of the rotor thrusts (n, 4) in newtons (motor_tau > 0)."""
         if self._motor is None:

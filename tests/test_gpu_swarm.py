@@ -110,3 +110,31 @@ def test_graph_captured_coupling_matches_eager():
     for k in ("pos", "vel", "quat", "omega"):
         np.testing.assert_array_equal(getattr(ga.batch, k), getattr(gb.batch, k), err_msg=k)
     assert np.all(_overlay(ga) == 0.0)
+
+
+def test_swarm_stats_match_host_reduction():
+    """Device swarm-wide reductions (alive count of World.alive_counts,
+    core.py:370; centroid; speeds; alive bounding box) == numpy over the
+    float64 mirror, deterministic run to run, dead rows excluded."""
+    from paper_2308_12698_b200 import B200QuadGroup, batch_create
+    rng = np.random.default_rng(11)
+    for n in (1, 300, 200_003):
+        pos = rng.uniform(-50, 50, (n, 3))
+        g = B200QuadGroup(0, batch_create(0, n, pos, vel=rng.uniform(-2, 2, (n, 3))))
+        g.mark_dead(list(range(0, n, 7)))
+        g.step_k(1e-3, 3)
+        st = g.swarm_stats()
+        b = g.batch
+        al = b.alive
+        assert st["alive"] == int(al.sum())
+        if al.any():
+            np.testing.assert_allclose(st["centroid"], b.pos[al].mean(axis=0), rtol=1e-12, atol=1e-9)
+            np.testing.assert_allclose(st["bbox_min"], b.pos[al].astype(np.float32).min(axis=0), rtol=0, atol=0)
+            np.testing.assert_allclose(st["bbox_max"], b.pos[al].astype(np.float32).max(axis=0), rtol=0, atol=0)
+            sp2 = np.sum(b.vel[al] ** 2, axis=1)
+            np.testing.assert_allclose(st["mean_speed_sq"], sp2.mean(), rtol=1e-6)
+            np.testing.assert_allclose(st["max_speed"], np.sqrt(sp2.max()), rtol=1e-6)
+        else:
+            assert np.all(np.isinf(st["bbox_min"]))
+        st2 = g.swarm_stats()
+        assert st2["centroid"].tobytes() == st["centroid"].tobytes()
