@@ -233,12 +233,30 @@ __device__ __forceinline__ void setup_level(const A &C, int level, int overlay_a
     }
 }
 
+// A non-finite position / velocity / quaternion / rate is absorbing: NaN and
+// inf survive every later tick's arithmetic (a zero quaternion norm turns
+// into NaN at the next renormalisation), so "some tick faulted" is exactly
+// "the final state is non-finite" and the fast pass tests once per launch.
+template <bool COMP, class T>
+__device__ __forceinline__ ssb::mask_t<T> state_finite(const RowT<T> &R)
+{
+    using namespace ssb;
+    T s = add(add(add(R.p_hi[0], R.p_hi[1]), add(R.p_hi[2], R.v[0])), add(add(R.v[1], R.v[2]), add(R.w[0], R.w[1])));
+    s = add(s, add(R.w[2], add(add(R.q[0], R.q[1]), add(R.q[2], R.q[3]))));
+    if (COMP) s = add(s, add(add(R.p_lo[0], R.p_lo[1]), R.p_lo[2]));
+    return eq(mul(bc<T>(0.0f), s), bc<T>(0.0f));
+}
+
 // K ticks at a fixed command level (the body of QuadGroup.step, core.py:
-// 166-202, repeated), state updated in place.  Returns the first tick at which
-// a lane faulted (the state registers are then garbage), or -1.  With RERUN
-// the loop stops after the controller part of tick pid_only_at (used to
-// rebuild a faulted row's state, see step_row).
-template <int LEVEL, bool COMP, bool RERUN, class T, class L>
+// 166-202, repeated), state updated in place.  Passes:
+//  * fast (default): no per-tick fault test; returns K if the state is
+//    non-finite after the last tick (some tick faulted), else -1;
+//  * CHECK: the reference's per-tick fault predicate (quad.py:404-430);
+//    returns the first tick at which a lane faulted (registers then garbage);
+//  * RERUN: stops after the controller part of tick pid_only_at (rebuilds a
+//    faulted row's state, see step_row).
+// All three execute identical arithmetic per tick, so they agree bit for bit.
+template <int LEVEL, bool COMP, bool RERUN, bool CHECK, class T, class L>
 __device__ __forceinline__ int run_ticks(const swarmstep_quad_params &P, const ssb::Derived &D,
                                          float dt, int K, int pid_only_at, RowT<T> &R, L &lag)
 {
@@ -266,7 +284,7 @@ __device__ __forceinline__ int run_ticks(const swarmstep_quad_params &P, const s
             ssb::lag_thrust(lag.f, u, lag.phi, fbar);
             ssb::thrust_wrench(fbar, P, f_c, tau);
             const bool ok = ssb::rk4_inplace<float, COMP>(R.p_hi, R.p_lo, R.v, R.q, R.w, f_c, tau, P, D, dt);
-            if (!ok) return k;
+            if (CHECK && !ok) return k;
             ssb::lag_thrust(lag.f, u, lag.e_full, lag.f);
         } else {
             if (LEVEL == SWARMSTEP_LEVEL_MOTOR) {
@@ -275,13 +293,14 @@ __device__ __forceinline__ int run_ticks(const swarmstep_quad_params &P, const s
                 ssb::mix_row(f_c, tau, P);
             }
             const auto ok = ssb::rk4_inplace<T, COMP>(R.p_hi, R.p_lo, R.v, R.q, R.w, f_c, tau, P, D, dt);
-            if (ssb::any(ssb::mnot(ok))) return k;
+            if (CHECK && ssb::any(ssb::mnot(ok))) return k;
         }
     }
+    if (!CHECK && !RERUN && ssb::any(ssb::mnot(state_finite<COMP>(R)))) return K;
     return -1;
 }
 
-template <bool COMP, bool RERUN, class T, class A, class L>
+template <bool COMP, bool RERUN, bool CHECK, class T, class A, class L>
 __device__ __forceinline__ int run_level(const A &C, int level, int overlay_active,
                                          const swarmstep_quad_params &P, const ssb::Derived &D,
                                          float dt, int K, int pid_only_at, RowT<T> &R, L &lag)
@@ -289,20 +308,20 @@ __device__ __forceinline__ int run_level(const A &C, int level, int overlay_acti
     // level-specialised tick loops: no per-tick level branches
     if (level == SWARMSTEP_LEVEL_POS) {
         if (!overlay_active)
-            return run_ticks<SWARMSTEP_LEVEL_POS, COMP, RERUN>(P, D, dt, K, pid_only_at, R, lag);
+            return run_ticks<SWARMSTEP_LEVEL_POS, COMP, RERUN, CHECK>(P, D, dt, K, pid_only_at, R, lag);
         // tick 0 sees v_sp + overlay (setup_level added it); the overlay lasts
         // one tick (core.py:172-175, 199-201), so tick 0 is peeled off
-        int f = run_ticks<SWARMSTEP_LEVEL_POS, COMP, RERUN>(P, D, dt, 1, pid_only_at, R, lag);
+        int f = run_ticks<SWARMSTEP_LEVEL_POS, COMP, RERUN, CHECK>(P, D, dt, 1, pid_only_at, R, lag);
         if (f >= 0 || K == 1 || (RERUN && pid_only_at == 0)) return f;
 #pragma unroll
         for (int i = 0; i < 3; i++) R.u[3 + i] = C.ldc(SWARMSTEP_COL_CMD + 3 + i);
-        f = run_ticks<SWARMSTEP_LEVEL_POS, COMP, RERUN>(P, D, dt, K - 1, pid_only_at - 1, R, lag);
+        f = run_ticks<SWARMSTEP_LEVEL_POS, COMP, RERUN, CHECK>(P, D, dt, K - 1, pid_only_at - 1, R, lag);
         return f >= 0 ? f + 1 : -1;
     }
     if (level == SWARMSTEP_LEVEL_RATE)
-        return run_ticks<SWARMSTEP_LEVEL_RATE, COMP, RERUN>(P, D, dt, K, pid_only_at, R, lag);
+        return run_ticks<SWARMSTEP_LEVEL_RATE, COMP, RERUN, CHECK>(P, D, dt, K, pid_only_at, R, lag);
     if constexpr (sizeof(T) == sizeof(float))
-        return run_ticks<SWARMSTEP_LEVEL_MOTOR, COMP, RERUN>(P, D, dt, K, pid_only_at, R, lag);
+        return run_ticks<SWARMSTEP_LEVEL_MOTOR, COMP, RERUN, CHECK>(P, D, dt, K, pid_only_at, R, lag);
     return -1;
 }
 
@@ -328,14 +347,23 @@ __device__ __forceinline__ uint8_t step_row(const A &C, uint8_t fl, int64_t r, i
     const int level = (fl & SWARMSTEP_LEVEL_MASK) >> SWARMSTEP_LEVEL_SHIFT;
     const bool has_prev = (fl & SWARMSTEP_FLAG_HAS_PREV) != 0;
     setup_level<L>(C, level, overlay_active, P, has_prev, R);
-    const int fault_k = run_level<COMP, false>(C, level, overlay_active, P, D, dt, K, -1, R, lag);
+    int fault_k = run_level<COMP, false, false>(C, level, overlay_active, P, D, dt, K, -1, R, lag);
     bool alive = true;
     if (fault_k >= 0) {
+        // the row faulted somewhere in the launch: find the tick with the
+        // per-tick predicate (re-executing from the launch inputs) ...
+        load_state<COMP>(C, R);
+        lag.load();
+        setup_level<L>(C, level, overlay_active, P, has_prev, R);
+        fault_k = run_level<COMP, false, true>(C, level, overlay_active, P, D, dt, K, -1, R, lag);
+    }
+    if (fault_k >= 0) {
+        // ... then rebuild its state at that tick
         alive = false;
         load_state<COMP>(C, R);
         lag.load();
         setup_level<L>(C, level, overlay_active, P, has_prev, R);
-        run_level<COMP, true>(C, level, overlay_active, P, D, dt, fault_k + 1, fault_k, R, lag);
+        run_level<COMP, true, false>(C, level, overlay_active, P, D, dt, fault_k + 1, fault_k, R, lag);
         const uint32_t slot = atomicAdd(&counters[0], 1u);
         const uint32_t tick = (tick_dev ? (uint32_t)*tick_dev : 0u) + tick_base + (uint32_t)fault_k;
         if ((int64_t)slot < fault_cap)
@@ -433,7 +461,7 @@ quad_step_pair_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int
         const ssb::m2 hp{(f0 & SWARMSTEP_FLAG_HAS_PREV) != 0, (f1 & SWARMSTEP_FLAG_HAS_PREV) != 0};
         setup_level(C, l0, overlay_active, P, hp, R);
         NoLag nolag;
-        if (run_level<COMP, false>(C, l0, overlay_active, P, D, dt, K, -1, R, nolag) >= 0) {
+        if (run_level<COMP, false, false>(C, l0, overlay_active, P, D, dt, K, -1, R, nolag) >= 0) {
             // a lane faulted: redo both rows on the scalar path from the
             // launch's inputs, still untouched in HBM
             reload = true;
