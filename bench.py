@@ -182,14 +182,18 @@ def run_b200(args, rank: int, world: int) -> None:
 
     from paper_2308_12698_b200 import B200QuadGroup
 
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = _local_device()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     n, k, dt = args.agents, args.substeps, args.dt
+    nccl = _backend() == "nccl"
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if nccl:
+                dist.barrier(device_ids=[local])
+            else:
+                dist.barrier()
 
     t_setup = time.perf_counter()
     pos, sp = workload(n, seed=rank, id_base=rank * n)
@@ -202,7 +206,7 @@ def run_b200(args, rank: int, world: int) -> None:
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=dev if nccl else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -372,6 +376,20 @@ def _traffic(key: str, n: int):
     return d["dram_bytes_per_agent"] * n
 
 
+def _backend() -> str:
+    # nccl (one rank per GPU, the driver's launch).  SWARMSTEP_BENCH_BACKEND=gloo
+    # is a plumbing check only: N ranks may then share one GPU (LOCAL_RANK mod
+    # device count) to exercise the multi-rank code path on a 1-GPU box; its
+    # numbers are not measurements.
+    return os.environ.get("SWARMSTEP_BENCH_BACKEND", "nccl")
+
+
+def _local_device() -> int:
+    import torch
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return local % max(1, torch.cuda.device_count()) if _backend() == "gloo" else local
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -382,8 +400,8 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(_local_device())
+        dist.init_process_group(_backend())
     try:
         run_b200(args, rank, world)
     finally:
