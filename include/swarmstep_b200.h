@@ -212,7 +212,28 @@ int swarmstep_neighbor_workspace_bytes(int64_t n_all, uint64_t *bytes);
  * overlay column block.  Deterministic summation order. */
 int swarmstep_neighbor_overlay(const swarmstep_group_view *g, const float *all_xyzw, int64_t n_all,
                                int64_t self_offset, float r_sense, float k_sep, float cell,
-                               int accumulate, void *workspace, uint64_t ws_bytes, void *stream);
+                               int accumulate, void *workspace, uint64_t ws_bytes,
+                               const uint32_t *slot_epoch, void *stream);
+/* slot_epoch: NULL (all_xyzw holds n_all float4), or the device epoch counter
+ * of the P2P exchange below (all_xyzw is its double buffer; the kernels read
+ * slot (*slot_epoch & 1), n_all float4 each). */
+
+/* The position all-gather fused into the pack kernel, over peer memory
+ * (NVLink P2P stores into every rank's symmetric buffer) -- the NCCL-free
+ * exchange of config 5.  peer_bufs: device array [world] of the ranks'
+ * double buffers (2 * world * n_pad float4 each); this rank's rows land at
+ * slot (E & 1), offset rank * n_pad, in every buffer, E = *epoch + 1.
+ * peer_signals: device array [world] of the ranks' signal pads (>= world
+ * uint32, zero-initialised); the last block release-stores E into
+ * peer_signals[q][rank] after a system fence.  arrive: this rank's device
+ * block counter (zero-initialised, left at zero).  swarmstep_p2p_wait then
+ * spins (acquire) until every writer's signal reached E and sets *epoch = E
+ * (it traps after 10 s without a peer instead of hanging).  Replaces:
+ * swarmstep_pack_positions + ncclAllGather (parallel.py NeighborSeparation). */
+int swarmstep_p2p_pack_push(const swarmstep_group_view *g, void *const *peer_bufs, int world, int rank,
+                            int64_t n_pad, uint32_t *const *peer_signals, const uint32_t *epoch,
+                            uint32_t *arrive, void *stream);
+int swarmstep_p2p_wait(const uint32_t *local_signals, int world, uint32_t *epoch, void *stream);
 
 /* ---- device-resident setpoint feed ---------------------- */
 

@@ -41,6 +41,7 @@ EXPORTS = (
     "swarmstep_quad_circle_setpoints", "swarmstep_tick_add", "swarmstep_quad_pack_wire",
     "swarmstep_pack_collision", "swarmstep_collision_workspace_bytes", "swarmstep_collision_pairs",
     "swarmstep_unicycle_step", "swarmstep_swarm_stats_workspace_bytes", "swarmstep_quad_swarm_stats",
+    "swarmstep_p2p_pack_push", "swarmstep_p2p_wait",
 )
 
 
@@ -96,7 +97,11 @@ def _declare(lib) -> None:
     lib.swarmstep_neighbor_workspace_bytes.restype = i32
     lib.swarmstep_neighbor_workspace_bytes.argtypes = [i64, ctypes.POINTER(ctypes.c_uint64)]
     lib.swarmstep_neighbor_overlay.restype = i32
-    lib.swarmstep_neighbor_overlay.argtypes = [view, vp, i64, i64, f32, f32, f32, i32, vp, ctypes.c_uint64, vp]
+    lib.swarmstep_neighbor_overlay.argtypes = [view, vp, i64, i64, f32, f32, f32, i32, vp, ctypes.c_uint64, vp, vp]
+    lib.swarmstep_p2p_pack_push.restype = i32
+    lib.swarmstep_p2p_pack_push.argtypes = [view, vp, i32, i32, i64, vp, vp, vp, vp]
+    lib.swarmstep_p2p_wait.restype = i32
+    lib.swarmstep_p2p_wait.argtypes = [vp, i32, vp, vp]
     lib.swarmstep_quad_circle_setpoints.restype = i32
     lib.swarmstep_quad_circle_setpoints.argtypes = [view, vp, i64, f64, f64, f64, f64, f64, f64, vp]
     lib.swarmstep_quad_pack_wire.restype = i32

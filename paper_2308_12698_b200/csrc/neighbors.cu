@@ -111,11 +111,19 @@ __global__ void pack_positions_kernel(const float *cols, const uint8_t *flags, i
     out[r] = p;
 }
 
-__global__ void hash_kernel(const float4 *pos, int64_t n_all, float inv_cell, uint32_t mask,
-                            uint32_t *keys, uint32_t *vals)
+// The gathered positions: one buffer, or (P2P exchange) slot (*slot_epoch & 1)
+// of a double buffer, chosen on the device so graph replays follow the epoch.
+__device__ __forceinline__ const float4 *gathered(const float4 *base, const uint32_t *slot_epoch, int64_t n_all)
+{
+    return slot_epoch ? base + (int64_t)(*slot_epoch & 1u) * n_all : base;
+}
+
+__global__ void hash_kernel(const float4 *pos_base, const uint32_t *slot_epoch, int64_t n_all, float inv_cell,
+                            uint32_t mask, uint32_t *keys, uint32_t *vals)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_all) return;
+    const float4 *pos = gathered(pos_base, slot_epoch, n_all);
     const float4 p = pos[i];
     // dead / padding rows (NaN) sort past every bucket
     keys[i] = isnan(p.x) ? mask + 1 : cell_hash(cell_of(p.x, inv_cell), cell_of(p.y, inv_cell),
@@ -129,11 +137,13 @@ __global__ void hash_kernel(const float4 *pos, int64_t n_all, float inv_cell, ui
 // gathered into bucket order so each range is read contiguously.  Thread i
 // fills the keys in (key[i-1], key[i]]: every entry is written exactly once,
 // no memset needed.
-__global__ void bucket_ranges_kernel(const uint32_t *keys_sorted, const uint32_t *vals_sorted, const float4 *pos,
-                                     int64_t n_all, uint32_t mask, uint32_t *cell_start, float4 *pos_sorted)
+__global__ void bucket_ranges_kernel(const uint32_t *keys_sorted, const uint32_t *vals_sorted,
+                                     const float4 *pos_base, const uint32_t *slot_epoch, int64_t n_all,
+                                     uint32_t mask, uint32_t *cell_start, float4 *pos_sorted)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i > n_all) return;
+    const float4 *pos = gathered(pos_base, slot_epoch, n_all);
     const int64_t m = (int64_t)mask + 1;
     const int64_t prev = i == 0 ? -1 : (int64_t)keys_sorted[i - 1];
     const int64_t cur = i == n_all ? m : (int64_t)keys_sorted[i];
@@ -244,7 +254,7 @@ int swarmstep_neighbor_workspace_bytes(int64_t n_all, uint64_t *bytes)
 
 int swarmstep_neighbor_overlay(const swarmstep_group_view *g, const float *all_xyzw, int64_t n_all,
                                int64_t self_offset, float r_sense, float k_sep, float cell, int accumulate,
-                               void *workspace, uint64_t ws_bytes, void *stream)
+                               void *workspace, uint64_t ws_bytes, const uint32_t *slot_epoch, void *stream)
 {
     if (!g || !g->cols || !g->flags || !all_xyzw || !workspace) return nb_err(SWARMSTEP_EINVAL, "null argument");
     if (!(r_sense > 0.0f) || !(cell >= r_sense)) return nb_err(SWARMSTEP_EINVAL, "need r_sense > 0 and cell >= r_sense");
@@ -256,13 +266,13 @@ int swarmstep_neighbor_overlay(const swarmstep_group_view *g, const float *all_x
     layout(n_all, (char *)workspace, &w);
     const float inv_cell = 1.0f / cell;
     const float4 *pos = (const float4 *)all_xyzw;
-    hash_kernel<<<grid_n(n_all, 256), 256, 0, s>>>(pos, n_all, inv_cell, w.mask, w.keys, w.vals);
+    hash_kernel<<<grid_n(n_all, 256), 256, 0, s>>>(pos, slot_epoch, n_all, inv_cell, w.mask, w.keys, w.vals);
     size_t cb = w.cub_bytes;
     if (cub::DeviceRadixSort::SortPairs(w.cub_tmp, cb, w.keys, w.keys_sorted, w.vals, w.vals_sorted,
                                         (int)n_all, 0, w.key_bits, s) != cudaSuccess)
         return nb_cuda("cub::DeviceRadixSort");
-    bucket_ranges_kernel<<<grid_n(n_all + 1, 256), 256, 0, s>>>(w.keys_sorted, w.vals_sorted, pos, n_all, w.mask,
-                                                                w.cell_start, w.pos_sorted);
+    bucket_ranges_kernel<<<grid_n(n_all + 1, 256), 256, 0, s>>>(w.keys_sorted, w.vals_sorted, pos, slot_epoch,
+                                                                n_all, w.mask, w.cell_start, w.pos_sorted);
     query_kernel<<<grid_n(n_all, 128), 128, 0, s>>>(w.pos_sorted, w.keys_sorted, w.vals_sorted, w.cell_start,
                                                    w.mask, r_sense, k_sep, n_all, g->n, self_offset, g->flags,
                                                    g->cols, accumulate);

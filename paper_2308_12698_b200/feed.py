@@ -68,7 +68,7 @@ class CircleFeed:
 class TickGraph:
     """``ticks`` ticks of [feed ->] [neighbour coupling ->] fused step (K=1 each)
     as one CUDA graph.  ``coupling`` is a ``parallel.NeighborSeparation`` on a
-    single-rank shard (its exchange is then device-only)."""
+    single-rank shard or uses the P2P exchange (its exchange is then device-only)."""
 
     def __init__(self, group, dt: float, ticks: int, feed: CircleFeed | None = None, coupling=None):
         if ticks < 1:
@@ -78,8 +78,9 @@ class TickGraph:
         group._flush_commands()
         self.group, self.dt, self.ticks = group, float(dt), int(ticks)
         self.feed = feed
-        if coupling is not None and coupling.shard.world != 1:
-            raise ValidationError("graph-captured coupling needs a single-rank shard (no NCCL in the graph)")
+        if coupling is not None and coupling.shard.world != 1 and coupling.exchange != "p2p":
+            raise ValidationError("graph-captured coupling needs a single-rank shard or the P2P exchange "
+                                  "(no NCCL call in the graph)")
         self.coupling = coupling
         self._lib = _lib.load()
         with torch.cuda.device(group.device):

@@ -8,8 +8,11 @@ contiguous agent index: rank r owns ids [lo_r, hi_r) in its own
 
 The only exchange is for the neighbour-coupled controller of config 5
 (``NeighborSeparation``): every tick each rank packs its alive positions
-(float4, NaN for dead rows), the ranks all-gather them over NCCL (NVLink /
-NVSwitch), and each rank computes the separation overlay of its own agents
+(float4, NaN for dead rows) and the ranks all-gather them -- either fused
+into the pack kernel over peer memory (``exchange="p2p"``: NVLink stores
+into every rank's symmetric buffer plus release/acquire signals,
+csrc/exchange.cu) or with NCCL (``exchange="nccl"``, the baseline) -- and
+each rank computes the separation overlay of its own agents
 against the whole swarm on its GPU (csrc/neighbors.cu), which enters the
 next tick through the group's one-tick velocity overlay (core.py:137-139,
 172-175).  The reference defines no such controller; its form follows
@@ -120,7 +123,7 @@ class NeighborSeparation:
     """
 
     def __init__(self, group, shard: ShardInfo, r_sense: float = 2.0, k_sep: float = 1.0,
-                 cell: float | None = None, process_group=None):
+                 cell: float | None = None, process_group=None, exchange: str = "nccl"):
         if not r_sense > 0.0:
             raise ValidationError("r_sense must be positive")
         self.group, self.shard = group, shard
@@ -129,18 +132,56 @@ class NeighborSeparation:
         if self.cell < self.r_sense:
             raise ValidationError("cell must be >= r_sense")
         self.pg = process_group
+        if exchange not in ("nccl", "p2p"):
+            raise ValidationError(f"exchange must be 'nccl' or 'p2p', got {exchange!r}")
+        self.exchange = exchange
         self._lib = _lib.load()
         dev = group.device
         n_all = shard.n_gathered
         self.n_all = n_all
-        self.local = torch.empty((shard.pad, 4), dtype=torch.float32, device=dev)
-        self.all = self.local if shard.world == 1 else torch.empty((n_all, 4), dtype=torch.float32, device=dev)
+        self._epoch = None
+        if exchange == "p2p":
+            self._init_p2p(dev)
+        else:
+            self.local = torch.empty((shard.pad, 4), dtype=torch.float32, device=dev)
+            self.all = self.local if shard.world == 1 else torch.empty((n_all, 4), dtype=torch.float32, device=dev)
         nbytes = ctypes.c_uint64()
         _lib.check(self._lib.swarmstep_neighbor_workspace_bytes(n_all, ctypes.byref(nbytes)))
         self.workspace = torch.empty(int(nbytes.value), dtype=torch.uint8, device=dev)
 
+    def _init_p2p(self, dev) -> None:
+        """Symmetric double buffer + signal pads across the process group
+        (torch.distributed._symmetric_memory: cuMem / IPC peer mappings)."""
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        if not dist.is_initialized():
+            raise ValidationError("exchange='p2p' needs an initialised torch.distributed process group")
+        pg = self.pg if self.pg is not None else dist.group.WORLD
+        if dist.get_world_size(pg) != self.shard.world or dist.get_rank(pg) != self.shard.rank:
+            raise ValidationError("shard does not match the process group")
+        with torch.cuda.device(dev):
+            self._buf = symm.empty((2 * self.n_all, 4), dtype=torch.float32, device=dev)
+            self._buf.fill_(float("nan"))
+            self._hdl = symm.rendezvous(self._buf, pg.group_name)
+            self._epoch = torch.zeros(1, dtype=torch.int32, device=dev)
+            self._arrive = torch.zeros(1, dtype=torch.int32, device=dev)
+            torch.cuda.synchronize(dev)
+        self._hdl.barrier()
+        self.all = self._buf
+        self._sig_local = int(self._hdl.signal_pad_ptrs[self.shard.rank])
+
     def gather(self) -> torch.Tensor:
         g = self.group
+        if self.exchange == "p2p":
+            s = ctypes.c_void_p(g.stream.cuda_stream)
+            with torch.cuda.device(g.device):
+                _lib.check(self._lib.swarmstep_p2p_pack_push(
+                    g._view_ref, ctypes.c_void_p(int(self._hdl.buffer_ptrs_dev)), self.shard.world,
+                    self.shard.rank, self.shard.pad, ctypes.c_void_p(int(self._hdl.signal_pad_ptrs_dev)),
+                    self._epoch.data_ptr(), self._arrive.data_ptr(), s))
+                _lib.check(self._lib.swarmstep_p2p_wait(ctypes.c_void_p(self._sig_local), self.shard.world,
+                                                        self._epoch.data_ptr(), s))
+            return self.all
         with torch.cuda.device(g.device), torch.cuda.stream(g.stream):
             _lib.check(self._lib.swarmstep_pack_positions(g._view_ref, self.local.data_ptr(), self.shard.pad,
                                                           ctypes.c_void_p(g.stream.cuda_stream)))
@@ -149,9 +190,19 @@ class NeighborSeparation:
                 dist.all_gather_into_tensor(self.all, self.local, group=self.pg)
         return self.all
 
+    def gathered_positions(self) -> torch.Tensor:
+        """The (n_all, 4) positions of the last exchange (the slot of the
+        current epoch for the P2P double buffer)."""
+        if self.exchange != "p2p":
+            return self.all
+        torch.cuda.synchronize(self.group.device)
+        e = int(self._epoch.item())
+        return self._buf[(e & 1) * self.n_all:((e & 1) + 1) * self.n_all]
+
     def launch(self, accumulate: bool = True) -> None:
         """Device work of one exchange: pack -> all-gather -> overlay kernel (no
-        host state change; graph-capturable when world == 1)."""
+        host state change; graph-capturable when world == 1 or with the P2P
+        exchange, whose slot selection happens on the device)."""
         g = self.group
         self.gather()
         with torch.cuda.device(g.device), torch.cuda.stream(g.stream):
@@ -159,6 +210,7 @@ class NeighborSeparation:
                 g._view_ref, self.all.data_ptr(), self.n_all, self.shard.self_offset,
                 ctypes.c_float(self.r_sense), ctypes.c_float(self.k_sep), ctypes.c_float(self.cell),
                 1 if accumulate else 0, self.workspace.data_ptr(), ctypes.c_uint64(self.workspace.numel()),
+                self._epoch.data_ptr() if self._epoch is not None else None,
                 ctypes.c_void_p(g.stream.cuda_stream)))
 
     def apply(self) -> None:

@@ -138,3 +138,58 @@ def test_swarm_stats_match_host_reduction():
             assert np.all(np.isinf(st["bbox_min"]))
         st2 = g.swarm_stats()
         assert st2["centroid"].tobytes() == st["centroid"].tobytes()
+
+
+@pytest.fixture
+def one_rank_group():
+    """A 1-rank torch.distributed group (the P2P exchange needs one for its
+    symmetric-memory rendezvous); world 1 runs the fused pack + peer-store +
+    signal + wait path with this GPU as the only peer."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+    if dist.is_initialized():
+        yield dist.group.WORLD
+        return
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        yield dist.group.WORLD
+    finally:
+        dist.destroy_process_group()
+
+
+def test_p2p_exchange_equals_nccl_path(one_rank_group):
+    """The fused P2P exchange (csrc/exchange.cu) gathers exactly the positions
+    the pack + all-gather path does, epoch after epoch (both slots of its
+    double buffer), eager and inside a CUDA graph: identical trajectories."""
+    import torch
+    from paper_2308_12698_b200.feed import TickGraph
+    from paper_2308_12698_b200.parallel import NeighborSeparation, make_shard
+    sc = _swarm(3000, 14.0, seed=5)
+    ga, gb = make_group(sc), make_group(sc)
+    ga.mark_dead([3, 99])
+    gb.mark_dead([3, 99])
+    na = NeighborSeparation(ga, make_shard(sc.n), r_sense=2.0, k_sep=1.0, exchange="nccl")
+    nb = NeighborSeparation(gb, make_shard(sc.n), r_sense=2.0, k_sep=1.0, exchange="p2p")
+    for t in range(5):
+        na.apply()
+        nb.apply()
+        assert na.gathered_positions().cpu().numpy().tobytes() == nb.gathered_positions().cpu().numpy().tobytes()
+        assert _overlay(ga).tobytes() == _overlay(gb).tobytes()
+        ga.step(1e-3)
+        gb.step(1e-3)
+    assert int(nb._epoch.item()) == 5
+    ta, tb = TickGraph(ga, 1e-3, 7, coupling=na), TickGraph(gb, 1e-3, 7, coupling=nb)
+    for _ in range(3):                      # odd tick count: the slot parity alternates across replays
+        ta.replay()
+        tb.replay()
+    torch.cuda.synchronize()
+    sa, sb = ga.batch, gb.batch
+    assert sa.pos.tobytes() == sb.pos.tobytes() and sa.vel.tobytes() == sb.vel.tobytes()
+    assert int(nb._epoch.item()) == 5 + 7 * 3   # capture records only; 3 replays of 7 ticks

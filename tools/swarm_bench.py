@@ -4,8 +4,11 @@ under torchrun).  100k quadrotors per GPU in a box at ~1 agent / 8 m^3, r_sense
 NCCL all-gather (world > 1) -> spatial hash + radix sort + 27-cell scan ->
 separation overlay -> fused step (K = 1).  Prints one JSON line (rank 0).
 
-  python tools/swarm_bench.py [agents_per_gpu] [ticks]
+  python tools/swarm_bench.py [agents_per_gpu] [ticks] [nccl|p2p]
   torchrun --nproc-per-node N tools/swarm_bench.py ...
+
+p2p = the position exchange fused into the pack kernel over peer memory
+(csrc/exchange.cu; needs a process group even at world 1).
 """
 
 from __future__ import annotations
@@ -38,21 +41,26 @@ class _B:
 def main():
     n_per = int(sys.argv[1]) if len(sys.argv) > 1 else 100_000
     ticks = int(sys.argv[2]) if len(sys.argv) > 2 else 200
+    exchange = sys.argv[3] if len(sys.argv) > 3 else "nccl"
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     pg = None
-    if world > 1:
+    if world > 1 or exchange == "p2p":
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        if world > 1:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("nccl", init_method="tcp://127.0.0.1:29555", rank=0, world_size=1,
+                                    device_id=torch.device("cuda", local))
     n_total = n_per * world
     shard = make_shard(n_total, rank, world)
     side = (8.0 * n_total) ** (1 / 3)                   # ~8 m^3 per agent
     rng = np.random.default_rng(1234)
     pos_all = rng.uniform(0, side, (n_total, 3)) + [0, 0, 10]
     g = B200QuadGroup(0, _B(pos_all[shard.lo:shard.hi], shard.lo), device=f"cuda:{local}")
-    ns = NeighborSeparation(g, shard, r_sense=2.0, k_sep=0.5, process_group=pg)
+    ns = NeighborSeparation(g, shard, r_sense=2.0, k_sep=0.5, process_group=pg, exchange=exchange)
     for _ in range(10):
         ns.step(1e-3)
     torch.cuda.synchronize()
@@ -75,7 +83,7 @@ def main():
     torch.cuda.synchronize()
     wall_ms = (time.perf_counter() - t0) / ticks * 1e3
     graph_ms = float("nan")
-    if world == 1:
+    if world == 1 or exchange == "p2p":
         # (c) the whole tick chain captured as CUDA graphs of 50 ticks
         from paper_2308_12698_b200.feed import TickGraph
         tg = TickGraph(g, 1e-3, 50, coupling=ns)
@@ -95,11 +103,12 @@ def main():
         torch.distributed.all_reduce(vals, op=torch.distributed.ReduceOp.MAX)
     if rank == 0:
         print(json.dumps({"config": "cfg5 neighbour-coupled swarm", "agents_total": n_total, "world": world,
+                          "exchange": exchange,
                           "r_sense": 2.0, "ticks": ticks, "device_ms_per_tick": float(vals[0]),
                           "wall_ms_per_tick": float(vals[1]), "graph_ms_per_tick": graph_ms,
                           "agent_steps_per_s_device": n_total / (float(vals[0]) * 1e-3),
                           "alive": int(g.batch.alive.sum())}), flush=True)
-    if world > 1:
+    if torch.distributed.is_initialized():
         torch.distributed.destroy_process_group()
 
 
