@@ -290,9 +290,12 @@ int swarmstep_collision_workspace_bytes(int64_t m, uint64_t *bytes);
  * float64 with the reference's operation order.  Colliding pairs
  * (d2 < (r_i + r_j)^2) go to coll[2k], coll[2k+1] and neighbour pairs
  * (d2 < r_sense^2) to near[...] as gathered indices (i, j); counts_dev[0],
- * counts_dev[1] receive the pair counts (all pairs are counted, only the
- * first *_cap stored; with fill == 0 nothing is stored) and counts_dev[2] is
- * non-zero if a cell coordinate left (-2^20, 2^20). */
+ * counts_dev[1] receive the pair counts and counts_dev[2] is non-zero if a
+ * cell coordinate left (-2^20, 2^20).  Two calls: fill == 0 sorts, counts
+ * the pairs per agent and scans the counts (nothing stored); fill == 1, with
+ * the same inputs and the workspace left as the fill == 0 call left it,
+ * stores the pairs (the first *_cap of each kind) at their scanned offsets --
+ * no atomics, deterministic order. */
 int swarmstep_collision_pairs(const double *xyzr, int64_t m, double cell, const int *offsets_dev, int n_off,
                               double r_sense, uint32_t *coll, uint64_t coll_cap, uint32_t *near,
                               uint64_t near_cap, uint64_t *counts_dev, void *workspace, uint64_t ws_bytes,

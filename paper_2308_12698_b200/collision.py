@@ -15,8 +15,8 @@ from __future__ import annotations
 
 import ctypes
 import math
+from collections.abc import Mapping
 from dataclasses import dataclass, field
-from typing import Mapping
 
 import numpy as np
 import torch
@@ -54,6 +54,48 @@ class CollisionReport:
     dropped: int = 0
 
 
+class NeighborSets(Mapping):
+    """The report's ``neighbor_sets`` (agent id -> sorted tuple of neighbour
+    ids, collision.py:168-175), built from the device pair list on first
+    access: an in-loop caller that only needs ``collisions`` (core.py:495-498)
+    never pays for the per-agent Python dict.  Compares equal to the plain
+    dict the reference returns."""
+
+    def __init__(self, ids_alive: np.ndarray, ids_all: np.ndarray, near):
+        # near: (k, 2) row pairs, numpy or a device tensor (copied on first use)
+        self._ids_alive, self._ids_all, self._near = ids_alive, ids_all, near
+        self._d = None
+
+    def _dict(self) -> dict:
+        if self._d is None:
+            d = {int(i): () for i in self._ids_alive}
+            near, ids_all = self._near, self._ids_all
+            if isinstance(near, torch.Tensor):
+                near = near.cpu().numpy().astype(np.int64).reshape(-1, 2)
+            na = np.concatenate([near[:, 0], near[:, 1]])
+            nb = np.concatenate([near[:, 1], near[:, 0]])
+            if na.size:
+                order = np.lexsort((ids_all[nb], ids_all[na]))
+                na, nb = na[order], nb[order]
+                bounds = np.nonzero(np.diff(na))[0] + 1
+                for chunk_a, chunk_b in zip(np.split(na, bounds), np.split(nb, bounds)):
+                    d[int(ids_all[chunk_a[0]])] = tuple(ids_all[chunk_b].tolist())
+            self._d = d
+        return self._d
+
+    def __getitem__(self, key):
+        return self._dict()[key]
+
+    def __iter__(self):
+        return iter(self._dict())
+
+    def __len__(self) -> int:
+        return int(self._ids_alive.shape[0])
+
+    def __repr__(self) -> str:
+        return repr(self._dict())
+
+
 def half_space_offsets(d_max: int, reach: float, cell: float) -> np.ndarray:
     """Cell offsets o > (0,0,0) lexicographically whose closest corners can be
     within ``reach`` (collision.py:86-95)."""
@@ -76,6 +118,26 @@ class GpuDetector:
         self._counts = torch.zeros(4, dtype=torch.int64, device=self.device)
 
     def detect(self, groups, tick: int, dropped: int = 0) -> CollisionReport:
+        ids_all, alive_all, coll_h, near_h = self.pairs(groups)
+        ids_alive = ids_all[alive_all]
+        if coll_h is None:
+            return CollisionReport(tick=tick, collisions=(), neighbor_sets={int(i): () for i in ids_alive},
+                                   dropped=dropped)
+        # host post-processing exactly as collision.py:160-175
+        src, dst = coll_h[:, 0], coll_h[:, 1]
+        ids_a = np.minimum(ids_all[src], ids_all[dst])
+        ids_b = np.maximum(ids_all[src], ids_all[dst])
+        order = np.lexsort((ids_b, ids_a))
+        collisions = tuple(zip(ids_a[order].tolist(), ids_b[order].tolist()))
+        return CollisionReport(tick=tick, collisions=collisions,
+                               neighbor_sets=NeighborSets(ids_alive, ids_all, near_h), dropped=dropped)
+
+    def pairs(self, groups):
+        """Device broad + narrow phase: (ids_all, alive_all, colliding row
+        pairs (k, 2) numpy, neighbour row pairs (k, 2) as a device int32
+        tensor) -- rows index ids_all; None when fewer than two agents are
+        alive.  Only the collision pairs cross PCIe here; the (large)
+        neighbour list is copied when the report's neighbor_sets is read."""
         cfg = self.config
         groups = sorted(groups, key=lambda g: g.type_id)
         for g in groups:
@@ -83,12 +145,14 @@ class GpuDetector:
                 raise ValidationError(f"no collision radius configured for type {g.type_id}")
             if g.device != self.device:
                 raise ValidationError("all groups must live on the detector's device")
-        alive = [g.batch.alive for g in groups]
-        ids_all = np.concatenate([g.batch.agent_ids.astype(np.int64) for g in groups]) if groups else np.empty(0, np.int64)
+        # host alive flags / ids without pulling the float64 state mirror: the
+        # device rows carry the same alive flags (dead rows are packed with
+        # a NaN radius and never paired)
+        alive = [g.alive_mask() for g in groups]
+        ids_all = np.concatenate([g.agent_ids.astype(np.int64) for g in groups]) if groups else np.empty(0, np.int64)
         alive_all = np.concatenate(alive) if groups else np.empty(0, bool)
-        neighbor_sets = {int(i): () for i in ids_all[alive_all]}
         if int(alive_all.sum()) < 2:
-            return CollisionReport(tick=tick, collisions=(), neighbor_sets=neighbor_sets, dropped=dropped)
+            return ids_all, alive_all, None, None
         rmax = max(cfg.r_collide[g.type_id] for g, a in zip(groups, alive) if a.any())
         reach = max(cfg.r_sense, 2.0 * float(rmax))
         d_max = int(math.ceil(reach / cfg.cell))
@@ -124,22 +188,7 @@ class GpuDetector:
             if n_coll or n_near:
                 run(coll.data_ptr(), n_coll, near.data_ptr(), n_near, 1)
             coll_h = coll[:2 * n_coll].cpu().numpy().astype(np.int64).reshape(-1, 2)
-            near_h = near[:2 * n_near].cpu().numpy().astype(np.int64).reshape(-1, 2)
-        # host post-processing exactly as collision.py:160-175
-        src, dst = coll_h[:, 0], coll_h[:, 1]
-        ids_a = np.minimum(ids_all[src], ids_all[dst])
-        ids_b = np.maximum(ids_all[src], ids_all[dst])
-        order = np.lexsort((ids_b, ids_a))
-        collisions = tuple(zip(ids_a[order].tolist(), ids_b[order].tolist()))
-        na = np.concatenate([near_h[:, 0], near_h[:, 1]])
-        nb = np.concatenate([near_h[:, 1], near_h[:, 0]])
-        if na.size:
-            order = np.lexsort((ids_all[nb], ids_all[na]))
-            na, nb = na[order], nb[order]
-            bounds = np.nonzero(np.diff(na))[0] + 1
-            for chunk_a, chunk_b in zip(np.split(na, bounds), np.split(nb, bounds)):
-                neighbor_sets[int(ids_all[chunk_a[0]])] = tuple(ids_all[chunk_b].tolist())
-        return CollisionReport(tick=tick, collisions=collisions, neighbor_sets=neighbor_sets, dropped=dropped)
+        return ids_all, alive_all, coll_h, near[:2 * n_near]
 
 
 def detect(groups, config: CollisionConfig, tick: int, dropped: int = 0) -> CollisionReport:

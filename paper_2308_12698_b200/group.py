@@ -556,6 +556,16 @@ class B200QuadGroup:
     def alive_count(self) -> int:
         return int(self._alive.sum())
 
+    def alive_mask(self) -> np.ndarray:
+        """Host alive flags as of the last collected step (no device read:
+        alive changes only through mark_dead and collected faults)."""
+        return self._alive
+
+    @property
+    def agent_ids(self) -> np.ndarray:
+        """The group's static agent ids (no device read)."""
+        return self._batch.agent_ids
+
     def pid_state(self) -> dict:
         """Host float64 copy of the PID columns (RatePidState, control.py:100-114)
         and the stale inner-loop setpoints (QuadGroup.omega_sp / f_c_sp)."""
