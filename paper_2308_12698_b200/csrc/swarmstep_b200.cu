@@ -40,12 +40,6 @@ int check_view(const swarmstep_group_view *g)
 // registers (no spills with the tiled layout) for 24 warps per SM.
 constexpr int kBlock = SSB_STEP_BLOCK;
 
-// one agent's row inside its tile: column k at p + k * 128 (constant offsets)
-struct Cols {
-    float *p;
-    __device__ __forceinline__ float *col(int k) const { return p + k * SWARMSTEP_TILE; }
-};
-
 // ---------------------------------------------------------------------------
 // The fused step kernel.
 // ---------------------------------------------------------------------------
