@@ -61,6 +61,19 @@ __device__ __forceinline__ float neg(float a) { return -a; }
 __device__ __forceinline__ f2 add(f2 a, f2 b) { return f2{__fadd2_rn(a.v, b.v)}; }
 __device__ __forceinline__ f2 sub(f2 a, f2 b) { return f2{__fadd2_rn(a.v, make_float2(-b.v.x, -b.v.y))}; }
 __device__ __forceinline__ f2 mul(f2 a, f2 b) { return f2{__fmul2_rn(a.v, b.v)}; }
+
+// mul_nc: a product whose result feeds an add / sub.  ptxas 12.9 contracts
+// mul.rn.f32x2 + add.rn.f32x2 into FFMA2 despite the explicit rounding (it
+// keeps scalar mul.rn / add.rn apart), which would make packed lanes round
+// differently from scalar rows.  Such a product is issued as fma(a, b, -0):
+// the same single rounding as mul.rn (round(a b) + -0 == round(a b), signed
+// zeros included), and an FFMA2 result cannot be contracted further.  The -0
+// lives in constant memory so ptxas cannot fold the FMA back into a multiply.
+// Products that feed only multiplications, FMA multiplicands or addends,
+// min / max or selects use plain mul (nothing to contract with).
+static __constant__ float c_neg_zero = -0.0f;
+__device__ __forceinline__ float mul_nc(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ f2 mul_nc(f2 a, f2 b) { return f2{__ffma2_rn(a.v, b.v, make_float2(c_neg_zero, c_neg_zero))}; }
 __device__ __forceinline__ f2 fma(f2 a, f2 b, f2 c) { return f2{__ffma2_rn(a.v, b.v, c.v)}; }
 __device__ __forceinline__ f2 fnma(f2 a, f2 b, f2 c) { return f2{__ffma2_rn(make_float2(-a.v.x, -a.v.y), b.v, c.v)}; }
 __device__ __forceinline__ f2 neg(f2 a) { return f2{make_float2(-a.v.x, -a.v.y)}; }
@@ -162,8 +175,8 @@ __device__ __forceinline__ void deriv(const T q[4], const T h[3], T fc2, T fcg, 
 {
     const T qw = q[0], qx = q[1], qy = q[2], qz = q[3];
     const T hx = h[0], hy = h[1], hz = h[2];
-    dv[0] = mul(fc2, fma(qx, qz, mul(qw, qy)));
-    dv[1] = mul(fc2, fnma(qw, qx, mul(qy, qz)));
+    dv[0] = mul_nc(fc2, fma(qx, qz, mul(qw, qy)));     // feed the RK4 stage sums
+    dv[1] = mul_nc(fc2, fnma(qw, qx, mul(qy, qz)));
     dv[2] = fnma(fc2, fma(qx, qx, mul(qy, qy)), fcg);
     dq[0] = neg(fma(qx, hx, fma(qy, hy, mul(qz, hz))));
     dq[1] = fma(qw, hx, fnma(qz, hy, mul(qy, hz)));
@@ -187,9 +200,9 @@ __device__ __forceinline__ mask_t<T> rk4_inplace(T p_hi[3], T p_lo[3], T v[3], T
     const T half = bc<T>(0.5f * dt), h6 = bc<T>(dt * (1.0f / 6.0f)), dtv = bc<T>(dt);
     const T qtr = bc<T>(0.25f * dt), hdt = bc<T>(0.5f * dt);  // stage steps on half rates
     const T two = bc<T>(2.0f);
-    const T fcm = mul(f_c, bc<T>(P.inv_m));
-    const T fc2 = add(fcm, fcm);
-    const T fcg = sub(fcm, bc<T>(D.g));
+    // fc2 = 2 f_c / m (exact doubling of f_c / m); fcg = f_c / m - g in one FMA
+    const T fc2 = mul(f_c, bc<T>(2.0f * P.inv_m));
+    const T fcg = fma(f_c, bc<T>(P.inv_m), bc<T>(-D.g));
     const T tI[3] = {mul(tau[0], bc<T>(P.inv_ixx)), mul(tau[1], bc<T>(P.inv_iyy)), mul(tau[2], bc<T>(P.inv_izz))};
     T kv[3], kq[4], kw[3];
     T av[3], aq[4], aw[3], ap[3];
@@ -232,16 +245,16 @@ __device__ __forceinline__ mask_t<T> rk4_inplace(T p_hi[3], T p_lo[3], T v[3], T
     for (int i = 0; i < 3; i++) {
         v[i] = fma(h6, av[i], v[i]);
         w[i] = fma(h6, aw[i], w[i]);
-        const T dp = mul(h6, ap[i]);
         if (COMP) {
-            // Fast2Sum: exact when |hi| >= |dp + lo| (a position against one
-            // tick's displacement); keeps |lo| <= ulp(hi)/2
-            const T b = add(dp, p_lo[i]);
+            // Fast2Sum of hi and b = dt/6 ap + lo (one FMA): exact when
+            // |hi| >= |b| (a position against one tick's displacement);
+            // keeps |lo| <= ulp(hi)/2
+            const T b = fma(h6, ap[i], p_lo[i]);
             const T sum = add(p_hi[i], b);
             p_lo[i] = sub(b, sub(sum, p_hi[i]));
             p_hi[i] = sum;
         } else {
-            p_hi[i] = add(p_hi[i], dp);
+            p_hi[i] = fma(h6, ap[i], p_hi[i]);
         }
     }
 #pragma unroll
@@ -269,9 +282,10 @@ __device__ __forceinline__ mask_t<T> rk4_inplace(T p_hi[3], T p_lo[3], T v[3], T
 template <class T>
 __device__ __forceinline__ void mix_row(T &f_c, T tau[3], const swarmstep_quad_params &P)
 {
-    const T F = mul(bc<T>(P.G_inv[0]), f_c), A = mul(bc<T>(P.G_inv[1]), tau[0]);
-    const T B = mul(bc<T>(fabsf(P.G_inv[2])), tau[1]), C = mul(bc<T>(P.G_inv[3]), tau[2]);
-    const T FpA = add(F, A), FmA = sub(F, A), BmC = sub(B, C), BpC = add(B, C);
+    // c0 f +- c1 tau_x and c2 tau_y -+ c3 tau_z, one product folded into an FMA
+    const T A = mul(bc<T>(P.G_inv[1]), tau[0]), C = mul(bc<T>(P.G_inv[3]), tau[2]);
+    const T c0 = bc<T>(P.G_inv[0]), c2 = bc<T>(fabsf(P.G_inv[2]));
+    const T FpA = fma(c0, f_c, A), FmA = fma(c0, f_c, neg(A)), BmC = fma(c2, tau[1], neg(C)), BpC = fma(c2, tau[1], C);
     T m[4] = {sub(FpA, BmC), sub(FmA, BpC), add(FmA, BpC), add(FpA, BmC)};
     const T lo = vmin(vmin(m[0], m[1]), vmin(m[2], m[3]));
     const T hi = vmax(vmax(m[0], m[1]), vmax(m[2], m[3]));
@@ -319,9 +333,9 @@ __device__ __forceinline__ void motor_wrench(const float rpm[4], const swarmstep
 // clamped mixer motor thrusts m = clip(G^-1 [f_c, tau], 0, f_max) (quad.py:153-160)
 __device__ __forceinline__ void mix_motors(float f_c, const float tau[3], const swarmstep_quad_params &P, float m[4])
 {
-    const float F = mul(P.G_inv[0], f_c), A = mul(P.G_inv[1], tau[0]);
-    const float B = mul(fabsf(P.G_inv[2]), tau[1]), C = mul(P.G_inv[3], tau[2]);
-    const float FpA = add(F, A), FmA = sub(F, A), BmC = sub(B, C), BpC = add(B, C);
+    const float A = mul(P.G_inv[1], tau[0]), C = mul(P.G_inv[3], tau[2]);
+    const float c0 = P.G_inv[0], c2 = fabsf(P.G_inv[2]);
+    const float FpA = fma(c0, f_c, A), FmA = fma(c0, f_c, -A), BmC = fma(c2, tau[1], -C), BpC = fma(c2, tau[1], C);
     m[0] = sub(FpA, BmC); m[1] = sub(FmA, BpC); m[2] = add(FmA, BpC); m[3] = add(FpA, BmC);
 #pragma unroll
     for (int i = 0; i < 4; i++) m[i] = clip(m[i], 0.0f, P.f_max);
@@ -426,7 +440,7 @@ __device__ __forceinline__ void outer_row(const T p_err[3], const T v[3], const 
     const T yr0 = neg(mul(z[2], sy)), yr1 = mul(z[2], cy), yr2 = fnma(z[1], cy, mul(z[0], sy));
     const T nysq = fma(yr0, yr0, fma(yr1, yr1, mul(yr2, yr2)));
     const T iy = rsqrt_a(nysq);
-    yd[0] = mul(yr0, iy); yd[1] = mul(yr1, iy); yd[2] = mul(yr2, iy);
+    yd[0] = mul_nc(yr0, iy); yd[1] = mul_nc(yr1, iy); yd[2] = mul_nc(yr2, iy);   // feed m_ij +- m_ji
     const mask_t<T> degen = mnot(ge(nysq, bc<T>(1e-12f)));
     if (any(degen)) {
         // x_alt = y_c x z, y_c = (-sy, cy, 0); y = z x x_alt / |x_alt|
