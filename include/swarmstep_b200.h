@@ -193,6 +193,49 @@ int swarmstep_quad_unpack_f64(const swarmstep_group_view *g, const double *pos,
                               const double *vel, const double *quat, const double *omega,
                               const uint8_t *alive, void *stream);
 
+/* ---- the reference's function-level API (SURVEY 8(b) kernel-level) -------
+ * One thread per row on the reference's own row-major layout: float32 (n,3)
+ * pos / vel / omega / tau, (n,4) quat, (n,) f_c, u8 alive / flags; all
+ * device pointers.  pos_lo (nullable): float32 low words of the positions
+ * (float64 host positions split hi + lo), carried like the group's columns. */
+
+/* dynamics_deriv (quad.py:320-335): derivative of every alive row; dead rows
+ * (alive[r] == 0; alive may be NULL = all alive) get exactly zero. */
+int swarmstep_op_deriv(int64_t n, const float *pos, const float *vel, const float *quat, const float *omega,
+                       const uint8_t *alive, const float *f_c, const float *tau, const swarmstep_quad_params *p,
+                       float *dpos, float *dvel, float *dquat, float *domega, void *stream);
+
+/* rk4_step (quad.py:350-437): one step in place for alive rows; a row whose
+ * result is non-finite (or has a zero quaternion norm) keeps its pre-step
+ * state, gets alive = 0 and fault = 1.  dt <= 0 -> SWARMSTEP_EINVAL. */
+int swarmstep_op_rk4(int64_t n, float *pos, float *pos_lo, float *vel, float *quat, float *omega, uint8_t *alive,
+                     const float *f_c, const float *tau, const swarmstep_quad_params *p, float dt, uint8_t *fault,
+                     void *stream);
+
+/* mix_to_motors (quad.py:143-168): motors (n,4) clamped to [0, f_max],
+ * realized (n,4) = (f_c, tau) the clamped motors produce (the request itself
+ * for unsaturated rows), saturated (n,). */
+int swarmstep_op_mix(int64_t n, const float *f_c, const float *tau, const swarmstep_quad_params *p, float *motors,
+                     float *realized, uint8_t *saturated, void *stream);
+
+/* rotor_thrust_torque (quad.py:130-140), elementwise over `count` speeds. */
+int swarmstep_op_rotor(int64_t count, const float *rpm, float k_t, float k_q, float omega_max, float *thrust,
+                       float *torque, uint8_t *saturated, void *stream);
+
+/* rate_pid_step (control.py:136-187): updates integral / prev_omega /
+ * has_prev in place, writes tau (n,3) and f_c (n,); dead rows: frozen state,
+ * zero output.  dt <= 0 -> SWARMSTEP_EINVAL. */
+int swarmstep_op_pid(int64_t n, const float *omega, const float *omega_sp, const float *f_c_sp,
+                     const swarmstep_quad_params *p, float dt, float *integral, float *prev_omega, uint8_t *has_prev,
+                     const uint8_t *alive, float *tau_out, float *f_c_out, void *stream);
+
+/* position_outer_loop (control.py:222-294): omega_sp (n,3), f_c_sp (n,),
+ * low (n,) free-fall floor flag; dead rows get zeros.  Non-finite inputs are
+ * the caller's to reject (the reference raises InvalidStateError). */
+int swarmstep_op_outer(int64_t n, const float *pos, const float *pos_lo, const float *vel, const float *quat,
+                       const uint8_t *alive, const float *p_sp, const float *v_sp, const float *yaw_sp,
+                       const swarmstep_quad_params *p, float *omega_sp, float *f_c_sp, uint8_t *low, void *stream);
+
 /* ---- neighbour-coupled swarm controller (config 5) --------- */
 
 /* Packs the alive rows' positions as float4 (x, y, z, 0) -- NaN for dead rows

@@ -42,6 +42,8 @@ EXPORTS = (
     "swarmstep_pack_collision", "swarmstep_collision_workspace_bytes", "swarmstep_collision_pairs",
     "swarmstep_unicycle_step", "swarmstep_swarm_stats_workspace_bytes", "swarmstep_quad_swarm_stats",
     "swarmstep_p2p_pack_push", "swarmstep_p2p_wait",
+    "swarmstep_op_deriv", "swarmstep_op_rk4", "swarmstep_op_mix", "swarmstep_op_rotor", "swarmstep_op_pid",
+    "swarmstep_op_outer",
 )
 
 
@@ -100,6 +102,18 @@ def _declare(lib) -> None:
     lib.swarmstep_neighbor_overlay.argtypes = [view, vp, i64, i64, f32, f32, f32, i32, vp, ctypes.c_uint64, vp, vp]
     lib.swarmstep_p2p_pack_push.restype = i32
     lib.swarmstep_p2p_pack_push.argtypes = [view, vp, i32, i32, i64, vp, vp, vp, vp]
+    lib.swarmstep_op_deriv.restype = i32
+    lib.swarmstep_op_deriv.argtypes = [i64] + [vp] * 8 + [vp] * 4 + [vp]
+    lib.swarmstep_op_rk4.restype = i32
+    lib.swarmstep_op_rk4.argtypes = [i64] + [vp] * 9 + [f32, vp, vp]
+    lib.swarmstep_op_mix.restype = i32
+    lib.swarmstep_op_mix.argtypes = [i64, vp, vp, vp, vp, vp, vp, vp]
+    lib.swarmstep_op_rotor.restype = i32
+    lib.swarmstep_op_rotor.argtypes = [i64, vp, f32, f32, f32, vp, vp, vp, vp]
+    lib.swarmstep_op_pid.restype = i32
+    lib.swarmstep_op_pid.argtypes = [i64, vp, vp, vp, vp, f32, vp, vp, vp, vp, vp, vp, vp]
+    lib.swarmstep_op_outer.restype = i32
+    lib.swarmstep_op_outer.argtypes = [i64] + [vp] * 9 + [vp, vp, vp, vp]
     lib.swarmstep_p2p_wait.restype = i32
     lib.swarmstep_p2p_wait.argtypes = [vp, i32, vp, vp]
     lib.swarmstep_quad_circle_setpoints.restype = i32

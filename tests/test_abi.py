@@ -94,3 +94,12 @@ def test_group_fails_loudly_without_gpu():
     from paper_2308_12698_b200 import B200QuadGroup, NativeLibraryError, batch_create
     with pytest.raises(NativeLibraryError):
         B200QuadGroup(0, batch_create(0, 2, np.zeros((2, 3))))
+
+
+def test_functional_api_fails_loudly_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2308_12698_b200 import NativeLibraryError, default_quad_params, functional
+    with pytest.raises(NativeLibraryError):
+        functional.mix_to_motors(np.array([9.81]), np.zeros((1, 3)), default_quad_params())
