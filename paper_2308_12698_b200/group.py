@@ -566,7 +566,7 @@ class B200QuadGroup:
         """The group's static agent ids (no device read)."""
         return self._batch.agent_ids
 
-    def pid_state(self) -> dict:
+    def pid_state_dict(self) -> dict:
         """Host float64 copy of the PID columns (RatePidState, control.py:100-114)
         and the stale inner-loop setpoints (QuadGroup.omega_sp / f_c_sp)."""
         blk = self.column_block(COL_INTEGRAL, COL_PREV + 3).double().cpu().numpy()
@@ -575,6 +575,27 @@ class B200QuadGroup:
             hp = ((self._flags[:self.n] & FLAG_HAS_PREV) != 0).cpu().numpy()
         return {"integral": blk[:, :3].copy(), "prev_omega": blk[:, 3:6].copy(), "has_prev": hp,
                 "omega_sp": sp[:, :3].copy(), "f_c_sp": sp[:, 3].copy()}
+
+    @property
+    def pid_state(self):
+        """QuadGroup.pid_state (core.py:93): a RatePidState-shaped snapshot
+        (integral, prev_omega, has_prev) read from the device; write back with
+        set_pid_state."""
+        from .functional import RatePidState
+        d = self.pid_state_dict()
+        st = RatePidState(self.n)
+        st.integral[:], st.prev_omega[:], st.has_prev[:] = d["integral"], d["prev_omega"], d["has_prev"]
+        return st
+
+    @property
+    def omega_sp(self) -> np.ndarray:
+        """QuadGroup.omega_sp (core.py:109): last tick's inner-loop rate setpoints."""
+        return self.pid_state_dict()["omega_sp"]
+
+    @property
+    def f_c_sp(self) -> np.ndarray:
+        """QuadGroup.f_c_sp (core.py:110): last tick's collective-thrust setpoints."""
+        return self.pid_state_dict()["f_c_sp"]
 
     def set_pid_state(self, integral=None, prev_omega=None, has_prev=None, omega_sp=None, f_c_sp=None) -> None:
         """Load PID / stale-setpoint columns (test and resume support)."""

@@ -25,7 +25,7 @@ def make_group(sc_or_arrays, compensated=True, **kw):
 
 def gpu_state(g) -> dict:
     b = g.batch
-    ps = g.pid_state()
+    ps = g.pid_state_dict()
     return dict(pos=b.pos.copy(), vel=b.vel.copy(), quat=b.quat.copy(), omega=b.omega.copy(),
                 alive=b.alive.copy(), integral=ps["integral"], prev_omega=ps["prev_omega"],
                 has_prev=ps["has_prev"], omega_sp=ps["omega_sp"], f_c_sp=ps["f_c_sp"],

@@ -26,7 +26,7 @@ def _outer(g, sp):
     """One tick at POS level; returns the outer loop's (omega_sp, f_c_sp)."""
     g.set_setpoints(np.asarray(sp, float).reshape(g.n, 7))
     g.step(1e-3)
-    ps = g.pid_state()
+    ps = g.pid_state_dict()
     return ps["omega_sp"], ps["f_c_sp"]
 
 
