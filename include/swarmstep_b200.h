@@ -136,6 +136,21 @@ int swarmstep_quad_step(const swarmstep_group_view *g, const swarmstep_quad_para
                         float dt, int k_substeps, int launch_flags, uint32_t tick_base,
                         const int64_t *tick_dev, void *stream);
 
+/* swarmstep_quad_step with the device circle strategy evaluated per tick
+ * inside the kernel (circle_swarm_strategy client.py:55-73 -> circle_reference
+ * control.py:297-315, as swarmstep_quad_circle_setpoints computes it): tick k
+ * of the launch puts every alive row at POS level with the circle setpoint of
+ * t = (*tick_dev + tick_base + k) * feed->dt and phase phase0 + dphase * row,
+ * so K ticks of a time-varying reference fuse into one launch, bit-identical
+ * to K x (swarmstep_quad_circle_setpoints + a 1-tick step).  The command
+ * columns are left holding the last tick's setpoints.  No overlay. */
+typedef struct swarmstep_circle_feed {
+    double dt, radius, omega, z, phase0, dphase;
+} swarmstep_circle_feed;
+int swarmstep_quad_step_circle(const swarmstep_group_view *g, const swarmstep_quad_params *p, float dt,
+                               int k_substeps, uint32_t tick_base, const int64_t *tick_dev,
+                               const swarmstep_circle_feed *feed, void *stream);
+
 /* swarmstep_quad_step with the opt-in first-order rotor lag of the north star
  * (absent in the reference; tau_m = 0 is swarmstep_quad_step
  * itself).  Each rotor thrust f_i follows its commanded thrust u_i (the

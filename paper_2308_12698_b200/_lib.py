@@ -34,7 +34,7 @@ STEP_OVERLAY, STEP_MOTOR, STEP_FORCE_DIRECT, STEP_FORCE_TMA, STEP_FORCE_PAIR = 0
 # every symbol include/swarmstep_b200.h declares
 EXPORTS = (
     "swarmstep_abi_version", "swarmstep_last_error", "swarmstep_device_info", "swarmstep_preload",
-    "swarmstep_quad_step", "swarmstep_quad_step_lag", "swarmstep_quad_apply_commands", "swarmstep_quad_set_setpoints",
+    "swarmstep_quad_step", "swarmstep_quad_step_lag", "swarmstep_quad_step_circle", "swarmstep_quad_apply_commands", "swarmstep_quad_set_setpoints",
     "swarmstep_quad_mark_dead", "swarmstep_quad_retarget_waypoint",
     "swarmstep_quad_pack_f64", "swarmstep_quad_unpack_f64",
     "swarmstep_pack_positions", "swarmstep_neighbor_workspace_bytes", "swarmstep_neighbor_overlay",
@@ -45,6 +45,11 @@ EXPORTS = (
     "swarmstep_op_deriv", "swarmstep_op_rk4", "swarmstep_op_mix", "swarmstep_op_rotor", "swarmstep_op_pid",
     "swarmstep_op_outer",
 )
+
+
+class CircleFeedParams(ctypes.Structure):
+    """swarmstep_circle_feed (include/swarmstep_b200.h)."""
+    _fields_ = [(k, ctypes.c_double) for k in ("dt", "radius", "omega", "z", "phase0", "dphase")]
 
 
 class GroupView(ctypes.Structure):
@@ -80,6 +85,8 @@ def _declare(lib) -> None:
     lib.swarmstep_swarm_stats_workspace_bytes.argtypes = [vp]
     lib.swarmstep_quad_swarm_stats.restype = i32
     lib.swarmstep_quad_swarm_stats.argtypes = [view, vp, vp, ctypes.c_uint64, vp]
+    lib.swarmstep_quad_step_circle.restype = i32
+    lib.swarmstep_quad_step_circle.argtypes = [view, vp, f32, i32, ctypes.c_uint32, vp, vp, vp]
     lib.swarmstep_quad_step_lag.restype = i32
     lib.swarmstep_quad_step_lag.argtypes = [view, vp, vp, f32, f32, i32, i32, ctypes.c_uint32, vp, vp]
     lib.swarmstep_quad_apply_commands.restype = i32

@@ -114,12 +114,16 @@ template <class T> __device__ __forceinline__ T zero_t() { return ssb::bc<T>(0.0
 // (quad_math.cuh), scalar rows only; the four rotor thrusts live in their own
 // tiled array (4 columns x 128 rows per tile) next to the state.
 struct NoLag {
-    static constexpr bool on = false;
+    static constexpr bool lag_on = false, feed_on = false;
+    template <class T> __device__ __forceinline__ void feed(int, RowT<T> &) const {}
+    template <class A> __device__ __forceinline__ void store_cmd(const A &, int) const {}
     __device__ __forceinline__ void load() {}
     __device__ __forceinline__ void store() const {}
 };
 struct MotorLag {
-    static constexpr bool on = true;
+    static constexpr bool lag_on = true, feed_on = false;
+    template <class T> __device__ __forceinline__ void feed(int, RowT<T> &) const {}
+    template <class A> __device__ __forceinline__ void store_cmd(const A &, int) const {}
     float *p;          // this row's rotor-thrust column 0 (column i at p + 128 i)
     float phi, e_full;      // (tau_m / dt)(1 - e^(-dt / tau_m)), e^(-dt / tau_m)
     float f[4];
@@ -132,6 +136,47 @@ struct MotorLag {
     {
 #pragma unroll
         for (int i = 0; i < 4; i++) p[i * SWARMSTEP_TILE] = f[i];
+    }
+};
+
+// In-kernel circle feed (the circle strategy of feed.cu evaluated per tick
+// inside the step, so K ticks of a time-varying reference fuse into one
+// launch).  Tick k of the launch uses circle_reference at t = (tick0 + k) dt
+// with this row's phase, computed exactly as circle_kernel computes it, so
+// the fused launch is bit-identical to K x (circle_kernel + 1-tick step).
+struct CircleFeedRow {
+    static constexpr bool lag_on = false, feed_on = true;
+    int64_t tick0;
+    double dt, radius, omega, z, phase;
+    __device__ __forceinline__ void load() {}
+    __device__ __forceinline__ void store() const {}
+    __device__ __forceinline__ void values(int k, float vals[7]) const
+    {
+        const double t = (double)(tick0 + k) * dt;
+        double th = omega * t + phase;
+        const double yaw = fmod(th + copysign(1.5707963267948966, omega), 6.283185307179586);
+        th = fmod(th, 6.283185307179586);
+        float s, c;
+        sincosf((float)th, &s, &c);
+        const float R = (float)radius, W = (float)omega;
+        vals[0] = R * c; vals[1] = R * s; vals[2] = (float)z;
+        vals[3] = -R * W * s; vals[4] = R * W * c; vals[5] = 0.0f; vals[6] = (float)yaw;
+    }
+    __device__ __forceinline__ void feed(int k, RowT<float> &R) const
+    {
+        float v[7];
+        values(k, v);
+#pragma unroll
+        for (int i = 0; i < 6; i++) R.u[i] = v[i];
+        sincosf(v[6], &R.u[7], &R.u[6]);
+    }
+    // the command columns the unfused feed would have left: tick k's values
+    template <class A> __device__ __forceinline__ void store_cmd(const A &C, int k) const
+    {
+        float v[7];
+        values(k, v);
+#pragma unroll
+        for (int i = 0; i < 7; i++) C.st(SWARMSTEP_COL_CMD + i, v[i]);
     }
 };
 
@@ -212,7 +257,7 @@ __device__ __forceinline__ void setup_level(const A &C, int level, int overlay_a
 #pragma unroll
         for (int i = 0; i < 3; i++) R.w_sp[i] = C.ldc(SWARMSTEP_COL_SP + i);
         R.f_sp = C.ldc(SWARMSTEP_COL_SP + 3);
-        if constexpr (L::on) {
+        if constexpr (L::lag_on) {
             // lagged: the commanded rotor thrusts k_t clip(rpm)^2 (quad.py:134-137)
 #pragma unroll
             for (int i = 0; i < 4; i++) {
@@ -257,6 +302,7 @@ __device__ __forceinline__ int run_ticks(const swarmstep_quad_params &P, const s
 #pragma unroll kTickUnroll
     for (int k = 0; k < K; k++) {
         if (LEVEL == SWARMSTEP_LEVEL_POS) {
+            if constexpr (L::feed_on) lag.feed(k, R);
             T p_err[3];
 #pragma unroll
             for (int i = 0; i < 3; i++) p_err[i] = ssb::sub(ssb::sub(R.u[i], R.p_hi[i]), R.p_lo[i]);
@@ -265,7 +311,7 @@ __device__ __forceinline__ int run_ticks(const swarmstep_quad_params &P, const s
         T tau[3], f_c = R.f_sp;
         ssb::pid_row(R.w, R.w_sp, P, D, dt, R.integ, R.prev, tau);
         if (RERUN && k == pid_only_at) return -1;
-        if constexpr (L::on) {
+        if constexpr (L::lag_on) {
             // commanded rotor thrusts u; the body integrates the wrench of the
             // tick-mean lagged thrust, the rotors end the tick lagged by e_full
             float u[4], fbar[4];
@@ -338,7 +384,8 @@ __device__ __forceinline__ uint8_t step_row(const A &C, uint8_t fl, int64_t r, i
         load_state<COMP>(C, R);
         lag.load();
     }
-    const int level = (fl & SWARMSTEP_LEVEL_MASK) >> SWARMSTEP_LEVEL_SHIFT;
+    // the circle feed puts every alive row at POS level (feed.cu)
+    const int level = L::feed_on ? SWARMSTEP_LEVEL_POS : (fl & SWARMSTEP_LEVEL_MASK) >> SWARMSTEP_LEVEL_SHIFT;
     const bool has_prev = (fl & SWARMSTEP_FLAG_HAS_PREV) != 0;
     setup_level<L>(C, level, overlay_active, P, has_prev, R);
     int fault_k = run_level<COMP, false, false>(C, level, overlay_active, P, D, dt, K, -1, R, lag);
@@ -365,8 +412,10 @@ __device__ __forceinline__ uint8_t step_row(const A &C, uint8_t fl, int64_t r, i
     }
     store_state<COMP>(C, level, R);
     lag.store();
+    lag.store_cmd(C, alive ? K - 1 : fault_k);
     // has_prev |= alive (control.py:181): every row reaching here was alive
-    return (uint8_t)((fl & SWARMSTEP_LEVEL_MASK) | (alive ? SWARMSTEP_FLAG_ALIVE : 0u) | SWARMSTEP_FLAG_HAS_PREV);
+    const uint8_t lv = L::feed_on ? (uint8_t)0 : (uint8_t)(fl & SWARMSTEP_LEVEL_MASK);
+    return (uint8_t)(lv | (alive ? SWARMSTEP_FLAG_ALIVE : 0u) | SWARMSTEP_FLAG_HAS_PREV);
 }
 
 // ---- direct kernel: one row per thread, loads/stores straight to HBM -------
@@ -415,6 +464,27 @@ quad_step_lag_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, floa
     Row R;
     const uint8_t nfl = step_row<COMP>(C, fl, r, overlay_active, P, D, dt, K, tick_base, tick_dev,
                                        counters, fault_log, fault_cap, R, false, lag);
+    if (nfl != fl) flags[r] = nfl;
+}
+
+// ---- circle-feed kernel: K ticks of the device circle strategy, fused -------
+template <bool COMP>
+__global__ void __launch_bounds__(kBlock, 4)
+quad_step_circle_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t n,
+                        uint32_t *__restrict__ counters, uint64_t *__restrict__ fault_log, int64_t fault_cap,
+                        uint32_t tick_base, const int64_t *tick_dev, const swarmstep_quad_params P,
+                        const ssb::Derived D, swarmstep_circle_feed feed, float dt, int K)
+{
+    const int64_t r = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    if (r >= n) return;
+    const uint8_t fl = flags[r];
+    if (!(fl & SWARMSTEP_FLAG_ALIVE)) return;    // the strategy skips dead agents (client.py:66-67)
+    const GlobalRow C{cols + ssb::tile_base(r)};
+    const CircleFeedRow cf{*tick_dev + (int64_t)tick_base, feed.dt, feed.radius, feed.omega, feed.z,
+                           feed.phase0 + feed.dphase * (double)r};
+    Row R;
+    const uint8_t nfl = step_row<COMP>(C, fl, r, 0, P, D, dt, K, tick_base, tick_dev, counters, fault_log,
+                                       fault_cap, R, false, cf);
     if (nfl != fl) flags[r] = nfl;
 }
 
@@ -764,6 +834,7 @@ int swarmstep_preload(void)
                          (const void *)quad_step_pair_kernel<true>, (const void *)quad_step_pair_kernel<false>,
                          (const void *)quad_step_tma_kernel<true>, (const void *)quad_step_tma_kernel<false>,
                          (const void *)quad_step_lag_kernel<true>, (const void *)quad_step_lag_kernel<false>,
+                         (const void *)quad_step_circle_kernel<true>, (const void *)quad_step_circle_kernel<false>,
                          (const void *)apply_commands_kernel, (const void *)set_setpoints_kernel,
                          (const void *)mark_dead_kernel, (const void *)retarget_kernel,
                          (const void *)pack_f64_kernel, (const void *)unpack_f64_kernel};
@@ -851,6 +922,28 @@ int swarmstep_quad_step_lag(const swarmstep_group_view *g, const swarmstep_quad_
         g->cols, g->flags, motor, g->n, g->counters, g->fault_log, fcap, overlay, tick_base, tick_dev, *p, D,
         phi, e_full, dt, k_substeps);
     return cuda_status("quad_step_lag_kernel");
+}
+
+int swarmstep_quad_step_circle(const swarmstep_group_view *g, const swarmstep_quad_params *p, float dt,
+                               int k_substeps, uint32_t tick_base, const int64_t *tick_dev,
+                               const swarmstep_circle_feed *feed, void *stream)
+{
+    int st = check_view(g);
+    if (st) return st;
+    if (!p || !feed || !tick_dev) return set_err(SWARMSTEP_EINVAL, "null params / feed / tick");
+    if (!(dt > 0.0f)) return set_err(SWARMSTEP_EINVAL, "dt must be positive");
+    if (!(feed->radius > 0.0)) return set_err(SWARMSTEP_EINVAL, "circle radius must be positive");
+    if (!(feed->dt > 0.0)) return set_err(SWARMSTEP_EINVAL, "feed dt must be positive");
+    if (k_substeps < 1) return set_err(SWARMSTEP_EINVAL, "k_substeps must be >= 1");
+    if (!g->counters) return set_err(SWARMSTEP_EINVAL, "null counters");
+    if (g->n == 0) return SWARMSTEP_OK;
+    const ssb::Derived D = ssb::derive(*p, 1.0f / dt);
+    const int64_t fcap = g->fault_log ? g->fault_cap : 0;
+    auto kern = g->compensated ? quad_step_circle_kernel<true> : quad_step_circle_kernel<false>;
+    kern<<<grid_for(g->n, kBlock), kBlock, 0, (cudaStream_t)stream>>>(
+        g->cols, g->flags, g->n, g->counters, g->fault_log, fcap, tick_base, tick_dev, *p, D, *feed, dt,
+        k_substeps);
+    return cuda_status("quad_step_circle_kernel");
 }
 
 int swarmstep_quad_apply_commands(const swarmstep_group_view *g, const int64_t *rows, const uint8_t *levels,

@@ -58,6 +58,32 @@ class CircleFeed:
                 self.z, self.phase0, self.dphase, ctypes.c_void_p(g.stream.cuda_stream)))
         g._cmd_stale = True
 
+    def step_fused(self, k: int) -> None:
+        """K ticks of [circle feed -> step] in ONE launch: the kernel evaluates
+        the circle setpoint of each tick itself (swarmstep_quad_step_circle),
+        bit-identical to K x (apply(); group.step(dt)) but with the state
+        register-resident across the K ticks.  Asynchronous like
+        group.step_async; collect_faults() gathers the per-tick fault ids."""
+        g = self.group
+        if k < 1:
+            raise ValidationError(f"k must be >= 1, got {k}")
+        if g._overlay_active:
+            raise ValidationError("the fused circle feed takes no velocity overlay")
+        if getattr(g, "_motor", None) is not None:
+            raise ValidationError("the fused circle feed runs the reference mixer (motor_tau = 0)")
+        g._flush_commands()
+        fp = _lib.CircleFeedParams(self.dt, self.radius, self.omega, self.z, self.phase0, self.dphase)
+        with torch.cuda.device(g.device), torch.cuda.stream(g.stream):
+            self.tick.fill_(g._tick)
+            _lib.check(self._lib.swarmstep_quad_step_circle(
+                g._view_ref, g._params_ref, ctypes.c_float(self.dt), int(k), ctypes.c_uint32(0),
+                self.tick.data_ptr(), ctypes.byref(fp), ctypes.c_void_p(g.stream.cuda_stream)))
+            g._counters_host.copy_(g._counters, non_blocking=True)
+        g._launched.append((g._tick, k))
+        g._tick += k
+        g._state_stale = True
+        g._cmd_stale = True
+
     def advance(self, k: int) -> None:
         g = self.group
         with torch.cuda.device(g.device):

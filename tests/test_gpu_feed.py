@@ -119,3 +119,40 @@ def test_closed_loop_circle_demo_shape():
     rms = float(np.max(np.sqrt(sq / samples)))
     assert rms < 0.3, rms
     assert worst_div < 1e-3, worst_div     # bounded divergence from the float64 oracle over 40 s
+
+
+@pytest.mark.parametrize("k", [1, 7, 25])
+def test_fused_circle_feed_bit_identical(k):
+    """K ticks of the circle strategy evaluated inside one launch ==
+    K x (feed kernel + 1-tick step): state, command columns, levels, faults
+    (row 9 faults on the first fed tick through a NaN D-term sample)."""
+    from paper_2308_12698_b200 import AgentCommand, CommandLevel
+    from paper_2308_12698_b200.feed import CircleFeed
+    outs = []
+    for fused in (False, True):
+        g = _circle_group(300)
+        g.apply_command(AgentCommand(5, CommandLevel.RATE, (0.0, 0.0, 0.0, 20.0)))   # the feed moves it to POS
+        g.mark_dead([7])
+        g.step(2e-3)                       # tick 0 outside the feed
+        prev = g.pid_state_dict()["prev_omega"]
+        prev[9] = np.nan
+        g.set_pid_state(prev_omega=prev)
+        feed = CircleFeed(g, 2e-3)
+        if fused:
+            feed.step_fused(k)
+            faults = g.collect_faults()
+        else:
+            faults = []
+            for _ in range(k):
+                feed.apply()
+                faults.append(g.step(2e-3))
+        st = g.batch
+        outs.append(dict(pos=st.pos.copy(), vel=st.vel.copy(), quat=st.quat.copy(), omega=st.omega.copy(),
+                         alive=st.alive.copy(), cmd=g.cmd_values.copy(), lvl=g.cmd_level.copy(),
+                         faults=[np.asarray(f).tolist() for f in faults], tick=g._tick))
+    assert outs[0]["faults"][0] == [9]
+    for key in outs[0]:
+        if key in ("faults", "tick"):
+            assert outs[0][key] == outs[1][key], key
+        else:
+            np.testing.assert_array_equal(outs[0][key], outs[1][key], err_msg=key)

@@ -10,7 +10,10 @@ three ways:
   * eager:  feed.apply() + group.step(dt) per tick through the Python group
             protocol, i.e. what the reference World loop calls (wall time,
             includes the per-tick fault-id readback);
-  * kernel: the fused step kernel alone at K = 1 (device time per launch).
+  * kernel: the fused step kernel alone at K = 1 (device time per launch);
+  * fused:  CircleFeed.step_fused(10) -- the circle strategy evaluated per
+            tick inside the step kernel, 10 ticks per launch (device time per
+            tick): the state stays in registers across the ticks.
 Writes JSON to argv[1] (default gpurun_out/latency.json).
 """
 
@@ -74,7 +77,13 @@ def measure(n: int, dt: float = 2e-3, T: int = 100) -> dict:
     eager_ms = (time.perf_counter() - t0) / ticks * 1e3
     kern_ms = ev_ms(lambda: g.step_async(dt, 1), 50, g.stream)
     g.collect_faults()
+    for _ in range(3):
+        feed.step_fused(10)
+    g.collect_faults()
+    fused_ms = ev_ms(lambda: feed.step_fused(10), 20, g.stream) / 10
+    g.collect_faults()
     return {"n": n, "graph_ms_per_tick": graph_ms, "eager_ms_per_tick": eager_ms, "kernel_ms": kern_ms,
+            "fused_k10_ms_per_tick": fused_ms,
             "graph_agent_steps_per_s": n / (graph_ms * 1e-3), "alive": int(g.batch.alive.sum())}
 
 
