@@ -143,12 +143,14 @@ int swarmstep_quad_step(const swarmstep_group_view *g, const swarmstep_quad_para
  * t = (*tick_dev + tick_base + k) * feed->dt and phase phase0 + dphase * row,
  * so K ticks of a time-varying reference fuse into one launch, bit-identical
  * to K x (swarmstep_quad_circle_setpoints + a 1-tick step).  The command
- * columns are left holding the last tick's setpoints.  No overlay. */
+ * columns are left holding the last tick's setpoints.  No overlay.
+ * launch_flags: SWARMSTEP_STEP_FORCE_DIRECT / _FORCE_PAIR as for
+ * swarmstep_quad_step (default: the paired FFMA2 kernel from K >= 2). */
 typedef struct swarmstep_circle_feed {
     double dt, radius, omega, z, phase0, dphase;
 } swarmstep_circle_feed;
 int swarmstep_quad_step_circle(const swarmstep_group_view *g, const swarmstep_quad_params *p, float dt,
-                               int k_substeps, uint32_t tick_base, const int64_t *tick_dev,
+                               int k_substeps, int launch_flags, uint32_t tick_base, const int64_t *tick_dev,
                                const swarmstep_circle_feed *feed, void *stream);
 
 /* swarmstep_quad_step with the opt-in first-order rotor lag of the north star

@@ -86,7 +86,7 @@ def _declare(lib) -> None:
     lib.swarmstep_quad_swarm_stats.restype = i32
     lib.swarmstep_quad_swarm_stats.argtypes = [view, vp, vp, ctypes.c_uint64, vp]
     lib.swarmstep_quad_step_circle.restype = i32
-    lib.swarmstep_quad_step_circle.argtypes = [view, vp, f32, i32, ctypes.c_uint32, vp, vp, vp]
+    lib.swarmstep_quad_step_circle.argtypes = [view, vp, f32, i32, i32, ctypes.c_uint32, vp, vp, vp]
     lib.swarmstep_quad_step_lag.restype = i32
     lib.swarmstep_quad_step_lag.argtypes = [view, vp, vp, f32, f32, i32, i32, ctypes.c_uint32, vp, vp]
     lib.swarmstep_quad_apply_commands.restype = i32

@@ -11,13 +11,12 @@
 #include <math.h>
 #include <stdint.h>
 
+#include "circle.cuh"
 #include "common.cuh"
 
 namespace {
 
-// circle_reference (control.py:297-315) for row r with phase phase0 + r*dphase
-// (make_circle_layout, client.py:43-52): p = (R cos th, R sin th, z),
-// v = (-R w sin th, R w cos th, 0), yaw = th + copysign(pi/2, w), th = w t + phase.
+// circle_reference for row r with phase phase0 + r*dphase (circle.cuh)
 __global__ void circle_kernel(float *cols, uint8_t *flags, int64_t n, int64_t stride, const int64_t *tick_dev,
                               int64_t tick_offset, double dt, double radius, double omega, double z,
                               double phase0, double dphase)
@@ -26,17 +25,8 @@ __global__ void circle_kernel(float *cols, uint8_t *flags, int64_t n, int64_t st
     if (r >= n) return;
     const uint8_t fl = flags[r];
     if (!(fl & SWARMSTEP_FLAG_ALIVE)) return;       // the strategy skips dead agents (client.py:66-67)
-    const double t = (double)(*tick_dev + tick_offset) * dt;
-    // the angle in double (|w t| grows without bound), reduced mod 2 pi
-    double th = omega * t + (phase0 + dphase * (double)r);
-    // heading reduced mod 2 pi as well: only cos / sin of yaw_sp are used
-    // (control.py:259-260), and float32 cannot hold an unreduced angle
-    const double yaw = fmod(th + copysign(1.5707963267948966, omega), 6.283185307179586);
-    th = fmod(th, 6.283185307179586);
-    float s, c;
-    sincosf((float)th, &s, &c);
-    const float R = (float)radius, W = (float)omega;
-    const float vals[7] = {R * c, R * s, (float)z, -R * W * s, R * W * c, 0.0f, (float)yaw};
+    float vals[7];
+    ssb::circle_values(*tick_dev + tick_offset, dt, radius, omega, z, phase0 + dphase * (double)r, vals);
 #pragma unroll
     for (int i = 0; i < 7; i++) cols[ssb::at(SWARMSTEP_COL_CMD + i, r)] = vals[i];
     const uint8_t nfl = (uint8_t)(fl & ~SWARMSTEP_LEVEL_MASK);  // POS level

@@ -12,6 +12,7 @@
 #include <string.h>
 
 #include "swarmstep_b200.h"
+#include "circle.cuh"
 #include "common.cuh"
 #include "quad_math.cuh"
 
@@ -152,15 +153,7 @@ struct CircleFeedRow {
     __device__ __forceinline__ void store() const {}
     __device__ __forceinline__ void values(int k, float vals[7]) const
     {
-        const double t = (double)(tick0 + k) * dt;
-        double th = omega * t + phase;
-        const double yaw = fmod(th + copysign(1.5707963267948966, omega), 6.283185307179586);
-        th = fmod(th, 6.283185307179586);
-        float s, c;
-        sincosf((float)th, &s, &c);
-        const float R = (float)radius, W = (float)omega;
-        vals[0] = R * c; vals[1] = R * s; vals[2] = (float)z;
-        vals[3] = -R * W * s; vals[4] = R * W * c; vals[5] = 0.0f; vals[6] = (float)yaw;
+        ssb::circle_values(tick0 + k, dt, radius, omega, z, phase, vals);
     }
     __device__ __forceinline__ void feed(int k, RowT<float> &R) const
     {
@@ -177,6 +170,35 @@ struct CircleFeedRow {
         values(k, v);
 #pragma unroll
         for (int i = 0; i < 7; i++) C.st(SWARMSTEP_COL_CMD + i, v[i]);
+    }
+};
+
+// Two rows' circle feeds as one f2 lane pair (the paired kernel).
+struct CircleFeedPair {
+    static constexpr bool lag_on = false, feed_on = true;
+    CircleFeedRow a, b;
+    __device__ __forceinline__ void load() {}
+    __device__ __forceinline__ void store() const {}
+    __device__ __forceinline__ void feed(int k, RowT<ssb::f2> &R) const
+    {
+        float va[7], vb[7];
+        a.values(k, va);
+        b.values(k, vb);
+#pragma unroll
+        for (int i = 0; i < 6; i++) R.u[i] = ssb::f2{make_float2(va[i], vb[i])};
+        float sa, ca, sb, cb;
+        sincosf(va[6], &sa, &ca);
+        sincosf(vb[6], &sb, &cb);
+        R.u[6] = ssb::f2{make_float2(ca, cb)};
+        R.u[7] = ssb::f2{make_float2(sa, sb)};
+    }
+    template <class A> __device__ __forceinline__ void store_cmd(const A &C, int k) const
+    {
+        float va[7], vb[7];
+        a.values(k, va);
+        b.values(k, vb);
+#pragma unroll
+        for (int i = 0; i < 7; i++) C.st(SWARMSTEP_COL_CMD + i, ssb::f2{make_float2(va[i], vb[i])});
     }
 };
 
@@ -500,19 +522,21 @@ quad_step_circle_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, i
 #ifndef SSB_PAIR_MINB
 #define SSB_PAIR_MINB 8   // 128 regs: 16 warps per SM (measured best, profiles/tune_r01_v4.json)
 #endif
-template <bool COMP>
-__global__ void __launch_bounds__(64, SSB_PAIR_MINB)
-quad_step_pair_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t n,
-                      uint32_t *__restrict__ counters, uint64_t *__restrict__ fault_log,
-                      int64_t fault_cap, int overlay_active, uint32_t tick_base, const int64_t *tick_dev,
-                      const swarmstep_quad_params P, const ssb::Derived D, float dt, int K)
+// The paired kernel's per-thread body.  PF / RF: the launch's policy for the
+// f2 pair and for a scalar row (NoLag, or the in-kernel circle feed, which
+// puts every alive row at POS level).
+template <bool COMP, class PF, class RF>
+__device__ __forceinline__ void pair_body(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t n,
+                                          uint32_t *__restrict__ counters, uint64_t *__restrict__ fault_log,
+                                          int64_t fault_cap, int overlay_active, uint32_t tick_base,
+                                          const int64_t *tick_dev, const swarmstep_quad_params &P,
+                                          const ssb::Derived &D, float dt, int K, int64_t r0, PF pf, RF rf0, RF rf1)
 {
-    const int64_t r0 = (int64_t)blockIdx.x * SWARMSTEP_TILE + threadIdx.x, r1 = r0 + 64;
-    if (r0 >= n) return;
+    const int64_t r1 = r0 + 64;
     const uint8_t f0 = flags[r0], f1 = r1 < n ? flags[r1] : 0;
     const bool a0 = f0 & SWARMSTEP_FLAG_ALIVE, a1 = f1 & SWARMSTEP_FLAG_ALIVE;
-    const int l0 = (f0 & SWARMSTEP_LEVEL_MASK) >> SWARMSTEP_LEVEL_SHIFT;
-    const int l1 = (f1 & SWARMSTEP_LEVEL_MASK) >> SWARMSTEP_LEVEL_SHIFT;
+    const int l0 = PF::feed_on ? SWARMSTEP_LEVEL_POS : (f0 & SWARMSTEP_LEVEL_MASK) >> SWARMSTEP_LEVEL_SHIFT;
+    const int l1 = PF::feed_on ? SWARMSTEP_LEVEL_POS : (f1 & SWARMSTEP_LEVEL_MASK) >> SWARMSTEP_LEVEL_SHIFT;
     const GlobalRow C0{cols + ssb::tile_base(r0)}, C1{cols + ssb::tile_base(r1)};
     const PairRow<GlobalRow> C{C0, C1};
     // both rows' loads in flight before any decision (see quad_step_kernel)
@@ -523,17 +547,19 @@ quad_step_pair_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int
     bool reload = false;
     if (paired) {
         const ssb::m2 hp{(f0 & SWARMSTEP_FLAG_HAS_PREV) != 0, (f1 & SWARMSTEP_FLAG_HAS_PREV) != 0};
-        setup_level(C, l0, overlay_active, P, hp, R);
-        NoLag nolag;
-        if (run_level<COMP, false, false>(C, l0, overlay_active, P, D, dt, K, -1, R, nolag) >= 0) {
+        setup_level<PF>(C, l0, overlay_active, P, hp, R);
+        if (run_level<COMP, false, false>(C, l0, overlay_active, P, D, dt, K, -1, R, pf) >= 0) {
             // a lane faulted: redo both rows on the scalar path from the
             // launch's inputs, still untouched in HBM
             reload = true;
         } else {
             store_state<COMP>(C, l0, R);
+            pf.store_cmd(C, K - 1);
             const uint8_t hpf = SWARMSTEP_FLAG_HAS_PREV;
-            if ((f0 | hpf) != f0) flags[r0] = f0 | hpf;
-            if ((f1 | hpf) != f1) flags[r1] = f1 | hpf;
+            const uint8_t n0 = PF::feed_on ? (uint8_t)((f0 & ~SWARMSTEP_LEVEL_MASK) | hpf) : (uint8_t)(f0 | hpf);
+            const uint8_t n1 = PF::feed_on ? (uint8_t)((f1 & ~SWARMSTEP_LEVEL_MASK) | hpf) : (uint8_t)(f1 | hpf);
+            if (n0 != f0) flags[r0] = n0;
+            if (n1 != f1) flags[r1] = n1;
             return;
         }
     }
@@ -542,15 +568,46 @@ quad_step_pair_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int
     if (a0) {
         Row Rs = lane_row(R, 0);
         const uint8_t nf = step_row<COMP>(C0, f0, r0, overlay_active, P, D, dt, K, tick_base, tick_dev,
-                                          counters, fault_log, fault_cap, Rs, !reload);
+                                          counters, fault_log, fault_cap, Rs, !reload, rf0);
         if (nf != f0) flags[r0] = nf;
     }
     if (a1) {
         Row Rs = lane_row(R, 1);
         const uint8_t nf = step_row<COMP>(C1, f1, r1, overlay_active, P, D, dt, K, tick_base, tick_dev,
-                                          counters, fault_log, fault_cap, Rs, !reload);
+                                          counters, fault_log, fault_cap, Rs, !reload, rf1);
         if (nf != f1) flags[r1] = nf;
     }
+}
+
+template <bool COMP>
+__global__ void __launch_bounds__(64, SSB_PAIR_MINB)
+quad_step_pair_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t n,
+                      uint32_t *__restrict__ counters, uint64_t *__restrict__ fault_log,
+                      int64_t fault_cap, int overlay_active, uint32_t tick_base, const int64_t *tick_dev,
+                      const swarmstep_quad_params P, const ssb::Derived D, float dt, int K)
+{
+    const int64_t r0 = (int64_t)blockIdx.x * SWARMSTEP_TILE + threadIdx.x;
+    if (r0 >= n) return;
+    pair_body<COMP>(cols, flags, n, counters, fault_log, fault_cap, overlay_active, tick_base, tick_dev, P, D, dt, K,
+                    r0, NoLag(), NoLag(), NoLag());
+}
+
+// the paired kernel with the in-kernel circle feed (every alive row at POS)
+template <bool COMP>
+__global__ void __launch_bounds__(64, SSB_PAIR_MINB)
+quad_step_pair_circle_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t n,
+                             uint32_t *__restrict__ counters, uint64_t *__restrict__ fault_log, int64_t fault_cap,
+                             uint32_t tick_base, const int64_t *tick_dev, const swarmstep_quad_params P,
+                             const ssb::Derived D, swarmstep_circle_feed feed, float dt, int K)
+{
+    const int64_t r0 = (int64_t)blockIdx.x * SWARMSTEP_TILE + threadIdx.x;
+    if (r0 >= n) return;
+    const int64_t tick0 = *tick_dev + (int64_t)tick_base;
+    const CircleFeedRow c0{tick0, feed.dt, feed.radius, feed.omega, feed.z, feed.phase0 + feed.dphase * (double)r0};
+    const CircleFeedRow c1{tick0, feed.dt, feed.radius, feed.omega, feed.z,
+                           feed.phase0 + feed.dphase * (double)(r0 + 64)};
+    pair_body<COMP>(cols, flags, n, counters, fault_log, fault_cap, 0, tick_base, tick_dev, P, D, dt, K, r0,
+                    CircleFeedPair{c0, c1}, c0, c1);
 }
 
 // ---- TMA kernel: persistent CTAs, tiles staged through shared memory --------
@@ -835,6 +892,8 @@ int swarmstep_preload(void)
                          (const void *)quad_step_tma_kernel<true>, (const void *)quad_step_tma_kernel<false>,
                          (const void *)quad_step_lag_kernel<true>, (const void *)quad_step_lag_kernel<false>,
                          (const void *)quad_step_circle_kernel<true>, (const void *)quad_step_circle_kernel<false>,
+                         (const void *)quad_step_pair_circle_kernel<true>,
+                         (const void *)quad_step_pair_circle_kernel<false>,
                          (const void *)apply_commands_kernel, (const void *)set_setpoints_kernel,
                          (const void *)mark_dead_kernel, (const void *)retarget_kernel,
                          (const void *)pack_f64_kernel, (const void *)unpack_f64_kernel};
@@ -925,7 +984,7 @@ int swarmstep_quad_step_lag(const swarmstep_group_view *g, const swarmstep_quad_
 }
 
 int swarmstep_quad_step_circle(const swarmstep_group_view *g, const swarmstep_quad_params *p, float dt,
-                               int k_substeps, uint32_t tick_base, const int64_t *tick_dev,
+                               int k_substeps, int launch_flags, uint32_t tick_base, const int64_t *tick_dev,
                                const swarmstep_circle_feed *feed, void *stream)
 {
     int st = check_view(g);
@@ -939,6 +998,14 @@ int swarmstep_quad_step_circle(const swarmstep_group_view *g, const swarmstep_qu
     if (g->n == 0) return SWARMSTEP_OK;
     const ssb::Derived D = ssb::derive(*p, 1.0f / dt);
     const int64_t fcap = g->fault_log ? g->fault_cap : 0;
+    if (!(launch_flags & SWARMSTEP_STEP_FORCE_DIRECT) &&
+        ((launch_flags & SWARMSTEP_STEP_FORCE_PAIR) || k_substeps >= SSB_PAIR_MIN_K)) {
+        auto kern = g->compensated ? quad_step_pair_circle_kernel<true> : quad_step_pair_circle_kernel<false>;
+        kern<<<(unsigned)((g->n + SWARMSTEP_TILE - 1) / SWARMSTEP_TILE), 64, 0, (cudaStream_t)stream>>>(
+            g->cols, g->flags, g->n, g->counters, g->fault_log, fcap, tick_base, tick_dev, *p, D, *feed, dt,
+            k_substeps);
+        return cuda_status("quad_step_pair_circle_kernel");
+    }
     auto kern = g->compensated ? quad_step_circle_kernel<true> : quad_step_circle_kernel<false>;
     kern<<<grid_for(g->n, kBlock), kBlock, 0, (cudaStream_t)stream>>>(
         g->cols, g->flags, g->n, g->counters, g->fault_log, fcap, tick_base, tick_dev, *p, D, *feed, dt,

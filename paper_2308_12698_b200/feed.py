@@ -76,7 +76,7 @@ class CircleFeed:
         with torch.cuda.device(g.device), torch.cuda.stream(g.stream):
             self.tick.fill_(g._tick)
             _lib.check(self._lib.swarmstep_quad_step_circle(
-                g._view_ref, g._params_ref, ctypes.c_float(self.dt), int(k), ctypes.c_uint32(0),
+                g._view_ref, g._params_ref, ctypes.c_float(self.dt), int(k), g._launch_flags(), ctypes.c_uint32(0),
                 self.tick.data_ptr(), ctypes.byref(fp), ctypes.c_void_p(g.stream.cuda_stream)))
             g._counters_host.copy_(g._counters, non_blocking=True)
         g._launched.append((g._tick, k))

@@ -121,8 +121,9 @@ def test_closed_loop_circle_demo_shape():
     assert worst_div < 1e-3, worst_div     # bounded divergence from the float64 oracle over 40 s
 
 
+@pytest.mark.parametrize("kern", ["direct", "pair"])
 @pytest.mark.parametrize("k", [1, 7, 25])
-def test_fused_circle_feed_bit_identical(k):
+def test_fused_circle_feed_bit_identical(k, kern):
     """K ticks of the circle strategy evaluated inside one launch ==
     K x (feed kernel + 1-tick step): state, command columns, levels, faults
     (row 9 faults on the first fed tick through a NaN D-term sample)."""
@@ -139,6 +140,7 @@ def test_fused_circle_feed_bit_identical(k):
         g.set_pid_state(prev_omega=prev)
         feed = CircleFeed(g, 2e-3)
         if fused:
+            g.kernel = kern
             feed.step_fused(k)
             faults = g.collect_faults()
         else:
