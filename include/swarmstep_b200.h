@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define SWARMSTEP_ABI_VERSION 1
+#define SWARMSTEP_ABI_VERSION 2
 
 enum {
     SWARMSTEP_OK = 0,

@@ -20,7 +20,7 @@ if _OVERRIDE:
     LIB_PATH = Path(_OVERRIDE)
 
 SWARMSTEP_OK, SWARMSTEP_EINVAL, SWARMSTEP_ECUDA, SWARMSTEP_ENODEV = 0, -1, -2, -3
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 # column block offsets (SWARMSTEP_COL_*)
 COL_POS, COL_VEL, COL_QUAT, COL_OMEGA = 0, 3, 6, 10
