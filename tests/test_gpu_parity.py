@@ -274,3 +274,25 @@ def test_pair_kernel_fault_fallback_bit_identical():
     assert faults[0] == faults[1] and faults[0][0] == [70]
     for q in outs[0]:
         np.testing.assert_array_equal(outs[0][q], outs[1][q], err_msg=q)
+
+
+def test_step_allocation_discipline():
+    """test_quad.py:237-256 (the reference's step reuses its workspaces): the
+    B200 step allocates no device memory once warm -- no per-tick
+    allocations, whatever K and level mix."""
+    import torch
+    sc = ALL["mixed"]()
+    g = make_group(sc)
+    run_script(g, Scenario(**{**sc.__dict__, "ticks": 5, "record": []}))
+    for k in (1, 10):
+        g.step_async(sc.dt, k)
+    g.collect_faults()
+    torch.cuda.synchronize()
+    before = torch.cuda.memory_stats()["allocation.all.allocated"]
+    for i in range(200):
+        g.step_async(sc.dt, 1 + i % 10)
+        if i % 50 == 0:
+            g.collect_faults()
+    g.collect_faults()
+    torch.cuda.synchronize()
+    assert torch.cuda.memory_stats()["allocation.all.allocated"] == before
