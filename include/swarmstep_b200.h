@@ -107,6 +107,13 @@ const char *swarmstep_last_error(void);
 /* Loads every kernel of the library on the current device (no side effects);
  * call before capturing launches into a CUDA graph. */
 int swarmstep_preload(void);
+
+/* Host-side plumbing for thin bindings: an async copy of `bytes` on `stream`
+ * (cudaMemcpyDefault: any direction, pinned host or device pointers), and a
+ * stream synchronisation that also reports any error the stream's work
+ * raised (SWARMSTEP_ECUDA + message). */
+int swarmstep_memcpy_async(void *dst, const void *src, uint64_t bytes, void *stream);
+int swarmstep_stream_sync(void *stream);
 /* Fills sm count and compute capability of the current device. */
 int swarmstep_device_info(int *sm_count, int *cc_major, int *cc_minor);
 

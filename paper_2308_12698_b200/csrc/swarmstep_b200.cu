@@ -882,6 +882,21 @@ int swarmstep_device_info(int *sm_count, int *cc_major, int *cc_minor)
     return SWARMSTEP_OK;
 }
 
+int swarmstep_memcpy_async(void *dst, const void *src, uint64_t bytes, void *stream)
+{
+    if (bytes == 0) return SWARMSTEP_OK;
+    if (!dst || !src) return set_err(SWARMSTEP_EINVAL, "null pointer");
+    if (cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDefault, (cudaStream_t)stream) != cudaSuccess)
+        return cuda_status("cudaMemcpyAsync");
+    return SWARMSTEP_OK;
+}
+
+int swarmstep_stream_sync(void *stream)
+{
+    if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return cuda_status("cudaStreamSynchronize");
+    return cuda_status("stream work");
+}
+
 int swarmstep_preload(void)
 {
     // force-load every kernel of this translation unit (lazy module loading

@@ -98,6 +98,8 @@ class B200QuadGroup:
                                counters=_ptr(self._counters), fault_log=_ptr(self._fault_log),
                                fault_cap=self._fault_cap, compensated=int(self.compensated))
         self._view_ref = ctypes.byref(self._view)
+        self._dev_idx = self.device.index
+        self._stream_h = ctypes.c_void_p(self.stream.cuda_stream)
         self._params_ref = ctypes.byref(self._dparams)
 
         # host mirrors (the reference's numpy columns)
@@ -138,11 +140,16 @@ class B200QuadGroup:
 
     # ------------------------------------------------------------------ utils
     def _call(self, fn, *args) -> None:
-        with torch.cuda.device(self.device):
+        # the device guard costs more than the launch itself on the per-tick
+        # path: only switch when the caller's current device differs
+        if torch.cuda.current_device() == self._dev_idx:
             _lib.check(fn(self._view_ref, *args))
+        else:
+            with torch.cuda.device(self.device):
+                _lib.check(fn(self._view_ref, *args))
 
     def _sync(self) -> None:
-        self.stream.synchronize()
+        _lib.check(self._lib.swarmstep_stream_sync(self._stream_h))
 
     @property
     def cols(self) -> torch.Tensor:
@@ -442,17 +449,18 @@ class B200QuadGroup:
             self._overlay_reset()
             raise InvalidStateError("non-finite quaternion input")
         self._flush_commands()
-        with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
-            self._launch(dt, k, self._launch_flags(), self._tick & 0xFFFFFF, None)
-            self._overlay_reset()
-            self._counters_host.copy_(self._counters, non_blocking=True)
+        self._launch(dt, k, self._launch_flags(), self._tick & 0xFFFFFF, None)
+        self._overlay_reset()
+        # fault counter to pinned host memory, in stream order (read by collect_faults)
+        _lib.check(self._lib.swarmstep_memcpy_async(self._counters_host.data_ptr(), self._counters.data_ptr(),
+                                                    self._counters.numel() * 4, self._stream_h))
         self._launched.append((self._tick, k))
         self._tick += k
         self._state_stale = True
 
     def _launch(self, dt: float, k: int, flags: int, tick_base: int, tick_dev) -> None:
         """One step launch on the group's stream (no host bookkeeping)."""
-        s = ctypes.c_void_p(self.stream.cuda_stream)
+        s = self._stream_h
         if self._motor is None:
             self._call(self._lib.swarmstep_quad_step, self._params_ref, ctypes.c_float(dt), int(k), flags,
                        ctypes.c_uint32(tick_base), tick_dev, s)
@@ -516,7 +524,7 @@ class B200QuadGroup:
 
     def _overlay_reset(self) -> None:
         if self._overlay_active:
-            with torch.cuda.stream(self.stream):
+            with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
                 self._cols[:, COL_OVERLAY:COL_OVERLAY + 3, :].zero_()
         self._overlay_active = False
         self._overlay_poison = False
