@@ -44,18 +44,21 @@ class CircleFeed:
         self._lib = _lib.load()
         with torch.cuda.device(group.device):
             self.tick = torch.full((1,), group._tick, dtype=torch.int64, device=group.device)
+            self._zero = torch.zeros(1, dtype=torch.int64, device=group.device)
 
     def apply(self, tick_offset: int = 0, sync_tick: bool = True) -> None:
-        """Write the setpoints of tick (*tick + tick_offset); by default the device
-        tick is first set to the group's current tick (the next one to step)."""
+        """Write the setpoints of the group's current tick (the next one to
+        step) + tick_offset; with sync_tick=False, of (*tick + tick_offset)
+        with the device tick counter as it stands (the graph-captured form)."""
         g = self.group
-        with torch.cuda.device(g.device):
-            if sync_tick:
-                with torch.cuda.stream(g.stream):
-                    self.tick.fill_(g._tick)
-            _lib.check(self._lib.swarmstep_quad_circle_setpoints(
-                g._view_ref, self.tick.data_ptr(), int(tick_offset), self.dt, self.radius, self.omega,
-                self.z, self.phase0, self.dphase, ctypes.c_void_p(g.stream.cuda_stream)))
+        if sync_tick:
+            # the host knows the tick: pass it as the offset from a zero counter
+            # (no device write, no torch launch on the per-tick path)
+            tick_ptr, off = self._zero.data_ptr(), g._tick + int(tick_offset)
+        else:
+            tick_ptr, off = self.tick.data_ptr(), int(tick_offset)
+        g._call(self._lib.swarmstep_quad_circle_setpoints, tick_ptr, off, self.dt, self.radius, self.omega,
+                self.z, self.phase0, self.dphase, g._stream_h)
         g._cmd_stale = True
 
     def step_fused(self, k: int) -> None:
