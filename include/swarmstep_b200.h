@@ -274,9 +274,10 @@ int swarmstep_neighbor_workspace_bytes(int64_t n_all, uint64_t *bytes);
 /* Separation overlay for the local rows from all gathered positions:
  *   v_i += sum_{j != i, alive, |p_i - p_j| < r_sense} k_sep (1 - d/r_sense) (p_i - p_j)/d
  * (wire.py:320-340 repel field per neighbour, strict < as collision.py:166).
- * Local row r is gathered row self_offset + r.  Spatial hash (cell >= r_sense)
- * + CUB radix sort + 27-cell scan; writes (or adds, accumulate != 0) the
- * overlay column block.  Deterministic summation order. */
+ * Local row r is gathered row self_offset + r.  Linear spatial hash (cell >=
+ * r_sense), counting sort by bucket, 27-cell scan in 9 contiguous x-rows;
+ * writes (or adds, accumulate != 0) the overlay column block.  Sums in 64-bit
+ * fixed point: bit-deterministic.  |k_sep| < 2^30. */
 int swarmstep_neighbor_overlay(const swarmstep_group_view *g, const float *all_xyzw, int64_t n_all,
                                int64_t self_offset, float r_sense, float k_sep, float cell,
                                int accumulate, void *workspace, uint64_t ws_bytes,

@@ -9,16 +9,20 @@
 // input of the group (core.py:137-139, 172-175).
 //
 // Pipeline per tick (one process per GPU): pack the local shard's positions
-// (float4, NaN for dead rows) -> NCCL all-gather across ranks (host side,
-// torch.distributed) -> spatial hash of every gathered agent -> radix sort
-// (CUB) -> bucket lower bounds + positions gathered into bucket order -> one
-// thread per local agent, in bucket order, scans the 9 x-rows of its 27
-// neighbouring cells.  Summation order is fixed: bit-deterministic results.
+// (float4, NaN for dead rows) -> all-gather across ranks (NCCL, or fused into
+// the pack kernel over peer memory, exchange.cu) -> counting sort by spatial
+// hash bucket: one kernel hashes every gathered agent and takes its rank in
+// its bucket with an atomic counter, a CUB exclusive scan of the counts gives
+// every bucket's start, one kernel scatters the positions into bucket order
+// -> one thread per local agent, in bucket order, scans the 9 x-rows of its 27
+// neighbouring cells.  The atomic ranks make the order inside a bucket vary
+// run to run, so the overlay is summed in 64-bit fixed point (2^-32 m/s
+// resolution): integer adds commute, and results are bit-deterministic.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
 
-#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include "common.cuh"
 
@@ -54,13 +58,13 @@ uint64_t next_pow2(uint64_t x)
 }
 
 struct Workspace {
-    uint32_t *keys, *vals, *keys_sorted, *vals_sorted;
-    uint32_t *cell_start;   // m + 1 entries: lower bound of every bucket in the sorted keys
+    uint32_t *keys, *ranks, *keys_sorted, *vals_sorted;
+    uint32_t *count;        // m + 1 bucket counts (bucket m: dead / padding rows)
+    uint32_t *cell_start;   // m + 1 exclusive-scan starts: bucket k is [start[k], start[k+1])
     float4 *pos_sorted;     // alive positions in bucket order, .w = original index bits
     void *cub_tmp;
     size_t cub_bytes;
     uint32_t mask;
-    int key_bits;
 };
 
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -70,25 +74,22 @@ size_t layout(int64_t n_all, char *base, Workspace *w)
 {
     const uint64_t m = next_pow2((uint64_t)(2 * (n_all > 0 ? n_all : 1)));
     size_t cub_bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (uint32_t *)nullptr, (uint32_t *)nullptr,
-                                    (uint32_t *)nullptr, (uint32_t *)nullptr, (int)n_all);
+    cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, (uint32_t *)nullptr, (uint32_t *)nullptr, (int)(m + 1));
     const size_t nb = align256(sizeof(uint32_t) * (size_t)n_all), mb = align256(sizeof(uint32_t) * (m + 1));
     const size_t pb = align256(sizeof(float4) * (size_t)n_all);
     if (w) {
         w->keys = (uint32_t *)base;
-        w->vals = (uint32_t *)(base + nb);
+        w->ranks = (uint32_t *)(base + nb);
         w->keys_sorted = (uint32_t *)(base + 2 * nb);
         w->vals_sorted = (uint32_t *)(base + 3 * nb);
-        w->cell_start = (uint32_t *)(base + 4 * nb);
-        w->pos_sorted = (float4 *)(base + 4 * nb + mb);
-        w->cub_tmp = base + 4 * nb + mb + pb;
+        w->count = (uint32_t *)(base + 4 * nb);
+        w->cell_start = (uint32_t *)(base + 4 * nb + mb);
+        w->pos_sorted = (float4 *)(base + 4 * nb + 2 * mb);
+        w->cub_tmp = base + 4 * nb + 2 * mb + pb;
         w->cub_bytes = cub_bytes;
         w->mask = (uint32_t)(m - 1);
-        int bits = 0;
-        while ((1ull << bits) <= m) bits++;   // keys in [0, m], m = sentinel
-        w->key_bits = bits;
     }
-    return 4 * nb + mb + pb + align256(cub_bytes);
+    return 4 * nb + 2 * mb + pb + align256(cub_bytes);
 }
 
 __global__ void pack_positions_kernel(const float *cols, const uint8_t *flags, int64_t n, int64_t stride,
@@ -118,63 +119,62 @@ __device__ __forceinline__ const float4 *gathered(const float4 *base, const uint
     return slot_epoch ? base + (int64_t)(*slot_epoch & 1u) * n_all : base;
 }
 
-__global__ void hash_kernel(const float4 *pos_base, const uint32_t *slot_epoch, int64_t n_all, float inv_cell,
-                            uint32_t mask, uint32_t *keys, uint32_t *vals)
+// bucket of every gathered agent (dead / padding rows: bucket m, past every
+// real bucket) and its rank inside the bucket
+__global__ void hash_count_kernel(const float4 *pos_base, const uint32_t *slot_epoch, int64_t n_all, float inv_cell,
+                                  uint32_t mask, uint32_t *keys, uint32_t *ranks, uint32_t *count)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_all) return;
-    const float4 *pos = gathered(pos_base, slot_epoch, n_all);
-    const float4 p = pos[i];
-    // dead / padding rows (NaN) sort past every bucket
-    keys[i] = isnan(p.x) ? mask + 1 : cell_hash(cell_of(p.x, inv_cell), cell_of(p.y, inv_cell),
-                                                 cell_of(p.z, inv_cell), mask);
-    vals[i] = (uint32_t)i;
+    const float4 p = gathered(pos_base, slot_epoch, n_all)[i];
+    const uint32_t k = isnan(p.x) ? mask + 1 : cell_hash(cell_of(p.x, inv_cell), cell_of(p.y, inv_cell),
+                                                          cell_of(p.z, inv_cell), mask);
+    keys[i] = k;
+    ranks[i] = atomicAdd(&count[k], 1u);
 }
 
-// cell_start[k] = first sorted position whose key is >= k, for k in [0, m]
-// (empty buckets included, so bucket k is [start[k], start[k+1]) and a run of
-// consecutive buckets is [start[lo], start[hi+1])); and the alive positions
-// gathered into bucket order so each range is read contiguously.  Thread i
-// fills the keys in (key[i-1], key[i]]: every entry is written exactly once,
-// no memset needed.
-__global__ void bucket_ranges_kernel(const uint32_t *keys_sorted, const uint32_t *vals_sorted,
-                                     const float4 *pos_base, const uint32_t *slot_epoch, int64_t n_all,
-                                     uint32_t mask, uint32_t *cell_start, float4 *pos_sorted)
+// counting-sort scatter: the agent goes to start[bucket] + rank, its position
+// (index in .w) with it
+__global__ void scatter_kernel(const float4 *pos_base, const uint32_t *slot_epoch, int64_t n_all, uint32_t mask,
+                               const uint32_t *keys, const uint32_t *ranks, const uint32_t *cell_start,
+                               uint32_t *keys_sorted, uint32_t *vals_sorted, float4 *pos_sorted)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i > n_all) return;
-    const float4 *pos = gathered(pos_base, slot_epoch, n_all);
-    const int64_t m = (int64_t)mask + 1;
-    const int64_t prev = i == 0 ? -1 : (int64_t)keys_sorted[i - 1];
-    const int64_t cur = i == n_all ? m : (int64_t)keys_sorted[i];
-    for (int64_t k = prev + 1; k <= cur; k++) cell_start[k] = (uint32_t)i;
-    if (i < n_all && cur <= (int64_t)mask) {
-        const uint32_t idx = vals_sorted[i];
-        float4 p = pos[idx];
-        p.w = __uint_as_float(idx);
-        pos_sorted[i] = p;
+    if (i >= n_all) return;
+    const uint32_t k = keys[i];
+    const uint32_t slot = cell_start[k] + ranks[i];
+    keys_sorted[slot] = k;
+    vals_sorted[slot] = (uint32_t)i;
+    if (k <= mask) {
+        float4 p = gathered(pos_base, slot_epoch, n_all)[i];
+        p.w = __uint_as_float((uint32_t)i);
+        pos_sorted[slot] = p;
     }
 }
 
+// overlay sums in 64-bit fixed point, 2^32 units per m/s: order-independent
+constexpr float kFix = 4294967296.0f;
+
 __device__ __forceinline__ void sep_accumulate(const float4 &p, const float4 &q, bool take, float r2, float inv_r,
-                                               float k_sep, float &ax, float &ay, float &az)
+                                               float k_sep, long long &ax, long long &ay, long long &az)
 {
     const float ddx = p.x - q.x, ddy = p.y - q.y, ddz = p.z - q.z;
     const float d2 = fmaf(ddx, ddx, fmaf(ddy, ddy, ddz * ddz));
     if (!take || !(d2 < r2) || !(d2 > 1e-24f)) return;   // strict <, d > 1e-12
     const float d = sqrtf(d2);
     const float s = k_sep * (1.0f - d * inv_r) / d;
-    ax = fmaf(s, ddx, ax);
-    ay = fmaf(s, ddy, ay);
-    az = fmaf(s, ddz, az);
+    // |s dd| <= |k_sep| < 2^30 (checked by the caller): exact scaling, one rounding
+    ax += __float2ll_rn(s * ddx * kFix);
+    ay += __float2ll_rn(s * ddy * kFix);
+    az += __float2ll_rn(s * ddz * kFix);
 }
 
 // One thread per agent in BUCKET order (neighbouring threads are neighbouring
 // cells, so their candidate ranges overlap and hit L1).  An agent's 27
 // neighbour cells are 9 x-rows, each one contiguous range of pos_sorted
 // (split in two only where the row wraps the table end); each range is read
-// four candidates at a time with independent loads.  Summation order is
-// fixed (row order, then sorted order): bit-deterministic run to run.
+// four candidates at a time with independent loads.  Fixed-point sums: the
+// result does not depend on the order the candidates are visited in.
 __global__ void __launch_bounds__(128) query_kernel(const float4 *pos_sorted, const uint32_t *keys_sorted,
                                                     const uint32_t *vals_sorted, const uint32_t *cell_start,
                                                     uint32_t mask, float r_sense, float k_sep, int64_t n_all,
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(128) query_kernel(const float4 *pos_sorted, co
     const int64_t r = (int64_t)vals_sorted[j] - self_offset;
     if (r < 0 || r >= n_local) return;                       // another rank's agent
     const uint32_t h = keys_sorted[j];
-    float ax = 0.0f, ay = 0.0f, az = 0.0f;
+    long long ax = 0, ay = 0, az = 0;
     if (h <= mask && (flags[r] & SWARMSTEP_FLAG_ALIVE)) {
         const float4 p = pos_sorted[j];
         const float r2 = r_sense * r_sense, inv_r = 1.0f / r_sense;
@@ -222,10 +222,11 @@ __global__ void __launch_bounds__(128) query_kernel(const float4 *pos_sorted, co
     float *ox = cols + ssb::at(SWARMSTEP_COL_OVERLAY + 0, r);
     float *oy = cols + ssb::at(SWARMSTEP_COL_OVERLAY + 1, r);
     float *oz = cols + ssb::at(SWARMSTEP_COL_OVERLAY + 2, r);
+    const float fx = (float)((double)ax / kFix), fy = (float)((double)ay / kFix), fz = (float)((double)az / kFix);
     if (accumulate) {
-        *ox += ax; *oy += ay; *oz += az;
+        *ox += fx; *oy += fy; *oz += fz;
     } else {
-        *ox = ax; *oy = ay; *oz = az;
+        *ox = fx; *oy = fy; *oz = fz;
     }
 }
 
@@ -266,13 +267,15 @@ int swarmstep_neighbor_overlay(const swarmstep_group_view *g, const float *all_x
     layout(n_all, (char *)workspace, &w);
     const float inv_cell = 1.0f / cell;
     const float4 *pos = (const float4 *)all_xyzw;
-    hash_kernel<<<grid_n(n_all, 256), 256, 0, s>>>(pos, slot_epoch, n_all, inv_cell, w.mask, w.keys, w.vals);
+    if (!(fabsf(k_sep) < 1073741824.0f)) return nb_err(SWARMSTEP_EINVAL, "need |k_sep| < 2^30 (fixed-point sums)");
+    cudaMemsetAsync(w.count, 0, sizeof(uint32_t) * ((size_t)w.mask + 2), s);
+    hash_count_kernel<<<grid_n(n_all, 256), 256, 0, s>>>(pos, slot_epoch, n_all, inv_cell, w.mask, w.keys, w.ranks,
+                                                         w.count);
     size_t cb = w.cub_bytes;
-    if (cub::DeviceRadixSort::SortPairs(w.cub_tmp, cb, w.keys, w.keys_sorted, w.vals, w.vals_sorted,
-                                        (int)n_all, 0, w.key_bits, s) != cudaSuccess)
-        return nb_cuda("cub::DeviceRadixSort");
-    bucket_ranges_kernel<<<grid_n(n_all + 1, 256), 256, 0, s>>>(w.keys_sorted, w.vals_sorted, pos, slot_epoch,
-                                                                n_all, w.mask, w.cell_start, w.pos_sorted);
+    if (cub::DeviceScan::ExclusiveSum(w.cub_tmp, cb, w.count, w.cell_start, (int)(w.mask + 2), s) != cudaSuccess)
+        return nb_cuda("cub::DeviceScan");
+    scatter_kernel<<<grid_n(n_all, 256), 256, 0, s>>>(pos, slot_epoch, n_all, w.mask, w.keys, w.ranks, w.cell_start,
+                                                      w.keys_sorted, w.vals_sorted, w.pos_sorted);
     query_kernel<<<grid_n(n_all, 128), 128, 0, s>>>(w.pos_sorted, w.keys_sorted, w.vals_sorted, w.cell_start,
                                                    w.mask, r_sense, k_sep, n_all, g->n, self_offset, g->flags,
                                                    g->cols, accumulate);
