@@ -27,7 +27,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import (COL_CMD, COL_INTEGRAL, COL_OVERLAY, COL_PREV, COL_SP, FLAG_ALIVE, FLAG_HAS_PREV,
+from ._lib import (COL_CMD, COL_INTEGRAL, COL_OVERLAY, COL_PREV, COL_SP, FLAG_HAS_PREV,
                    LEVEL_MASK, LEVEL_SHIFT, NCOL, STEP_FORCE_DIRECT, STEP_FORCE_PAIR, STEP_FORCE_TMA, STEP_MOTOR,
                    STEP_OVERLAY, TILE, GroupView)
 from .commands import LEVEL_MOTOR, LEVEL_POS, LEVEL_RATE, level_code

@@ -2,7 +2,6 @@
 command levels, layouts, wire framing, collision helpers, scenario fixtures,
 and property checks with hypothesis."""
 
-import math
 import struct
 
 import numpy as np
