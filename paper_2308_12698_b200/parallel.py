@@ -106,9 +106,17 @@ class ShardedSwarm:
         return self.gather_ids(local)
 
     def gather_ids(self, local: np.ndarray) -> np.ndarray:
+        """Every rank's fault ids of the tick (one integer per
+        rank per tick; the ids themselves only move when some rank faulted)."""
         if self.shard.world == 1:
             return np.sort(local).astype(np.uint64)
         import torch.distributed as dist
+        backend = dist.get_backend(self.pg)
+        dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+        cnt = torch.tensor([int(local.size)], dtype=torch.int64, device=dev)
+        dist.all_reduce(cnt, group=self.pg)
+        if int(cnt.item()) == 0:
+            return np.empty(0, dtype=np.uint64)
         out = [None] * self.shard.world
         dist.all_gather_object(out, local.tolist(), group=self.pg)
         return np.sort(np.array([i for part in out for i in part], dtype=np.int64)).astype(np.uint64)

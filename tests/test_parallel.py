@@ -70,6 +70,7 @@ def _worker(rank, world, port, n_total, pos, alive, result_q):
         results = [sw.apply_command(type("C", (), dict(agent_id=a, level="pos", values=(0,) * 7))())
                    for a in range(n_total)]
         faults = sw.step(1e-3).tolist()
+        assert sw.step(1e-3).size == 0            # no rank faulted: only the count moves
         # position all-gather exactly as NeighborSeparation lays it out
         local = torch.full((shard.pad, 4), float("nan"))
         mine = np.arange(shard.lo, shard.hi)
