@@ -110,3 +110,34 @@ def test_two_type_world_and_frames():
     assert (t0, n0) == (0, 2)
     off = 13 + 6 + 61 * 2
     assert struct.unpack_from("<HI", frame, off) == (1, 2)
+
+
+def test_groups_stepped_from_worker_threads_bit_identical():
+    """World steps its groups on a thread pool (core.py:455-465, SWARMSTEP_THREADS);
+    each B200 group owns its stream, so concurrent stepping from worker threads
+    gives the same bits as stepping one after the other (test_core.py:314-339)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_2308_12698_b200 import B200QuadGroup, batch_create
+    from paper_2308_12698_b200.unicycle import B200UnicycleGroup
+
+    def make():
+        rng = np.random.default_rng(4)
+        qa = B200QuadGroup(0, batch_create(0, 5000, rng.uniform(-20, 20, (5000, 3))))
+        qb = B200QuadGroup(2, batch_create(2, 3000, rng.uniform(-20, 20, (3000, 3)), id_base=10_000))
+        uc = B200UnicycleGroup(1, batch_create(1, 700, rng.uniform(-20, 20, (700, 3)), id_base=20_000))
+        qa.set_setpoints(np.hstack([rng.uniform(-20, 20, (5000, 3)), np.zeros((5000, 4))]))
+        qb.set_setpoints(np.hstack([rng.uniform(-1, 1, (3000, 3)), np.full((3000, 1), 10.0)]), level="rate")
+        return [qa, qb, uc]
+
+    seq = make()
+    for _ in range(40):
+        for g in seq:
+            g.step(2e-3)
+    par = make()
+    with ThreadPoolExecutor(max_workers=3) as ex:
+        for _ in range(40):
+            list(ex.map(lambda g: g.step(2e-3), par))
+    for a, b in zip(seq, par):
+        assert a.batch.pos.tobytes() == b.batch.pos.tobytes()
+        assert a.batch.quat.tobytes() == b.batch.quat.tobytes()
