@@ -50,6 +50,7 @@ class CircleFeed:
         step) + tick_offset; with sync_tick=False, of (*tick + tick_offset)
         with the device tick counter as it stands (the graph-captured form)."""
         g = self.group
+        g._flush_commands()          # earlier apply_command calls land first (latest wins)
         if sync_tick:
             # the host knows the tick: pass it as the offset from a zero counter
             # (no device write, no torch launch on the per-tick path)

@@ -234,6 +234,10 @@ class B200QuadGroup:
             lv = ((self._flags[:self.n] & LEVEL_MASK) >> LEVEL_SHIFT).cpu().numpy()
         self._cmd_values[:] = vals
         self._cmd_level[:] = lv
+        # commands queued since the device columns were last written are newer
+        for row, (lvl, full) in self._pending.items():
+            self._cmd_level[row] = lvl
+            self._cmd_values[row] = full
         self._cmd_stale = False
 
     def _flush_commands(self) -> None:
@@ -244,7 +248,7 @@ class B200QuadGroup:
         vals = np.empty((rows.shape[0], 7), dtype=np.float32)
         for i, (lvl, v) in enumerate(self._pending.values()):
             levels[i] = lvl
-            vals[i] = v
+            vals[i] = v          # float64 -> float32
         self._pending.clear()
         with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
             d_rows = torch.from_numpy(rows).to(self.device)
@@ -287,7 +291,8 @@ class B200QuadGroup:
         want = 7 if lvl == LEVEL_POS else 4
         if vals.shape[0] != want:
             raise ValidationError(f"level takes {want} values, got {vals.shape[0]}")
-        self._pull_commands()
+        # no device read: the row goes to the (possibly stale) host mirror and
+        # the pending queue, which _pull_commands re-applies over the device copy
         full = np.zeros(7)
         full[:want] = vals
         self._cmd_level[row] = lvl
@@ -298,7 +303,7 @@ class B200QuadGroup:
             self._nonfinite_rows.discard(row)
         else:
             self._nonfinite_rows.add(row)
-        self._pending[row] = (lvl, full.astype(np.float32))
+        self._pending[row] = (lvl, full)
         return True
 
     def set_setpoints(self, values, level=LEVEL_POS, row0: int = 0, columns: bool = False) -> None:
@@ -386,7 +391,6 @@ class B200QuadGroup:
         """Alive rows within ``radius`` of ``point`` go to POS hold there (core.py:141-149)."""
         pt = (ctypes.c_double * 3)(*[float(x) for x in np.asarray(point, dtype=float).ravel()[:3]])
         self._flush_commands()
-        self._pull_commands()
         with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
             self._call(self._lib.swarmstep_quad_retarget_waypoint, pt, ctypes.c_double(float(radius)),
                        ctypes.c_void_p(self.stream.cuda_stream))

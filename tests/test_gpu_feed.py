@@ -158,3 +158,27 @@ def test_fused_circle_feed_bit_identical(k, kern):
             assert outs[0][key] == outs[1][key], key
         else:
             np.testing.assert_array_equal(outs[0][key], outs[1][key], err_msg=key)
+
+
+def test_command_store_latest_wins_across_device_writers():
+    """apply_command (host queue) vs device-side writers (bulk setpoints, the
+    circle feed): whichever came last wins (core.py:117-135), and the host
+    mirror shows exactly what the device will step on."""
+    from paper_2308_12698_b200 import AgentCommand, CommandLevel
+    from paper_2308_12698_b200.feed import CircleFeed
+    g = _circle_group(200)
+    sp = np.tile([1.0, 2.0, 3.0, 0.0, 0.0, 0.0, 0.5], (200, 1))
+    g.set_setpoints(sp)                                               # device writer
+    g.apply_command(AgentCommand(3, CommandLevel.RATE, (0.1, 0.2, 0.3, 9.0)))   # later: wins for row 3
+    cv, lv = g.cmd_values.copy(), g.cmd_level.copy()
+    assert lv[3] == 1 and np.allclose(cv[3], [0.1, 0.2, 0.3, 9.0, 0, 0, 0])
+    assert np.allclose(cv[4], sp[4]) and lv[4] == 0
+    feed = CircleFeed(g, 2e-3)
+    g.apply_command(AgentCommand(5, CommandLevel.RATE, (0.0, 0.0, 0.0, 9.0)))   # then the feed: feed wins
+    feed.apply()
+    assert g.cmd_level[5] == 0 and g.cmd_level[3] == 0
+    g.step(2e-3)
+    g.apply_command(AgentCommand(6, CommandLevel.MOTOR, (1e4, 1e4, 1e4, 1e4)))   # after the feed: wins
+    assert g.cmd_level[6] == 2
+    g.step(2e-3)
+    assert g.cmd_level[6] == 2 and np.allclose(g.cmd_values[6, :4], 1e4)
