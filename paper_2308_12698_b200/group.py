@@ -47,6 +47,62 @@ def _ptr(t: torch.Tensor) -> int:
     return t.data_ptr()
 
 
+class DeviceBatchView:
+    """``group.batch``: the AgentBatch interface (state.py:43-102) over a B200
+    group.  ``type_id``, ``agent_ids``, ``n`` and ``alive`` come from the host
+    without a device read (alive changes only through mark_dead and collected
+    faults), so the World's per-tick alive counts (core.py:370) stay cheap; the
+    float64 ``pos`` / ``vel`` / ``quat`` / ``omega`` mirror is pulled from the
+    device on first access after a step."""
+
+    def __init__(self, group):
+        self._g = group
+
+    @property
+    def type_id(self) -> int:
+        return self._g._batch.type_id
+
+    @property
+    def agent_ids(self) -> np.ndarray:
+        return self._g._batch.agent_ids
+
+    @property
+    def n(self) -> int:
+        return self._g.n
+
+    @property
+    def alive(self) -> np.ndarray:
+        if self._g._launched:           # faults of launches not collected yet live on the device
+            self._g._pull_state()
+        return self._g._alive
+
+    def _full(self) -> AgentBatch:
+        self._g._pull_state()
+        return self._g._batch
+
+    @property
+    def pos(self) -> np.ndarray:
+        return self._full().pos
+
+    @property
+    def vel(self) -> np.ndarray:
+        return self._full().vel
+
+    @property
+    def quat(self) -> np.ndarray:
+        return self._full().quat
+
+    @property
+    def omega(self) -> np.ndarray:
+        return self._full().omega
+
+    def validate(self) -> None:
+        self._full().validate()
+
+    def index_of(self, agent_id: int):
+        return self._g.rows_for(agent_id)
+
+
 class B200QuadGroup:
     """One quadrotor type stepped by the sm_100a fused kernel."""
 
@@ -115,6 +171,7 @@ class B200QuadGroup:
         self._row = {int(a): i for i, a in enumerate(self._batch.agent_ids)}
         self._ids_dev = None             # device copy of agent_ids (wire packing), on demand
         self._alive = self._batch.alive  # exact: changes only via mark_dead / faults
+        self._batch_view = DeviceBatchView(self)
         self._state_stale = False        # device state newer than the host mirror
         # command store (core.py:98-104): position hold at the initial pose
         self._cmd_level = np.full(n, LEVEL_POS, dtype=np.uint8)
@@ -261,10 +318,9 @@ class B200QuadGroup:
 
     # ------------------------------------------------------- group protocol
     @property
-    def batch(self) -> AgentBatch:
-        """Host float64 view of the state table, synchronised on access."""
-        self._pull_state()
-        return self._batch
+    def batch(self) -> DeviceBatchView:
+        """The AgentBatch view of the state table (DeviceBatchView)."""
+        return self._batch_view
 
     @property
     def cmd_values(self) -> np.ndarray:

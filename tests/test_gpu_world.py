@@ -141,3 +141,20 @@ def test_groups_stepped_from_worker_threads_bit_identical():
     for a, b in zip(seq, par):
         assert a.batch.pos.tobytes() == b.batch.pos.tobytes()
         assert a.batch.quat.tobytes() == b.batch.quat.tobytes()
+
+
+def test_batch_view_alive_counts_without_state_pull():
+    """World.alive_counts (core.py:370) reads batch.alive every tick: the
+    B200 batch view answers from the host (exact after collected faults)
+    without pulling the float64 state mirror."""
+    from paper_2308_12698_b200 import B200QuadGroup, batch_create
+    g = B200QuadGroup(0, batch_create(0, 1000, np.zeros((1000, 3))))
+    g.mark_dead([1, 2, 3])
+    g.step(1e-3)
+    assert g._state_stale
+    assert int(g.batch.alive.sum()) == 997 and g.batch.n == 1000 and g.batch.type_id == 0
+    assert g._state_stale                       # no device read so far
+    assert g.batch.pos.shape == (1000, 3) and not g._state_stale
+    g.step_async(1e-3, 3)                       # uncollected launches: alive comes from the device
+    assert int(g.batch.alive.sum()) == 997
+    g.collect_faults()
