@@ -85,12 +85,12 @@ class B200UnicycleGroup(B200QuadGroup):
         if k < 1:
             raise ValidationError(f"k must be >= 1, got {k}")
         self._flush_commands()
-        with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
-            self._call(self._lib.swarmstep_unicycle_step, ctypes.c_float(self.params.v_max),
-                       ctypes.c_float(self.params.omega_max), ctypes.c_float(dt), int(k),
-                       STEP_OVERLAY if self._overlay_active else 0, ctypes.c_void_p(self.stream.cuda_stream))
-            self._overlay_reset()
-            self._counters_host.copy_(self._counters, non_blocking=True)
+        self._call(self._lib.swarmstep_unicycle_step, ctypes.c_float(self.params.v_max),
+                   ctypes.c_float(self.params.omega_max), ctypes.c_float(dt), int(k),
+                   STEP_OVERLAY if self._overlay_active else 0, self._stream_h)
+        self._overlay_reset()
+        _lib.check(self._lib.swarmstep_memcpy_async(self._counters_host.data_ptr(), self._counters.data_ptr(),
+                                                    self._counters.numel() * 4, self._stream_h))
         self._launched.append((self._tick, k))
         self._tick += k
         self._state_stale = True
