@@ -70,6 +70,18 @@ typedef struct swarmstep_quad_params {
     float _pad[2];
 } swarmstep_quad_params;
 
+/* Physical constants and controller gains in float64, for hosts that do not
+ * pack swarmstep_quad_params themselves: QuadParams (quad.py:39-69),
+ * PidGains (control.py:40-53) and OuterGains (control.py:56-68). */
+typedef struct swarmstep_quad_physics {
+    double m, ixx, iyy, izz, g, k_t, k_q, arm_length, arm_angle, omega_max;
+} swarmstep_quad_physics;
+typedef struct swarmstep_quad_gains {
+    double kp[3], ki[3], kd[3], i_limit[3];
+    double kp_pos[3], kv[3], k_att[3];
+    double omega_sp_max, a_cmd_min;
+} swarmstep_quad_gains;
+
 /* Column offsets inside a tile (each block is k consecutive columns).  The
  * order puts everything the step kernel reads first (cols [0, 29)) and keeps
  * the columns it writes in two runs ([0, 22) and [29, 33)). */
@@ -108,6 +120,15 @@ const char *swarmstep_last_error(void);
  * call before capturing launches into a CUDA graph. */
 int swarmstep_preload(void);
 
+/* Packs the kernel's float32 per-type constants: G and its exact inverse
+ * (G^-1 = G^T diag(1/|row|^2), the rows of the X-geometry G being orthogonal;
+ * quad.py:106-122), f_max = k_t omega_max^2, fc_max = 4 f_max (control.py:253),
+ * 1/m, 1/I and the gains.  Host-only (no device needed).  Errors as
+ * QuadParams: non-positive / non-finite constants or a singular geometry ->
+ * SWARMSTEP_EINVAL (quad.py:56-60). */
+int swarmstep_quad_params_init(swarmstep_quad_params *p, const swarmstep_quad_physics *phys,
+                               const swarmstep_quad_gains *gains);
+
 /* Host-side plumbing for thin bindings: an async copy of `bytes` on `stream`
  * (cudaMemcpyDefault: any direction, pinned host or device pointers), and a
  * stream synchronisation that also reports any error the stream's work
@@ -125,8 +146,8 @@ int swarmstep_device_info(int *sm_count, int *cc_major, int *cc_minor);
  * column block is added to v_sp on substep 0 only with SWARMSTEP_STEP_OVERLAY
  * (core.py:172-175, 199-201); the caller clears it afterwards.  Without
  * SWARMSTEP_STEP_MOTOR no row may be at MOTOR level (the stale-setpoint
- * columns are then not read).  Few-tick launches run the TMA-staged kernel
- * (HBM-bound regime), many-tick launches the direct kernel.
+ * columns are then not read).  K = 1 launches run the direct kernel (HBM-bound
+ * regime), K >= 2 the paired FFMA2 kernel (FP32-bound); FORCE_* select one.
  * Faulted rows are appended to fault_log as ((tick_base + substep) mod 2^24)
  * << 40 | row and counted in counters[0], which only ever grows: a row can
  * fault at most once (dead rows never revive), so fault_cap >= n never

@@ -34,7 +34,7 @@ STEP_OVERLAY, STEP_MOTOR, STEP_FORCE_DIRECT, STEP_FORCE_TMA, STEP_FORCE_PAIR = 0
 # every symbol include/swarmstep_b200.h declares
 EXPORTS = (
     "swarmstep_abi_version", "swarmstep_last_error", "swarmstep_device_info", "swarmstep_preload",
-    "swarmstep_memcpy_async", "swarmstep_stream_sync",
+    "swarmstep_memcpy_async", "swarmstep_stream_sync", "swarmstep_quad_params_init",
     "swarmstep_quad_step", "swarmstep_quad_step_lag", "swarmstep_quad_step_circle", "swarmstep_quad_apply_commands", "swarmstep_quad_set_setpoints",
     "swarmstep_quad_mark_dead", "swarmstep_quad_retarget_waypoint",
     "swarmstep_quad_pack_f64", "swarmstep_quad_unpack_f64",
@@ -78,6 +78,8 @@ def _declare(lib) -> None:
     lib.swarmstep_last_error.argtypes = []
     lib.swarmstep_preload.restype = i32
     lib.swarmstep_preload.argtypes = []
+    lib.swarmstep_quad_params_init.restype = i32
+    lib.swarmstep_quad_params_init.argtypes = [vp, vp, vp]
     lib.swarmstep_memcpy_async.restype = i32
     lib.swarmstep_memcpy_async.argtypes = [vp, vp, ctypes.c_uint64, vp]
     lib.swarmstep_stream_sync.restype = i32

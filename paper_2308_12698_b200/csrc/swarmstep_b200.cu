@@ -882,6 +882,48 @@ int swarmstep_device_info(int *sm_count, int *cc_major, int *cc_minor)
     return SWARMSTEP_OK;
 }
 
+int swarmstep_quad_params_init(swarmstep_quad_params *p, const swarmstep_quad_physics *phys,
+                               const swarmstep_quad_gains *gains)
+{
+    if (!p || !phys || !gains) return set_err(SWARMSTEP_EINVAL, "null argument");
+    const double vals[] = {phys->m, phys->ixx, phys->iyy, phys->izz, phys->g, phys->k_t, phys->k_q,
+                           phys->arm_length, phys->arm_angle, phys->omega_max};
+    for (double v : vals)
+        if (!(v > 0.0) || !isfinite(v))     // quad.py:56-60
+            return set_err(SWARMSTEP_EINVAL, "all quadrotor parameters must be strictly positive and finite");
+    // G (quad.py:106-122): rows mutually orthogonal, so G^-1 = G^T diag(1 / |row|^2)
+    const double ls = phys->arm_length * sin(phys->arm_angle), lc = phys->arm_length * cos(phys->arm_angle);
+    const double kr = phys->k_q / phys->k_t;
+    const double G[16] = {1, 1, 1, 1, ls, -ls, -ls, ls, -lc, -lc, lc, lc, kr, -kr, kr, -kr};
+    const double det = 256.0 * ls * ls * lc * lc * kr * kr;     // |det G| = prod |row| (orthogonal rows)
+    if (!(fabs(det) > 1e-12)) return set_err(SWARMSTEP_EINVAL, "allocation matrix is singular (degenerate arm angle)");
+    memset(p, 0, sizeof(*p));
+    p->m = (float)phys->m;
+    p->inv_m = (float)(1.0 / phys->m);
+    p->g = (float)phys->g;
+    p->ixx = (float)phys->ixx; p->iyy = (float)phys->iyy; p->izz = (float)phys->izz;
+    p->inv_ixx = (float)(1.0 / phys->ixx); p->inv_iyy = (float)(1.0 / phys->iyy); p->inv_izz = (float)(1.0 / phys->izz);
+    p->k_t = (float)phys->k_t;
+    p->omega_max = (float)phys->omega_max;
+    const double f_max = phys->k_t * phys->omega_max * phys->omega_max;
+    p->f_max = (float)f_max;
+    p->fc_max = (float)(4.0 * f_max);
+    const double rsq[4] = {4.0, 4.0 * ls * ls, 4.0 * lc * lc, 4.0 * kr * kr};
+    for (int i = 0; i < 4; i++)
+        for (int j = 0; j < 4; j++) {
+            p->G[i * 4 + j] = (float)G[i * 4 + j];
+            p->G_inv[i * 4 + j] = (float)(G[j * 4 + i] / rsq[j]);
+        }
+    for (int i = 0; i < 3; i++) {
+        p->kp[i] = (float)gains->kp[i]; p->ki[i] = (float)gains->ki[i]; p->kd[i] = (float)gains->kd[i];
+        p->i_limit[i] = (float)gains->i_limit[i];
+        p->kp_pos[i] = (float)gains->kp_pos[i]; p->kv[i] = (float)gains->kv[i]; p->k_att[i] = (float)gains->k_att[i];
+    }
+    p->omega_sp_max = (float)gains->omega_sp_max;
+    p->a_cmd_min = (float)gains->a_cmd_min;
+    return SWARMSTEP_OK;
+}
+
 int swarmstep_memcpy_async(void *dst, const void *src, uint64_t bytes, void *stream)
 {
     if (bytes == 0) return SWARMSTEP_OK;

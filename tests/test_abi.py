@@ -103,3 +103,38 @@ def test_functional_api_fails_loudly_without_gpu():
     from paper_2308_12698_b200 import NativeLibraryError, default_quad_params, functional
     with pytest.raises(NativeLibraryError):
         functional.mix_to_motors(np.array([9.81]), np.zeros((1, 3)), default_quad_params())
+
+
+def test_c_params_packer_matches_python(lib):
+    """swarmstep_quad_params_init (for non-Python hosts) packs the same float32
+    constants as params.pack_device_params -- host-only, no GPU needed."""
+    import ctypes
+
+    from paper_2308_12698_b200 import QuadParams, default_outer_gains, default_rate_gains
+    from paper_2308_12698_b200.params import DeviceParams, pack_device_params
+
+    class Phys(ctypes.Structure):
+        _fields_ = [(k, ctypes.c_double) for k in ("m", "ixx", "iyy", "izz", "g", "k_t", "k_q", "arm_length",
+                                                   "arm_angle", "omega_max")]
+
+    class Gains(ctypes.Structure):
+        _fields_ = [(k, ctypes.c_double * 3) for k in ("kp", "ki", "kd", "i_limit", "kp_pos", "kv", "k_att")] + \
+                   [("omega_sp_max", ctypes.c_double), ("a_cmd_min", ctypes.c_double)]
+
+    for qp in (QuadParams(), QuadParams(m=1.7, i_diag=(0.02, 0.03, 0.05), arm_length=0.31, arm_angle=0.6, k_q=3e-10)):
+        rg, og = default_rate_gains(), default_outer_gains()
+        want = pack_device_params(qp, rg, og)
+        ph = Phys(qp.m, *qp.i_diag, qp.g, qp.k_t, qp.k_q, qp.arm_length, qp.arm_angle, qp.omega_max)
+        gn = Gains()
+        for k in ("kp", "ki", "kd", "i_limit"):
+            getattr(gn, k)[:] = [float(v) for v in np.broadcast_to(getattr(rg, k), 3)]
+        for k in ("kp_pos", "kv", "k_att"):
+            getattr(gn, k)[:] = [float(v) for v in np.broadcast_to(getattr(og, k), 3)]
+        gn.omega_sp_max, gn.a_cmd_min = og.omega_sp_max, og.a_cmd_min
+        got = DeviceParams()
+        assert lib.swarmstep_quad_params_init(ctypes.byref(got), ctypes.byref(ph), ctypes.byref(gn)) == 0
+        a = np.frombuffer(bytes(got), dtype=np.float32)
+        b = np.frombuffer(bytes(want), dtype=np.float32)
+        np.testing.assert_allclose(a, b, rtol=2e-7, atol=0)
+    bad = Phys(0.0, 0.01, 0.01, 0.02, 9.81, 1e-8, 1e-10, 0.2, 0.78, 4e4)
+    assert lib.swarmstep_quad_params_init(ctypes.byref(DeviceParams()), ctypes.byref(bad), ctypes.byref(Gains())) != 0
