@@ -331,30 +331,32 @@ __device__ __forceinline__ void motor_wrench(const float rpm[4], const swarmstep
 // tau_m -> 0 recovers the reference's instantaneous mixer.
 
 // clamped mixer motor thrusts m = clip(G^-1 [f_c, tau], 0, f_max) (quad.py:153-160)
-__device__ __forceinline__ void mix_motors(float f_c, const float tau[3], const swarmstep_quad_params &P, float m[4])
+template <class T>
+__device__ __forceinline__ void mix_motors(T f_c, const T tau[3], const swarmstep_quad_params &P, T m[4])
 {
-    const float A = mul(P.G_inv[1], tau[0]), C = mul(P.G_inv[3], tau[2]);
-    const float c0 = P.G_inv[0], c2 = fabsf(P.G_inv[2]);
-    const float FpA = fma(c0, f_c, A), FmA = fma(c0, f_c, -A), BmC = fma(c2, tau[1], -C), BpC = fma(c2, tau[1], C);
+    const T A = mul(bc<T>(P.G_inv[1]), tau[0]), C = mul(bc<T>(P.G_inv[3]), tau[2]);
+    const T c0 = bc<T>(P.G_inv[0]), c2 = bc<T>(fabsf(P.G_inv[2]));
+    const T FpA = fma(c0, f_c, A), FmA = fma(c0, f_c, neg(A)), BmC = fma(c2, tau[1], neg(C)), BpC = fma(c2, tau[1], C);
     m[0] = sub(FpA, BmC); m[1] = sub(FmA, BpC); m[2] = add(FmA, BpC); m[3] = add(FpA, BmC);
 #pragma unroll
-    for (int i = 0; i < 4; i++) m[i] = clip(m[i], 0.0f, P.f_max);
+    for (int i = 0; i < 4; i++) m[i] = clip(m[i], bc<T>(0.0f), bc<T>(P.f_max));
 }
 
 // wrench of four rotor thrusts: (f_c, tau) = G f (quad.py:138-140)
-__device__ __forceinline__ void thrust_wrench(const float f[4], const swarmstep_quad_params &P, float &f_c,
-                                              float tau[3])
+template <class T>
+__device__ __forceinline__ void thrust_wrench(const T f[4], const swarmstep_quad_params &P, T &f_c, T tau[3])
 {
     f_c = add(add(f[0], f[1]), add(f[2], f[3]));
 #pragma unroll
     for (int i = 0; i < 3; i++)
-        tau[i] = fma(P.G[(i + 1) * 4 + 0], f[0], fma(P.G[(i + 1) * 4 + 1], f[1],
-                 fma(P.G[(i + 1) * 4 + 2], f[2], mul(P.G[(i + 1) * 4 + 3], f[3]))));
+        tau[i] = fma(bc<T>(P.G[(i + 1) * 4 + 0]), f[0], fma(bc<T>(P.G[(i + 1) * 4 + 1]), f[1],
+                 fma(bc<T>(P.G[(i + 1) * 4 + 2]), f[2], mul(bc<T>(P.G[(i + 1) * 4 + 3]), f[3]))));
 }
 
 // rotor thrusts lagging towards u: u + (f - u) e (e = e^(-dt/tau_m) for the
 // end of the tick, e = phi for the tick mean)
-__device__ __forceinline__ void lag_thrust(const float f[4], const float u[4], float e, float out[4])
+template <class T>
+__device__ __forceinline__ void lag_thrust(const T f[4], const T u[4], T e, T out[4])
 {
 #pragma unroll
     for (int i = 0; i < 4; i++) out[i] = fma(sub(f[i], u[i]), e, u[i]);

@@ -140,6 +140,29 @@ struct MotorLag {
     }
 };
 
+// Two rows' rotor thrusts as one f2 lane pair (the paired kernel).
+struct MotorLagPair {
+    static constexpr bool lag_on = true, feed_on = false;
+    template <class T> __device__ __forceinline__ void feed(int, RowT<T> &) const {}
+    template <class A> __device__ __forceinline__ void store_cmd(const A &, int) const {}
+    float *p0, *p1;          // rows t and t + 64 of one tile (column i at + 128 i)
+    float phi, e_full;
+    ssb::f2 f[4];
+    __device__ __forceinline__ void load()
+    {
+#pragma unroll
+        for (int i = 0; i < 4; i++) f[i] = ssb::f2{make_float2(p0[i * SWARMSTEP_TILE], p1[i * SWARMSTEP_TILE])};
+    }
+    __device__ __forceinline__ void store() const
+    {
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            p0[i * SWARMSTEP_TILE] = f[i].v.x;
+            p1[i * SWARMSTEP_TILE] = f[i].v.y;
+        }
+    }
+};
+
 // In-kernel circle feed (the circle strategy of feed.cu evaluated per tick
 // inside the step, so K ticks of a time-varying reference fuse into one
 // launch).  Tick k of the launch uses circle_reference at t = (tick0 + k) dt
@@ -336,18 +359,18 @@ __device__ __forceinline__ int run_ticks(const swarmstep_quad_params &P, const s
         if constexpr (L::lag_on) {
             // commanded rotor thrusts u; the body integrates the wrench of the
             // tick-mean lagged thrust, the rotors end the tick lagged by e_full
-            float u[4], fbar[4];
+            T u[4], fbar[4];
             if (LEVEL == SWARMSTEP_LEVEL_MOTOR) {
 #pragma unroll
                 for (int i = 0; i < 4; i++) u[i] = R.u[i];
             } else {
                 ssb::mix_motors(f_c, tau, P, u);
             }
-            ssb::lag_thrust(lag.f, u, lag.phi, fbar);
+            ssb::lag_thrust(lag.f, u, ssb::bc<T>(lag.phi), fbar);
             ssb::thrust_wrench(fbar, P, f_c, tau);
-            const bool ok = ssb::rk4_inplace<float, COMP>(R.p_hi, R.p_lo, R.v, R.q, R.w, f_c, tau, P, D, dt);
-            if (CHECK && !ok) return k;
-            ssb::lag_thrust(lag.f, u, lag.e_full, lag.f);
+            const auto ok = ssb::rk4_inplace<T, COMP>(R.p_hi, R.p_lo, R.v, R.q, R.w, f_c, tau, P, D, dt);
+            if (CHECK && ssb::any(ssb::mnot(ok))) return k;
+            ssb::lag_thrust(lag.f, u, ssb::bc<T>(lag.e_full), lag.f);
         } else {
             if (LEVEL == SWARMSTEP_LEVEL_MOTOR) {
                 f_c = R.u[0]; tau[0] = R.u[1]; tau[1] = R.u[2]; tau[2] = R.u[3];
@@ -402,10 +425,8 @@ __device__ __forceinline__ uint8_t step_row(const A &C, uint8_t fl, int64_t r, i
                                             uint32_t *counters, uint64_t *fault_log, int64_t fault_cap,
                                             Row &R, bool preloaded = false, L lag = L())
 {
-    if (!preloaded) {
-        load_state<COMP>(C, R);
-        lag.load();
-    }
+    if (!preloaded) load_state<COMP>(C, R);
+    lag.load();
     // the circle feed puts every alive row at POS level (feed.cu)
     const int level = L::feed_on ? SWARMSTEP_LEVEL_POS : (fl & SWARMSTEP_LEVEL_MASK) >> SWARMSTEP_LEVEL_SHIFT;
     const bool has_prev = (fl & SWARMSTEP_FLAG_HAS_PREV) != 0;
@@ -544,6 +565,7 @@ __device__ __forceinline__ void pair_body(float *__restrict__ cols, uint8_t *__r
     load_state<COMP>(C, R);
     __threadfence_block();
     const bool paired = a0 && a1 && l0 == l1 && l0 != SWARMSTEP_LEVEL_MOTOR;
+    if (paired) pf.load();
     bool reload = false;
     if (paired) {
         const ssb::m2 hp{(f0 & SWARMSTEP_FLAG_HAS_PREV) != 0, (f1 & SWARMSTEP_FLAG_HAS_PREV) != 0};
@@ -554,6 +576,7 @@ __device__ __forceinline__ void pair_body(float *__restrict__ cols, uint8_t *__r
             reload = true;
         } else {
             store_state<COMP>(C, l0, R);
+            pf.store();
             pf.store_cmd(C, K - 1);
             const uint8_t hpf = SWARMSTEP_FLAG_HAS_PREV;
             const uint8_t n0 = PF::feed_on ? (uint8_t)((f0 & ~SWARMSTEP_LEVEL_MASK) | hpf) : (uint8_t)(f0 | hpf);
@@ -590,6 +613,23 @@ quad_step_pair_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int
     if (r0 >= n) return;
     pair_body<COMP>(cols, flags, n, counters, fault_log, fault_cap, overlay_active, tick_base, tick_dev, P, D, dt, K,
                     r0, NoLag(), NoLag(), NoLag());
+}
+
+// the paired kernel with the opt-in rotor lag
+template <bool COMP>
+__global__ void __launch_bounds__(64, SSB_PAIR_MINB)
+quad_step_pair_lag_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, float *__restrict__ motor, int64_t n,
+                          uint32_t *__restrict__ counters, uint64_t *__restrict__ fault_log, int64_t fault_cap,
+                          int overlay_active, uint32_t tick_base, const int64_t *tick_dev,
+                          const swarmstep_quad_params P, const ssb::Derived D, float phi, float e_full, float dt,
+                          int K)
+{
+    const int64_t r0 = (int64_t)blockIdx.x * SWARMSTEP_TILE + threadIdx.x;
+    if (r0 >= n) return;
+    float *m0 = motor + (r0 >> 7) * (4 * SWARMSTEP_TILE) + (r0 & (SWARMSTEP_TILE - 1)), *m1 = m0 + 64;
+    pair_body<COMP>(cols, flags, n, counters, fault_log, fault_cap, overlay_active, tick_base, tick_dev, P, D, dt, K,
+                    r0, MotorLagPair{m0, m1, phi, e_full, {}}, MotorLag{m0, phi, e_full, {}},
+                    MotorLag{m1, phi, e_full, {}});
 }
 
 // the paired kernel with the in-kernel circle feed (every alive row at POS)
@@ -950,6 +990,7 @@ int swarmstep_preload(void)
                          (const void *)quad_step_lag_kernel<true>, (const void *)quad_step_lag_kernel<false>,
                          (const void *)quad_step_circle_kernel<true>, (const void *)quad_step_circle_kernel<false>,
                          (const void *)quad_step_pair_circle_kernel<true>,
+                         (const void *)quad_step_pair_lag_kernel<true>, (const void *)quad_step_pair_lag_kernel<false>,
                          (const void *)quad_step_pair_circle_kernel<false>,
                          (const void *)apply_commands_kernel, (const void *)set_setpoints_kernel,
                          (const void *)mark_dead_kernel, (const void *)retarget_kernel,
@@ -1033,6 +1074,14 @@ int swarmstep_quad_step_lag(const swarmstep_group_view *g, const swarmstep_quad_
     const float e_full = (float)exp(-(double)dt / (double)tau_m);
     const int overlay = launch_flags & SWARMSTEP_STEP_OVERLAY;
     const int64_t fcap = g->fault_log ? g->fault_cap : 0;
+    if (!(launch_flags & SWARMSTEP_STEP_FORCE_DIRECT) &&
+        ((launch_flags & SWARMSTEP_STEP_FORCE_PAIR) || k_substeps >= SSB_PAIR_MIN_K)) {
+        auto kern = g->compensated ? quad_step_pair_lag_kernel<true> : quad_step_pair_lag_kernel<false>;
+        kern<<<(unsigned)((g->n + SWARMSTEP_TILE - 1) / SWARMSTEP_TILE), 64, 0, (cudaStream_t)stream>>>(
+            g->cols, g->flags, motor, g->n, g->counters, g->fault_log, fcap, overlay, tick_base, tick_dev, *p, D,
+            phi, e_full, dt, k_substeps);
+        return cuda_status("quad_step_pair_lag_kernel");
+    }
     auto kern = g->compensated ? quad_step_lag_kernel<true> : quad_step_lag_kernel<false>;
     kern<<<grid_for(g->n, kBlock), kBlock, 0, (cudaStream_t)stream>>>(
         g->cols, g->flags, motor, g->n, g->counters, g->fault_log, fcap, overlay, tick_base, tick_dev, *p, D,

@@ -102,3 +102,22 @@ def test_tau_zero_is_the_reference_path():
         b.motor_thrusts()
     with pytest.raises(ValidationError):
         make_group(sc, motor_tau=-1.0)
+
+
+@pytest.mark.parametrize("k", [1, 7])
+def test_lag_kernel_variants_bit_identical(k):
+    """The paired (FFMA2) rotor-lag kernel == the direct one, bit for bit,
+    state and rotor thrusts, all levels and faults included."""
+    outs = []
+    for kern in ("direct", "pair"):
+        sc = ALL["fault_nan"](n=256, ticks=12)
+        g = make_group(sc, motor_tau=TAU)
+        g.kernel = kern
+        run_script(g, Scenario(**{**sc.__dict__, "ticks": 8, "record": []}))
+        for _ in range(3):
+            g.step_k(sc.dt, k)
+        st = gpu_state(g)
+        outs.append({**{q: st[q].copy() for q in ("pos", "vel", "quat", "omega", "integral", "alive")},
+                     "motor": g.motor_thrusts()})
+    for q in outs[0]:
+        np.testing.assert_array_equal(outs[0][q], outs[1][q], err_msg=q)
