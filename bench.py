@@ -42,6 +42,8 @@ UNIT = "agent-steps/s"
 ALG_BYTES_PER_AGENT_LAUNCH = 221
 # algorithmic flops per agent-tick at position level (FMA = 2)
 ALG_FLOPS_PER_AGENT_TICK = 705
+PORT_NOTE = ("the port runs ~5x faster than the reference's own numpy QuadGroup.step on one core "
+             "(4.7-5.5x, same results to 2e-15 m; profiles/cpu_ref_vs_port_r01.json): a conservative baseline")
 
 
 def parse():
@@ -169,7 +171,8 @@ def run_reference(args, rank: int) -> None:
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"cfg3/cfg4 recipe, sampled: {sample}", "agents_sampled": n_sample,
                    "substeps": args.substeps, "dt": args.dt, "level": "pos"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
+                         "note": PORT_NOTE},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -307,7 +310,7 @@ def run_b200(args, rank: int, world: int) -> None:
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         n_s = 262_144
         v, threads, reps, el = cpu_leg(n_s, k, dt, args.cpu_seconds, motor_tau=args.motor_tau)
-        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "note": PORT_NOTE,
                "sample": f"{n_s} agents x {k} ticks x {reps} reps ({el:.1f} s), same recipe, float64 C oracle "
                          f"(restatement of the reference QuadGroup.step), {threads} threads"}
 
