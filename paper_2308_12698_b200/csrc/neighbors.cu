@@ -248,7 +248,8 @@ int swarmstep_pack_positions(const swarmstep_group_view *g, float *out_xyzw, int
 
 int swarmstep_neighbor_workspace_bytes(int64_t n_all, uint64_t *bytes)
 {
-    if (n_all < 0 || n_all > 0x7fffffffLL || !bytes) return nb_err(SWARMSTEP_EINVAL, "bad n_all");
+    // m = next_pow2(2 n_all) + 1 bucket counts are scanned with an int count
+    if (n_all < 0 || n_all > (1LL << 29) || !bytes) return nb_err(SWARMSTEP_EINVAL, "bad n_all (0 .. 2^29)");
     *bytes = (uint64_t)layout(n_all, nullptr, nullptr);
     return SWARMSTEP_OK;
 }
@@ -260,6 +261,7 @@ int swarmstep_neighbor_overlay(const swarmstep_group_view *g, const float *all_x
     if (!g || !g->cols || !g->flags || !all_xyzw || !workspace) return nb_err(SWARMSTEP_EINVAL, "null argument");
     if (!(r_sense > 0.0f) || !(cell >= r_sense)) return nb_err(SWARMSTEP_EINVAL, "need r_sense > 0 and cell >= r_sense");
     if (self_offset < 0 || self_offset + g->n > n_all) return nb_err(SWARMSTEP_EINVAL, "local shard outside n_all");
+    if (n_all > (1LL << 29)) return nb_err(SWARMSTEP_EINVAL, "n_all above 2^29");
     if (ws_bytes < (uint64_t)layout(n_all, nullptr, nullptr)) return nb_err(SWARMSTEP_EINVAL, "workspace too small");
     if (n_all == 0 || g->n == 0) return SWARMSTEP_OK;
     cudaStream_t s = (cudaStream_t)stream;
