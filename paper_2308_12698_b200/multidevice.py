@@ -1,0 +1,184 @@
+"""One homogeneous group spread over several GPUs of ONE process.
+
+The reference's ``World`` is single-process (core.py:308-505) and keys its
+bookkeeping by ``type_id`` (alive counts core.py:370, the id map core.py:314-
+318), so one agent type cannot simply become eight groups.  ``MultiDeviceQuadGroup``
+is one protocol-level group whose rows are sharded by contiguous index over
+``devices`` ("contiguous agent-index ranges across 2/4/8
+devices, one stream per device, from a single host thread"): ``step`` launches
+every shard's fused kernel before waiting on any, so the devices run
+concurrently; agents are independent (quad.py:6-7), so there is no exchange.
+
+(``bench.py`` and ``parallel.ShardedSwarm`` cover the one-process-per-GPU
+layout; this class is the drop-in for an unchanged single-process World.)
+"""
+
+from __future__ import annotations
+
+from collections.abc import Iterable
+
+import numpy as np
+
+from .errors import ValidationError
+from .group import B200QuadGroup
+from .parallel import shard_range
+from .state import AgentBatch, batch_snapshot
+
+
+class _ShardBatchView:
+    """``group.batch`` over the shards: ids / alive / n without a device read,
+    state columns concatenated from the shards' float64 mirrors."""
+
+    def __init__(self, mg):
+        self._mg = mg
+
+    @property
+    def type_id(self) -> int:
+        return self._mg.type_id
+
+    @property
+    def n(self) -> int:
+        return self._mg.n
+
+    @property
+    def agent_ids(self) -> np.ndarray:
+        return self._mg._ids
+
+    def _cat(self, name):
+        return np.concatenate([getattr(s.batch, name) for s in self._mg.shards])
+
+    @property
+    def alive(self) -> np.ndarray:
+        return self._cat("alive")
+
+    @property
+    def pos(self) -> np.ndarray:
+        return self._cat("pos")
+
+    @property
+    def vel(self) -> np.ndarray:
+        return self._cat("vel")
+
+    @property
+    def quat(self) -> np.ndarray:
+        return self._cat("quat")
+
+    @property
+    def omega(self) -> np.ndarray:
+        return self._cat("omega")
+
+    def index_of(self, agent_id: int):
+        return self._mg.rows_for(agent_id)
+
+
+class MultiDeviceQuadGroup:
+    """A quadrotor group sharded over ``devices`` (same process, one stream each)."""
+
+    kind = "quadrotor"
+
+    def __init__(self, type_id: int, batch, params=None, rate_gains=None, outer_gains=None, *, devices,
+                 **group_kw):
+        devices = list(devices)
+        if not devices:
+            raise ValidationError("need at least one device")
+        n = int(np.asarray(batch.agent_ids).shape[0])
+        if n < len(devices):
+            raise ValidationError("fewer agents than devices")
+        self.type_id = int(type_id)
+        self.n = n
+        self._ids = np.array(batch.agent_ids, dtype=np.uint64)
+        self.shards: list[B200QuadGroup] = []
+        self._lo: list[int] = []
+        for i, dev in enumerate(devices):
+            lo, hi = shard_range(n, i, len(devices))
+            sub = AgentBatch(type_id=int(getattr(batch, "type_id", type_id)), agent_ids=self._ids[lo:hi],
+                             pos=np.asarray(batch.pos, float)[lo:hi], vel=np.asarray(batch.vel, float)[lo:hi],
+                             quat=np.asarray(batch.quat, float)[lo:hi], omega=np.asarray(batch.omega, float)[lo:hi],
+                             alive=np.asarray(batch.alive, bool)[lo:hi])
+            self.shards.append(B200QuadGroup(type_id, sub, params, rate_gains, outer_gains, device=dev, **group_kw))
+            self._lo.append(lo)
+        self._lo_arr = np.array(self._lo + [n])
+        self.params = self.shards[0].params
+        self._owner = {int(a): i for i, s in enumerate(self.shards) for a in s.agent_ids}
+        self._view = _ShardBatchView(self)
+
+    # ------------------------------------------------------------ protocol
+    @property
+    def batch(self) -> _ShardBatchView:
+        return self._view
+
+    def _shard_of(self, agent_id):
+        i = self._owner.get(int(agent_id))
+        return None if i is None else self.shards[i]
+
+    def rows_for(self, agent_id: int):
+        i = self._owner.get(int(agent_id))
+        if i is None:
+            return None
+        return self._lo[i] + self.shards[i].rows_for(agent_id)
+
+    @property
+    def cmd_values(self) -> np.ndarray:
+        return np.concatenate([s.cmd_values for s in self.shards])
+
+    @property
+    def cmd_level(self) -> np.ndarray:
+        return np.concatenate([s.cmd_level for s in self.shards])
+
+    def apply_command(self, cmd) -> bool:
+        s = self._shard_of(cmd.agent_id)
+        return False if s is None else s.apply_command(cmd)
+
+    def mark_dead(self, agent_ids: Iterable[int]) -> list[int]:
+        per = [[] for _ in self.shards]
+        for a in agent_ids:
+            i = self._owner.get(int(a))
+            if i is not None:
+                per[i].append(a)
+        killed = []
+        for s, ids in zip(self.shards, per):
+            if ids:
+                killed += s.mark_dead(ids)
+        return killed
+
+    def _split(self, rows_array):
+        return [rows_array[lo:hi] for lo, hi in zip(self._lo_arr[:-1], self._lo_arr[1:])]
+
+    def add_velocity_overlay(self, offsets) -> None:
+        for s, part in zip(self.shards, self._split(np.asarray(offsets, dtype=float).reshape(self.n, 3))):
+            s.add_velocity_overlay(part)
+
+    def retarget_waypoint(self, point, radius: float) -> None:
+        for s in self.shards:
+            s.retarget_waypoint(point, radius)
+
+    def set_setpoints(self, values, level=0, columns: bool = False) -> None:
+        v = np.asarray(values)
+        if columns:
+            v = v.T
+        for s, part in zip(self.shards, self._split(v)):
+            s.set_setpoints(np.ascontiguousarray(part), level=level)
+
+    def step_async(self, dt: float, k: int = 1) -> None:
+        """Queue k fused ticks on every shard's device (no waiting)."""
+        for s in self.shards:
+            s.step_async(dt, k)
+
+    def collect_faults(self) -> list[np.ndarray]:
+        per = [s.collect_faults() for s in self.shards]
+        return [np.sort(np.concatenate([p[t] for p in per])) for t in range(len(per[0]))]
+
+    def step_k(self, dt: float, k: int = 1) -> np.ndarray:
+        self.step_async(dt, k)
+        ticks = self.collect_faults()
+        return np.concatenate(ticks) if len(ticks) > 1 else ticks[0]
+
+    def step(self, dt: float) -> np.ndarray:
+        """One tick on every device concurrently; the fault ids of all shards."""
+        return self.step_k(dt, 1)
+
+    def snapshot(self, tick: int):
+        return batch_snapshot(self.batch, tick)
+
+    def alive_count(self) -> int:
+        return sum(s.alive_count() for s in self.shards)

@@ -158,3 +158,42 @@ def test_batch_view_alive_counts_without_state_pull():
     g.step_async(1e-3, 3)                       # uncollected launches: alive comes from the device
     assert int(g.batch.alive.sum()) == 997
     g.collect_faults()
+
+
+def test_multi_device_group_equals_single_group():
+    """MultiDeviceQuadGroup (one logical group, rows sharded over devices of one
+    process, launched concurrently) gives the same bits, faults, commands and
+    snapshots as one B200QuadGroup.  Run here with two shards on this GPU."""
+    import torch
+
+    from paper_2308_12698_b200 import AgentCommand, B200QuadGroup, CommandLevel, batch_create
+    from paper_2308_12698_b200.multidevice import MultiDeviceQuadGroup
+    rng = np.random.default_rng(8)
+    n = 1001
+    pos = rng.uniform(-30, 30, (n, 3))
+
+    def drive(g):
+        sp = np.hstack([pos + rng_sp.uniform(-2, 2, (n, 3)), np.zeros((n, 3)), rng_sp.uniform(-3, 3, (n, 1))])
+        g.set_setpoints(sp)
+        g.apply_command(AgentCommand(10, CommandLevel.RATE, (0.1, 0.0, 0.0, 9.0)))
+        g.apply_command(AgentCommand(700, CommandLevel.MOTOR, (1e4, 1.1e4, 1e4, 1.1e4)))
+        g.mark_dead([3, 600])
+        g.add_velocity_overlay(np.full((n, 3), 0.1))
+        faults = [g.step(1e-3).tolist()]
+        g.retarget_waypoint(pos[900], 0.5)
+        faults.append(g.step_k(1e-3, 5).tolist())
+        return faults
+
+    rng_sp = np.random.default_rng(1)
+    single = B200QuadGroup(0, batch_create(0, n, pos))
+    fa = drive(single)
+    rng_sp = np.random.default_rng(1)
+    multi = MultiDeviceQuadGroup(0, batch_create(0, n, pos), devices=[torch.device("cuda", 0)] * 2)
+    fb = drive(multi)
+    assert fa == fb
+    for q in ("pos", "vel", "quat", "omega", "alive"):
+        np.testing.assert_array_equal(getattr(single.batch, q), getattr(multi.batch, q), err_msg=q)
+    np.testing.assert_array_equal(single.cmd_values, multi.cmd_values)
+    np.testing.assert_array_equal(single.cmd_level, multi.cmd_level)
+    assert multi.rows_for(700) == 700 and multi.alive_count() == n - 2
+    assert multi.snapshot(5).pos.tobytes() == single.snapshot(5).pos.tobytes()
