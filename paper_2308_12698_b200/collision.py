@@ -61,14 +61,15 @@ class NeighborSets(Mapping):
     never pays for the per-agent Python dict.  Compares equal to the plain
     dict the reference returns."""
 
-    def __init__(self, ids_alive: np.ndarray, ids_all: np.ndarray, near):
+    def __init__(self, alive_all: np.ndarray, ids_all: np.ndarray, near, n_alive: int | None = None):
         # near: (k, 2) row pairs, numpy or a device tensor (copied on first use)
-        self._ids_alive, self._ids_all, self._near = ids_alive, ids_all, near
+        self._alive_all, self._ids_all, self._near = alive_all, ids_all, near
+        self._n = int(alive_all.sum()) if n_alive is None else int(n_alive)
         self._d = None
 
     def _dict(self) -> dict:
         if self._d is None:
-            d = {int(i): () for i in self._ids_alive}
+            d = {int(i): () for i in self._ids_all[self._alive_all]}
             near, ids_all = self._near, self._ids_all
             if isinstance(near, torch.Tensor):
                 near = near.cpu().numpy().astype(np.int64).reshape(-1, 2)
@@ -90,7 +91,7 @@ class NeighborSets(Mapping):
         return iter(self._dict())
 
     def __len__(self) -> int:
-        return int(self._ids_alive.shape[0])
+        return self._n
 
     def __repr__(self) -> str:
         return repr(self._dict())
@@ -116,12 +117,13 @@ class GpuDetector:
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self._lib = _lib.load()
         self._counts = torch.zeros(4, dtype=torch.int64, device=self.device)
+        self._ids_key, self._ids_all, self._n_alive = None, None, 0
+        self._offs_key, self._offs, self._offs_d = None, None, None
 
     def detect(self, groups, tick: int, dropped: int = 0) -> CollisionReport:
         ids_all, alive_all, coll_h, near_h = self.pairs(groups)
-        ids_alive = ids_all[alive_all]
         if coll_h is None:
-            return CollisionReport(tick=tick, collisions=(), neighbor_sets={int(i): () for i in ids_alive},
+            return CollisionReport(tick=tick, collisions=(), neighbor_sets={int(i): () for i in ids_all[alive_all]},
                                    dropped=dropped)
         # host post-processing exactly as collision.py:160-175
         src, dst = coll_h[:, 0], coll_h[:, 1]
@@ -130,7 +132,7 @@ class GpuDetector:
         order = np.lexsort((ids_b, ids_a))
         collisions = tuple(zip(ids_a[order].tolist(), ids_b[order].tolist()))
         return CollisionReport(tick=tick, collisions=collisions,
-                               neighbor_sets=NeighborSets(ids_alive, ids_all, near_h), dropped=dropped)
+                               neighbor_sets=NeighborSets(alive_all, ids_all, near_h, self._n_alive), dropped=dropped)
 
     def pairs(self, groups):
         """Device broad + narrow phase: (ids_all, alive_all, colliding row
@@ -149,14 +151,27 @@ class GpuDetector:
         # device rows carry the same alive flags (dead rows are packed with
         # a NaN radius and never paired)
         alive = [g.alive_mask() for g in groups]
-        ids_all = np.concatenate([g.agent_ids.astype(np.int64) for g in groups]) if groups else np.empty(0, np.int64)
+        key = tuple(id(g) for g in groups)
+        if self._ids_key != key:                 # ids are static per group: concatenate once
+            self._ids_key = key
+            self._ids_all = (np.concatenate([g.agent_ids.astype(np.int64) for g in groups]) if groups
+                             else np.empty(0, np.int64))
+        ids_all = self._ids_all
         alive_all = np.concatenate(alive) if groups else np.empty(0, bool)
-        if int(alive_all.sum()) < 2:
+        counts_alive = [g.alive_count() for g in groups]
+        self._n_alive = sum(counts_alive)
+        if self._n_alive < 2:
             return ids_all, alive_all, None, None
-        rmax = max(cfg.r_collide[g.type_id] for g, a in zip(groups, alive) if a.any())
+        rmax = max(cfg.r_collide[g.type_id] for g, c in zip(groups, counts_alive) if c)
         reach = max(cfg.r_sense, 2.0 * float(rmax))
         d_max = int(math.ceil(reach / cfg.cell))
-        offs = half_space_offsets(d_max, reach, cfg.cell).astype(np.int32)
+        okey = (d_max, reach, cfg.cell)
+        if self._offs_key != okey:
+            self._offs_key = okey
+            self._offs = half_space_offsets(d_max, reach, cfg.cell).astype(np.int32)
+            self._offs_d = (torch.from_numpy(self._offs.reshape(-1)).to(self.device) if self._offs.size
+                            else torch.zeros(3, dtype=torch.int32, device=self.device))
+        offs, offs_d = self._offs, self._offs_d
         m = int(ids_all.shape[0])
         stream = torch.cuda.current_stream(self.device)
         with torch.cuda.device(self.device):
@@ -170,7 +185,6 @@ class GpuDetector:
             nbytes = ctypes.c_uint64()
             _lib.check(self._lib.swarmstep_collision_workspace_bytes(m, ctypes.byref(nbytes)))
             ws = torch.empty(int(nbytes.value), dtype=torch.uint8, device=self.device)
-            offs_d = torch.from_numpy(offs.reshape(-1)).to(self.device) if offs.size else torch.zeros(3, dtype=torch.int32, device=self.device)
 
             def run(coll, cc, near, nc, fill):
                 _lib.check(self._lib.swarmstep_collision_pairs(
