@@ -121,3 +121,28 @@ def test_lag_kernel_variants_bit_identical(k):
                      "motor": g.motor_thrusts()})
     for q in outs[0]:
         np.testing.assert_array_equal(outs[0][q], outs[1][q], err_msg=q)
+
+
+def test_lag_graph_replay_bit_identical():
+    """TickGraph (CUDA graph of circle feed + 1-tick steps) drives the rotor-lag
+    kernel like eager ticks, bit for bit, rotor thrusts included."""
+    from paper_2308_12698_b200 import B200QuadGroup, batch_create
+    from paper_2308_12698_b200.feed import CircleFeed, TickGraph
+    n, dt, T = 300, 2e-3, 20
+
+    def grp():
+        ph = 2 * np.pi * np.arange(n) / n
+        pos = np.stack([5 * np.cos(ph), 5 * np.sin(ph), np.full(n, 10.0)], axis=1)
+        return B200QuadGroup(0, batch_create(0, n, pos), motor_tau=TAU)
+
+    ga, gb = grp(), grp()
+    graph = TickGraph(ga, dt, T, feed=CircleFeed(ga, dt))
+    for _ in range(3):
+        graph.replay()
+    ga.collect_faults()
+    fb = CircleFeed(gb, dt)
+    for _ in range(3 * T):
+        fb.apply()
+        gb.step(dt)
+    assert ga.batch.pos.tobytes() == gb.batch.pos.tobytes()
+    np.testing.assert_array_equal(ga.motor_thrusts(), gb.motor_thrusts())
