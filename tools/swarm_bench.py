@@ -1,7 +1,7 @@
 """Config 5: neighbour-coupled swarm, per-tick cost on one B200 (and per rank
 under torchrun).  100k quadrotors per GPU in a box at ~1 agent / 8 m^3, r_sense
 2 m, POS level holding their start positions; every tick: pack positions ->
-NCCL all-gather (world > 1) -> spatial hash + radix sort + 27-cell scan ->
+all-gather (NCCL or the fused P2P exchange) -> spatial hash + counting sort + 27-cell scan ->
 separation overlay -> fused step (K = 1).  Prints one JSON line (rank 0).
 
   python tools/swarm_bench.py [agents_per_gpu] [ticks] [nccl|p2p]
