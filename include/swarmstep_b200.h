@@ -303,7 +303,9 @@ int swarmstep_neighbor_overlay(const swarmstep_group_view *g, const float *all_x
                                int64_t self_offset, float r_sense, float k_sep, float cell,
                                int accumulate, void *workspace, uint64_t ws_bytes,
                                const uint32_t *slot_epoch, void *stream);
-/* slot_epoch: NULL (all_xyzw holds n_all float4), or the device epoch counter
+/* all_xyzw = NULL: a single rank reads its own rows from the columns (n_all
+ * == n, self_offset 0) -- no pack pass, same bits as packing first.
+ * slot_epoch: NULL (all_xyzw holds n_all float4), or the device epoch counter
  * of the P2P exchange below (all_xyzw is its double buffer; the kernels read
  * slot (*slot_epoch & 1), n_all float4 each). */
 

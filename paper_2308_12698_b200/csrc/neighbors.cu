@@ -119,14 +119,43 @@ __device__ __forceinline__ const float4 *gathered(const float4 *base, const uint
     return slot_epoch ? base + (int64_t)(*slot_epoch & 1u) * n_all : base;
 }
 
+// Where the pipeline reads the swarm's positions: the gathered float4 buffer,
+// or -- a single rank, no exchange -- the group's own columns directly (the
+// pack kernel's arithmetic: hi + lo, NaN for dead rows), saving the pack pass.
+struct PosSrc {
+    const float4 *base;          // gathered buffer, or null: read the columns
+    const uint32_t *slot_epoch;
+    const float *cols;
+    const uint8_t *flags;
+    int compensated;
+    __device__ __forceinline__ float4 get(int64_t i, int64_t n_all) const
+    {
+        if (base) return gathered(base, slot_epoch, n_all)[i];
+        const float nan = __int_as_float(0x7fc00000);
+        float4 p = make_float4(nan, nan, nan, 0.0f);
+        if (flags[i] & SWARMSTEP_FLAG_ALIVE) {
+            float x = cols[ssb::at(SWARMSTEP_COL_POS + 0, i)];
+            float y = cols[ssb::at(SWARMSTEP_COL_POS + 1, i)];
+            float z = cols[ssb::at(SWARMSTEP_COL_POS + 2, i)];
+            if (compensated) {
+                x += cols[ssb::at(SWARMSTEP_COL_POS_LO + 0, i)];
+                y += cols[ssb::at(SWARMSTEP_COL_POS_LO + 1, i)];
+                z += cols[ssb::at(SWARMSTEP_COL_POS_LO + 2, i)];
+            }
+            p = make_float4(x, y, z, 0.0f);
+        }
+        return p;
+    }
+};
+
 // bucket of every gathered agent (dead / padding rows: bucket m, past every
 // real bucket) and its rank inside the bucket
-__global__ void hash_count_kernel(const float4 *pos_base, const uint32_t *slot_epoch, int64_t n_all, float inv_cell,
-                                  uint32_t mask, uint32_t *keys, uint32_t *ranks, uint32_t *count)
+__global__ void hash_count_kernel(const PosSrc src, int64_t n_all, float inv_cell, uint32_t mask, uint32_t *keys,
+                                  uint32_t *ranks, uint32_t *count)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_all) return;
-    const float4 p = gathered(pos_base, slot_epoch, n_all)[i];
+    const float4 p = src.get(i, n_all);
     const uint32_t k = isnan(p.x) ? mask + 1 : cell_hash(cell_of(p.x, inv_cell), cell_of(p.y, inv_cell),
                                                           cell_of(p.z, inv_cell), mask);
     keys[i] = k;
@@ -135,9 +164,9 @@ __global__ void hash_count_kernel(const float4 *pos_base, const uint32_t *slot_e
 
 // counting-sort scatter: the agent goes to start[bucket] + rank, its position
 // (index in .w) with it
-__global__ void scatter_kernel(const float4 *pos_base, const uint32_t *slot_epoch, int64_t n_all, uint32_t mask,
-                               const uint32_t *keys, const uint32_t *ranks, const uint32_t *cell_start,
-                               uint32_t *keys_sorted, uint32_t *vals_sorted, float4 *pos_sorted)
+__global__ void scatter_kernel(const PosSrc src, int64_t n_all, uint32_t mask, const uint32_t *keys,
+                               const uint32_t *ranks, const uint32_t *cell_start, uint32_t *keys_sorted,
+                               uint32_t *vals_sorted, float4 *pos_sorted)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_all) return;
@@ -146,7 +175,7 @@ __global__ void scatter_kernel(const float4 *pos_base, const uint32_t *slot_epoc
     keys_sorted[slot] = k;
     vals_sorted[slot] = (uint32_t)i;
     if (k <= mask) {
-        float4 p = gathered(pos_base, slot_epoch, n_all)[i];
+        float4 p = src.get(i, n_all);
         p.w = __uint_as_float((uint32_t)i);
         pos_sorted[slot] = p;
     }
@@ -258,7 +287,9 @@ int swarmstep_neighbor_overlay(const swarmstep_group_view *g, const float *all_x
                                int64_t self_offset, float r_sense, float k_sep, float cell, int accumulate,
                                void *workspace, uint64_t ws_bytes, const uint32_t *slot_epoch, void *stream)
 {
-    if (!g || !g->cols || !g->flags || !all_xyzw || !workspace) return nb_err(SWARMSTEP_EINVAL, "null argument");
+    if (!g || !g->cols || !g->flags || !workspace) return nb_err(SWARMSTEP_EINVAL, "null argument");
+    if (!all_xyzw && (n_all != g->n || self_offset != 0 || slot_epoch))
+        return nb_err(SWARMSTEP_EINVAL, "all_xyzw = NULL reads the group's own rows: needs n_all == n, offset 0");
     if (!(r_sense > 0.0f) || !(cell >= r_sense)) return nb_err(SWARMSTEP_EINVAL, "need r_sense > 0 and cell >= r_sense");
     if (self_offset < 0 || self_offset + g->n > n_all) return nb_err(SWARMSTEP_EINVAL, "local shard outside n_all");
     if (n_all > (1LL << 29)) return nb_err(SWARMSTEP_EINVAL, "n_all above 2^29");
@@ -268,15 +299,14 @@ int swarmstep_neighbor_overlay(const swarmstep_group_view *g, const float *all_x
     Workspace w;
     layout(n_all, (char *)workspace, &w);
     const float inv_cell = 1.0f / cell;
-    const float4 *pos = (const float4 *)all_xyzw;
+    const PosSrc src{(const float4 *)all_xyzw, slot_epoch, g->cols, g->flags, g->compensated};
     if (!(fabsf(k_sep) < 1073741824.0f)) return nb_err(SWARMSTEP_EINVAL, "need |k_sep| < 2^30 (fixed-point sums)");
     cudaMemsetAsync(w.count, 0, sizeof(uint32_t) * ((size_t)w.mask + 2), s);
-    hash_count_kernel<<<grid_n(n_all, 256), 256, 0, s>>>(pos, slot_epoch, n_all, inv_cell, w.mask, w.keys, w.ranks,
-                                                         w.count);
+    hash_count_kernel<<<grid_n(n_all, 256), 256, 0, s>>>(src, n_all, inv_cell, w.mask, w.keys, w.ranks, w.count);
     size_t cb = w.cub_bytes;
     if (cub::DeviceScan::ExclusiveSum(w.cub_tmp, cb, w.count, w.cell_start, (int)(w.mask + 2), s) != cudaSuccess)
         return nb_cuda("cub::DeviceScan");
-    scatter_kernel<<<grid_n(n_all, 256), 256, 0, s>>>(pos, slot_epoch, n_all, w.mask, w.keys, w.ranks, w.cell_start,
+    scatter_kernel<<<grid_n(n_all, 256), 256, 0, s>>>(src, n_all, w.mask, w.keys, w.ranks, w.cell_start,
                                                       w.keys_sorted, w.vals_sorted, w.pos_sorted);
     query_kernel<<<grid_n(n_all, 128), 128, 0, s>>>(w.pos_sorted, w.keys_sorted, w.vals_sorted, w.cell_start,
                                                    w.mask, r_sense, k_sep, n_all, g->n, self_offset, g->flags,

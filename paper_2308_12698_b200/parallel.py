@@ -202,6 +202,9 @@ class NeighborSeparation:
         """The (n_all, 4) positions of the last exchange (the slot of the
         current epoch for the P2P double buffer)."""
         if self.exchange != "p2p":
+            if self.shard.world == 1:
+                self.gather()          # the single-rank launch reads the columns directly
+            torch.cuda.synchronize(self.group.device)
             return self.all
         torch.cuda.synchronize(self.group.device)
         e = int(self._epoch.item())
@@ -212,10 +215,12 @@ class NeighborSeparation:
         host state change; graph-capturable when world == 1 or with the P2P
         exchange, whose slot selection happens on the device)."""
         g = self.group
-        self.gather()
+        single = self.shard.world == 1 and self.exchange != "p2p"
+        if not single:
+            self.gather()
         with torch.cuda.device(g.device), torch.cuda.stream(g.stream):
             _lib.check(self._lib.swarmstep_neighbor_overlay(
-                g._view_ref, self.all.data_ptr(), self.n_all, self.shard.self_offset,
+                g._view_ref, None if single else self.all.data_ptr(), self.n_all, self.shard.self_offset,
                 ctypes.c_float(self.r_sense), ctypes.c_float(self.k_sep), ctypes.c_float(self.cell),
                 1 if accumulate else 0, self.workspace.data_ptr(), ctypes.c_uint64(self.workspace.numel()),
                 self._epoch.data_ptr() if self._epoch is not None else None,
