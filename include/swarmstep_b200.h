@@ -106,7 +106,7 @@ typedef struct swarmstep_group_view {
     int64_t stride;         /* row capacity (>= n, multiple of 128)         */
     float *cols;            /* [stride/128][SWARMSTEP_NCOL][128] float32    */
     uint8_t *flags;         /* [stride]                                     */
-    uint32_t *counters;     /* device [4]: 0 faults logged (monotonic), 1 scratch count */
+    uint32_t *counters;     /* device [4]: 0 faults logged (monotonic), 1 retarget count, 2 viewer count */
     uint64_t *fault_log;    /* device [fault_cap]: (tick << 40) | row       */
     int64_t fault_cap;
     int32_t compensated;    /* 1: position = hi + lo (COL_POS_LO in use)    */
@@ -222,6 +222,17 @@ int swarmstep_quad_mark_dead(const swarmstep_group_view *g, const int64_t *rows,
  * (quat.py:139-143).  counters[1] += number of rows retargeted. */
 int swarmstep_quad_retarget_waypoint(const swarmstep_group_view *g, const double *point3,
                                      double radius, void *stream);
+
+/* Viewer ATTRACT / REPEL influence (World._apply_viewer_input, core.py:445-453)
+ * on the device: for alive rows with 1e-12 < d = |point - p| < radius the
+ * overlay columns get += float32(gain * (1 - d/radius) / d * (point - p)),
+ * evaluated in float64 in viewer_velocity_offsets' order (wire.py:320-340);
+ * gain = +strength (attract) or -strength (repel).  counters[2] += rows whose
+ * offset is non-zero, the reference's `offsets.any()` gate for
+ * add_velocity_overlay.  The caller zeroes the overlay columns first when no
+ * overlay is pending.  radius <= 0 is a no-op (wire.py:331). */
+int swarmstep_quad_viewer_overlay(const swarmstep_group_view *g, const double *point3,
+                                  double radius, double gain, void *stream);
 
 /* Device-side snapshot packing (batch_snapshot, state.py:193-204): writes
  * float64 row-major pos (n,3), vel (n,3), quat (n,4), omega (n,3) and

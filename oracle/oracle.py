@@ -428,6 +428,24 @@ def neighbor_overlay(pos, alive, r_sense: float, k_sep: float, rows=None, chunk:
     return out
 
 
+def viewer_offsets(mode: str, point, radius: float, strength: float, pos, alive) -> np.ndarray:
+    """viewer_velocity_offsets (wire.py:320-340) restated: (n, 3) float64
+    attract / repel offsets, zero for WAYPOINT, radius <= 0, dead rows and
+    rows outside 1e-12 < d < radius."""
+    pos = np.asarray(pos, dtype=float)
+    alive = np.asarray(alive, dtype=bool)
+    out = np.zeros((pos.shape[0], 3))
+    if mode == "waypoint" or not radius > 0.0:
+        return out
+    delta = np.asarray(point, dtype=float) - pos
+    d = np.sqrt((delta[:, 0] * delta[:, 0] + delta[:, 1] * delta[:, 1]) + delta[:, 2] * delta[:, 2])
+    inside = (d < radius) & (d > 1e-12) & alive
+    sign = 1.0 if mode == "attract" else -1.0
+    scale = sign * strength * (1.0 - d[inside] / radius) / d[inside]
+    out[inside] = delta[inside] * scale[:, None]
+    return out
+
+
 def cpu_count() -> int:
     try:
         return len(os.sched_getaffinity(0))

@@ -36,7 +36,7 @@ EXPORTS = (
     "swarmstep_abi_version", "swarmstep_last_error", "swarmstep_device_info", "swarmstep_preload",
     "swarmstep_memcpy_async", "swarmstep_stream_sync", "swarmstep_quad_params_init",
     "swarmstep_quad_step", "swarmstep_quad_step_lag", "swarmstep_quad_step_circle", "swarmstep_quad_apply_commands", "swarmstep_quad_set_setpoints",
-    "swarmstep_quad_mark_dead", "swarmstep_quad_retarget_waypoint",
+    "swarmstep_quad_mark_dead", "swarmstep_quad_retarget_waypoint", "swarmstep_quad_viewer_overlay",
     "swarmstep_quad_pack_f64", "swarmstep_quad_unpack_f64",
     "swarmstep_pack_positions", "swarmstep_neighbor_workspace_bytes", "swarmstep_neighbor_overlay",
     "swarmstep_quad_circle_setpoints", "swarmstep_tick_add", "swarmstep_quad_pack_wire",
@@ -104,6 +104,8 @@ def _declare(lib) -> None:
     lib.swarmstep_quad_mark_dead.argtypes = [view, vp, vp, i64, vp]
     lib.swarmstep_quad_retarget_waypoint.restype = i32
     lib.swarmstep_quad_retarget_waypoint.argtypes = [view, ctypes.POINTER(f64), f64, vp]
+    lib.swarmstep_quad_viewer_overlay.restype = i32
+    lib.swarmstep_quad_viewer_overlay.argtypes = [view, ctypes.POINTER(f64), f64, f64, vp]
     lib.swarmstep_quad_pack_f64.restype = i32
     lib.swarmstep_quad_pack_f64.argtypes = [view, vp, vp, vp, vp, vp, vp]
     lib.swarmstep_quad_unpack_f64.restype = i32

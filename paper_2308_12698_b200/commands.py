@@ -1,4 +1,5 @@
-"""Command levels and per-agent commands, mirroring wire.py:54-76.
+"""Command levels, per-agent commands and viewer influence messages, mirroring
+wire.py:54-113.
 
 The group accepts these or the reference's own ``AgentCommand`` objects:
 only ``agent_id``, ``level`` (an enum whose ``.value`` is "pos" / "rate" /
@@ -36,6 +37,29 @@ class AgentCommand:
         if len(self.values) != self.level.n_values:
             raise ValidationError(
                 f"level {self.level.value} takes {self.level.n_values} values, got {len(self.values)}")
+
+
+class InfluenceMode(str, Enum):
+    """Viewer influence modes (wire.py:92-95)."""
+
+    ATTRACT = "attract"
+    REPEL = "repel"
+    WAYPOINT = "waypoint"
+
+
+@dataclass(frozen=True)
+class ViewerInputMsg:
+    """A viewer influence message (wire.py:103-113); the groups' device
+    ``apply_viewer_input`` also takes the reference's own message objects."""
+
+    mode: InfluenceMode
+    world_point: tuple[float, float, float]
+    radius: float
+    strength: float
+
+    def __post_init__(self):
+        if self.radius < 0.0 or self.strength < 0.0:
+            raise ValidationError("radius and strength must be non-negative")
 
 
 # device level codes (core.py:73; include/swarmstep_b200.h SWARMSTEP_LEVEL_*)

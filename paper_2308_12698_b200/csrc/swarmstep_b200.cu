@@ -824,6 +824,45 @@ __global__ void mark_dead_kernel(uint8_t *flags, const int64_t *rows, uint8_t *w
     flags[r] = (uint8_t)(fl & ~SWARMSTEP_FLAG_ALIVE);
 }
 
+__device__ __forceinline__ double norm3_rn(double x, double y, double z)
+{
+    return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z)));
+}
+
+// World._apply_viewer_input for ATTRACT / REPEL (core.py:445-453) with
+// viewer_velocity_offsets (wire.py:320-340) evaluated per row in float64 in
+// the reference's operation order, added to the one-tick overlay in float32
+// like add_velocity_overlay's host path.  counters[2] counts rows whose
+// offset is non-zero (the reference's `offsets.any()` gate).
+__global__ void viewer_overlay_kernel(float *cols, const uint8_t *flags, int64_t n, int64_t stride,
+                                      int compensated, double px, double py, double pz, double radius,
+                                      double gain, uint32_t *counters)
+{
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool hit = false;
+    if (r < n && (flags[r] & SWARMSTEP_FLAG_ALIVE)) {
+        double p[3];
+        for (int i = 0; i < 3; i++) {
+            p[i] = (double)cols[ssb::at(SWARMSTEP_COL_POS + i, r)];
+            if (compensated) p[i] += (double)cols[ssb::at(SWARMSTEP_COL_POS_LO + i, r)];
+        }
+        const double delta[3] = {__dadd_rn(px, -p[0]), __dadd_rn(py, -p[1]), __dadd_rn(pz, -p[2])};
+        const double d = norm3_rn(delta[0], delta[1], delta[2]);
+        if (d < radius && d > 1e-12) {
+            // sign * strength * (1.0 - d / radius) / d
+            const double scale = __ddiv_rn(__dmul_rn(gain, __dadd_rn(1.0, -__ddiv_rn(d, radius))), d);
+            for (int i = 0; i < 3; i++) {
+                const double o = __dmul_rn(delta[i], scale);
+                hit |= o != 0.0;
+                const int64_t at = ssb::at(SWARMSTEP_COL_OVERLAY + i, r);
+                cols[at] = __fadd_rn(cols[at], (float)o);
+            }
+        }
+    }
+    const unsigned hits = __ballot_sync(0xffffffffu, hit);
+    if (hits && (threadIdx.x & 31) == 0) atomicAdd(&counters[2], (uint32_t)__popc(hits));
+}
+
 __global__ void retarget_kernel(float *cols, uint8_t *flags, int64_t n, int64_t stride, int compensated,
                                 double px, double py, double pz, double radius, uint32_t *counters)
 {
@@ -836,8 +875,8 @@ __global__ void retarget_kernel(float *cols, uint8_t *flags, int64_t n, int64_t 
         p[i] = (double)cols[ssb::at(SWARMSTEP_COL_POS + i, r)];
         if (compensated) p[i] += (double)cols[ssb::at(SWARMSTEP_COL_POS_LO + i, r)];
     }
-    const double dx = p[0] - px, dy = p[1] - py, dz = p[2] - pz;
-    const double d = sqrt(dx * dx + dy * dy + dz * dz);
+    // np.linalg.norm(pos - point, axis=1): ((dx^2 + dy^2) + dz^2), no contraction
+    const double d = norm3_rn(__dadd_rn(p[0], -px), __dadd_rn(p[1], -py), __dadd_rn(p[2], -pz));
     if (!(d < radius)) return;
     const double w = cols[ssb::at(SWARMSTEP_COL_QUAT + 0, r)];
     const double x = cols[ssb::at(SWARMSTEP_COL_QUAT + 1, r)];
@@ -994,6 +1033,7 @@ int swarmstep_preload(void)
                          (const void *)quad_step_pair_circle_kernel<false>,
                          (const void *)apply_commands_kernel, (const void *)set_setpoints_kernel,
                          (const void *)mark_dead_kernel, (const void *)retarget_kernel,
+                         (const void *)viewer_overlay_kernel,
                          (const void *)pack_f64_kernel, (const void *)unpack_f64_kernel};
     for (const void *f : fns)
         if (cudaFuncGetAttributes(&a, f) != cudaSuccess) return cuda_status("cudaFuncGetAttributes");
@@ -1167,6 +1207,19 @@ int swarmstep_quad_retarget_waypoint(const swarmstep_group_view *g, const double
     retarget_kernel<<<grid_for(g->n, 256), 256, 0, (cudaStream_t)stream>>>(
         g->cols, g->flags, g->n, g->stride, g->compensated, point3[0], point3[1], point3[2], radius, g->counters);
     return cuda_status("retarget_kernel");
+}
+
+int swarmstep_quad_viewer_overlay(const swarmstep_group_view *g, const double *point3, double radius,
+                                  double gain, void *stream)
+{
+    int st = check_view(g);
+    if (st) return st;
+    if (!point3 || !g->counters) return set_err(SWARMSTEP_EINVAL, "null point / counters");
+    if (g->n == 0 || !(radius > 0.0)) return SWARMSTEP_OK;   // wire.py:331-332
+    viewer_overlay_kernel<<<grid_for(g->n, 256), 256, 0, (cudaStream_t)stream>>>(
+        g->cols, g->flags, g->n, g->stride, g->compensated, point3[0], point3[1], point3[2], radius, gain,
+        g->counters);
+    return cuda_status("viewer_overlay_kernel");
 }
 
 int swarmstep_quad_pack_f64(const swarmstep_group_view *g, double *pos, double *vel, double *quat,

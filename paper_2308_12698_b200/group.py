@@ -443,6 +443,40 @@ class B200QuadGroup:
             self._cols_write(COL_OVERLAY, t, add=True)
         self._overlay_active = True
 
+    def apply_viewer_input(self, msg) -> bool:
+        """``World._apply_viewer_input`` for this group (core.py:445-453) without
+        pulling positions to the host: WAYPOINT retargets (core.py:447-449);
+        ATTRACT / REPEL evaluate ``viewer_velocity_offsets`` (wire.py:320-340) on
+        the device into the one-tick overlay, which is activated only if some
+        offset is non-zero (the reference's ``offsets.any()``).  Returns whether
+        an overlay was added.  One 4-byte device read."""
+        mode = getattr(msg.mode, "value", msg.mode)
+        if mode == "waypoint":
+            self.retarget_waypoint(msg.world_point, msg.radius)
+            return False
+        if mode not in ("attract", "repel"):
+            raise ValidationError(f"unknown influence mode {msg.mode!r}")
+        radius = float(msg.radius)
+        if not radius > 0.0:
+            return False
+        gain = float(msg.strength) if mode == "attract" else -float(msg.strength)
+        pt = (ctypes.c_double * 3)(*[float(x) for x in np.asarray(msg.world_point, dtype=float).ravel()[:3]])
+        with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
+            self._counters[2].zero_()
+            if not self._overlay_active:
+                self._cols[:, COL_OVERLAY:COL_OVERLAY + 3, :].zero_()
+            self._call(self._lib.swarmstep_quad_viewer_overlay, pt, ctypes.c_double(radius), ctypes.c_double(gain),
+                       self._stream_h)
+            _lib.check(self._lib.swarmstep_memcpy_async(self._counters_host.data_ptr(), self._counters.data_ptr(),
+                                                        self._counters.numel() * 4, self._stream_h))
+        self._sync()
+        if int(self._counters_host[2]) == 0:
+            return False
+        if not np.isfinite(gain):
+            self._overlay_poison = True
+        self._overlay_active = True
+        return True
+
     def retarget_waypoint(self, point, radius: float) -> None:
         """Alive rows within ``radius`` of ``point`` go to POS hold there (core.py:141-149)."""
         pt = (ctypes.c_double * 3)(*[float(x) for x in np.asarray(point, dtype=float).ravel()[:3]])

@@ -152,6 +152,10 @@ class MultiDeviceQuadGroup:
         for s in self.shards:
             s.retarget_waypoint(point, radius)
 
+    def apply_viewer_input(self, msg) -> bool:
+        """Device viewer influence on every shard (core.py:445-453)."""
+        return any([s.apply_viewer_input(msg) for s in self.shards])
+
     def set_setpoints(self, values, level=0, columns: bool = False) -> None:
         v = np.asarray(values)
         if columns:

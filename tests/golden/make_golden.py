@@ -242,7 +242,53 @@ def gen_unicycle() -> None:
     print(f"unicycles: n={sc.n} ticks={sc.ticks}")
 
 
+def viewer_cases():
+    """(mode, point, radius, strength) messages of the viewer golden set; the
+    point of case 3 sits exactly on agent 5 (the d > 1e-12 guard)."""
+    return [("attract", (1.0, -2.0, 10.5), 6.0, 1.5), ("repel", (-3.25, 4.0, 9.0), 4.0, 0.75),
+            ("attract", (0.0, 0.0, 10.0), 0.0, 2.0), ("repel", None, 5.0, 1.0),
+            ("attract", (1.0, 1.0, 10.0), 3.0, 0.0), ("waypoint", (2.0, 2.0, 11.0), 5.0, 1.0),
+            ("attract", (50.0, 50.0, 50.0), 2.0, 1.0)]
+
+
+def gen_viewer() -> None:
+    """World._apply_viewer_input (core.py:445-453): viewer_velocity_offsets
+    (wire.py:320-340) per message, and the command store after a WAYPOINT
+    retarget (core.py:141-149).  Positions are multiples of 2^-20 (exact as a
+    float32 hi + lo pair, so the device sees the same float64 positions)."""
+    from swarmstep.wire import InfluenceMode, ViewerInputMsg, viewer_velocity_offsets
+    rng = np.random.default_rng(31)
+    n = 200
+    pos = np.round(rng.uniform(-6.0, 6.0, (n, 3)) * 2.0**20) / 2.0**20
+    pos[:, 2] += 10.0
+    alive = rng.random(n) > 0.15
+    alive[5] = True
+    quat = rng.normal(size=(n, 4))
+    quat /= np.linalg.norm(quat, axis=1, keepdims=True)
+    quat = np.round(quat * 2.0**20) / 2.0**20      # exact in float32
+    out = {"pos": pos, "alive": alive, "quat": quat}
+    for i, (mode, point, radius, strength) in enumerate(viewer_cases()):
+        point = tuple(pos[5]) if point is None else point
+        msg = ViewerInputMsg(mode=InfluenceMode(mode), world_point=point, radius=radius, strength=strength)
+        off = viewer_velocity_offsets(msg, pos, alive)
+        out[f"v{i}_point"] = np.array(point, dtype=float)
+        out[f"v{i}_msg"] = np.array([mode, radius, strength], dtype=object).astype(str)
+        out[f"v{i}_off"] = off
+        out[f"v{i}_any"] = np.array(bool(off.any()))
+        if mode == "waypoint":
+            b = batch_create(0, n, pos, quat=quat)
+            b.alive[:] = alive
+            g = QuadGroup(0, b, P)
+            g.retarget_waypoint(point, radius)
+            out[f"v{i}_cmd_level"] = g.cmd_level.copy()
+            out[f"v{i}_cmd_values"] = g.cmd_values.copy()
+    out["cases"] = np.array(len(viewer_cases()))
+    np.savez_compressed(HERE / "viewer.npz", **out)
+    print(f"viewer: {len(viewer_cases())} messages over n={n}")
+
+
 if __name__ == "__main__":
+    gen_viewer()
     gen_unicycle()
     gen_collision()
     gen_functions()

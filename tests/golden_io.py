@@ -25,3 +25,18 @@ def load_scenario(name):
     for t, a in zip(z["fault_tick"], z["fault_id"]):
         faults.setdefault(int(t), []).append(int(a))
     return sc, rec, z["cmd_ok"], faults, int(z["raise_tick"])
+
+
+def load_viewer():
+    """tests/golden/viewer.npz: (pos, alive, quat, [case dicts]) for the
+    viewer influence messages (World._apply_viewer_input, core.py:445-453)."""
+    z = dict(np.load(GOLDEN / "viewer.npz"))
+    cases = []
+    for i in range(int(z["cases"])):
+        mode, radius, strength = (str(x) for x in z[f"v{i}_msg"])
+        c = dict(mode=mode, radius=float(radius), strength=float(strength), point=z[f"v{i}_point"],
+                 off=z[f"v{i}_off"], any=bool(z[f"v{i}_any"]))
+        if f"v{i}_cmd_level" in z:
+            c["cmd_level"], c["cmd_values"] = z[f"v{i}_cmd_level"], z[f"v{i}_cmd_values"]
+        cases.append(c)
+    return z["pos"], z["alive"], z["quat"], cases
