@@ -170,6 +170,7 @@ class B200QuadGroup:
         )
         self._row = {int(a): i for i, a in enumerate(self._batch.agent_ids)}
         self._ids_dev = None             # device copy of agent_ids (wire packing), on demand
+        self._wire_bufs = None           # wire_section's device / pinned buffers, on demand
         self._alive = self._batch.alive  # exact: changes only via mark_dead / faults
         self._batch_view = DeviceBatchView(self)
         self._state_stale = False        # device state newer than the host mirror
@@ -516,14 +517,25 @@ class B200QuadGroup:
         u16 type_id, u32 n, then 61*n bytes of columns."""
         import struct
         n = self.n
-        with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
-            if self._ids_dev is None:
+        if self._wire_bufs is None:   # cached: device columns + pinned host copy
+            self._wire_bufs = (torch.empty(61 * n + 8, dtype=torch.uint8, device=self.device),
+                               torch.empty(61 * n, dtype=torch.uint8, pin_memory=True))
+        dev, host = self._wire_bufs
+        self.pack_wire_async(dev)
+        _lib.check(self._lib.swarmstep_memcpy_async(host.data_ptr(), dev.data_ptr(), 61 * n, self._stream_h))
+        self._sync()
+        return b"".join((struct.pack("<HI", self._batch.type_id, n), host.numpy().data))
+
+    def pack_wire_async(self, buf: torch.Tensor) -> None:
+        """Enqueue the device packing of this group's 61*n section column bytes
+        (ids, alive, pos, vel, canonical quat, omega; wire.py:162-178) into the
+        device buffer ``buf`` on the group's stream, after its queued ticks."""
+        if buf.device != self.device or buf.dtype != torch.uint8 or buf.numel() < 61 * self.n:
+            raise ValidationError("pack_wire_async needs a uint8 buffer of >= 61*n bytes on the group's device")
+        if self._ids_dev is None:
+            with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
                 self._ids_dev = torch.from_numpy(self._batch.agent_ids.view(np.int64).copy()).to(self.device)
-            buf = torch.empty(61 * n + 8, dtype=torch.uint8, device=self.device)
-            self._call(self._lib.swarmstep_quad_pack_wire, _ptr(self._ids_dev), _ptr(buf),
-                       ctypes.c_void_p(self.stream.cuda_stream))
-            host = buf[:61 * n].cpu().numpy().tobytes()
-        return struct.pack("<HI", self._batch.type_id, n) + host
+        self._call(self._lib.swarmstep_quad_pack_wire, _ptr(self._ids_dev), _ptr(buf), self._stream_h)
 
     # ------------------------------------------------------------ stepping
     def _any_pos_rows(self) -> bool:

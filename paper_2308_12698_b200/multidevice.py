@@ -184,5 +184,18 @@ class MultiDeviceQuadGroup:
     def snapshot(self, tick: int):
         return batch_snapshot(self.batch, tick)
 
+    def wire_section(self) -> bytes:
+        """The type's SnapshotMsg section (wire.py:162-178): each column block
+        is the concatenation of the shards' blocks."""
+        import struct
+        secs = [memoryview(s.wire_section())[6:] for s in self.shards]
+        ns = [s.n for s in self.shards]
+        parts, offs = [struct.pack("<HI", self.type_id, self.n)], [0] * len(secs)
+        for w in (8, 1, 12, 12, 16, 12):      # ids, alive, pos, vel, quat, omega
+            for k, (b, n) in enumerate(zip(secs, ns)):
+                parts.append(b[offs[k]:offs[k] + w * n])
+                offs[k] += w * n
+        return b"".join(parts)
+
     def alive_count(self) -> int:
         return sum(s.alive_count() for s in self.shards)

@@ -32,4 +32,7 @@ def snapshot_frame(tick: int, groups, empty_types=()) -> bytes:
     sections = [(g.type_id, g.wire_section()) for g in groups]
     sections += [(int(t), struct.pack("<HI", int(t), 0)) for t in empty_types]
     sections.sort(key=lambda s: s[0])
-    return encode_frame(MSG_SNAPSHOT, struct.pack("<Q", int(tick)) + b"".join(s for _, s in sections))
+    length = 1 + 8 + sum(len(s) for _, s in sections)
+    if length > MAX_FRAME_LEN:
+        raise ValidationError(f"frame of {length} bytes exceeds the {MAX_FRAME_LEN} cap")
+    return b"".join([struct.pack("<IBQ", length, MSG_SNAPSHOT, int(tick))] + [s for _, s in sections])
