@@ -287,7 +287,78 @@ def gen_viewer() -> None:
     print(f"viewer: {len(viewer_cases())} messages over n={n}")
 
 
+def world_script():
+    """Inbox items per tick for the World golden run: commands of every level
+    (including rejected ones: unknown id, wrong level, dead agents) and viewer
+    inputs of every mode.  Plain data so the GPU test replays it without the
+    reference."""
+    return {
+        "0": [["cmd", 0, "pos", [2.2, 0.0, 5.0, 0.0, 0.0, 0.0, 0.0]],     # agents 0 and 1 fly head on
+              ["cmd", 1, "pos", [-0.7, 0.0, 5.0, 0.0, 0.0, 0.0, 0.0]],
+              ["cmd", 40, "unicycle", [0.8, 0.3]], ["cmd", 41, "unicycle", [0.5, -0.2]],
+              ["cmd", 9999, "pos", [0.0] * 7], ["cmd", 42, "pos", [0.0] * 7]],
+        "30": [["viewer", "attract", [6.0, 3.0, 5.5], 3.0, 1.5]],
+        "60": [["cmd", 7, "rate", [0.3, -0.2, 0.1, 10.5]], ["cmd", 8, "motor", [11000.0, 10000.0, 11000.0, 10000.0]],
+               ["viewer", "repel", [3.0, 4.5, 5.0], 2.5, 2.0]],
+        "90": [["viewer", "waypoint", [9.0, 6.0, 5.0], 2.0, 1.0], ["cmd", 20, "pos", [7.0, 7.0, 6.0, 0.5, 0.0, 0.0, 1.0]]],
+        "120": [["cmd", 7, "pos", [4.5, 1.5, 5.0, 0.0, 0.0, 0.0, -0.5]], ["cmd", 8, "rate", [0.0, 0.0, 0.0, 9.81]],
+                ["viewer", "attract", [1.0, 1.0, 5.0], 0.0, 3.0]],
+        "200": [["cmd", 0, "pos", [0.0] * 7], ["cmd", 1, "rate", [0.0, 0.0, 0.0, 9.0]],
+                ["viewer", "repel", [7.5, 7.5, 5.0], 4.0, 0.5]],
+    }
+
+
+WORLD_QUADS, WORLD_UNIS, WORLD_TICKS, WORLD_DT = 40, 10, 300, 1.0 / 512.0
+
+
+def world_layout():
+    """Quads on a 1.5 m grid at z = 5 (8 columns), unicycles on a line at y = -3."""
+    q = np.array([[1.5 * (i % 8), 1.5 * (i // 8), 5.0] for i in range(WORLD_QUADS)])
+    u = np.array([[2.0 * i, -3.0, 0.0] for i in range(WORLD_UNIS)])
+    return q, u
+
+
+def gen_world() -> None:
+    """The reference World (core.py:308-505) itself -- events -> inbox ->
+    step groups -> in-loop collision detect -> deaths -> publish -- over a
+    quad group and a unicycle group for WORLD_TICKS ticks of world_script();
+    records the event log and the float64 state every 20 ticks."""
+    import json
+    from swarmstep.collision import CollisionConfig
+    from swarmstep.core import UnicycleGroup, UnicycleParams, World
+    from swarmstep.wire import InfluenceMode, ViewerInputMsg
+    qpos, upos = world_layout()
+    quads = QuadGroup(0, batch_create(0, WORLD_QUADS, qpos), P)
+    unis = UnicycleGroup(1, batch_create(1, WORLD_UNIS, upos, id_base=WORLD_QUADS), UnicycleParams())
+    cfg = CollisionConfig(r_collide={0: 0.2, 1: 0.3}, r_sense=1.2, cell=1.2)
+    world = World([quads, unis], dt=WORLD_DT, collision_config=cfg, collision_in_loop=True)
+    script = world_script()
+    out = {}
+    for t in range(WORLD_TICKS):
+        for item in script.get(str(t), []):
+            if item[0] == "cmd":
+                world.submit_commands([make_cmd(item[1], {"pos": 0, "rate": 1, "motor": 2, "unicycle": 3}[item[2]],
+                                                item[3])])
+            else:
+                world.submit_viewer_input(ViewerInputMsg(mode=InfluenceMode(item[1]), world_point=tuple(item[2]),
+                                                         radius=item[3], strength=item[4]))
+        world.tick()
+        if (t + 1) % 20 == 0:
+            for g in world.groups:
+                b = g.batch
+                for k in ("pos", "vel", "quat", "omega", "alive"):
+                    out[f"t{t}_g{g.type_id}_{k}"] = getattr(b, k).copy()
+    events = [[e.tick, e.kind.value, list(e.agent_ids)] for e in world.event_log]
+    out["events"] = np.array(json.dumps(events))
+    out["script"] = np.array(json.dumps(script))
+    out["qpos"], out["upos"] = qpos, upos
+    out["dt"], out["ticks"] = np.array(WORLD_DT), np.array(WORLD_TICKS)
+    np.savez_compressed(HERE / "world.npz", **out)
+    print(f"world: {WORLD_TICKS} ticks, events {events}")
+
+
 if __name__ == "__main__":
+    gen_world()
     gen_viewer()
     gen_unicycle()
     gen_collision()
