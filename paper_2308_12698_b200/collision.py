@@ -69,19 +69,33 @@ class NeighborSets(Mapping):
 
     def _dict(self) -> dict:
         if self._d is None:
-            d = {int(i): () for i in self._ids_all[self._alive_all]}
-            near, ids_all = self._near, self._ids_all
+            ids_all, alive = self._ids_all, self._alive_all
+            m = int(ids_all.shape[0])
+            rows = np.nonzero(alive)[0]
+            near = self._near
+            k = (near.numel() // 2) if isinstance(near, torch.Tensor) else int(np.asarray(near).shape[0])
+            if k == 0:
+                self._d = dict.fromkeys(ids_all[rows].tolist(), ())
+                return self._d
+            # both directions of every pair, ordered by (row a, id b) through one
+            # sort of int64 keys row_a * m + rank(id_b) (on the device when the
+            # pairs are there); then one slice of the sorted id list per agent
+            by_id = np.argsort(ids_all, kind="stable")
+            rank = np.empty(m, dtype=np.int64)
+            rank[by_id] = np.arange(m, dtype=np.int64)
             if isinstance(near, torch.Tensor):
-                near = near.cpu().numpy().astype(np.int64).reshape(-1, 2)
-            na = np.concatenate([near[:, 0], near[:, 1]])
-            nb = np.concatenate([near[:, 1], near[:, 0]])
-            if na.size:
-                order = np.lexsort((ids_all[nb], ids_all[na]))
-                na, nb = na[order], nb[order]
-                bounds = np.nonzero(np.diff(na))[0] + 1
-                for chunk_a, chunk_b in zip(np.split(na, bounds), np.split(nb, bounds)):
-                    d[int(ids_all[chunk_a[0]])] = tuple(ids_all[chunk_b].tolist())
-            self._d = d
+                nr = near.reshape(-1, 2).long()
+                na, nb = torch.cat([nr[:, 0], nr[:, 1]]), torch.cat([nr[:, 1], nr[:, 0]])
+                key = na * m + torch.from_numpy(rank).to(near.device)[nb]
+                key = torch.sort(key).values.cpu().numpy()
+            else:
+                nr = np.asarray(near, dtype=np.int64).reshape(-1, 2)
+                na, nb = np.concatenate([nr[:, 0], nr[:, 1]]), np.concatenate([nr[:, 1], nr[:, 0]])
+                key = np.sort(na * m + rank[nb])
+            row_a = key // m
+            nb_ids = ids_all[by_id[key - row_a * m]].tolist()
+            offs = np.searchsorted(row_a, np.arange(m + 1)).tolist()
+            self._d = {i: tuple(nb_ids[offs[r]:offs[r + 1]]) for r, i in zip(rows.tolist(), ids_all[rows].tolist())}
         return self._d
 
     def __getitem__(self, key):
@@ -163,15 +177,6 @@ class GpuDetector:
         if self._n_alive < 2:
             return ids_all, alive_all, None, None
         rmax = max(cfg.r_collide[g.type_id] for g, c in zip(groups, counts_alive) if c)
-        reach = max(cfg.r_sense, 2.0 * float(rmax))
-        d_max = int(math.ceil(reach / cfg.cell))
-        okey = (d_max, reach, cfg.cell)
-        if self._offs_key != okey:
-            self._offs_key = okey
-            self._offs = half_space_offsets(d_max, reach, cfg.cell).astype(np.int32)
-            self._offs_d = (torch.from_numpy(self._offs.reshape(-1)).to(self.device) if self._offs.size
-                            else torch.zeros(3, dtype=torch.int32, device=self.device))
-        offs, offs_d = self._offs, self._offs_d
         m = int(ids_all.shape[0])
         stream = torch.cuda.current_stream(self.device)
         with torch.cuda.device(self.device):
@@ -182,6 +187,25 @@ class GpuDetector:
                 _lib.check(self._lib.swarmstep_pack_collision(g._view_ref, float(cfg.r_collide[g.type_id]),
                                                               xyzr.data_ptr(), off, ctypes.c_void_p(stream.cuda_stream)))
                 off += g.n
+        coll_h, near = self._pairs_xyzr(xyzr, float(rmax))
+        return ids_all, alive_all, coll_h, near
+
+    def _pairs_xyzr(self, xyzr: torch.Tensor, rmax: float):
+        """Broad + narrow phase over packed (m, 4) float64 rows (x, y, z, radius;
+        NaN radius = dead): (colliding row pairs numpy, neighbour row pairs device)."""
+        cfg = self.config
+        reach = max(cfg.r_sense, 2.0 * rmax)
+        d_max = int(math.ceil(reach / cfg.cell))
+        okey = (d_max, reach, cfg.cell)
+        if self._offs_key != okey:
+            self._offs_key = okey
+            self._offs = half_space_offsets(d_max, reach, cfg.cell).astype(np.int32)
+            self._offs_d = (torch.from_numpy(self._offs.reshape(-1)).to(self.device) if self._offs.size
+                            else torch.zeros(3, dtype=torch.int32, device=self.device))
+        offs, offs_d = self._offs, self._offs_d
+        m = int(xyzr.shape[0])
+        stream = torch.cuda.current_stream(self.device)
+        with torch.cuda.device(self.device):
             nbytes = ctypes.c_uint64()
             _lib.check(self._lib.swarmstep_collision_workspace_bytes(m, ctypes.byref(nbytes)))
             ws = torch.empty(int(nbytes.value), dtype=torch.uint8, device=self.device)
@@ -202,7 +226,76 @@ class GpuDetector:
             if n_coll or n_near:
                 run(coll.data_ptr(), n_coll, near.data_ptr(), n_near, 1)
             coll_h = coll[:2 * n_coll].cpu().numpy().astype(np.int64).reshape(-1, 2)
-        return ids_all, alive_all, coll_h, near[:2 * n_near]
+        return coll_h, near[:2 * n_near]
+
+    def detect_snapshot(self, snapshot, dropped: int = 0) -> CollisionReport:
+        """``swarmstep.collision.detect(snapshot, config, dropped)``
+        (collision.py:110-176) on the GPU for a host ``WorldSnapshot`` of any
+        groups (the out-of-loop detector's input): same validation, same
+        report.  The float64 positions are uploaded as they are."""
+        cfg = self.config
+        ids, pos, rad, alive = [], [], [], []
+        for b in snapshot.batches:                    # collision.py:66-80
+            if b.tick != snapshot.tick:
+                raise ValidationError("snapshot sections disagree on tick")
+            if b.type_id not in cfg.r_collide:
+                raise ValidationError(f"no collision radius configured for type {b.type_id}")
+            ids.append(np.asarray(b.agent_ids).astype(np.int64))
+            pos.append(np.asarray(b.pos, dtype=np.float64).reshape(-1, 3))
+            live = np.asarray(b.alive, dtype=bool)
+            alive.append(live)
+            rad.append(np.where(live, float(cfg.r_collide[b.type_id]), np.nan))
+        ids_all = np.concatenate(ids) if ids else np.empty(0, np.int64)
+        alive_all = np.concatenate(alive) if alive else np.empty(0, bool)
+        n_alive = int(alive_all.sum())
+        if n_alive < 2:
+            return CollisionReport(tick=snapshot.tick, collisions=(),
+                                   neighbor_sets={int(i): () for i in ids_all[alive_all]}, dropped=dropped)
+        rmax = max(float(cfg.r_collide[b.type_id]) for b, a in zip(snapshot.batches, alive) if a.any())
+        host = np.empty((ids_all.shape[0], 4))
+        host[:, :3] = np.concatenate(pos)
+        host[:, 3] = np.concatenate(rad)
+        xyzr = torch.from_numpy(host).to(self.device)
+        coll_h, near = self._pairs_xyzr(xyzr, rmax)
+        self._n_alive = n_alive
+        src, dst = coll_h[:, 0], coll_h[:, 1]
+        ids_a = np.minimum(ids_all[src], ids_all[dst])
+        ids_b = np.maximum(ids_all[src], ids_all[dst])
+        order = np.lexsort((ids_b, ids_a))
+        collisions = tuple(zip(ids_a[order].tolist(), ids_b[order].tolist()))
+        return CollisionReport(tick=snapshot.tick, collisions=collisions,
+                               neighbor_sets=NeighborSets(alive_all, ids_all, near, n_alive), dropped=dropped)
+
+
+def run_detector(in_q, out_q, config: CollisionConfig, device=None) -> None:
+    """The out-of-loop detector task (collision.py:179-215) on the GPU: consume
+    tick-ordered WorldSnapshots, emit one report per consumed snapshot, jump to
+    the newest pending snapshot when behind (skips counted in the next
+    report's ``dropped``), echo the ``None`` sentinel downstream."""
+    import queue
+    det = GpuDetector(config, device)
+    try:
+        pending_drops = 0
+        closing = False
+        item = in_q.get()
+        while item is not None:
+            out_q.put(det.detect_snapshot(item, dropped=pending_drops))
+            pending_drops = 0
+            if closing:
+                break
+            item = in_q.get()
+            while item is not None:
+                try:
+                    nxt = in_q.get_nowait()
+                except queue.Empty:
+                    break
+                if nxt is None:
+                    closing = True
+                    break
+                item = nxt
+                pending_drops += 1
+    finally:
+        out_q.put(None)
 
 
 def detect(groups, config: CollisionConfig, tick: int, dropped: int = 0) -> CollisionReport:

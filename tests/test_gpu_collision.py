@@ -95,3 +95,65 @@ def test_degenerate_worlds():
     g = _group(0, np.array([[0.0, 0.0, 5.0], [0.5, 0.0, 5.0], [0.25, 0.0, 5.0]]), np.array([True, False, True]), 0)
     rep = detect([g], cfg, tick=0)
     assert rep.collisions == ((0, 2),) and rep.neighbor_sets == {0: (2,), 2: (0,)}
+
+
+def _snapshot(z, w, tick):
+    from paper_2308_12698_b200.state import BatchSnapshot, WorldSnapshot
+    p0, p1, a0, a1, cfgv, coll, nb = _world(z, w)
+    bs = [BatchSnapshot(tick=tick, type_id=0, agent_ids=np.arange(p0.shape[0], dtype=np.uint64), pos=p0,
+                        vel=np.zeros_like(p0), quat=np.tile([1.0, 0, 0, 0], (p0.shape[0], 1)),
+                        omega=np.zeros_like(p0), alive=a0)]
+    if p1.shape[0]:
+        n0 = p0.shape[0]
+        bs.append(BatchSnapshot(tick=tick, type_id=1, agent_ids=np.arange(n0, n0 + p1.shape[0], dtype=np.uint64),
+                                pos=p1, vel=np.zeros_like(p1), quat=np.tile([1.0, 0, 0, 0], (p1.shape[0], 1)),
+                                omega=np.zeros_like(p1), alive=a1))
+    return WorldSnapshot(tick=tick, batches=tuple(bs)), cfgv, coll, nb
+
+
+def test_snapshot_detector_matches_reference_detect_golden():
+    """GpuDetector.detect_snapshot: the reference's detect(snapshot, config)
+    signature (the out-of-loop detector's input, any groups) on the GPU."""
+    from paper_2308_12698_b200.collision import CollisionConfig, GpuDetector
+    z = dict(np.load(GOLDEN / "collision.npz"))
+    for w in range(int(z["worlds"])):
+        snap, (r0, r1, r_sense, cell), coll, nb = _snapshot(z, w, tick=w)
+        cfg = CollisionConfig(r_collide={0: r0, 1: r1}, r_sense=r_sense, cell=cell)
+        rep = GpuDetector(cfg, "cuda:0").detect_snapshot(snap, dropped=3)
+        assert rep.tick == w and rep.dropped == 3
+        assert rep.collisions == coll, w
+        assert rep.neighbor_sets == nb, w
+
+
+def test_snapshot_detector_validation_and_run_detector_semantics():
+    """collision.py:66-80 validation and run_detector's jump-to-newest /
+    dropped counting / sentinel echo (collision.py:179-215, test_collision.py:
+    140-175)."""
+    import dataclasses
+    import queue
+
+    from paper_2308_12698_b200.collision import CollisionConfig, GpuDetector, run_detector
+    from paper_2308_12698_b200.errors import ValidationError
+    from paper_2308_12698_b200.state import WorldSnapshot
+    z = dict(np.load(GOLDEN / "collision.npz"))
+    snap, (r0, r1, r_sense, cell), coll, nb = _snapshot(z, 0, tick=4)
+    cfg = CollisionConfig(r_collide={0: r0, 1: r1}, r_sense=r_sense, cell=cell)
+    det = GpuDetector(cfg, "cuda:0")
+    bad = WorldSnapshot(tick=5, batches=snap.batches)
+    with pytest.raises(ValidationError):
+        det.detect_snapshot(bad)                                  # sections disagree on tick
+    with pytest.raises(ValidationError):
+        GpuDetector(CollisionConfig(r_collide={0: r0}, r_sense=r_sense, cell=cell), "cuda:0").detect_snapshot(
+            WorldSnapshot(tick=4, batches=tuple(dataclasses.replace(b, type_id=7) for b in snap.batches[:1])))
+    in_q, out_q = queue.Queue(), queue.Queue()
+    snaps = [WorldSnapshot(tick=t, batches=tuple(dataclasses.replace(b, tick=t) for b in snap.batches))
+             for t in range(3)]
+    for s in snaps:
+        in_q.put(s)
+    in_q.put(None)
+    run_detector(in_q, out_q, cfg, "cuda:0")
+    reports = []
+    while (r := out_q.get_nowait()) is not None:
+        reports.append(r)
+    assert [r.tick for r in reports] == [0, 2] and [r.dropped for r in reports] == [0, 1]
+    assert all(r.collisions == coll for r in reports)

@@ -148,3 +148,29 @@ def test_oracle_rows_are_independent(n, seed):
         full.step(1e-3)
         sub.step(1e-3)
     np.testing.assert_array_equal(full.state13()[rows], sub.state13())
+
+
+def test_neighbor_sets_from_pair_list():
+    """NeighborSets (the report's lazy neighbor_sets) equals the reference's
+    dict construction (collision.py:166-175): alive ids in batch order, each
+    with its sorted neighbour ids; dead agents absent."""
+    from paper_2308_12698_b200.collision import NeighborSets
+    rng = np.random.default_rng(0)
+    m = 500
+    ids = rng.permutation(10_000)[:m].astype(np.int64)
+    alive = rng.random(m) > 0.2
+    pairs = set()
+    while len(pairs) < 2000:
+        a, b = rng.integers(0, m, 2)
+        if a != b and alive[a] and alive[b]:
+            pairs.add((min(a, b), max(a, b)))
+    near = np.array(sorted(pairs))
+    want = {int(i): [] for i in ids[alive]}
+    for a, b in near:
+        want[int(ids[a])].append(int(ids[b]))
+        want[int(ids[b])].append(int(ids[a]))
+    want = {k: tuple(sorted(v)) for k, v in want.items()}
+    ns = NeighborSets(alive, ids, near)
+    assert len(ns) == len(want)
+    assert dict(ns) == want and list(ns) == list(want)
+    assert dict(NeighborSets(alive, ids, np.empty((0, 2), np.int64))) == {k: () for k in want}

@@ -6,7 +6,8 @@ Agents uniformly at ~1 per 8 m^3 (the cfg5 density), r_collide 0.15 m,
 r_sense 2 m, cell 2 m.  Prints one JSON line: wall time of GpuDetector.detect returning the
 collisions (neighbour sets left on the device until read -- the in-loop
 collision-death use, core.py:495-498), and with the reference's per-agent
-neighbor_sets dict materialised.
+neighbor_sets dict materialised, and the out-of-loop form (detect_snapshot on a host
+WorldSnapshot, upload included).
 With --reference (build container only) it times the reference's own
 collision.detect (numpy) on the same positions instead.
 """
@@ -65,8 +66,17 @@ def main():
         rep = det.detect([g], 0)
         n_neigh = sum(len(v) for v in rep.neighbor_sets.values())   # materialise the reference's dict
     full_ms = (time.perf_counter() - t0) / reps * 1e3
+    # out-of-loop form: detect(snapshot, config) on a host WorldSnapshot (float64 upload included)
+    from paper_2308_12698_b200.state import WorldSnapshot, batch_snapshot
+    snap = WorldSnapshot(tick=0, batches=(batch_snapshot(g.batch, 0),))
+    rep_s = det.detect_snapshot(snap)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        rep_s = det.detect_snapshot(snap)
+    snap_ms = (time.perf_counter() - t0) / reps * 1e3
+    assert rep_s.collisions == rep.collisions
     print(json.dumps({"impl": "b200", "agents": n, "detect_ms": detect_ms, "detect_with_neighbor_sets_ms": full_ms,
-                      "collisions": len(rep.collisions), "neighbor_entries": n_neigh}))
+                      "detect_snapshot_ms": snap_ms, "collisions": len(rep.collisions), "neighbor_entries": n_neigh}))
 
 
 if __name__ == "__main__":
