@@ -137,3 +137,22 @@ def test_shard_wire_section_equals_single_group():
     m.step(1e-3)
     one.step(1e-3)
     assert snapshot_frame(1, [m]) == snapshot_frame(1, [one])
+
+
+def test_subscriber_error_surfaces_and_slots_recover():
+    from paper_2308_12698_b200.publish import FramePublisher
+    a, _ = _twins(300, 9)
+    calls = []
+
+    def bad(frame):
+        calls.append(len(frame))
+        raise OSError("socket closed")
+    pub = FramePublisher([a], [bad], slots=1)
+    a.step(1e-3)
+    pub.publish(0)
+    with pytest.raises(RuntimeError):
+        pub.flush()
+    with pytest.raises(RuntimeError):
+        pub.publish(1)
+    pub.close()
+    assert calls == [13 + 6 + 61 * 300]
