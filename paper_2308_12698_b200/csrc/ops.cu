@@ -221,7 +221,7 @@ int swarmstep_op_rk4(int64_t n, float *pos, float *pos_lo, float *vel, float *qu
     if (!(dt > 0.0f)) return bad("dt must be positive");
     if (n == 0) return SWARMSTEP_OK;
     if (!pos || !vel || !quat || !omega || !alive || !f_c || !tau || !fault) return bad("null argument");
-    const ssb::Derived D = ssb::derive(*p, 1.0f / dt);
+    const ssb::Derived D = ssb::derive(*p, dt);
     if (pos_lo)
         op_rk4_kernel<true><<<blocks(n), kT, 0, (cudaStream_t)stream>>>(n, pos, pos_lo, vel, quat, omega, alive,
                                                                        f_c, tau, *p, D, dt, fault);

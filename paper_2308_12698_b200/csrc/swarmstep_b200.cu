@@ -1051,7 +1051,7 @@ int swarmstep_quad_step(const swarmstep_group_view *g, const swarmstep_quad_para
     if (k_substeps < 1) return set_err(SWARMSTEP_EINVAL, "k_substeps must be >= 1");
     if (!g->counters) return set_err(SWARMSTEP_EINVAL, "null counters");
     if (g->n == 0) return SWARMSTEP_OK;
-    const ssb::Derived D = ssb::derive(*p, 1.0f / dt);
+    const ssb::Derived D = ssb::derive(*p, dt);
     const int overlay = launch_flags & SWARMSTEP_STEP_OVERLAY;
     const int motor = (launch_flags & SWARMSTEP_STEP_MOTOR) ? 1 : 0;
     const bool use_tma = (launch_flags & SWARMSTEP_STEP_FORCE_DIRECT) ? false
@@ -1109,7 +1109,7 @@ int swarmstep_quad_step_lag(const swarmstep_group_view *g, const swarmstep_quad_
     if (!g->counters) return set_err(SWARMSTEP_EINVAL, "null counters");
     if ((reinterpret_cast<uintptr_t>(motor) & 15u) != 0) return set_err(SWARMSTEP_EINVAL, "motor must be 16-byte aligned");
     if (g->n == 0) return SWARMSTEP_OK;
-    const ssb::Derived D = ssb::derive(*p, 1.0f / dt);
+    const ssb::Derived D = ssb::derive(*p, dt);
     const float phi = (float)(-((double)tau_m / (double)dt) * expm1(-(double)dt / (double)tau_m));
     const float e_full = (float)exp(-(double)dt / (double)tau_m);
     const int overlay = launch_flags & SWARMSTEP_STEP_OVERLAY;
@@ -1142,7 +1142,7 @@ int swarmstep_quad_step_circle(const swarmstep_group_view *g, const swarmstep_qu
     if (k_substeps < 1) return set_err(SWARMSTEP_EINVAL, "k_substeps must be >= 1");
     if (!g->counters) return set_err(SWARMSTEP_EINVAL, "null counters");
     if (g->n == 0) return SWARMSTEP_OK;
-    const ssb::Derived D = ssb::derive(*p, 1.0f / dt);
+    const ssb::Derived D = ssb::derive(*p, dt);
     const int64_t fcap = g->fault_log ? g->fault_cap : 0;
     if (!(launch_flags & SWARMSTEP_STEP_FORCE_DIRECT) &&
         ((launch_flags & SWARMSTEP_STEP_FORCE_PAIR) || k_substeps >= SSB_PAIR_MIN_K)) {
