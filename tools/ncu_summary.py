@@ -51,9 +51,10 @@ def main():
                     return float(r[hdr.index(k)].replace(",", "")) * scale
                 except (ValueError, IndexError):
                     return None
-            unit = units[hdr.index("dram__bytes_read.sum")]
-            sc = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
-            rd, wr = num("dram__bytes_read.sum", sc), num("dram__bytes_write.sum", sc)
+            def scale(k):   # each metric carries its own unit
+                return {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(units[hdr.index(k)], 1)
+            rd = num("dram__bytes_read.sum", scale("dram__bytes_read.sum"))
+            wr = num("dram__bytes_write.sum", scale("dram__bytes_write.sum"))
             if rd is not None and wr is not None:
                 d["dram_bytes_per_agent"] = (rd + wr) / agents
         kernels.append(d)
