@@ -164,6 +164,14 @@ int swarmstep_quad_step(const swarmstep_group_view *g, const swarmstep_quad_para
                         float dt, int k_substeps, int launch_flags, uint32_t tick_base,
                         const int64_t *tick_dev, void *stream);
 
+/* The synchronous World tick in one call: swarmstep_quad_step(..., tick_dev =
+ * NULL, ...), then the four counters copied to counters_host (pinned host
+ * memory) and the stream synchronised.  counters_host[0] is the fault-log
+ * count after the launch (QuadGroup.step returns the ids, core.py:166-202). */
+int swarmstep_quad_step_collect(const swarmstep_group_view *g, const swarmstep_quad_params *p,
+                                float dt, int k_substeps, int launch_flags, uint32_t tick_base,
+                                uint32_t *counters_host, void *stream);
+
 /* swarmstep_quad_step with the device circle strategy evaluated per tick
  * inside the kernel (circle_swarm_strategy client.py:55-73 -> circle_reference
  * control.py:297-315, as swarmstep_quad_circle_setpoints computes it): tick k

@@ -1095,6 +1095,22 @@ int swarmstep_quad_step(const swarmstep_group_view *g, const swarmstep_quad_para
     return cuda_status("quad_step_kernel");
 }
 
+int swarmstep_quad_step_collect(const swarmstep_group_view *g, const swarmstep_quad_params *p, float dt,
+                                int k_substeps, int launch_flags, uint32_t tick_base, uint32_t *counters_host,
+                                void *stream)
+{
+    // the World-facing synchronous tick in one call: launch, fault counter to
+    // pinned host memory, wait (three host API calls, one crossing of the FFI)
+    int st = swarmstep_quad_step(g, p, dt, k_substeps, launch_flags, tick_base, nullptr, stream);
+    if (st) return st;
+    if (!counters_host) return set_err(SWARMSTEP_EINVAL, "null counters_host");
+    if (cudaMemcpyAsync(counters_host, g->counters, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                        (cudaStream_t)stream) != cudaSuccess)
+        return cuda_status("cudaMemcpyAsync");
+    if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return cuda_status("cudaStreamSynchronize");
+    return cuda_status("quad step");
+}
+
 int swarmstep_quad_step_lag(const swarmstep_group_view *g, const swarmstep_quad_params *p, float *motor,
                             float tau_m, float dt, int k_substeps, int launch_flags, uint32_t tick_base,
                             const int64_t *tick_dev, void *stream)

@@ -150,6 +150,8 @@ class B200QuadGroup:
                     self._motor = torch.full((self.ntiles, 4, TILE), self.params.hover_thrust / 4.0,
                                              dtype=torch.float32, device=self.device)
             self._counters_host = torch.zeros(4, dtype=torch.int32, pin_memory=True)
+        self._counters_np = self._counters_host.numpy()          # same pinned memory, cheap reads
+        self._counters_host_ptr = ctypes.c_void_p(self._counters_host.data_ptr())
         self._view = GroupView(n=n, stride=self.stride, cols=_ptr(self._cols), flags=_ptr(self._flags),
                                counters=_ptr(self._counters), fault_log=_ptr(self._fault_log),
                                fault_cap=self._fault_cap, compensated=int(self.compensated))
@@ -471,7 +473,7 @@ class B200QuadGroup:
             _lib.check(self._lib.swarmstep_memcpy_async(self._counters_host.data_ptr(), self._counters.data_ptr(),
                                                         self._counters.numel() * 4, self._stream_h))
         self._sync()
-        if int(self._counters_host[2]) == 0:
+        if int(self._counters_np[2]) == 0:
             return False
         if not np.isfinite(gain):
             self._overlay_poison = True
@@ -639,8 +641,11 @@ class B200QuadGroup:
         """Wait for the launches since the last call; fault ids per tick, in row order."""
         self._sync()
         launched, self._launched = self._launched, []
-        ticks = [t0 + j for t0, k in launched for j in range(k)]
-        count = int(self._counters_host[0])
+        return self._faults_for([t0 + j for t0, k in launched for j in range(k)])
+
+    def _faults_for(self, ticks) -> list[np.ndarray]:
+        """Fault ids per tick from the fault log (the counters are on the host)."""
+        count = int(self._counters_np[0])
         if count == self._fault_seen:
             return [np.empty(0, dtype=np.uint64) for _ in ticks]
         if count > self._fault_cap:
@@ -662,9 +667,25 @@ class B200QuadGroup:
         per = self.collect_faults()
         return np.concatenate(per) if len(per) > 1 else per[0]
 
+    _fast_step = True   # the single-call synchronous tick below applies to this class
+
     def step(self, dt: float) -> np.ndarray:
         """Advance one tick in place; returns fault ids (core.py:166-202)."""
-        return self.step_k(dt, 1)
+        if (not self._fast_step or self._launched or self._pending or self._motor is not None
+                or self._nonfinite_rows or self._overlay_poison or not dt > 0.0):
+            return self.step_k(dt, 1)
+        # the World's per-tick call: launch + fault counter readback + wait in
+        # one FFI crossing (swarmstep_quad_step_collect)
+        self._call(self._lib.swarmstep_quad_step_collect, self._params_ref, ctypes.c_float(dt), 1,
+                   self._launch_flags(), ctypes.c_uint32(self._tick & 0xFFFFFF), self._counters_host_ptr,
+                   self._stream_h)
+        self._overlay_reset()
+        tick = self._tick
+        self._tick += 1
+        self._state_stale = True
+        if int(self._counters_np[0]) == self._fault_seen:
+            return np.empty(0, dtype=np.uint64)
+        return self._faults_for([tick])[0]
 
     # -------------------------------------------------------------- extras
     def alive_count(self) -> int:

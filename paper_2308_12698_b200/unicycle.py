@@ -38,6 +38,7 @@ class B200UnicycleGroup(B200QuadGroup):
     """One unicycle type (drop-in for swarmstep.core.UnicycleGroup)."""
 
     kind = "unicycle"
+    _fast_step = False   # step() goes through this class's step_async
 
     def __init__(self, type_id: int, batch, params: UnicycleParams | None = None, *, device=None):
         super().__init__(type_id, batch, device=device, compensated=True)
