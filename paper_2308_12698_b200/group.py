@@ -173,6 +173,7 @@ class B200QuadGroup:
         self._row = {int(a): i for i, a in enumerate(self._batch.agent_ids)}
         self._ids_dev = None             # device copy of agent_ids (wire packing), on demand
         self._wire_bufs = None           # wire_section's device / pinned buffers, on demand
+        self._pull_bufs = None           # _pull_state's device staging, on demand
         self._alive = self._batch.alive  # exact: changes only via mark_dead / faults
         self._batch_view = DeviceBatchView(self)
         self._state_stale = False        # device state newer than the host mirror
@@ -271,20 +272,30 @@ class B200QuadGroup:
             return
         n = self.n
         b = self._batch
-        with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
-            buf = torch.empty(n * 13, dtype=torch.float64, device=self.device)
-            alive = torch.empty(n, dtype=torch.uint8, device=self.device)
-            p = _ptr(buf)
-            self._call(self._lib.swarmstep_quad_pack_f64, p, p + n * 3 * 8, p + n * 6 * 8, p + n * 10 * 8,
-                       _ptr(alive), ctypes.c_void_p(self.stream.cuda_stream))
-            host = buf.cpu().numpy()
-            alive_h = alive.cpu().numpy()
-        b.pos[:] = host[: n * 3].reshape(n, 3)
-        b.vel[:] = host[n * 3: n * 6].reshape(n, 3)
-        b.quat[:] = host[n * 6: n * 10].reshape(n, 4)
-        b.omega[:] = host[n * 10:].reshape(n, 3)
-        b.alive[:] = alive_h.astype(bool)
+        if self._pull_bufs is None:     # device staging for the float64 pack, reused
+            with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
+                self._pull_bufs = (torch.empty(n * 13, dtype=torch.float64, device=self.device),
+                                   torch.empty(n, dtype=torch.uint8, device=self.device))
+        buf, alive = self._pull_bufs
+        p = _ptr(buf)
+        self._call(self._lib.swarmstep_quad_pack_f64, p, p + n * 3 * 8, p + n * 6 * 8, p + n * 10 * 8,
+                   _ptr(alive), self._stream_h)
+        # straight into the mirror arrays (no intermediate host buffer); a
+        # mirror array that is not a plain contiguous buffer goes via a copy
+        for col, off, width in ((b.pos, 0, 3), (b.vel, 3, 3), (b.quat, 6, 4), (b.omega, 10, 3)):
+            self._d2h(col, p + off * n * 8, width * n * 8)
+        self._d2h(b.alive, _ptr(alive), n)
+        self._sync()
         self._state_stale = False
+
+    def _d2h(self, dst: np.ndarray, src: int, nbytes: int) -> None:
+        if dst.flags.c_contiguous and dst.flags.writeable and dst.nbytes == nbytes:
+            _lib.check(self._lib.swarmstep_memcpy_async(dst.ctypes.data, src, nbytes, self._stream_h))
+        else:
+            tmp = np.empty(dst.shape, dtype=dst.dtype)
+            _lib.check(self._lib.swarmstep_memcpy_async(tmp.ctypes.data, src, nbytes, self._stream_h))
+            self._sync()
+            dst[...] = tmp
 
     def _pull_commands(self) -> None:
         if not self._cmd_stale:
