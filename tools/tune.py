@@ -18,6 +18,7 @@ VARIANTS = {
     "default": [],
     "p6": ["-DSSB_PAIR_MINB=6"],
     "p7": ["-DSSB_PAIR_MINB=7"],
+    "p9": ["-DSSB_PAIR_MINB=9"],
 }
 
 CHILD = r'''
