@@ -21,6 +21,7 @@ device; use ``push_host_state()`` after editing them.
 from __future__ import annotations
 
 import ctypes
+import math
 from typing import Iterable
 
 import numpy as np
@@ -37,6 +38,7 @@ from .params import (default_outer_gains, default_quad_params, default_rate_gain
 from .state import AgentBatch, batch_snapshot, quat_yaw
 
 _ROW_ALIGN = TILE  # row capacity is a whole number of 128-agent tiles
+_ZEROS = (0.0,) * 7
 
 
 def _round_up(x: int, m: int) -> int:
@@ -314,12 +316,11 @@ class B200QuadGroup:
     def _flush_commands(self) -> None:
         if not self._pending:
             return
-        rows = np.fromiter(self._pending.keys(), dtype=np.int64, count=len(self._pending))
-        levels = np.empty(rows.shape[0], dtype=np.uint8)
-        vals = np.empty((rows.shape[0], 7), dtype=np.float32)
-        for i, (lvl, v) in enumerate(self._pending.values()):
-            levels[i] = lvl
-            vals[i] = v          # float64 -> float32
+        count = len(self._pending)
+        rows = np.fromiter(self._pending.keys(), dtype=np.int64, count=count)
+        pend = list(self._pending.values())
+        levels = np.fromiter((lvl for lvl, _ in pend), dtype=np.uint8, count=count)
+        vals = np.array([v for _, v in pend], dtype=np.float32).reshape(count, 7)   # float64 -> float32
         self._pending.clear()
         with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
             d_rows = torch.from_numpy(rows).to(self.device)
@@ -357,19 +358,21 @@ class B200QuadGroup:
         lvl = level_code(cmd.level)
         if lvl is None:
             return False
-        vals = np.asarray(cmd.values, dtype=float).ravel()
         want = 7 if lvl == LEVEL_POS else 4
-        if vals.shape[0] != want:
-            raise ValidationError(f"level takes {want} values, got {vals.shape[0]}")
+        try:      # the common case, a flat tuple of numbers: plain Python floats
+            vals = tuple(map(float, cmd.values))
+        except TypeError:
+            vals = tuple(np.asarray(cmd.values, dtype=float).ravel().tolist())
+        if len(vals) != want:
+            raise ValidationError(f"level takes {want} values, got {len(vals)}")
         # no device read: the row goes to the (possibly stale) host mirror and
         # the pending queue, which _pull_commands re-applies over the device copy
-        full = np.zeros(7)
-        full[:want] = vals
+        full = vals + _ZEROS[:7 - want]
         self._cmd_level[row] = lvl
         self._cmd_values[row] = full
         if lvl == LEVEL_MOTOR:
             self._motor_possible = True
-        if np.all(np.isfinite(full)):
+        if all(map(math.isfinite, full)):
             self._nonfinite_rows.discard(row)
         else:
             self._nonfinite_rows.add(row)
