@@ -39,6 +39,7 @@ from .state import AgentBatch, batch_snapshot, quat_yaw
 
 _ROW_ALIGN = TILE  # row capacity is a whole number of 128-agent tiles
 _ZEROS = (0.0,) * 7
+_PINNED_MIRROR_MAX = 8_000_000   # agents: 0.83 GB of pinned float64 mirror
 
 
 def _round_up(x: int, m: int) -> int:
@@ -162,16 +163,15 @@ class B200QuadGroup:
         self._stream_h = ctypes.c_void_p(self.stream.cuda_stream)
         self._params_ref = ctypes.byref(self._dparams)
 
-        # host mirrors (the reference's numpy columns)
-        self._batch = AgentBatch(
-            type_id=int(getattr(batch, "type_id", type_id)),
-            agent_ids=np.array(batch.agent_ids, dtype=np.uint64),
-            pos=np.array(batch.pos, dtype=float).reshape(n, 3),
-            vel=np.array(batch.vel, dtype=float).reshape(n, 3),
-            quat=np.array(batch.quat, dtype=float).reshape(n, 4),
-            omega=np.array(batch.omega, dtype=float).reshape(n, 3),
-            alive=np.array(batch.alive, dtype=bool).reshape(n),
-        )
+        # host mirrors (the reference's numpy columns); up to _PINNED_MIRROR_MAX
+        # agents they live in pinned memory, so a state pull is one DMA per column
+        cols = self._mirror_columns(n)
+        for name, width, src in (("pos", 3, batch.pos), ("vel", 3, batch.vel), ("quat", 4, batch.quat),
+                                 ("omega", 3, batch.omega)):
+            cols[name][...] = np.asarray(src, dtype=float).reshape(n, width)
+        cols["alive"][...] = np.asarray(batch.alive, dtype=bool).reshape(n)
+        self._batch = AgentBatch(type_id=int(getattr(batch, "type_id", type_id)),
+                                 agent_ids=np.array(batch.agent_ids, dtype=np.uint64), **cols)
         self._row = {int(a): i for i, a in enumerate(self._batch.agent_ids)}
         self._ids_dev = None             # device copy of agent_ids (wire packing), on demand
         self._wire_bufs = None           # wire_section's device / pinned buffers, on demand
@@ -202,6 +202,25 @@ class B200QuadGroup:
         self.push_host_state(upload_commands=True)
 
     # ------------------------------------------------------------------ utils
+    def _mirror_columns(self, n: int) -> dict:
+        """Float64 pos / vel / quat / omega and bool alive host columns, laid out
+        as the device pack writes them; pinned when small enough (else pageable)."""
+        f64 = alive = None
+        self._mirror_pinned = None
+        if n <= _PINNED_MIRROR_MAX:
+            try:
+                self._mirror_pinned = (torch.empty(13 * n, dtype=torch.float64, pin_memory=True),
+                                       torch.empty(n, dtype=torch.uint8, pin_memory=True))
+                f64 = self._mirror_pinned[0].numpy()
+                alive = self._mirror_pinned[1].numpy().view(np.bool_)
+            except RuntimeError:      # pinned memory exhausted: pageable mirror
+                self._mirror_pinned = None
+                f64 = None
+        if f64 is None:
+            f64, alive = np.empty(13 * n), np.empty(n, dtype=bool)
+        return dict(pos=f64[:3 * n].reshape(n, 3), vel=f64[3 * n:6 * n].reshape(n, 3),
+                    quat=f64[6 * n:10 * n].reshape(n, 4), omega=f64[10 * n:].reshape(n, 3), alive=alive)
+
     def _call(self, fn, *args) -> None:
         # the device guard costs more than the launch itself on the per-tick
         # path: only switch when the caller's current device differs
