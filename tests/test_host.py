@@ -174,3 +174,50 @@ def test_neighbor_sets_from_pair_list():
     assert len(ns) == len(want)
     assert dict(ns) == want and list(ns) == list(want)
     assert dict(NeighborSets(alive, ids, np.empty((0, 2), np.int64))) == {k: () for k in want}
+
+
+def test_frame_layout_places_every_shard_block():
+    """publish.frame_layout: copying each part's packed columns to the offsets
+    it gives reproduces the SnapshotMsg frame built from whole sections
+    (wire.py:162-178), for random types, shard splits and empty types."""
+    import struct
+
+    from paper_2308_12698_b200.publish import _BLOCKS, frame_layout
+    from paper_2308_12698_b200.wire import MSG_SNAPSHOT, encode_frame
+    rng = np.random.default_rng(3)
+
+    class Part:
+        def __init__(self, n):
+            self.n = n
+
+    for _ in range(50):
+        types = []
+        for t in sorted(rng.choice(20, size=int(rng.integers(1, 4)), replace=False)):
+            parts = [Part(int(rng.integers(1, 9))) for _ in range(int(rng.integers(1, 4)))]
+            types.append((int(t), parts))
+        used = {t for t, _ in types}
+        empty = [int(t) for t in rng.choice(20, size=2, replace=False) if int(t) not in used]
+        length, headers, copies = frame_layout(types, empty)
+        frame = np.zeros(length, dtype=np.uint8)
+        hdr = struct.pack("<IBQ", length - 4, MSG_SNAPSHOT, 7)
+        frame[:13] = np.frombuffer(hdr, dtype=np.uint8)
+        for off, b in headers:
+            frame[off:off + len(b)] = np.frombuffer(b, dtype=np.uint8)
+        sections = []
+        for t, parts in types:
+            # per part: its own packed columns (block w of the part is w * n bytes)
+            packed = [rng.integers(0, 256, 61 * p.n, dtype=np.uint8) for p in parts]
+            for p, buf in zip(parts, packed):
+                for src, dst, nb in copies[id(p)]:
+                    frame[dst:dst + nb] = buf[src:src + nb]
+            # the whole-type section: each column block concatenated across parts
+            body, offs = [], [0] * len(parts)
+            for w in _BLOCKS:
+                for k, (p, buf) in enumerate(zip(parts, packed)):
+                    body.append(buf[offs[k]:offs[k] + w * p.n].tobytes())
+                    offs[k] += w * p.n
+            sections.append((t, struct.pack("<HI", t, sum(p.n for p in parts)) + b"".join(body)))
+        sections += [(t, struct.pack("<HI", t, 0)) for t in empty]
+        sections.sort(key=lambda s: s[0])
+        want = encode_frame(MSG_SNAPSHOT, struct.pack("<Q", 7) + b"".join(s for _, s in sections))
+        assert frame.tobytes() == want
