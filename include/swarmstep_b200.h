@@ -115,9 +115,14 @@ typedef struct swarmstep_group_view {
 
 /* Library / device info.  Returns SWARMSTEP_ABI_VERSION. */
 int swarmstep_abi_version(void);
+/* Message of the calling thread's last non-zero status: the text of the
+ * exception the reference would raise (errors.py ValidationError /
+ * InvalidStateError; bindings map the status code back to that class). */
 const char *swarmstep_last_error(void);
 /* Loads every kernel of the library on the current device (no side effects);
- * call before capturing launches into a CUDA graph. */
+ * call before capturing launches into a CUDA graph.  Infrastructure, no
+ * reference counterpart (likewise memcpy_async, stream_sync, device_info and
+ * the *_workspace_bytes queries below). */
 int swarmstep_preload(void);
 
 /* Packs the kernel's float32 per-type constants: G and its exact inverse
@@ -216,7 +221,8 @@ int swarmstep_quad_apply_commands(const swarmstep_group_view *g, const int64_t *
 
 /* Bulk device setpoints: every row in [row0, row0+count) gets `level` and
  * values from the plain column block `values` ([7][ld] float32, device), alive
- * rows only.  The device-resident setpoint feed. */
+ * rows only.  Replaces one QuadGroup.apply_command (core.py:117-135) per agent
+ * for whole swarms: the device-resident setpoint feed. */
 int swarmstep_quad_set_setpoints(const swarmstep_group_view *g, int64_t row0, int64_t count,
                                  int level, const float *values, int64_t ld, void *stream);
 
@@ -249,7 +255,8 @@ int swarmstep_quad_viewer_overlay(const swarmstep_group_view *g, const double *p
 int swarmstep_quad_pack_f64(const swarmstep_group_view *g, double *pos, double *vel,
                             double *quat, double *omega, uint8_t *alive, void *stream);
 
-/* Inverse of the above: loads float64 row-major host-layout columns (device
+/* Inverse of the above (the state a group is built from: batch_create,
+ * state.py:143-190): loads float64 row-major host-layout columns (device
  * pointers) into the float32 SoA columns, splitting position into hi + lo
  * when compensated.  Flags: alive from `alive` (u8), has_prev cleared,
  * level left unchanged. */
@@ -304,7 +311,8 @@ int swarmstep_op_outer(int64_t n, const float *pos, const float *pos_lo, const f
 
 /* Packs the alive rows' positions as float4 (x, y, z, 0) -- NaN for dead rows
  * and for padding rows [n, n_out) -- into out_xyzw (device, n_out float4):
- * the per-rank contribution to the NCCL all-gather. */
+ * the per-rank contribution to the NCCL all-gather (the alive-only gather of
+ * collision.py:66-80, by rank). */
 int swarmstep_pack_positions(const swarmstep_group_view *g, float *out_xyzw, int64_t n_out,
                              void *stream);
 
@@ -358,7 +366,8 @@ int swarmstep_quad_circle_setpoints(const swarmstep_group_view *g, const int64_t
                                     int64_t tick_offset, double dt, double radius, double omega,
                                     double z, double phase0, double dphase, void *stream);
 
-/* *tick_dev += delta (one thread; graph-capturable tick counter). */
+/* *tick_dev += delta (one thread; graph-capturable tick counter: the device
+ * copy of SimClock.tick, state.py:24-40). */
 int swarmstep_tick_add(int64_t *tick_dev, int64_t delta, void *stream);
 
 /* ---- device snapshot packing ----------------------------- */
@@ -387,7 +396,8 @@ int swarmstep_quad_pack_wire(const swarmstep_group_view *g, const uint64_t *agen
 /* ---- GPU collision / neighbour detection ----------------- */
 
 /* Gathers a group's rows as float64 (x, y, z, r) into xyzr[offset + row]
- * (r = NaN for dead rows, which the detector skips); position is hi + lo. */
+ * (r = NaN for dead rows, which the detector skips; _gather_alive,
+ * collision.py:66-80); position is hi + lo. */
 int swarmstep_pack_collision(const swarmstep_group_view *g, double radius, double *xyzr, int64_t offset,
                              void *stream);
 
