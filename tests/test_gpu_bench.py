@@ -1,0 +1,36 @@
+"""bench.py's B200 arm at a small size keeps the driver's JSON contract:
+roofline with traffic, cpu_baseline, an end-to-end number with real host
+copies, clocks sampled during the timed region and a launch count."""
+
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+from conftest import cuda_ok
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_ok(), reason="needs CUDA")]
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def test_bench_line_contract():
+    p = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--agents", "200000", "--steps", "4", "--warmup", "3",
+                        "--cpu-seconds", "1"], capture_output=True, text=True, timeout=900, env=dict(os.environ))
+    assert p.returncode == 0, p.stderr[-3000:]
+    d = json.loads(p.stdout.strip().splitlines()[-1])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "clocks",
+                "gpu_launches"):
+        assert key in d, key
+    assert d["n_gpus"] == 1 and d["steps"] == 4 and d["warmup"] == 3 and d["scaling"] == "weak"
+    assert d["value"] > 0 and d["config"]["agents_per_gpu"] == 200000
+    r = d["roofline"]
+    assert r["bound"] in ("fp32", "hbm", "tensor") and 0 < r["frac"] <= 1.0 and r["peak"] > 0
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0 and d["e2e"]["value"] > 0
+    assert d["cpu_baseline"]["cores"] >= 1 and d["cpu_baseline"]["value"] > 0
+    assert d["gpu_launches"] >= d["steps"]
+    assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
