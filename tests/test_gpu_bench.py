@@ -34,3 +34,20 @@ def test_bench_line_contract():
     assert d["cpu_baseline"]["cores"] >= 1 and d["cpu_baseline"]["value"] > 0
     assert d["gpu_launches"] >= d["steps"]
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+
+
+def test_bench_two_rank_plumbing():
+    """The torchrun path (one JSON line from rank 0, whole-job value, max over
+    ranks), exercised with the gloo plumbing backend: both ranks share this
+    GPU, so the number is not a measurement -- only the contract is checked."""
+    env = dict(os.environ, SWARMSTEP_BENCH_BACKEND="gloo")
+    p = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29517", str(ROOT / "bench.py"),
+                        "--gpus", "2", "--agents", "100000", "--steps", "3", "--warmup", "3", "--no-cpu-baseline",
+                        "--no-k1"], capture_output=True, text=True, timeout=900, env=env)
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [ln for ln in p.stdout.strip().splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["agents_total"] == 200000 and d["scaling"] == "weak"
+    assert d["value"] > 0
