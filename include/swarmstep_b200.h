@@ -258,8 +258,8 @@ int swarmstep_quad_pack_f64(const swarmstep_group_view *g, double *pos, double *
 /* Inverse of the above (the state a group is built from: batch_create,
  * state.py:143-190): loads float64 row-major host-layout columns (device
  * pointers) into the float32 SoA columns, splitting position into hi + lo
- * when compensated.  Flags: alive from `alive` (u8), has_prev cleared,
- * level left unchanged. */
+ * when compensated.  Flags: alive from `alive` (u8); has_prev and level
+ * left unchanged (a new group's flags start at 0: no previous sample). */
 int swarmstep_quad_unpack_f64(const swarmstep_group_view *g, const double *pos,
                               const double *vel, const double *quat, const double *omega,
                               const uint8_t *alive, void *stream);

@@ -11,6 +11,8 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <mutex>
+
 #include "swarmstep_b200.h"
 #include "circle.cuh"
 #include "common.cuh"
@@ -929,11 +931,22 @@ __global__ void unpack_f64_kernel(float *cols, uint8_t *flags, int64_t n, int64_
         for (int i = 0; i < 4; i++) cols[ssb::at(SWARMSTEP_COL_QUAT + i, r)] = (float)quat[r * 4 + i];
     if (alive) {
         const uint8_t fl = flags[r];
-        flags[r] = (uint8_t)((fl & SWARMSTEP_LEVEL_MASK) | (alive[r] ? SWARMSTEP_FLAG_ALIVE : 0u));
+        // the PID's has_prev survives a host-state push: the reference never
+        // resets pid_state.has_prev when batch state is edited (control.py:100-114)
+        flags[r] = (uint8_t)((fl & (SWARMSTEP_LEVEL_MASK | SWARMSTEP_FLAG_HAS_PREV)) |
+                             (alive[r] ? SWARMSTEP_FLAG_ALIVE : 0u));
     }
 }
 
 inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 1) / block); }
+
+// TMA kernel launch configuration, per device and per variant
+constexpr int kMaxDevices = 64;
+struct TmaLaunchCfg {
+    int blocks_per_sm, sm_count;
+};
+TmaLaunchCfg g_tma_cfg[kMaxDevices][2];
+std::mutex g_tma_mu;
 
 }  // namespace
 
@@ -1059,21 +1072,30 @@ int swarmstep_quad_step(const swarmstep_group_view *g, const swarmstep_quad_para
                        : k_substeps <= SSB_TMA_MAX_K;
     const int64_t fcap = g->fault_log ? g->fault_cap : 0;
     if (use_tma) {
-        static int blocks_per_sm[2] = {0, 0};
-        static int sm_count = 0;
+        // the > 48 KB dynamic shared memory opt-in is per device and per
+        // kernel: configure once per (device, variant), under a lock
         const size_t smem = sizeof(TmaSmem);
         auto kern = g->compensated ? quad_step_tma_kernel<true> : quad_step_tma_kernel<false>;
         const int ci = g->compensated ? 1 : 0;
-        if (!blocks_per_sm[ci]) {
-            int dev = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev);
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm[ci], kern, SWARMSTEP_TILE, smem);
-            if (blocks_per_sm[ci] < 1) blocks_per_sm[ci] = 1;
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess) return cuda_status("cudaGetDevice");
+        if (dev < 0 || dev >= kMaxDevices) return set_err(SWARMSTEP_EINVAL, "device ordinal out of range");
+        int blocks_per_sm = 0, sm_count = 0;
+        {
+            std::lock_guard<std::mutex> lock(g_tma_mu);
+            TmaLaunchCfg &cfg = g_tma_cfg[dev][ci];
+            if (!cfg.blocks_per_sm) {
+                cudaDeviceGetAttribute(&cfg.sm_count, cudaDevAttrMultiProcessorCount, dev);
+                if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+                    return cuda_status("cudaFuncSetAttribute");
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cfg.blocks_per_sm, kern, SWARMSTEP_TILE, smem);
+                if (cfg.blocks_per_sm < 1) cfg.blocks_per_sm = 1;
+            }
+            blocks_per_sm = cfg.blocks_per_sm;
+            sm_count = cfg.sm_count;
         }
         const int64_t ntiles = (g->n + SWARMSTEP_TILE - 1) / SWARMSTEP_TILE;
-        int64_t grid = (int64_t)sm_count * blocks_per_sm[ci];
+        int64_t grid = (int64_t)sm_count * blocks_per_sm;
         if (grid > ntiles) grid = ntiles;
         kern<<<(unsigned)grid, SWARMSTEP_TILE, smem, (cudaStream_t)stream>>>(
             g->cols, g->flags, ntiles, g->counters, g->fault_log, fcap, overlay, motor, tick_base, tick_dev,

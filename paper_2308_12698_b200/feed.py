@@ -22,7 +22,7 @@ import torch
 
 from . import _lib
 from ._lib import COL_OVERLAY, STEP_OVERLAY
-from .errors import ValidationError
+from .errors import InvalidStateError, ValidationError
 
 
 class CircleFeed:
@@ -141,6 +141,15 @@ class TickGraph:
     def replay(self) -> None:
         """Run the captured ticks (asynchronously on the group's stream)."""
         g = self.group
+        # the captured launches have fixed flags: a pending one-tick overlay
+        # would be ignored (and land on a later eager tick) or overwritten by
+        # the coupling, so it is refused; non-finite POS commands raise like
+        # step_async does (quat.py:84), before any state changes
+        if g._overlay_active:
+            raise ValidationError("a velocity overlay is pending: a graph replay does not apply it "
+                                  "(step eagerly or let the coupling compute the overlay)")
+        if self.feed is None and g._nonfinite_rows and g._any_pos_rows():
+            raise InvalidStateError("non-finite quaternion input")
         if g._pending:
             g._flush_commands()
         with torch.cuda.device(g.device), torch.cuda.stream(g.stream):

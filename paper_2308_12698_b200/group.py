@@ -421,29 +421,48 @@ class B200QuadGroup:
         count = int(t.shape[1] if columns else t.shape[0])
         if row0 < 0 or row0 + count > self.n:
             raise ValidationError("setpoint rows out of range")
-        if t.dtype != torch.float32:
+        if t.dtype != torch.float32 and not t.is_cuda:
             t = t.float()
         self._flush_commands()
+        if t.is_cuda and t.device != self.device:
+            raise ValidationError(f"setpoints on {t.device}, group on {self.device}")
         with torch.cuda.device(self.device):
             if t.is_cuda:
-                cols = t if columns else t.T
-                if cols.stride(1) != 1:
-                    cols = cols.contiguous()
+                # the caller produced the tensor on its own stream: order this
+                # group's (non-blocking) stream after it before any conversion
+                # or launch reads it, and tell the allocator the group's stream
+                # uses it
+                self.stream.wait_stream(torch.cuda.current_stream(t.device))
                 with torch.cuda.stream(self.stream):
+                    if t.dtype != torch.float32:
+                        t = t.float()
+                    cols = t if columns else t.T
+                    if cols.stride(1) != 1:
+                        cols = cols.contiguous()
                     self._call(self._lib.swarmstep_quad_set_setpoints, ctypes.c_int64(row0), ctypes.c_int64(count),
                                int(lvl), _ptr(cols), ctypes.c_int64(cols.stride(0)),
                                ctypes.c_void_p(self.stream.cuda_stream))
-                self._staging_sp = cols
+                cols.record_stream(self.stream)
+                values.record_stream(self.stream)
             else:
                 if not columns:
                     t = t.T.contiguous()
                 slot = self._sp_slot
                 self._sp_slot ^= 1
                 if self._sp_stage[slot] is None or self._sp_stage[slot].shape[1] < count:
-                    self._sp_stage[slot] = torch.empty((7, max(count, 1)), dtype=torch.float32, device=self.device)
-                    self._sp_consumed[slot] = None
                     if self._copy_stream is None:
                         self._copy_stream = torch.cuda.Stream(self.device)
+                    old = self._sp_stage[slot]
+                    if old is not None:
+                        # a queued scatter / copy may still use the old buffer:
+                        # its memory is reusable only after both streams pass here
+                        old.record_stream(self.stream)
+                        old.record_stream(self._copy_stream)
+                    with torch.cuda.stream(self.stream):
+                        self._sp_stage[slot] = torch.empty((7, max(count, 1)), dtype=torch.float32,
+                                                           device=self.device)
+                    self._sp_stage[slot].record_stream(self._copy_stream)
+                    self._sp_consumed[slot] = None
                 buf = self._sp_stage[slot][:want, :count]
                 with torch.cuda.stream(self._copy_stream):
                     if self._sp_consumed[slot] is not None:
@@ -469,6 +488,10 @@ class B200QuadGroup:
 
     def add_velocity_overlay(self, offsets) -> None:
         """One-tick velocity offsets added to v_sp of POS rows (core.py:137-139)."""
+        if isinstance(offsets, torch.Tensor) and offsets.is_cuda:
+            # produced on the caller's stream: order the group's stream after it
+            self.stream.wait_stream(torch.cuda.current_stream(offsets.device))
+            offsets.record_stream(self.stream)
         with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
             t = offsets if isinstance(offsets, torch.Tensor) else torch.from_numpy(np.asarray(offsets, dtype=np.float32))
             t = t.to(self.device, torch.float32).reshape(self.n, 3)

@@ -78,15 +78,21 @@ class ShardedSwarm:
 
     ``group`` is the rank-local group (a ``B200QuadGroup`` holding ids
     [lo, hi)); commands for ids outside the shard are ignored locally (every
-    rank sees the full command stream and applies its own), and fault ids of
-    a tick are all-gathered so every rank can emit the same FAULT_DEATH
-    event (core.py:460-465).
+    rank sees the full command stream and applies its own).  Stepping is
+    collective-free (no per-tick exchange on the uncoupled
+    path): ``step`` / ``step_k`` return this rank's fault ids and log them
+    with their tick; ``collect()`` exchanges the logged ids of every rank in
+    ONE all-gather, so every rank can emit the same FAULT_DEATH events
+    (core.py:460-465) at the cadence the caller chooses (every tick, every
+    K ticks, or at the end).
     """
 
     def __init__(self, group, shard: ShardInfo, process_group=None):
         self.group = group
         self.shard = shard
         self.pg = process_group
+        self.tick = 0
+        self._log: list[tuple[int, np.ndarray]] = []    # (tick, local fault ids) not yet collected
 
     def owns(self, agent_id: int) -> bool:
         return self.shard.lo <= int(agent_id) < self.shard.hi
@@ -100,25 +106,49 @@ class ShardedSwarm:
     def mark_dead(self, agent_ids) -> list[int]:
         return self.group.mark_dead([a for a in agent_ids if self.owns(a)])
 
+    def _log_faults(self, per_tick) -> None:
+        for j, ids in enumerate(per_tick):
+            if len(ids):
+                self._log.append((self.tick + j, np.asarray(ids, dtype=np.uint64)))
+        self.tick += len(per_tick)
+
     def step(self, dt: float) -> np.ndarray:
-        """One tick; returns the fault ids of the whole swarm (sorted)."""
-        local = np.asarray(self.group.step(dt), dtype=np.int64)
-        return self.gather_ids(local)
+        """One tick of this rank's shard; returns its local fault ids (no collective)."""
+        local = np.asarray(self.group.step(dt), dtype=np.uint64)
+        self._log_faults([local])
+        return local
+
+    def step_k(self, dt: float, k: int = 1) -> np.ndarray:
+        """k fused ticks of this rank's shard (one launch); local fault ids."""
+        self.group.step_async(dt, k)
+        per = self.group.collect_faults()
+        self._log_faults(per)
+        return np.concatenate(per) if per else np.empty(0, dtype=np.uint64)
+
+    def collect(self) -> list[tuple[int, np.ndarray]]:
+        """Every rank's fault ids since the last collect, as (tick, sorted ids)
+        in tick order -- one all-gather of the logs (the only collective on
+        the uncoupled path; the caller decides how often)."""
+        log, self._log = self._log, []
+        if self.shard.world == 1:
+            parts = [log]
+        else:
+            import torch.distributed as dist
+            parts = [None] * self.shard.world
+            dist.all_gather_object(parts, [(t, ids.tolist()) for t, ids in log], group=self.pg)
+        by_tick: dict[int, list[int]] = {}
+        for part in parts:
+            for t, ids in part:
+                by_tick.setdefault(int(t), []).extend(int(i) for i in ids)
+        return [(t, np.sort(np.array(v, dtype=np.uint64))) for t, v in sorted(by_tick.items())]
 
     def gather_ids(self, local: np.ndarray) -> np.ndarray:
-        """Every rank's fault ids of the tick (one integer per
-        rank per tick; the ids themselves only move when some rank faulted)."""
+        """All ranks' ids of ``local`` (collective; sorted)."""
         if self.shard.world == 1:
-            return np.sort(local).astype(np.uint64)
+            return np.sort(np.asarray(local, dtype=np.uint64))
         import torch.distributed as dist
-        backend = dist.get_backend(self.pg)
-        dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
-        cnt = torch.tensor([int(local.size)], dtype=torch.int64, device=dev)
-        dist.all_reduce(cnt, group=self.pg)
-        if int(cnt.item()) == 0:
-            return np.empty(0, dtype=np.uint64)
         out = [None] * self.shard.world
-        dist.all_gather_object(out, local.tolist(), group=self.pg)
+        dist.all_gather_object(out, np.asarray(local, dtype=np.int64).tolist(), group=self.pg)
         return np.sort(np.array([i for part in out for i in part], dtype=np.int64)).astype(np.uint64)
 
 

@@ -69,8 +69,13 @@ def _worker(rank, world, port, n_total, pos, alive, result_q):
         cmd = type("C", (), {})
         results = [sw.apply_command(type("C", (), dict(agent_id=a, level="pos", values=(0,) * 7))())
                    for a in range(n_total)]
-        faults = sw.step(1e-3).tolist()
-        assert sw.step(1e-3).size == 0            # no rank faulted: only the count moves
+        local = sw.step(1e-3).tolist()             # no collective: this rank's ids only
+        assert all(shard.lo <= f < shard.hi for f in local)
+        assert sw.step(1e-3).size == 0
+        coll = sw.collect()                        # one exchange for both ticks
+        assert [t for t, _ in coll] == [0]
+        faults = coll[0][1].tolist()
+        assert sw.collect() == []
         # position all-gather exactly as NeighborSeparation lays it out
         local = torch.full((shard.pad, 4), float("nan"))
         mine = np.arange(shard.lo, shard.hi)
