@@ -2,19 +2,23 @@
 """Headline benchmark: quadrotor agent-steps/s of the fused dynamics+control step.
 
 Workload (BASELINE.json metric "quadrotor agent-steps/sec (dynamics+control) at
-N=1M/10M", configs 3/4): per GPU ``--agents`` quadrotors (default 10M) on the
-reference bench's grid layout (bench.py:87-93 of the reference: spacing 3 m,
-origin (0,0,10)), identity attitude, at rest, POSITION level with random
-setpoints p_sp = p0 + U(-1,1)^3, v_sp = 0, yaw U(-pi,pi),
+N=1M/10M, 1/2/4/8 B200", configs 3/4): ``--agents`` quadrotors in total
+(default 10,000,000) on the reference bench's grid layout (bench.py:87-93 of
+the reference: spacing 3 m, origin (0,0,10)), identity attitude, at rest,
+POSITION level with random setpoints p_sp = p0 + U(-1,1)^3, v_sp = 0,
+yaw U(-pi,pi) (paper_2308_12698_b200/synthetic.py),
 dt = 1 ms, K = 10 fused ticks per launch.  One bench "step" = one launch =
 K ticks for every agent, so value = N_total * K * steps / time.
 
-Agents shard by index across ranks (one process per GPU, torchrun); there is
-no collective on this path, so per-GPU work is fixed ("scaling": "weak").
+Multi-GPU (cfg4): the N_total agents are split by contiguous index across
+the ranks (one process per GPU, torchrun), each rank stepping its own rows
+with no data-path collective, so total work is fixed ("scaling": "strong");
+``--agents-per-gpu`` selects weak scaling instead.
 
-``--impl reference`` times the reference's CPU path instead: the float64 C
-restatement in oracle/ (the reference itself is Python that does not travel
-to the GPU box) on all host cores, rank 0 only.
+``--impl reference`` times the reference's own CPU path instead: the
+unmodified ``swarmstep.core.QuadGroup.step`` (core.py:166-202, installed in
+oracle/_ref by build()) on the same N_total-agent swarm, sharded over every
+host core (oracle/ref_runner.py), rank 0 only.
 """
 
 from __future__ import annotations
@@ -36,14 +40,16 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "quadrotor agent-steps/sec (dynamics+control) at N=1M/10M, 1/2/4/8 B200"
 UNIT = "agent-steps/s"
-# algorithmic bytes per agent per launch, position level, compensated position
-# (DESIGN.md "Roofline"): read 13 state + 3 pos-lo + 6 PID + 7 command floats +
-# 1 flag byte = 117 B; write 13 + 3 + 6 + 4 stale-setpoint floats = 104 B.
-ALG_BYTES_PER_AGENT_LAUNCH = 221
+# Algorithmic bytes per agent per launch at position level:
+# read 13 state + 6 PID + 7 setpoint floats + 1 flag byte = 105 B, write
+# 13 state + 6 PID floats + 1 flag byte = 77 B.
+ALG_BYTES_PER_AGENT_LAUNCH = 182
+# ... plus what this implementation also moves: the compensated
+# position's lo words (12 B read + 12 B written) and the stale inner-loop
+# setpoints written for a later MOTOR command (16 B) -- overhead, not algorithm
+BYTES_WITH_OVERHEAD = 221
 # algorithmic flops per agent-tick at position level (FMA = 2)
 ALG_FLOPS_PER_AGENT_TICK = 705
-PORT_NOTE = ("the port runs ~5x faster than the reference's own numpy QuadGroup.step on one core "
-             "(4.7-5.5x, same results to 2e-15 m; profiles/cpu_ref_vs_port_r01.json): a conservative baseline")
 
 
 def parse():
@@ -52,10 +58,17 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--agents", type=int, default=10_000_000, help="agents per GPU")
+    ap.add_argument("--agents", type=int, default=10_000_000,
+                    help="agents in total, split across the GPUs (strong scaling)")
+    ap.add_argument("--agents-per-gpu", type=int, default=None,
+                    help="weak scaling: this many agents on every GPU instead of --agents in total")
     ap.add_argument("--substeps", type=int, default=10, help="fused ticks per launch (K)")
     ap.add_argument("--dt", type=float, default=1e-3)
-    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="cpu_baseline sample budget")
+    ap.add_argument("--cpu-samples", type=int, default=4,
+                    help="cpu_baseline: timed reference ticks of the whole swarm (after one warm tick)")
+    ap.add_argument("--cpu-seconds", type=float, default=4.0, help="cpu_baseline: C-port sample budget")
+    ap.add_argument("--ref-ticks", type=int, default=1,
+                    help="--impl reference: ticks of the whole swarm per timed step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-k1", action="store_true", help="skip the K=1 HBM-roofline leg")
     ap.add_argument("--no-e2e", action="store_true")
@@ -65,16 +78,31 @@ def parse():
 
 
 # ----------------------------------------------------------------- workload
-def workload(n: int, seed: int, id_base: int = 0):
-    """Initial state + POS setpoints (float64 host arrays) for n agents."""
-    from paper_2308_12698_b200.layout import layout_poses
-    pos, _ = layout_poses({"kind": "grid", "spacing": 3.0, "origin": (0.0, 0.0, 10.0)}, n)
-    rng = np.random.default_rng(seed)
-    sp = np.empty((7, n), dtype=np.float32)
-    sp[0:3] = (pos + rng.uniform(-1.0, 1.0, (n, 3))).T
-    sp[3:6] = 0.0
-    sp[6] = rng.uniform(-np.pi, np.pi, n)
-    return pos, sp
+def layout(args, world: int) -> tuple[int, str]:
+    """(total agents, scaling) of the run."""
+    if args.agents_per_gpu is not None:
+        return args.agents_per_gpu * world, "weak"
+    return args.agents, "strong"
+
+
+def rank_rows(args, rank: int, world: int) -> tuple[int, int]:
+    from paper_2308_12698_b200.parallel import shard_range
+    if args.agents_per_gpu is not None:
+        return rank * args.agents_per_gpu, (rank + 1) * args.agents_per_gpu
+    return shard_range(args.agents, rank, world)
+
+
+def config(args, world: int) -> dict:
+    n_total, scaling = layout(args, world)
+    per = ("per GPU" if scaling == "weak" else f"in total, split by agent index over {world} GPU(s)")
+    return {"workload": f"{n_total:,} quadrotors {per}, POS level, random setpoints, K={args.substeps} fused ticks "
+                        f"per launch (cfg3 recipe; cfg4 = 10M over 2/4/8 GPUs)",
+            "agents_total": n_total, "agents_per_gpu": -(-n_total // world), "substeps": args.substeps,
+            "dt": args.dt, "level": "pos", "compensated_position": True, "motor_tau": args.motor_tau,
+            "l2": f"inputs larger than L2 ({-(-n_total // world) * BYTES_WITH_OVERHEAD / 1e9:.2f} GB touched per "
+                  f"launch per GPU vs 0.126 GB L2)" if -(-n_total // world) * BYTES_WITH_OVERHEAD > 126e6 else
+                  "per-GPU state smaller than L2: launches may hit L2 (not an HBM measurement)",
+            "parallelism": f"agent-index shards x{world}, no collective"}
 
 
 class _Batch:
@@ -132,12 +160,16 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------- CPU legs
-def cpu_leg(n_sample: int, k: int, dt: float, budget_s: float, min_reps: int = 1, motor_tau: float = 0.0):
-    """Time the float64 oracle (reference algorithm) on all host cores."""
+def port_leg(n_total: int, k: int, dt: float, budget_s: float, motor_tau: float = 0.0) -> dict:
+    """The float64 C restatement of QuadGroup.step (oracle/quad_oracle.c) on all
+    host threads, on the first rows of the same swarm, for ~budget_s seconds."""
     from oracle import oracle as orc
+
+    from paper_2308_12698_b200.synthetic import swarm
     threads = orc.cpu_count()
-    pos, sp = workload(n_sample, seed=0)
-    g = orc.OracleGroup(0, _Batch(n_sample, pos, 0), motor_tau=motor_tau)
+    n_s = min(262_144, n_total)
+    pos, sp = swarm(n_total, 0, n_s)
+    g = orc.OracleGroup(0, _Batch(n_s, pos, 0), motor_tau=motor_tau)
     g.cmd_values[:] = sp.T.astype(np.float64)
     g.step(dt, nthreads=threads)  # warm
     reps, t0 = 0, time.perf_counter()
@@ -146,33 +178,67 @@ def cpu_leg(n_sample: int, k: int, dt: float, budget_s: float, min_reps: int = 1
             g.step(dt, nthreads=threads)
         reps += 1
         el = time.perf_counter() - t0
-        if reps >= min_reps and el >= budget_s:
+        if el >= budget_s:
             break
-    return n_sample * k * reps / el, threads, reps, el
+    return {"value": n_s * k * reps / el, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"rows [0, {n_s}) of the same swarm x {k} ticks x {reps} reps ({el:.1f} s), float64 C "
+                      f"restatement of QuadGroup.step (oracle/quad_oracle.c), {threads} threads"}
+
+
+def _ref_rows(n_total: int) -> int:
+    """How many of the swarm's rows the reference workers can hold (~1.8 KB of
+    numpy state + workspaces per agent, measured) in half the free memory."""
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:  # noqa: BLE001
+        return n_total
+    return max(1, min(n_total, int(avail * 0.5 / 2000)))
+
+
+def reference_leg(n_total: int, dt: float, ticks: int, samples: int, warm: int) -> dict | None:
+    """The unmodified reference QuadGroup.step (oracle/_ref) on the swarm's rows,
+    sharded over every host core; None when the reference is not installed."""
+    from oracle import ref_runner
+    if not ref_runner.available():
+        return None
+    n_ref = _ref_rows(n_total)
+    r = ref_runner.run_quadgroup(n_total, dt, ticks=ticks, samples=samples, warm=warm, n_rows=n_ref)
+    rows = f"all {n_total:,} agents" if n_ref == n_total else f"rows [0, {n_ref:,}) of the {n_total:,} agents"
+    return {"value": r["value"], "unit": UNIT, "cores": r["procs"], "kind": "reference",
+            "sample": f"the unmodified reference swarmstep QuadGroup.step (core.py:166-202, oracle/_ref) on {rows} "
+                      f"of this swarm, sharded by index over {r['procs']} processes (numpy 1 thread each), "
+                      f"{samples} x {ticks} tick(s) timed after {warm} warm tick(s); sample time = max over "
+                      f"processes; {r['wall_s']:.1f} s",
+            "agents": n_ref, "ms_per_sample": [t * 1e3 for t in r["sample_s"]],
+            "per_core_median": r["per_core_median"], "faults": r["faults"]}
 
 
 def run_reference(args, rank: int) -> None:
     if rank != 0:
         return
-    n_sample = 262_144
-    threads = None
-    vals = []
-    for i in range(args.warmup + args.steps):
-        v, threads, reps, el = cpu_leg(n_sample, args.substeps, args.dt, 0.0, min_reps=1, motor_tau=args.motor_tau)
-        if i >= args.warmup:
-            vals.append(v)
-    value = float(np.mean(vals))
-    sample = (f"{n_sample} agents x {args.substeps} ticks per step (POS level, random setpoints, "
-              f"float64 C oracle, {threads} threads)")
+    world = max(1, args.gpus)
+    n_total, scaling = layout(args, world)
+    port = port_leg(n_total, args.substeps, args.dt, args.cpu_seconds, args.motor_tau)
+    ref = None if args.motor_tau > 0 else reference_leg(n_total, args.dt, args.ref_ticks, args.steps,
+                                                        args.warmup * args.ref_ticks)
+    cfg = config(args, world)
+    if ref is not None:
+        value, cb = ref["value"], dict(ref)
+        ms = statistics.mean(ref["ms_per_sample"])
+        cfg["ticks_per_step"] = args.ref_ticks
+        cfg["note"] = (f"one timed step = {args.ref_ticks} tick(s) of the whole swarm (the reference has no "
+                       f"fused launch); same agents, setpoints and metric as the B200 arm")
+    else:
+        # motor lag (absent in the reference) or no oracle/_ref: the C port
+        value, cb = port["value"], dict(port)
+        ms = (min(262_144, n_total) * args.substeps) / value * 1e3
+        cfg["note"] = "reference not runnable for this config: float64 C port of QuadGroup.step"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": n_sample * args.substeps / value * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"cfg3/cfg4 recipe, sampled: {sample}", "agents_sampled": n_sample,
-                   "substeps": args.substeps, "dt": args.dt, "level": "pos"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
-                         "note": PORT_NOTE},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
+        "cpu_baseline": cb, "port": port if ref is not None else None,
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -184,11 +250,14 @@ def run_b200(args, rank: int, world: int) -> None:
     import torch.distributed as dist
 
     from paper_2308_12698_b200 import B200QuadGroup
+    from paper_2308_12698_b200.synthetic import swarm
 
     local = _local_device()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    n, k, dt = args.agents, args.substeps, args.dt
+    n_total, scaling = layout(args, world)
+    lo, hi = rank_rows(args, rank, world)
+    n, k, dt = hi - lo, args.substeps, args.dt
     nccl = _backend() == "nccl"
 
     def barrier():
@@ -199,8 +268,8 @@ def run_b200(args, rank: int, world: int) -> None:
                 dist.barrier()
 
     t_setup = time.perf_counter()
-    pos, sp = workload(n, seed=rank, id_base=rank * n)
-    g = B200QuadGroup(0, _Batch(n, pos, rank * n), device=dev, motor_tau=args.motor_tau)
+    pos, sp = swarm(n_total, lo, hi)
+    g = B200QuadGroup(0, _Batch(n, pos, lo), device=dev, motor_tau=args.motor_tau)
     sp_dev = torch.from_numpy(sp).to(dev)
     g.set_setpoints(sp_dev, columns=True)
     torch.cuda.synchronize(dev)
@@ -223,7 +292,7 @@ def run_b200(args, rank: int, world: int) -> None:
         e1.record(stream)
         torch.cuda.synchronize(dev)
         barrier()
-        return max_over_ranks(e0.elapsed_time(e1))
+        return e0.elapsed_time(e1)
 
     # ---- device-resident leg (value): K fused ticks per launch
     for _ in range(args.warmup):
@@ -238,28 +307,30 @@ def run_b200(args, rank: int, world: int) -> None:
         for _ in range(8):
             g.step_async(dt, k)
         g.collect_faults()
-    ms = timed(lambda: g.step_async(dt, k), args.steps, g.stream)
+    ms_rank = timed(lambda: g.step_async(dt, k), args.steps, g.stream)
     clk = clocks.stop()
+    ms = max_over_ranks(ms_rank)
     faults = sum(f.size for f in g.collect_faults())
     ms_per_step = ms / args.steps
-    value = world * n * k * args.steps / (ms * 1e-3)
-    launch_s = ms_per_step * 1e-3
+    value = n_total * k * args.steps / (ms * 1e-3)
+    # roofline of this rank's kernel (rank 0 prints): its own launches and rows
+    launch_s = ms_rank / args.steps * 1e-3
     achieved_tf = n * k * ALG_FLOPS_PER_AGENT_TICK / launch_s / 1e12
     sm_mhz = clk.get("sm_max_mhz") or 1965.0
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     fp32_nominal_tf = sms * 128 * 2 * sm_mhz * 1e6 / 1e12
     fp32_meas = _fp32_peak()
+    nominal_src = f"{sms} SMs x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz"
     if fp32_meas:
         fp32_peak_tf = fp32_meas["tflops"]
-        peak_source = (f"measured: FP32 microbenchmark tools/fp32_peak.cu (best of FFMA register / immediate / "
-                       f"packed FFMA2: {fp32_meas['form']}) on this GPU; nominal {fp32_nominal_tf:.1f} TFLOP/s = "
-                       f"{sms} SMs x 128 lanes x 2 x {sm_mhz:.0f} MHz")
+        peak_source = (f"builder-measured: FP32 microbenchmark tools/fp32_peak.cu on this GPU (best of FFMA "
+                       f"register / immediate / packed FFMA2: {fp32_meas['form']}); MEASURED_PEAKS.json has no "
+                       f"FP32 SIMT figure; nominal {fp32_nominal_tf:.1f} TFLOP/s = {nominal_src} (frac_nominal)")
     else:
         fp32_peak_tf = fp32_nominal_tf
-        peak_source = (f"derived: {sms} SMs x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz "
-                       "(MEASURED_PEAKS.json has no FP32 SIMT figure)")
+        peak_source = f"nominal: {nominal_src} (MEASURED_PEAKS.json has no FP32 SIMT figure)"
 
-    # ---- K=1 leg: the same kernel in its HBM-bound regime
+    # ---- K=1 leg: the same step in its HBM-bound regime
     k1 = None
     if not args.no_k1:
         for _ in range(3):
@@ -269,11 +340,16 @@ def run_b200(args, rank: int, world: int) -> None:
         g.collect_faults()
         t1 = ms1 / args.steps * 1e-3
         peaks = _peaks()
-        k1 = {"bound": "hbm", "achieved": ALG_BYTES_PER_AGENT_LAUNCH * n / t1 / 1e9,
-              "peak": peaks["hbm_gbs"], "unit": "GB/s",
-              "frac": ALG_BYTES_PER_AGENT_LAUNCH * n / t1 / 1e9 / peaks["hbm_gbs"],
-              "traffic": _traffic("k1", n), "ms_per_launch": t1 * 1e3,
-              "agent_steps_per_s": world * n / t1, "peak_source": peaks["source"]}
+        gbs = ALG_BYTES_PER_AGENT_LAUNCH * n / t1 / 1e9
+        gbs_ovh = BYTES_WITH_OVERHEAD * n / t1 / 1e9
+        k1 = {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+              "frac": gbs / peaks["hbm_gbs"], "traffic": _traffic("k1", n),
+              "bytes_per_agent": ALG_BYTES_PER_AGENT_LAUNCH,
+              "bytes_basis": "SURVEY.md 8(d): 182 B per agent per launch (state, PID, setpoints, flags)",
+              "with_overhead": {"bytes_per_agent": BYTES_WITH_OVERHEAD, "achieved": gbs_ovh,
+                                "frac": gbs_ovh / peaks["hbm_gbs"],
+                                "note": "182 B + position lo words (24 B) + stale MOTOR setpoints (16 B) as moved"},
+              "ms_per_launch": t1 * 1e3, "agent_steps_per_s": n / t1, "peak_source": peaks["source"]}
 
     # ---- end-to-end leg through the public API with host buffers:
     # every step uploads a fresh whole-swarm POS setpoint block from pinned host
@@ -301,34 +377,31 @@ def run_b200(args, rank: int, world: int) -> None:
         torch.cuda.synchronize(dev)
         el = max_over_ranks(time.perf_counter() - t0)
         barrier()
-        e2e = {"value": world * n * k * args.steps / el, "unit": UNIT,
-               "h2d_bytes_per_step": int(7 * 4 * n), "d2h_bytes_per_step": 16,
+        e2e = {"value": n_total * k * args.steps / el, "unit": UNIT,
+               "h2d_bytes_per_step": int(7 * 4 * n_total), "d2h_bytes_per_step": 16 * world,
                "ms_per_step": el / args.steps * 1e3,
-               "path": "B200QuadGroup.set_setpoints(pinned host) + step_async(dt, K) + collect_faults()"}
+               "path": "B200QuadGroup.set_setpoints(pinned host) + step_async(dt, K) + collect_faults() per rank"}
 
+    # ---- the reference's CPU path beside the GPU number (rank 0, after the
+    # timed regions; every N): the unmodified reference QuadGroup.step on this
+    # swarm over all host cores, plus the float64 C port
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        n_s = 262_144
-        v, threads, reps, el = cpu_leg(n_s, k, dt, args.cpu_seconds, motor_tau=args.motor_tau)
-        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "note": PORT_NOTE,
-               "sample": f"{n_s} agents x {k} ticks x {reps} reps ({el:.1f} s), same recipe, float64 C oracle "
-                         f"(restatement of the reference QuadGroup.step), {threads} threads"}
+    if rank == 0 and not args.no_cpu_baseline:
+        port = port_leg(n_total, k, dt, args.cpu_seconds, args.motor_tau)
+        ref = None if args.motor_tau > 0 else reference_leg(n_total, dt, 1, args.cpu_samples, 1)
+        cpu = dict(ref, port=port) if ref is not None else port
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{n:,} quadrotors per GPU, POS level, random setpoints, "
-                                   f"K={k} fused ticks per launch (cfg3 recipe at cfg4 size)",
-                       "agents_per_gpu": n, "agents_total": n * world, "substeps": k, "dt": dt,
-                       "level": "pos", "compensated_position": True, "motor_tau": args.motor_tau,
-                       "l2": f"inputs larger than L2 ({n * 221 / 1e9:.2f} GB touched per launch vs 0.126 GB L2)",
-                       "parallelism": f"agent-index shards x{world}, no collective"},
+            "scaling": scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": config(args, world),
             "roofline": {"bound": "fp32", "achieved": achieved_tf, "peak": fp32_peak_tf, "unit": "TFLOP/s",
-                         "frac": achieved_tf / fp32_peak_tf, "traffic": _traffic("k10", n),
-                         "flops_per_agent_tick": ALG_FLOPS_PER_AGENT_TICK, "peak_source": peak_source,
-                         "fp32_peak_measurements": fp32_meas},
+                         "frac": achieved_tf / fp32_peak_tf, "frac_nominal": achieved_tf / fp32_nominal_tf,
+                         "peak_nominal": fp32_nominal_tf, "traffic": _traffic("k10", n),
+                         "flops_per_agent_tick": ALG_FLOPS_PER_AGENT_TICK, "agents_per_launch": n,
+                         "peak_source": peak_source, "fp32_peak_measurements": fp32_meas},
             "roofline_k1": k1,
             "cpu_baseline": cpu,
             "e2e": e2e,

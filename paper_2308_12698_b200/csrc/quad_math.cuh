@@ -116,6 +116,23 @@ __device__ __forceinline__ f2 vmin(f2 a, f2 b) { return f2{make_float2(fminf(a.v
 __device__ __forceinline__ f2 vmax(f2 a, f2 b) { return f2{make_float2(fmaxf(a.v.x, b.v.x), fmaxf(a.v.y, b.v.y))}; }
 __device__ __forceinline__ f2 vabs(f2 a) { return f2{make_float2(fabsf(a.v.x), fabsf(a.v.y))}; }
 
+// NaN-propagating min / max (PTX max.NaN / min.NaN, sm_80+): the same cost
+// as fminf / fmaxf, but a NaN operand yields NaN instead of the other operand
+__device__ __forceinline__ float vmax_nan(float a, float b)
+{
+    float r;
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ float vmin_nan(float a, float b)
+{
+    float r;
+    asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ f2 vmax_nan(f2 a, f2 b) { return f2{make_float2(vmax_nan(a.v.x, b.v.x), vmax_nan(a.v.y, b.v.y))}; }
+__device__ __forceinline__ f2 vmin_nan(f2 a, f2 b) { return f2{make_float2(vmin_nan(a.v.x, b.v.x), vmin_nan(a.v.y, b.v.y))}; }
+
 __device__ __forceinline__ bool lt(float a, float b) { return a < b; }
 __device__ __forceinline__ bool gt(float a, float b) { return a > b; }
 __device__ __forceinline__ bool ge(float a, float b) { return a >= b; }
@@ -141,6 +158,12 @@ __device__ __forceinline__ f2 sel(m2 m, f2 a, f2 b) { return f2{make_float2(m.x 
 
 __device__ __forceinline__ float lane(float a, int) { return a; }
 __device__ __forceinline__ float lane(f2 a, int i) { return i ? a.v.y : a.v.x; }
+
+// double -> float, finite values beyond float32 range saturate at +-FLT_MAX
+__device__ __forceinline__ float f32_sat(double x)
+{
+    return isfinite(x) ? (float)fmin(fmax(x, -3.4028234663852886e38), 3.4028234663852886e38) : (float)x;
+}
 
 // np.clip semantics: NaN passes through
 template <class T> __device__ __forceinline__ T clip(T x, T lo, T hi)
@@ -436,7 +459,26 @@ __device__ __forceinline__ void outer_row(const T p_err[3], const T v[3], const 
 #pragma unroll
     for (int i = 0; i < 3; i++) a[i] = fma(bc<T>(P.kp_pos[i]), p_err[i], mul(bc<T>(P.kv[i]), sub(v_sp[i], v[i])));
     a[2] = add(a[2], bc<T>(P.g));
-    const T asq = fma(a[0], a[0], fma(a[1], a[1], mul(a[2], a[2])));
+    T asq = fma(a[0], a[0], fma(a[1], a[1], mul(a[2], a[2])));
+    // |a|^2 beyond float32 range (setpoints near the float32 limit; the
+    // float64 reference has the range): only a's direction and the sign of
+    // z_body . a matter below (|a| >= 1.8e19 is never below the free-fall
+    // floor), so take them from a copy scaled by 2^-100 -- |a| <= ~41 FLT_MAX
+    // with saturated setpoints, so the scaled |a|^2 stays finite -- and scale
+    // the thrust back (it saturates at fc_max).  Finite rows skip this.
+    const mask_t<T> ovf = mnot(le(asq, bc<T>(3.4028234663852886e38f)));
+    if (any(ovf)) {
+        const T s = bc<T>(0x1p-100f);
+        T as[3];
+#pragma unroll
+        for (int i = 0; i < 3; i++)
+            as[i] = fma(bc<T>(P.kp_pos[i]), mul(p_err[i], s), mul(bc<T>(P.kv[i]), mul(sub(v_sp[i], v[i]), s)));
+        as[2] = add(as[2], mul(bc<T>(P.g), s));
+        const T asq_s = fma(as[0], as[0], fma(as[1], as[1], mul(as[2], as[2])));
+#pragma unroll
+        for (int i = 0; i < 3; i++) a[i] = sel(ovf, as[i], a[i]);
+        asq = sel(ovf, asq_s, asq);
+    }
     const T qw = q[0], qx = q[1], qy = q[2], qz = q[3];
     const T zb0 = mul(bc<T>(2.0f), fma(qx, qz, mul(qw, qy)));
     const T zb1 = mul(bc<T>(2.0f), fnma(qw, qx, mul(qy, qz)));
@@ -444,12 +486,13 @@ __device__ __forceinline__ void outer_row(const T p_err[3], const T v[3], const 
     const float amin = P.a_cmd_min;
     // free-fall floor (control.py:243-247): |a| < a_min -> z_des = e_z, |a| := a_min;
     // else m |a| (z_body . a/|a|) = m (z_body . a)
-    const mask_t<T> low = lt(asq, bc<T>(amin * amin));
+    const mask_t<T> low = mand(lt(asq, bc<T>(amin * amin)), mnot(ovf));
     const T ia = rsqrt_a(asq);
     z[0] = sel(low, zero, mul(a[0], ia));
     z[1] = sel(low, zero, mul(a[1], ia));
     z[2] = sel(low, one, mul(a[2], ia));
-    const T fc = sel(low, mul(bc<T>(P.m * amin), zb2), mul(bc<T>(P.m), fma(zb0, a[0], fma(zb1, a[1], mul(zb2, a[2])))));
+    T fc = sel(low, mul(bc<T>(P.m * amin), zb2), mul(bc<T>(P.m), fma(zb0, a[0], fma(zb1, a[1], mul(zb2, a[2])))));
+    if (any(ovf)) fc = sel(ovf, mul(fc, bc<T>(0x1p100f)), fc);   // undo the 2^-100 (overflows to +-inf)
     f_c_sp = vmin(vmax(fc, zero), bc<T>(P.fc_max));
 
     // y = z x x_c / |z x x_c| with x_c = (cy, sy, 0); degenerate fallback from y_c
@@ -506,12 +549,13 @@ __device__ __forceinline__ void outer_row(const T p_err[3], const T v[3], const 
     const T ssq = fma(e1, e1, fma(e2, e2, mul(e3, e3)));
     T factor = axis_angle_factor(sqrt_a(ssq), vabs(e0));
     factor = sel(lt(e0, zero), neg(factor), factor);
-    // |w_sp| <= omega_sp_max.  min/max (not NaN-propagating) is safe here:
-    // non-finite outer-loop inputs are rejected before launch (InvalidState).
+    // |w_sp| <= omega_sp_max, NaN propagating (np.clip): a NaN setpoint that
+    // reached the device (the bulk feed does not screen) faults its row
+    // through the PID and RK4 instead of flying a clamped garbage command
     const T wm = bc<T>(P.omega_sp_max), nwm = bc<T>(-P.omega_sp_max);
-    w_sp[0] = vmin(vmax(mul(bc<T>(P.k_att[0]), mul(e1, factor)), nwm), wm);
-    w_sp[1] = vmin(vmax(mul(bc<T>(P.k_att[1]), mul(e2, factor)), nwm), wm);
-    w_sp[2] = vmin(vmax(mul(bc<T>(P.k_att[2]), mul(e3, factor)), nwm), wm);
+    w_sp[0] = vmin_nan(vmax_nan(mul(bc<T>(P.k_att[0]), mul(e1, factor)), nwm), wm);
+    w_sp[1] = vmin_nan(vmax_nan(mul(bc<T>(P.k_att[1]), mul(e2, factor)), nwm), wm);
+    w_sp[2] = vmin_nan(vmax_nan(mul(bc<T>(P.k_att[2]), mul(e3, factor)), nwm), wm);
 }
 
 }  // namespace ssb

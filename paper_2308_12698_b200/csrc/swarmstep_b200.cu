@@ -886,7 +886,8 @@ __global__ void retarget_kernel(float *cols, uint8_t *flags, int64_t n, int64_t 
     const double z = cols[ssb::at(SWARMSTEP_COL_QUAT + 3, r)];
     const double yaw = atan2(2.0 * (w * z + x * y), 1.0 - 2.0 * (y * y + z * z));  // quat.py:139-143
     flags[r] = (uint8_t)(fl & ~SWARMSTEP_LEVEL_MASK);  // POS level
-    const float vals[7] = {(float)px, (float)py, (float)pz, 0.0f, 0.0f, 0.0f, (float)yaw};
+    // a point beyond float32 range saturates (like the host command store)
+    const float vals[7] = {ssb::f32_sat(px), ssb::f32_sat(py), ssb::f32_sat(pz), 0.0f, 0.0f, 0.0f, (float)yaw};
     for (int c = 0; c < 7; c++) cols[ssb::at(SWARMSTEP_COL_CMD + c, r)] = vals[c];
     atomicAdd(&counters[1], 1u);
 }

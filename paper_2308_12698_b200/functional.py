@@ -110,6 +110,9 @@ def _stream():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+_F32_MAX = float(np.finfo(np.float32).max)
+
+
 def _p(t: torch.Tensor | None):
     # callers keep every tensor passed here in a local until the launch is
     # queued: a temporary freed inside the argument list would hand its memory
@@ -122,7 +125,15 @@ def _f32(x, shape, dev) -> torch.Tensor:
     if isinstance(x, torch.Tensor):
         t = x.to(device=dev, dtype=torch.float32)
     else:
-        t = torch.from_numpy(np.array(np.broadcast_to(np.asarray(x, dtype=np.float32), shape))).to(dev)
+        a = np.asarray(x)
+        if a.dtype != np.float32:
+            # finite values beyond float32 range saturate (like the group's
+            # command store) instead of becoming inf
+            a = np.asarray(a, dtype=np.float64)
+            fin = np.isfinite(a)
+            if not fin.all() or np.abs(a).max(initial=0.0) > _F32_MAX:
+                a = np.where(fin, np.clip(a, -_F32_MAX, _F32_MAX), a)
+        t = torch.from_numpy(np.array(np.broadcast_to(a.astype(np.float32), shape))).to(dev)
     return t.reshape(shape).contiguous()
 
 
@@ -290,6 +301,11 @@ def position_outer_loop(pos, vel, quat, alive, sp, params, gains) -> OuterResult
     w_sp, f_sp = torch.empty((n, 3), device=dev), torch.empty(n, device=dev)
     low = torch.empty(n, dtype=torch.uint8, device=dev)
     v, q, al = _f32(vel, (n, 3), dev), _f32(quat, (n, 4), dev), _u8(alive, n, dev)
+    if not as_torch:
+        # yaw enters only through cos / sin: reduce to [-pi, pi] in float64
+        # before the float32 rounding (group.f32_commands)
+        yaw = np.broadcast_to(np.asarray(yaw, dtype=np.float64), (n,))
+        yaw = yaw - np.round(yaw / (2.0 * np.pi)) * (2.0 * np.pi)
     ps, vs, ys = _f32(sp.p_sp, (n, 3), dev), _f32(sp.v_sp, (n, 3), dev), _f32(yaw, (n,), dev)
     _check(lib.swarmstep_op_outer(n, _p(p_hi), _p(p_lo), _p(v), _p(q), _p(al), _p(ps), _p(vs), _p(ys),
                                   ctypes.byref(P), _p(w_sp), _p(f_sp), _p(low), _stream()))

@@ -42,6 +42,33 @@ _ZEROS = (0.0,) * 7
 _PINNED_MIRROR_MAX = 8_000_000   # agents: 0.83 GB of pinned float64 mirror
 
 
+_F32_MAX = float(np.finfo(np.float32).max)
+_TWO_PI = 2.0 * math.pi
+
+
+def f32_commands(vals: np.ndarray, pos_rows) -> np.ndarray:
+    """float64 command values (rows x 7) -> the float32 device command store.
+
+    Two conversions keep float32 commands faithful to the float64 reference:
+    * POS yaw setpoints are reduced to [-pi, pi] in float64 first (the outer
+      loop only uses cos / sin of yaw, control.py:252-256): a float32 yaw of
+      |yaw| ~ 1000 rad would carry ~6e-5 rad of rounding, far above the 1e-5
+      parity budget, the reduced one <= 1.2e-7;
+    * finite values beyond float32 range saturate at +-FLT_MAX instead of
+      becoming inf (the outer loop then takes the direction of an overflowing
+      acceleration command from a scaled copy, quad_math.cuh outer_row).
+    Non-finite values pass unchanged (they raise or fault like the reference).
+    """
+    v = np.array(vals, dtype=np.float64, copy=True).reshape(-1, 7)
+    y = v[pos_rows, 6]
+    fin = np.isfinite(y)
+    y[fin] -= np.round(y[fin] / _TWO_PI) * _TWO_PI
+    v[pos_rows, 6] = y
+    fin = np.isfinite(v)
+    v[fin] = np.clip(v[fin], -_F32_MAX, _F32_MAX)
+    return v.astype(np.float32)
+
+
 def _round_up(x: int, m: int) -> int:
     return (x + m - 1) // m * m
 
@@ -277,7 +304,7 @@ class B200QuadGroup:
             if upload_commands:
                 if np.any(self._cmd_level == LEVEL_MOTOR):
                     self._motor_possible = True
-                vals = torch.from_numpy(self._cmd_values.astype(np.float32)).to(self.device)
+                vals = torch.from_numpy(f32_commands(self._cmd_values, self._cmd_level == LEVEL_POS)).to(self.device)
                 self._cols_write(COL_CMD, vals)
                 lv = torch.from_numpy(self._cmd_level.astype(np.uint8)).to(self.device)
                 fl = self._flags[:self.n]
@@ -339,7 +366,7 @@ class B200QuadGroup:
         rows = np.fromiter(self._pending.keys(), dtype=np.int64, count=count)
         pend = list(self._pending.values())
         levels = np.fromiter((lvl for lvl, _ in pend), dtype=np.uint8, count=count)
-        vals = np.array([v for _, v in pend], dtype=np.float32).reshape(count, 7)   # float64 -> float32
+        vals = f32_commands([v for _, v in pend], levels == LEVEL_POS)   # float64 -> float32
         self._pending.clear()
         with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
             d_rows = torch.from_numpy(rows).to(self.device)
@@ -415,7 +442,19 @@ class B200QuadGroup:
         if lvl not in (LEVEL_POS, LEVEL_RATE, LEVEL_MOTOR):
             raise ValidationError(f"bad level {level!r}")
         want = 7 if lvl == LEVEL_POS else 4
-        t = values if isinstance(values, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(values, dtype=np.float32))
+        if isinstance(values, torch.Tensor) and (values.is_cuda or values.dtype == torch.float32):
+            t = values
+        else:
+            # host data in another precision: the same float32 conversion as
+            # apply_command (yaw reduction, saturation)
+            a = values.numpy() if isinstance(values, torch.Tensor) else np.asarray(values)
+            if a.dtype != np.float32 and a.ndim == 2 and (a.shape[0] if columns else a.shape[1]) == want:
+                rows = a.T if columns else a
+                full = np.zeros((rows.shape[0], 7))
+                full[:, :want] = rows
+                conv = f32_commands(full, np.full(rows.shape[0], lvl == LEVEL_POS))[:, :want]
+                a = conv.T if columns else conv
+            t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32))
         if t.dim() != 2 or (t.shape[0] if columns else t.shape[1]) != want:
             raise ValidationError(f"setpoints must be ({want}, count) / (count, {want})")
         count = int(t.shape[1] if columns else t.shape[0])

@@ -357,7 +357,51 @@ def gen_world() -> None:
     print(f"world: {WORLD_TICKS} ticks, events {events}")
 
 
+CFG1_N, CFG1_TICKS, CFG1_EVERY = 1000, 10_000, 1000
+
+
+def gen_cfg1() -> None:
+    """SURVEY.md 8(d) cfg1 at its stated size and horizon, through the reference
+    QuadGroup itself: 1,000 quads on the bench grid (3 m, z = 10), RATE hover
+    (0, 0, 0, m g) with initial rates 0.5 unit(N(0, I)) (test_control.py:
+    227-233), dt = 1 ms, 10,000 ticks; float64 checkpoints every 1,000 ticks.
+    Inputs are float32-representable (initial state, hover thrust, dt), so the
+    B200 path starts from the identical state and commands and the recorded
+    divergence is arithmetic only (the pattern of test_acceptance.py:38-68)."""
+    sc = scenarios.hover_rate(n=CFG1_N, ticks=CFG1_TICKS)
+
+    def f32(a):
+        return np.asarray(a, dtype=float).astype(np.float32).astype(np.float64)
+
+    dt = float(np.float32(sc.dt))
+    batch = batch_create(0, sc.n, f32(sc.pos), quat=f32(sc.quat), vel=f32(sc.vel), omega=f32(sc.omega))
+    init = dict(pos=batch.pos.copy(), vel=batch.vel.copy(), quat=batch.quat.copy(), omega=batch.omega.copy())
+    g = QuadGroup(0, batch, P)
+    vals = {}
+    for _, agent, lvl, v in sc.cmds:
+        vals[agent] = tuple(f32(v).tolist())
+        assert g.apply_command(make_cmd(agent, lvl, vals[agent]))
+    out = {f"init_{k}": v for k, v in init.items()}
+    out["cmd_values"] = np.array([vals[i] for i in range(sc.n)])
+    out["dt"], out["every"] = np.array(dt), np.array(CFG1_EVERY)
+    faults = 0
+    for t in range(CFG1_TICKS):
+        faults += len(g.step(dt))
+        if (t + 1) % CFG1_EVERY == 0:
+            b = g.batch
+            for k in ("pos", "vel", "quat", "omega"):
+                out[f"t{t + 1}_{k}"] = getattr(b, k).copy()
+            out[f"t{t + 1}_integral"] = g.pid_state.integral.copy()
+    assert faults == 0
+    np.savez_compressed(HERE / "cfg1.npz", **out)
+    print(f"cfg1: n={sc.n} ticks={CFG1_TICKS} checkpoints every {CFG1_EVERY}")
+
+
 if __name__ == "__main__":
+    if "--cfg1" in sys.argv:
+        gen_cfg1()
+        sys.exit(0)
+    gen_cfg1()
     gen_world()
     gen_viewer()
     gen_unicycle()

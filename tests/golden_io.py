@@ -40,3 +40,8 @@ def load_viewer():
             c["cmd_level"], c["cmd_values"] = z[f"v{i}_cmd_level"], z[f"v{i}_cmd_values"]
         cases.append(c)
     return z["pos"], z["alive"], z["quat"], cases
+
+
+def load(name):
+    """A plain golden fixture tests/golden/<name>.npz as a dict."""
+    return dict(np.load(GOLDEN / f"{name}.npz"))

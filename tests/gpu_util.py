@@ -9,11 +9,11 @@ from oracle import oracle as orc
 # Per-step parity metric (north_star: per-step relative error <= 1e-5 in FP32).
 # err_q = max |x32 - x64| / max(|x64|_inf(row), floor_q), per quantity q, taken
 # over all rows after ONE step from an identical (float32-representable) state.
-# The floors are each quantity's natural scale: positions are in metres
-# (|p| up to ~150 m here), velocities in m/s, unit quaternions, body rates in
-# rad/s, PID integral in rad (clamped to i_limit = 0.2).
+# The floors are SURVEY.md 8(c)'s per-quantity absolute floors (s_pos = 1 m,
+# s_vel = 0.1 m/s, s_quat = 1, s_omega = 1e-3 rad/s, s_I = 1e-3): below them
+# a component counts as near zero and the error is taken against the floor.
 PER_STEP_TOL = 1e-5
-FLOORS = dict(pos=1.0, vel=1.0, quat=1.0, omega=1.0, integral=0.2)
+FLOORS = dict(pos=1.0, vel=0.1, quat=1.0, omega=1e-3, integral=1e-3)
 
 
 def make_group(sc_or_arrays, compensated=True, **kw):

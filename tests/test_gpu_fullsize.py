@@ -20,9 +20,10 @@ N = 10_000_000
 
 
 def _group():
-    from bench import _Batch, workload
+    from bench import _Batch
     from paper_2308_12698_b200 import B200QuadGroup
-    pos, sp = workload(N, seed=0)
+    from paper_2308_12698_b200.synthetic import swarm
+    pos, sp = swarm(N)
     g = B200QuadGroup(0, _Batch(N, pos, 0), device="cuda:0")
     g.set_setpoints(torch.from_numpy(sp).cuda(), columns=True)
     return g

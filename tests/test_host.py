@@ -221,3 +221,39 @@ def test_frame_layout_places_every_shard_block():
         sections.sort(key=lambda s: s[0])
         want = encode_frame(MSG_SNAPSHOT, struct.pack("<Q", 7) + b"".join(s for _, s in sections))
         assert frame.tobytes() == want
+
+
+def test_f32_commands_reduce_yaw_and_saturate():
+    """Host float64 -> float32 command conversion (group.f32_commands)."""
+    import math
+
+    from paper_2308_12698_b200.group import f32_commands
+    v = np.array([[1.0, 2.0, 3.0, 0.0, 0.0, 0.0, 0.3],            # in range: bit-exact cast
+                  [1e39, -2e39, 5.0, 0.0, 0.0, 0.0, 1000.3],       # saturate, reduce yaw
+                  [float("nan"), float("inf"), 0.0, 0.0, 0.0, 0.0, -7.0],
+                  [0.1, 0.2, 0.3, 9.81, 0.0, 0.0, 0.0]])           # a RATE row: no yaw column
+    out = f32_commands(v, np.array([True, True, True, False]))
+    assert out.dtype == np.float32
+    np.testing.assert_array_equal(out[0], v[0].astype(np.float32))
+    fmax = np.finfo(np.float32).max
+    assert out[1, 0] == fmax and out[1, 1] == -fmax and out[1, 2] == 5.0
+    assert abs(out[1, 6]) <= math.pi and abs(math.cos(out[1, 6]) - math.cos(1000.3)) < 2e-7
+    assert math.isnan(out[2, 0]) and out[2, 1] == np.inf               # non-finite values pass unchanged
+    assert abs(out[2, 6] - (-7.0 + 2 * math.pi)) < 1e-6
+    np.testing.assert_array_equal(out[3], v[3].astype(np.float32))
+
+
+def test_synthetic_swarm_slices_are_shard_independent():
+    """Any shard of the bench swarm builds exactly its own rows of one fixed
+    workload (bench.py ranks, the reference arm's host processes)."""
+    from paper_2308_12698_b200.synthetic import BLOCK, swarm
+    n = 3 * BLOCK + 123
+    pos, sp = swarm(n)
+    want_pos, _ = layout_poses({"kind": "grid", "spacing": 3.0, "origin": (0.0, 0.0, 10.0)}, n)
+    np.testing.assert_array_equal(pos, want_pos)
+    for w in (2, 3, 7):
+        parts = [swarm(n, *shard_range(n, r, w)) for r in range(w)]
+        np.testing.assert_array_equal(np.concatenate([p for p, _ in parts]), pos)
+        np.testing.assert_array_equal(np.concatenate([s for _, s in parts], axis=1), sp)
+    off = sp[:3].T.astype(np.float64) - pos
+    assert np.all(np.abs(off) <= 1.0 + 1e-5) and np.all(sp[3:6] == 0.0) and np.all(np.abs(sp[6]) <= np.pi)

@@ -24,10 +24,11 @@ VARIANTS = {
 CHILD = r'''
 import json, sys, torch, numpy as np
 sys.path.insert(0, "%(root)s")
-from bench import workload, _Batch
+from bench import _Batch
+from paper_2308_12698_b200.synthetic import swarm as workload
 from paper_2308_12698_b200 import B200QuadGroup
 n = %(n)d
-pos, sp = workload(n, 0)
+pos, sp = workload(n)
 g = B200QuadGroup(0, _Batch(n, pos, 0), device="cuda:0")
 g.set_setpoints(torch.from_numpy(sp).cuda(), columns=True)
 out = {}
