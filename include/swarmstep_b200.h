@@ -353,6 +353,21 @@ int swarmstep_p2p_pack_push(const swarmstep_group_view *g, void *const *peer_buf
                             uint32_t *arrive, void *stream);
 int swarmstep_p2p_wait(const uint32_t *local_signals, int world, uint32_t *epoch, void *stream);
 
+/* Single-process form of the fused exchange (one host process driving several
+ * shards: MultiDeviceQuadGroup, the drop-in for the single-process World,
+ * core.py:308-505).  Packs this shard's rows as float4 (NaN for dead / padding
+ * rows) straight into EVERY shard's gathered buffer: bufs is a device array
+ * [world] of float4 buffers, rows land at offset + rank * n_pad.  No signals:
+ * the caller orders each reader after every writer with CUDA events.  Buffers
+ * on other devices need swarmstep_enable_peer_access(reader_dev, writer_dev)
+ * first (NVLink peer stores). */
+int swarmstep_pack_scatter(const swarmstep_group_view *g, void *const *bufs, int world, int rank, int64_t n_pad,
+                           int64_t offset, void *stream);
+
+/* cudaDeviceEnablePeerAccess(peer) from `device` (idempotent; OK for device
+ * == peer).  SWARMSTEP_ENODEV when the pair has no peer access. */
+int swarmstep_enable_peer_access(int device, int peer);
+
 /* ---- device-resident setpoint feed ---------------------- */
 
 /* circle_swarm_strategy (client.py:55-73) + circle_reference (control.py:

@@ -43,7 +43,7 @@ EXPORTS = (
     "swarmstep_quad_circle_setpoints", "swarmstep_tick_add", "swarmstep_quad_pack_wire",
     "swarmstep_pack_collision", "swarmstep_collision_workspace_bytes", "swarmstep_collision_pairs",
     "swarmstep_unicycle_step", "swarmstep_swarm_stats_workspace_bytes", "swarmstep_quad_swarm_stats",
-    "swarmstep_p2p_pack_push", "swarmstep_p2p_wait",
+    "swarmstep_p2p_pack_push", "swarmstep_p2p_wait", "swarmstep_pack_scatter", "swarmstep_enable_peer_access",
     "swarmstep_op_deriv", "swarmstep_op_rk4", "swarmstep_op_mix", "swarmstep_op_rotor", "swarmstep_op_pid",
     "swarmstep_op_outer",
 )
@@ -135,6 +135,10 @@ def _declare(lib) -> None:
     lib.swarmstep_op_outer.argtypes = [i64] + [vp] * 9 + [vp, vp, vp, vp]
     lib.swarmstep_p2p_wait.restype = i32
     lib.swarmstep_p2p_wait.argtypes = [vp, i32, vp, vp]
+    lib.swarmstep_pack_scatter.restype = i32
+    lib.swarmstep_pack_scatter.argtypes = [view, vp, i32, i32, i64, i64, vp]
+    lib.swarmstep_enable_peer_access.restype = i32
+    lib.swarmstep_enable_peer_access.argtypes = [i32, i32]
     lib.swarmstep_quad_circle_setpoints.restype = i32
     lib.swarmstep_quad_circle_setpoints.argtypes = [view, vp, i64, f64, f64, f64, f64, f64, f64, vp]
     lib.swarmstep_quad_pack_wire.restype = i32

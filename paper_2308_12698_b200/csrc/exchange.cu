@@ -93,9 +93,68 @@ __global__ void wait_kernel(const uint32_t *signals, int world, uint32_t *epoch)
     if (threadIdx.x == 0) *epoch = E;
 }
 
+// Single-process variant (several devices, or several shards on one device):
+// the pack is the all-gather -- every thread stores its row's float4 into
+// every shard's gathered buffer (NVLink peer stores between devices with
+// peer access enabled) -- and completion is ordered by CUDA events on the
+// host side (each reader's stream waits for every writer's pack), so there
+// are no device-side signals or spins.
+__global__ void pack_scatter_kernel(const float *cols, const uint8_t *flags, int64_t n, int compensated,
+                                    int64_t n_pad, int world, int rank, float4 *const *bufs, int64_t offset)
+{
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n_pad) return;
+    const float nan = __int_as_float(0x7fc00000);
+    float4 p = make_float4(nan, nan, nan, 0.0f);
+    if (r < n && (flags[r] & SWARMSTEP_FLAG_ALIVE)) {
+        float x = cols[ssb::at(SWARMSTEP_COL_POS + 0, r)];
+        float y = cols[ssb::at(SWARMSTEP_COL_POS + 1, r)];
+        float z = cols[ssb::at(SWARMSTEP_COL_POS + 2, r)];
+        if (compensated) {
+            x += cols[ssb::at(SWARMSTEP_COL_POS_LO + 0, r)];
+            y += cols[ssb::at(SWARMSTEP_COL_POS_LO + 1, r)];
+            z += cols[ssb::at(SWARMSTEP_COL_POS_LO + 2, r)];
+        }
+        p = make_float4(x, y, z, 0.0f);
+    }
+    const int64_t dst = offset + (int64_t)rank * n_pad + r;
+    for (int q = 0; q < world; q++) bufs[q][dst] = p;
+}
+
 }  // namespace
 
 extern "C" {
+
+int swarmstep_pack_scatter(const swarmstep_group_view *g, void *const *bufs, int world, int rank, int64_t n_pad,
+                           int64_t offset, void *stream)
+{
+    if (!g || !g->cols || !g->flags || !bufs) return ssb::set_err(SWARMSTEP_EINVAL, "null argument");
+    if (world < 1 || rank < 0 || rank >= world) return ssb::set_err(SWARMSTEP_EINVAL, "bad world / rank");
+    if (n_pad < g->n || offset < 0) return ssb::set_err(SWARMSTEP_EINVAL, "n_pad < n or negative offset");
+    if (n_pad == 0) return SWARMSTEP_OK;
+    pack_scatter_kernel<<<(unsigned)((n_pad + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        g->cols, g->flags, g->n, g->compensated, n_pad, world, rank, (float4 *const *)bufs, offset);
+    return ssb::cuda_status("pack_scatter_kernel");
+}
+
+int swarmstep_enable_peer_access(int device, int peer)
+{
+    if (device == peer) return SWARMSTEP_OK;
+    int can = 0;
+    if (cudaDeviceCanAccessPeer(&can, device, peer) != cudaSuccess) return ssb::cuda_status("cudaDeviceCanAccessPeer");
+    if (!can) return ssb::set_err(SWARMSTEP_ENODEV, "no peer access between these devices");
+    int cur = 0;
+    if (cudaGetDevice(&cur) != cudaSuccess) return ssb::cuda_status("cudaGetDevice");
+    if (cudaSetDevice(device) != cudaSuccess) return ssb::cuda_status("cudaSetDevice");
+    const cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+    cudaSetDevice(cur);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();   // clear the (non-sticky) "already enabled" error
+        return SWARMSTEP_OK;
+    }
+    if (e != cudaSuccess) return ssb::cuda_status("cudaDeviceEnablePeerAccess");
+    return SWARMSTEP_OK;
+}
 
 int swarmstep_p2p_pack_push(const swarmstep_group_view *g, void *const *peer_bufs, int world, int rank,
                             int64_t n_pad, uint32_t *const *peer_signals, const uint32_t *epoch, uint32_t *arrive,

@@ -7,7 +7,17 @@ is one protocol-level group whose rows are sharded by contiguous index over
 ``devices`` ("contiguous agent-index ranges across 2/4/8
 devices, one stream per device, from a single host thread"): ``step`` launches
 every shard's fused kernel before waiting on any, so the devices run
-concurrently; agents are independent (quad.py:6-7), so there is no exchange.
+concurrently; agents are independent (quad.py:6-7), so stepping needs no
+exchange.
+
+The neighbour-coupled controller of config 5 does need every shard's
+positions each tick: ``MultiDeviceNeighborSeparation`` is its single-process
+form -- each shard's pack kernel stores its rows straight into every shard's
+gathered buffer (NVLink peer stores between devices, csrc/exchange.cu
+``swarmstep_pack_scatter``), CUDA events order every reader after every
+writer, and each shard then computes its overlay against the whole swarm on
+its own device (csrc/neighbors.cu), exactly as ``parallel.NeighborSeparation``
+does per rank.
 
 (``bench.py`` and ``parallel.ShardedSwarm`` cover the one-process-per-GPU
 layout; this class is the drop-in for an unchanged single-process World.)
@@ -15,10 +25,13 @@ layout; this class is the drop-in for an unchanged single-process World.)
 
 from __future__ import annotations
 
+import ctypes
 from collections.abc import Iterable
 
 import numpy as np
+import torch
 
+from . import _lib
 from .errors import ValidationError
 from .group import B200QuadGroup
 from .parallel import shard_range
@@ -199,3 +212,85 @@ class MultiDeviceQuadGroup:
 
     def alive_count(self) -> int:
         return sum(s.alive_count() for s in self.shards)
+
+
+class MultiDeviceNeighborSeparation:
+    """Config 5's separation controller over a ``MultiDeviceQuadGroup`` (one process).
+
+    Per tick (``apply()``, or ``step(dt)`` = apply + the group's step): every
+    shard packs its alive positions (float4, NaN for dead / padding rows) into
+    slot ``tick & 1`` of EVERY shard's gathered buffer -- the pack is the
+    all-gather, NVLink stores for shards on other devices -- then each shard's
+    stream waits for all packs (CUDA events) and the overlay kernel adds
+    v_i += sum_j k_sep (1 - d/r_sense) (p_i - p_j)/d over the whole swarm into
+    the shard's one-tick velocity overlay (core.py:137-139, 172-175).  The
+    double buffer lets a shard pack tick t+1 while another still reads tick t:
+    a pack of tick t+2 is stream-ordered after its shard's overlay of t+1,
+    which waited for every pack of t+1, each after its shard's overlay of t.
+    Overlays sum in fixed point, so results are bit-identical to one
+    ``B200QuadGroup`` under ``parallel.NeighborSeparation`` at world 1.
+    """
+
+    def __init__(self, mg: MultiDeviceQuadGroup, r_sense: float = 2.0, k_sep: float = 1.0,
+                 cell: float | None = None):
+        if not r_sense > 0.0:
+            raise ValidationError("r_sense must be positive")
+        self.mg = mg
+        self.r_sense, self.k_sep = float(r_sense), float(k_sep)
+        self.cell = float(cell) if cell is not None else float(r_sense)
+        if self.cell < self.r_sense:
+            raise ValidationError("cell must be >= r_sense")
+        self._lib = _lib.load()
+        shards = mg.shards
+        self.world = len(shards)
+        self.pad = max(s.n for s in shards)
+        self.n_all = self.world * self.pad
+        devs = sorted({s.device.index for s in shards})
+        for d in devs:                      # NVLink peer stores between the shards' devices
+            for q in devs:
+                _lib.check(self._lib.swarmstep_enable_peer_access(d, q))
+        self.bufs, self.ptrs, self.ws, self.events = [], [], [], []
+        nbytes = ctypes.c_uint64()
+        _lib.check(self._lib.swarmstep_neighbor_workspace_bytes(self.n_all, ctypes.byref(nbytes)))
+        for s in shards:
+            with torch.cuda.device(s.device), torch.cuda.stream(s.stream):
+                self.bufs.append(torch.full((2 * self.n_all, 4), float("nan"), dtype=torch.float32, device=s.device))
+                self.ws.append(torch.empty(int(nbytes.value), dtype=torch.uint8, device=s.device))
+        for s in shards:
+            with torch.cuda.device(s.device), torch.cuda.stream(s.stream):
+                self.ptrs.append(torch.tensor([b.data_ptr() for b in self.bufs], dtype=torch.int64, device=s.device))
+                self.events.append(torch.cuda.Event())
+        for s in shards:
+            s.stream.synchronize()
+        self.epoch = 0
+
+    def gathered_positions(self, shard: int = 0) -> torch.Tensor:
+        """(n_all, 4) positions of the last exchange as seen by ``shard``."""
+        s = self.mg.shards[shard]
+        s.stream.synchronize()
+        slot = (self.epoch - 1) & 1
+        return self.bufs[shard][slot * self.n_all:(slot + 1) * self.n_all]
+
+    def apply(self) -> None:
+        """This tick's exchange + overlay on every shard (asynchronous)."""
+        shards = self.mg.shards
+        off = (self.epoch & 1) * self.n_all
+        for j, s in enumerate(shards):
+            with torch.cuda.device(s.device):
+                _lib.check(self._lib.swarmstep_pack_scatter(s._view_ref, ctypes.c_void_p(self.ptrs[j].data_ptr()),
+                                                            self.world, j, self.pad, off, s._stream_h))
+            self.events[j].record(s.stream)
+        for i, s in enumerate(shards):
+            for ev in self.events:
+                s.stream.wait_event(ev)
+            with torch.cuda.device(s.device):
+                _lib.check(self._lib.swarmstep_neighbor_overlay(
+                    s._view_ref, self.bufs[i].data_ptr() + off * 16, self.n_all, i * self.pad,
+                    ctypes.c_float(self.r_sense), ctypes.c_float(self.k_sep), ctypes.c_float(self.cell), 1,
+                    self.ws[i].data_ptr(), ctypes.c_uint64(self.ws[i].numel()), None, s._stream_h))
+            s._overlay_active = True
+        self.epoch += 1
+
+    def step(self, dt: float) -> np.ndarray:
+        self.apply()
+        return self.mg.step(dt)

@@ -170,8 +170,8 @@ class NeighborSeparation:
         if self.cell < self.r_sense:
             raise ValidationError("cell must be >= r_sense")
         self.pg = process_group
-        if exchange not in ("nccl", "p2p"):
-            raise ValidationError(f"exchange must be 'nccl' or 'p2p', got {exchange!r}")
+        if exchange not in ("nccl", "p2p", "host"):
+            raise ValidationError(f"exchange must be 'nccl', 'p2p' or 'host', got {exchange!r}")
         self.exchange = exchange
         self._lib = _lib.load()
         dev = group.device
@@ -180,6 +180,14 @@ class NeighborSeparation:
         self._epoch = None
         if exchange == "p2p":
             self._init_p2p(dev)
+        elif exchange == "host":
+            # host-staged transport for CPU (gloo) process groups: the test
+            # harness of the multi-rank path on a one-GPU box, not a
+            # performance path (the device packs, the host gathers, the
+            # device computes the overlay)
+            self.local = torch.empty((shard.pad, 4), dtype=torch.float32, device=dev)
+            self.all = torch.empty((n_all, 4), dtype=torch.float32, device=dev)
+            self._h_parts = [torch.empty((shard.pad, 4), dtype=torch.float32) for _ in range(shard.world)]
         else:
             self.local = torch.empty((shard.pad, 4), dtype=torch.float32, device=dev)
             self.all = self.local if shard.world == 1 else torch.empty((n_all, 4), dtype=torch.float32, device=dev)
@@ -223,7 +231,15 @@ class NeighborSeparation:
         with torch.cuda.device(g.device), torch.cuda.stream(g.stream):
             _lib.check(self._lib.swarmstep_pack_positions(g._view_ref, self.local.data_ptr(), self.shard.pad,
                                                           ctypes.c_void_p(g.stream.cuda_stream)))
-            if self.shard.world > 1:
+            if self.exchange == "host":
+                import torch.distributed as dist
+                mine = self.local.cpu()                       # waits for the pack (stream order)
+                if self.shard.world > 1:
+                    dist.all_gather(self._h_parts, mine, group=self.pg)
+                else:
+                    self._h_parts[0].copy_(mine)
+                self.all.copy_(torch.cat(self._h_parts))
+            elif self.shard.world > 1:
                 import torch.distributed as dist
                 dist.all_gather_into_tensor(self.all, self.local, group=self.pg)
         return self.all
@@ -245,7 +261,7 @@ class NeighborSeparation:
         host state change; graph-capturable when world == 1 or with the P2P
         exchange, whose slot selection happens on the device)."""
         g = self.group
-        single = self.shard.world == 1 and self.exchange != "p2p"
+        single = self.shard.world == 1 and self.exchange == "nccl"
         if not single:
             self.gather()
         with torch.cuda.device(g.device), torch.cuda.stream(g.stream):

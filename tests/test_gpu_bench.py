@@ -51,12 +51,13 @@ def test_bench_two_rank_plumbing():
     env = dict(os.environ, SWARMSTEP_BENCH_BACKEND="gloo")
     p = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                         "--master-addr", "127.0.0.1", "--master-port", "29517", str(ROOT / "bench.py"),
-                        "--gpus", "2", "--agents", "200000", "--steps", "3", "--warmup", "3", "--cpu-samples", "1",
-                        "--cpu-seconds", "0.3", "--no-k1"], capture_output=True, text=True, timeout=900, env=env)
+                        "--gpus", "2", "--steps", "3", "--warmup", "3", "--cpu-samples", "1", "--cpu-seconds", "0.3",
+                        "--no-k1"], capture_output=True, text=True, timeout=900, env=env)
     assert p.returncode == 0, p.stderr[-3000:]
     lines = [ln for ln in p.stdout.strip().splitlines() if ln.startswith("{")]
     assert len(lines) == 1
     d = json.loads(lines[0])
-    assert d["n_gpus"] == 2 and d["config"]["agents_total"] == 200000 and d["scaling"] == "strong"
-    assert d["config"]["agents_per_gpu"] == 100000
+    # the default workload is cfg4: 10M agents in total, split over the ranks
+    assert d["n_gpus"] == 2 and d["config"]["agents_total"] == 10_000_000 and d["scaling"] == "strong"
+    assert d["config"]["agents_per_gpu"] == 5_000_000
     assert d["value"] > 0 and d["cpu_baseline"]["value"] > 0
