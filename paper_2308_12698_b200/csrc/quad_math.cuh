@@ -459,26 +459,7 @@ __device__ __forceinline__ void outer_row(const T p_err[3], const T v[3], const 
 #pragma unroll
     for (int i = 0; i < 3; i++) a[i] = fma(bc<T>(P.kp_pos[i]), p_err[i], mul(bc<T>(P.kv[i]), sub(v_sp[i], v[i])));
     a[2] = add(a[2], bc<T>(P.g));
-    T asq = fma(a[0], a[0], fma(a[1], a[1], mul(a[2], a[2])));
-    // |a|^2 beyond float32 range (setpoints near the float32 limit; the
-    // float64 reference has the range): only a's direction and the sign of
-    // z_body . a matter below (|a| >= 1.8e19 is never below the free-fall
-    // floor), so take them from a copy scaled by 2^-100 -- |a| <= ~41 FLT_MAX
-    // with saturated setpoints, so the scaled |a|^2 stays finite -- and scale
-    // the thrust back (it saturates at fc_max).  Finite rows skip this.
-    const mask_t<T> ovf = mnot(le(asq, bc<T>(3.4028234663852886e38f)));
-    if (any(ovf)) {
-        const T s = bc<T>(0x1p-100f);
-        T as[3];
-#pragma unroll
-        for (int i = 0; i < 3; i++)
-            as[i] = fma(bc<T>(P.kp_pos[i]), mul(p_err[i], s), mul(bc<T>(P.kv[i]), mul(sub(v_sp[i], v[i]), s)));
-        as[2] = add(as[2], mul(bc<T>(P.g), s));
-        const T asq_s = fma(as[0], as[0], fma(as[1], as[1], mul(as[2], as[2])));
-#pragma unroll
-        for (int i = 0; i < 3; i++) a[i] = sel(ovf, as[i], a[i]);
-        asq = sel(ovf, asq_s, asq);
-    }
+    const T asq = fma(a[0], a[0], fma(a[1], a[1], mul(a[2], a[2])));
     const T qw = q[0], qx = q[1], qy = q[2], qz = q[3];
     const T zb0 = mul(bc<T>(2.0f), fma(qx, qz, mul(qw, qy)));
     const T zb1 = mul(bc<T>(2.0f), fnma(qw, qx, mul(qy, qz)));
@@ -486,13 +467,12 @@ __device__ __forceinline__ void outer_row(const T p_err[3], const T v[3], const 
     const float amin = P.a_cmd_min;
     // free-fall floor (control.py:243-247): |a| < a_min -> z_des = e_z, |a| := a_min;
     // else m |a| (z_body . a/|a|) = m (z_body . a)
-    const mask_t<T> low = mand(lt(asq, bc<T>(amin * amin)), mnot(ovf));
+    const mask_t<T> low = lt(asq, bc<T>(amin * amin));
     const T ia = rsqrt_a(asq);
     z[0] = sel(low, zero, mul(a[0], ia));
     z[1] = sel(low, zero, mul(a[1], ia));
     z[2] = sel(low, one, mul(a[2], ia));
-    T fc = sel(low, mul(bc<T>(P.m * amin), zb2), mul(bc<T>(P.m), fma(zb0, a[0], fma(zb1, a[1], mul(zb2, a[2])))));
-    if (any(ovf)) fc = sel(ovf, mul(fc, bc<T>(0x1p100f)), fc);   // undo the 2^-100 (overflows to +-inf)
+    const T fc = sel(low, mul(bc<T>(P.m * amin), zb2), mul(bc<T>(P.m), fma(zb0, a[0], fma(zb1, a[1], mul(zb2, a[2])))));
     f_c_sp = vmin(vmax(fc, zero), bc<T>(P.fc_max));
 
     // y = z x x_c / |z x x_c| with x_c = (cy, sy, 0); degenerate fallback from y_c

@@ -301,12 +301,19 @@ def position_outer_loop(pos, vel, quat, alive, sp, params, gains) -> OuterResult
     w_sp, f_sp = torch.empty((n, 3), device=dev), torch.empty(n, device=dev)
     low = torch.empty(n, dtype=torch.uint8, device=dev)
     v, q, al = _f32(vel, (n, 3), dev), _f32(quat, (n, 4), dev), _u8(alive, n, dev)
-    if not as_torch:
-        # yaw enters only through cos / sin: reduce to [-pi, pi] in float64
-        # before the float32 rounding (group.f32_commands)
-        yaw = np.broadcast_to(np.asarray(yaw, dtype=np.float64), (n,))
-        yaw = yaw - np.round(yaw / (2.0 * np.pi)) * (2.0 * np.pi)
-    ps, vs, ys = _f32(sp.p_sp, (n, 3), dev), _f32(sp.v_sp, (n, 3), dev), _f32(yaw, (n,), dev)
+    if as_torch:
+        ps, vs, ys = _f32(sp.p_sp, (n, 3), dev), _f32(sp.v_sp, (n, 3), dev), _f32(yaw, (n,), dev)
+    else:
+        # the group's float32 command conversion (yaw reduced to [-pi, pi],
+        # setpoints beyond float32 range scaled: group.f32_commands)
+        from .group import f32_commands
+        cmd = np.empty((n, 7))
+        cmd[:, 0:3] = np.broadcast_to(np.asarray(sp.p_sp, dtype=np.float64), (n, 3))
+        cmd[:, 3:6] = np.broadcast_to(np.asarray(sp.v_sp, dtype=np.float64), (n, 3))
+        cmd[:, 6] = np.broadcast_to(np.asarray(yaw, dtype=np.float64), (n,))
+        c32 = f32_commands(cmd, np.ones(n, dtype=bool))
+        ps, vs, ys = (_f32(np.ascontiguousarray(c32[:, 0:3]), (n, 3), dev),
+                      _f32(np.ascontiguousarray(c32[:, 3:6]), (n, 3), dev), _f32(c32[:, 6].copy(), (n,), dev))
     _check(lib.swarmstep_op_outer(n, _p(p_hi), _p(p_lo), _p(v), _p(q), _p(al), _p(ps), _p(vs), _p(ys),
                                   ctypes.byref(P), _p(w_sp), _p(f_sp), _p(low), _stream()))
     if as_torch:

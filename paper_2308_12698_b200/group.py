@@ -44,6 +44,7 @@ _PINNED_MIRROR_MAX = 8_000_000   # agents: 0.83 GB of pinned float64 mirror
 
 _F32_MAX = float(np.finfo(np.float32).max)
 _TWO_PI = 2.0 * math.pi
+_POS_SCALE_MAX = 1e15
 
 
 def f32_commands(vals: np.ndarray, pos_rows) -> np.ndarray:
@@ -54,16 +55,30 @@ def f32_commands(vals: np.ndarray, pos_rows) -> np.ndarray:
       loop only uses cos / sin of yaw, control.py:252-256): a float32 yaw of
       |yaw| ~ 1000 rad would carry ~6e-5 rad of rounding, far above the 1e-5
       parity budget, the reduced one <= 1.2e-7;
-    * finite values beyond float32 range saturate at +-FLT_MAX instead of
-      becoming inf (the outer loop then takes the direction of an overflowing
-      acceleration command from a scaled copy, quad_math.cuh outer_row).
+    * POS position / velocity setpoints so large that the acceleration
+      command |a| = |kp (p_sp - p) + kv (v_sp - v) + g| would overflow
+      float32 when squared (the float64 reference has the range) are scaled
+      down together to |.| <= 1e15: the outer loop uses only a's direction and
+      the sign of z_body . a (the thrust saturates), and scaling both by one
+      factor moves that direction by ~|p| / 1e15 (< 1e-10 rad for any
+      position the float32 state can hold precisely);
+    * other finite values beyond float32 range saturate at +-FLT_MAX instead
+      of becoming inf.
     Non-finite values pass unchanged (they raise or fault like the reference).
     """
     v = np.array(vals, dtype=np.float64, copy=True).reshape(-1, 7)
+    pos_rows = np.asarray(pos_rows, dtype=bool).reshape(-1)
     y = v[pos_rows, 6]
     fin = np.isfinite(y)
     y[fin] -= np.round(y[fin] / _TWO_PI) * _TWO_PI
     v[pos_rows, 6] = y
+    pv = v[pos_rows, :6]
+    big = np.max(np.abs(np.where(np.isfinite(pv), pv, 0.0)), axis=1, initial=0.0) > _POS_SCALE_MAX
+    if big.any():
+        rows = np.flatnonzero(pos_rows)[big]
+        blk = v[rows, :6]
+        scale = _POS_SCALE_MAX / np.max(np.abs(np.where(np.isfinite(blk), blk, 0.0)), axis=1)
+        v[rows, :6] = blk * scale[:, None]
     fin = np.isfinite(v)
     v[fin] = np.clip(v[fin], -_F32_MAX, _F32_MAX)
     return v.astype(np.float32)

@@ -231,13 +231,17 @@ def test_f32_commands_reduce_yaw_and_saturate():
     v = np.array([[1.0, 2.0, 3.0, 0.0, 0.0, 0.0, 0.3],            # in range: bit-exact cast
                   [1e39, -2e39, 5.0, 0.0, 0.0, 0.0, 1000.3],       # saturate, reduce yaw
                   [float("nan"), float("inf"), 0.0, 0.0, 0.0, 0.0, -7.0],
-                  [0.1, 0.2, 0.3, 9.81, 0.0, 0.0, 0.0]])           # a RATE row: no yaw column
-    out = f32_commands(v, np.array([True, True, True, False]))
+                  [0.1, 0.2, 0.3, 9.81, 0.0, 0.0, 0.0],            # a RATE row: no yaw column
+                  [1e40, -3.0, 0.0, 0.0, 0.0, 0.0, 0.0]])          # RATE beyond float32: saturates
+    out = f32_commands(v, np.array([True, True, True, False, False]))
     assert out.dtype == np.float32
     np.testing.assert_array_equal(out[0], v[0].astype(np.float32))
     fmax = np.finfo(np.float32).max
-    assert out[1, 0] == fmax and out[1, 1] == -fmax and out[1, 2] == 5.0
+    # POS position / velocity setpoints scaled together to |.| <= 1e15 (direction kept)
+    np.testing.assert_allclose(out[1, :3], np.float32([5e14, -1e15, 2.5e-24]), rtol=1e-7)
+    assert np.all(out[1, 3:6] == 0.0)
     assert abs(out[1, 6]) <= math.pi and abs(math.cos(out[1, 6]) - math.cos(1000.3)) < 2e-7
+    assert out[4, 0] == fmax and out[4, 1] == -3.0
     assert math.isnan(out[2, 0]) and out[2, 1] == np.inf               # non-finite values pass unchanged
     assert abs(out[2, 6] - (-7.0 + 2 * math.pi)) < 1e-6
     np.testing.assert_array_equal(out[3], v[3].astype(np.float32))
