@@ -45,9 +45,10 @@ UNIT = "agent-steps/s"
 # 13 state + 6 PID floats + 1 flag byte = 77 B.
 ALG_BYTES_PER_AGENT_LAUNCH = 182
 # ... plus what this implementation also moves: the compensated
-# position's lo words (12 B read + 12 B written) and the stale inner-loop
-# setpoints written for a later MOTOR command (16 B) -- overhead, not algorithm
-BYTES_WITH_OVERHEAD = 221
+# position's packed low-part word (4 B read + 4 B written) and the stale
+# inner-loop setpoints written for a later MOTOR command (16 B) -- overhead,
+# not algorithm
+BYTES_WITH_OVERHEAD = 206
 # algorithmic flops per agent-tick at position level (FMA = 2)
 ALG_FLOPS_PER_AGENT_TICK = 705
 
@@ -348,7 +349,7 @@ def run_b200(args, rank: int, world: int) -> None:
               "bytes_basis": "SURVEY.md 8(d): 182 B per agent per launch (state, PID, setpoints, flags)",
               "with_overhead": {"bytes_per_agent": BYTES_WITH_OVERHEAD, "achieved": gbs_ovh,
                                 "frac": gbs_ovh / peaks["hbm_gbs"],
-                                "note": "182 B + position lo words (24 B) + stale MOTOR setpoints (16 B) as moved"},
+                                "note": "182 B + packed position low-part word (8 B) + stale MOTOR setpoints (16 B) as moved"},
               "ms_per_launch": t1 * 1e3, "agent_steps_per_s": n / t1, "peak_source": peaks["source"]}
 
     # ---- end-to-end leg through the public API with host buffers:

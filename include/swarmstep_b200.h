@@ -19,7 +19,7 @@
  *    Calls on distinct streams over distinct groups are thread-safe.
  *  - State is a tiled structure of arrays ("AoSoA") of float32: one column
  *    per scalar component, agents grouped in tiles of SWARMSTEP_TILE = 128;
- *    a tile stores its SWARMSTEP_NCOL columns contiguously (18,432 bytes),
+ *    a tile stores its SWARMSTEP_NCOL columns contiguously (17,408 bytes),
  *    so element (column c, row r) is
  *        cols[(r / 128) * (NCOL * 128) + c * 128 + r % 128].
  *    A warp's access to one component is one 128-byte line, every column
@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define SWARMSTEP_ABI_VERSION 2
+#define SWARMSTEP_ABI_VERSION 3
 
 enum {
     SWARMSTEP_OK = 0,
@@ -83,21 +83,28 @@ typedef struct swarmstep_quad_gains {
 } swarmstep_quad_gains;
 
 /* Column offsets inside a tile (each block is k consecutive columns).  The
- * order puts everything the step kernel reads first (cols [0, 29)) and keeps
- * the columns it writes in two runs ([0, 22) and [29, 33)). */
+ * order puts everything the step kernel reads first (cols [0, 27)) and keeps
+ * the columns it writes in two runs ([0, 20) and [27, 31)).
+ * COL_POS_LO is ONE 32-bit word per row holding the compensated-position
+ * low parts of x, y, z: bits [10 i, 10 i + 10) = signed q_i, and
+ * lo_i = q_i * ulp(hi_i) / 512 (ulp of the float32 position word hi_i; the
+ * unit is floored at 2^-126, the smallest normal float; ssb::pos_lo_* in
+ * csrc/common.cuh).
+ * |lo| <= ulp(hi)/2 always holds, so |q| <= 256: position carries 33
+ * significant bits in 4 bytes instead of 12. */
 #define SWARMSTEP_TILE 128
 enum {
     SWARMSTEP_COL_POS = 0,      /* px py pz          (state.py:57)          */
     SWARMSTEP_COL_VEL = 3,      /* vx vy vz                                 */
     SWARMSTEP_COL_QUAT = 6,     /* qw qx qy qz (scalar-first Hamilton)      */
     SWARMSTEP_COL_OMEGA = 10,   /* wx wy wz (body rates)                    */
-    SWARMSTEP_COL_POS_LO = 13,  /* compensated-position low words           */
-    SWARMSTEP_COL_INTEGRAL = 16,/* RatePidState.integral (control.py:103)   */
-    SWARMSTEP_COL_PREV = 19,    /* RatePidState.prev_omega                  */
-    SWARMSTEP_COL_CMD = 22,     /* QuadGroup.cmd_values[0..6] (core.py:99)  */
-    SWARMSTEP_COL_SP = 29,      /* QuadGroup.omega_sp xyz, f_c_sp (core.py:109-110) */
-    SWARMSTEP_COL_OVERLAY = 33, /* QuadGroup.v_overlay (core.py:106)        */
-    SWARMSTEP_NCOL = 36
+    SWARMSTEP_COL_POS_LO = 13,  /* packed compensated-position low parts    */
+    SWARMSTEP_COL_INTEGRAL = 14,/* RatePidState.integral (control.py:103)   */
+    SWARMSTEP_COL_PREV = 17,    /* RatePidState.prev_omega                  */
+    SWARMSTEP_COL_CMD = 20,     /* QuadGroup.cmd_values[0..6] (core.py:99)  */
+    SWARMSTEP_COL_SP = 27,      /* QuadGroup.omega_sp xyz, f_c_sp (core.py:109-110) */
+    SWARMSTEP_COL_OVERLAY = 31, /* QuadGroup.v_overlay (core.py:106)        */
+    SWARMSTEP_NCOL = 34
 };
 
 /* A borrowed view of one group's device columns. */

@@ -50,19 +50,46 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > mtime for p in deps)
 
 
+def _compile(src: Path, obj: Path, extra: list[str]) -> subprocess.CompletedProcess:
+    flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    return subprocess.run([_nvcc(), *flags, *extra, f"-I{INCLUDE}", f"-I{CSRC}", "-c", "-o", str(obj), str(src)],
+                          capture_output=True, text=True)
+
+
+def build_to(out: Path, extra: list[str] | None = None) -> str:
+    """Compile every translation unit (in parallel, one nvcc per file) and link
+    them into the shared library `out`; returns the ptxas report."""
+    import tempfile
+    from concurrent.futures import ThreadPoolExecutor
+
+    extra = list(extra or [])
+    srcs = sources()
+    with tempfile.TemporaryDirectory(prefix="ssb_build_") as tmpd:
+        objs = [Path(tmpd) / (s.stem + ".o") for s in srcs]
+        # the largest translation unit first: it bounds the wall time
+        order = sorted(range(len(srcs)), key=lambda i: -srcs[i].stat().st_size)
+        with ThreadPoolExecutor(max_workers=max(1, min(len(srcs), os.cpu_count() or 1))) as ex:
+            futs = {i: ex.submit(_compile, srcs[i], objs[i], extra) for i in order}
+            res = {i: f.result() for i, f in futs.items()}
+        for i in range(len(srcs)):
+            if res[i].returncode != 0:
+                raise RuntimeError(f"nvcc failed on {srcs[i].name} ({res[i].returncode}):\n{res[i].stderr[-4000:]}")
+        tmp = out.with_suffix(".so.tmp")
+        link = subprocess.run([_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
+                               "-o", str(tmp), *map(str, objs)], capture_output=True, text=True)
+        if link.returncode != 0:
+            raise RuntimeError(f"nvcc link failed ({link.returncode}):\n{link.stderr[-4000:]}")
+        os.replace(tmp, out)
+    return "".join(res[i].stderr for i in range(len(srcs)))
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not _stale():
         return LIB
-    tmp = LIB.with_suffix(".so.tmp")
-    cmd = [_nvcc(), *NVCC_FLAGS, f"-I{INCLUDE}", f"-I{CSRC}", "-o", str(tmp),
-           *[str(s) for s in sources()]]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    if res.returncode != 0:
-        raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stderr[-4000:]}")
+    report = build_to(LIB)
     if verbose:
-        sys.stderr.write(res.stderr)
-    os.replace(tmp, LIB)
-    (PKG / "ptxas_info.txt").write_text(res.stderr)
+        sys.stderr.write(report)
+    (PKG / "ptxas_info.txt").write_text(report)
     return LIB
 
 

@@ -20,12 +20,12 @@ if _OVERRIDE:
     LIB_PATH = Path(_OVERRIDE)
 
 SWARMSTEP_OK, SWARMSTEP_EINVAL, SWARMSTEP_ECUDA, SWARMSTEP_ENODEV = 0, -1, -2, -3
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 # column block offsets (SWARMSTEP_COL_*)
 COL_POS, COL_VEL, COL_QUAT, COL_OMEGA = 0, 3, 6, 10
-COL_POS_LO, COL_INTEGRAL, COL_PREV, COL_CMD, COL_SP, COL_OVERLAY = 13, 16, 19, 22, 29, 33
-NCOL = 36
+COL_POS_LO, COL_INTEGRAL, COL_PREV, COL_CMD, COL_SP, COL_OVERLAY = 13, 14, 17, 20, 27, 31
+NCOL = 34
 TILE = 128   # agents per tile of the tiled SoA layout (SWARMSTEP_TILE)
 FLAG_ALIVE, FLAG_HAS_PREV, LEVEL_SHIFT, LEVEL_MASK = 0x01, 0x02, 2, 0x0C
 # swarmstep_quad_step launch flags (SWARMSTEP_STEP_*)
@@ -47,6 +47,23 @@ EXPORTS = (
     "swarmstep_op_deriv", "swarmstep_op_rk4", "swarmstep_op_mix", "swarmstep_op_rotor", "swarmstep_op_pid",
     "swarmstep_op_outer",
 )
+
+
+def pos_lo_decode(words, hi):
+    """Low parts (n, 3) float64 of the packed COL_POS_LO words (uint32 (n,))
+    against the float32 position words hi (n, 3): the host restatement of
+    ssb::pos_lo_decode (csrc/common.cuh; layout in include/swarmstep_b200.h)."""
+    import numpy as np
+
+    w = np.asarray(words, dtype=np.uint32)
+    e = (np.asarray(hi, dtype=np.float32).view(np.uint32) >> np.uint32(23)) & np.uint32(0xFF)
+    unit = np.ldexp(1.0, np.maximum(e.astype(np.int64), 33) - 159)
+    out = np.empty(unit.shape, dtype=np.float64)
+    for i in range(3):
+        q = ((w >> np.uint32(10 * i)) & np.uint32(0x3FF)).astype(np.int64)
+        q = np.where(q >= 512, q - 1024, q)
+        out[:, i] = q * unit[:, i]
+    return out
 
 
 class CircleFeedParams(ctypes.Structure):

@@ -40,7 +40,7 @@ __global__ void pack_collision_kernel(const float *cols, const uint8_t *flags, i
     double *o = xyzr + 4 * (offset + r);
     for (int i = 0; i < 3; i++) {
         double p = (double)cols[ssb::at(SWARMSTEP_COL_POS + i, r)];
-        if (compensated) p += (double)cols[ssb::at(SWARMSTEP_COL_POS_LO + i, r)];
+        if (compensated) p += (double)ssb::pos_lo(cols, r, i);
         o[i] = p;
     }
     o[3] = (flags[r] & SWARMSTEP_FLAG_ALIVE) ? radius : __longlong_as_double(0x7ff8000000000000LL);  // NaN = dead

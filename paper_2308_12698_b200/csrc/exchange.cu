@@ -54,9 +54,9 @@ __global__ void pack_push_kernel(const float *cols, const uint8_t *flags, int64_
             float y = cols[ssb::at(SWARMSTEP_COL_POS + 1, r)];
             float z = cols[ssb::at(SWARMSTEP_COL_POS + 2, r)];
             if (compensated) {
-                x += cols[ssb::at(SWARMSTEP_COL_POS_LO + 0, r)];
-                y += cols[ssb::at(SWARMSTEP_COL_POS_LO + 1, r)];
-                z += cols[ssb::at(SWARMSTEP_COL_POS_LO + 2, r)];
+                x += ssb::pos_lo(cols, r, 0);
+                y += ssb::pos_lo(cols, r, 1);
+                z += ssb::pos_lo(cols, r, 2);
             }
             p = make_float4(x, y, z, 0.0f);
         }
@@ -111,9 +111,9 @@ __global__ void pack_scatter_kernel(const float *cols, const uint8_t *flags, int
         float y = cols[ssb::at(SWARMSTEP_COL_POS + 1, r)];
         float z = cols[ssb::at(SWARMSTEP_COL_POS + 2, r)];
         if (compensated) {
-            x += cols[ssb::at(SWARMSTEP_COL_POS_LO + 0, r)];
-            y += cols[ssb::at(SWARMSTEP_COL_POS_LO + 1, r)];
-            z += cols[ssb::at(SWARMSTEP_COL_POS_LO + 2, r)];
+            x += ssb::pos_lo(cols, r, 0);
+            y += ssb::pos_lo(cols, r, 1);
+            z += ssb::pos_lo(cols, r, 2);
         }
         p = make_float4(x, y, z, 0.0f);
     }

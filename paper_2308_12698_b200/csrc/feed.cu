@@ -90,8 +90,8 @@ __global__ void unicycle_kernel(float *cols, const uint8_t *flags, int64_t n, fl
     float qw = col(SWARMSTEP_COL_QUAT + 0), qx = col(SWARMSTEP_COL_QUAT + 1);
     float qy = col(SWARMSTEP_COL_QUAT + 2), qz = col(SWARMSTEP_COL_QUAT + 3);
     float th = atan2f(2.0f * (qw * qz + qx * qy), 1.0f - 2.0f * (qy * qy + qz * qz));   // quat.py:139-143
-    double px = (double)col(SWARMSTEP_COL_POS + 0) + (double)col(SWARMSTEP_COL_POS_LO + 0);
-    double py = (double)col(SWARMSTEP_COL_POS + 1) + (double)col(SWARMSTEP_COL_POS_LO + 1);
+    double px = ssb::pos_f64(cols, r, 0, true);
+    double py = ssb::pos_f64(cols, r, 1, true);
     float v_cmd = col(SWARMSTEP_COL_CMD + 0);
     const float w_cmd = col(SWARMSTEP_COL_CMD + 1);
     if (overlay_active) {
@@ -124,8 +124,11 @@ __global__ void unicycle_kernel(float *cols, const uint8_t *flags, int64_t n, fl
     const float hx = (float)px, hy = (float)py;
     col(SWARMSTEP_COL_POS + 0) = hx;
     col(SWARMSTEP_COL_POS + 1) = hy;
-    col(SWARMSTEP_COL_POS_LO + 0) = (float)(px - (double)hx);
-    col(SWARMSTEP_COL_POS_LO + 1) = (float)(py - (double)hy);
+    // packed low parts (common.cuh): new x, y fields, z's kept
+    const uint32_t low = __float_as_uint(col(SWARMSTEP_COL_POS_LO));
+    col(SWARMSTEP_COL_POS_LO) = __uint_as_float(ssb::pos_lo_field((float)(px - (double)hx), 0, hx) |
+                                                ssb::pos_lo_field((float)(py - (double)hy), 1, hy) |
+                                                (low & (0x3FFu << 20)));
     float s, co;
     sincosf(0.5f * th1, &s, &co);                     // yaw_quat (quat.py:129-136)
     col(SWARMSTEP_COL_QUAT + 0) = co;

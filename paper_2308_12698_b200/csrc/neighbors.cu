@@ -103,9 +103,9 @@ __global__ void pack_positions_kernel(const float *cols, const uint8_t *flags, i
         float y = cols[ssb::at(SWARMSTEP_COL_POS + 1, r)];
         float z = cols[ssb::at(SWARMSTEP_COL_POS + 2, r)];
         if (compensated) {
-            x += cols[ssb::at(SWARMSTEP_COL_POS_LO + 0, r)];
-            y += cols[ssb::at(SWARMSTEP_COL_POS_LO + 1, r)];
-            z += cols[ssb::at(SWARMSTEP_COL_POS_LO + 2, r)];
+            x += ssb::pos_lo(cols, r, 0);
+            y += ssb::pos_lo(cols, r, 1);
+            z += ssb::pos_lo(cols, r, 2);
         }
         p = make_float4(x, y, z, 0.0f);
     }
@@ -138,9 +138,9 @@ struct PosSrc {
             float y = cols[ssb::at(SWARMSTEP_COL_POS + 1, i)];
             float z = cols[ssb::at(SWARMSTEP_COL_POS + 2, i)];
             if (compensated) {
-                x += cols[ssb::at(SWARMSTEP_COL_POS_LO + 0, i)];
-                y += cols[ssb::at(SWARMSTEP_COL_POS_LO + 1, i)];
-                z += cols[ssb::at(SWARMSTEP_COL_POS_LO + 2, i)];
+                x += ssb::pos_lo(cols, i, 0);
+                y += ssb::pos_lo(cols, i, 1);
+                z += ssb::pos_lo(cols, i, 2);
             }
             p = make_float4(x, y, z, 0.0f);
         }

@@ -39,12 +39,13 @@ __global__ void op_deriv_kernel(int64_t n, const float *pos, const float *vel, c
     float dv[3] = {0, 0, 0}, dq[4] = {0, 0, 0, 0}, dw[3] = {0, 0, 0}, dp[3] = {0, 0, 0};
     if (!alive || alive[r]) {
         const float q[4] = {quat[4 * r], quat[4 * r + 1], quat[4 * r + 2], quat[4 * r + 3]};
-        const float h[3] = {0.5f * omega[3 * r], 0.5f * omega[3 * r + 1], 0.5f * omega[3 * r + 2]};
+        const float w[3] = {omega[3 * r], omega[3 * r + 1], omega[3 * r + 2]};
         const float fc = f_c[r];
         const float fc2 = ssb::mul(fc, 2.0f * P.inv_m), fcg = ssb::fma(fc, P.inv_m, -D.g);
         const float tI[3] = {ssb::mul(tau[3 * r], P.inv_ixx), ssb::mul(tau[3 * r + 1], P.inv_iyy),
                              ssb::mul(tau[3 * r + 2], P.inv_izz)};
-        ssb::deriv(q, h, fc2, fcg, tI, D, dv, dq, dw);
+        ssb::deriv(q, w, fc2, fcg, tI, D, dv, dq, dw);
+        for (int i = 0; i < 4; i++) dq[i] = 0.5f * dq[i];   // deriv returns 2 qdot (exact halving)
         for (int i = 0; i < 3; i++) dp[i] = vel[3 * r + i];
     }
     for (int i = 0; i < 3; i++) {
@@ -178,9 +179,11 @@ __global__ void op_outer_kernel(int64_t n, const float *pos, const float *pos_lo
             vs[i] = v_sp[3 * r + i];
         }
         for (int i = 0; i < 4; i++) q[i] = quat[4 * r + i];
-        float s, c;
+        float s, c, sh, ch;
         sincosf(yaw_sp[r], &s, &c);
-        ssb::outer_row(pe, v, q, vs, c, s, P, w_sp, f);
+        sincosf(0.5f * yaw_sp[r], &sh, &ch);
+        float S[3];
+        ssb::outer_row(pe, v, q, vs, c, s, ch, sh, P, w_sp, f, S);
         float asq = 0.0f;
         for (int i = 0; i < 3; i++) {
             float ai = ssb::fma(P.kp_pos[i], pe[i], ssb::mul(P.kv[i], ssb::sub(vs[i], v[i])));

@@ -177,12 +177,13 @@ template <class T> __device__ __forceinline__ T clip(T x, T lo, T hi)
 // ---------------------------------------------------------------------------
 struct Derived {
     float g;
-    float gx, gy, gz;        // 4 (I_zz - I_yy) / I_xx, ... (products of half rates)
+    float gx, gy, gz;        // (I_zz - I_yy) / I_xx, ... (gyroscopic coefficients)
     float kd_dt[3];          // kd / dt
     // RK4 step constants and 2: kernel parameters (uniform registers) rather
     // than values the kernel computes or materialises into vector registers,
     // so the FFMA2s using them read two vector registers (see fma below)
-    float dt, half_dt, quarter_dt, sixth_dt, two;
+    float dt, half_dt, quarter_dt, sixth_dt, twelfth_dt, two;
+    float dt2_sixth;         // dt^2 / 6: the position increment's acceleration weight
 };
 
 __host__ __device__ __forceinline__ Derived derive(const swarmstep_quad_params &P, float dt)
@@ -190,76 +191,129 @@ __host__ __device__ __forceinline__ Derived derive(const swarmstep_quad_params &
     Derived d;
     const float inv_dt = 1.0f / dt;
     d.g = P.g;
-    d.gx = 4.0f * (P.izz - P.iyy) * P.inv_ixx;
-    d.gy = 4.0f * (P.ixx - P.izz) * P.inv_iyy;
-    d.gz = 4.0f * (P.iyy - P.ixx) * P.inv_izz;
+    d.gx = (P.izz - P.iyy) * P.inv_ixx;
+    d.gy = (P.ixx - P.izz) * P.inv_iyy;
+    d.gz = (P.iyy - P.ixx) * P.inv_izz;
 #pragma unroll
     for (int i = 0; i < 3; i++) d.kd_dt[i] = P.kd[i] * inv_dt;
     d.dt = dt;
     d.half_dt = 0.5f * dt;
     d.quarter_dt = 0.25f * dt;
     d.sixth_dt = dt * (1.0f / 6.0f);
+    d.twelfth_dt = 0.5f * d.sixth_dt;
     d.two = 2.0f;
+    d.dt2_sixth = (float)((double)dt * (double)dt / 6.0);
     return d;
 }
 
-// d/dt of (v, q, w) at (q, h = w/2) for a held wrench (quad.py:222-310):
-//   vdot = (f_c/m) R(q) e_z - g e_z ; qdot = q (x) (0, h) ;
-//   wdot = tau/I - 4 c (h_j h_k)  (gyroscopic term, diagonal inertia).
-// fc2 = 2 f_c / m, fcg = f_c / m - g, tI = tau / I.
+// d/dt of (v, 2 q, w) at (q, w) for a held wrench (quad.py:222-310):
+//   vdot = (f_c/m) R(q) e_z - g e_z ; 2 qdot = q (x) (0, w) ;
+//   wdot = tau/I - c (w_j w_k)  (gyroscopic term, diagonal inertia).
+// fc2 = 2 f_c / m, fcg = f_c / m - g, tI = tau / I.  The quaternion rate is
+// returned doubled (the RK4 stage weights carry the 1/2): all three stage
+// inputs are then plain state values, and every product is the reference
+// formula's scaled by an exact power of two.
+// thrust direction terms of R(q) e_z = (2 S0, 2 S1, 1 - 2 S2):
+// S0 = qx qz + qw qy, S1 = qy qz - qw qx, S2 = qx^2 + qy^2
 template <class T>
-__device__ __forceinline__ void deriv(const T q[4], const T h[3], T fc2, T fcg, const T tI[3], const Derived &D,
-                                      T dv[3], T dq[4], T dw[3])
+__device__ __forceinline__ void thrust_terms(const T q[4], T S[3])
 {
     const T qw = q[0], qx = q[1], qy = q[2], qz = q[3];
-    const T hx = h[0], hy = h[1], hz = h[2];
-    dv[0] = mul_nc(fc2, fma(qx, qz, mul(qw, qy)));     // feed the RK4 stage sums
-    dv[1] = mul_nc(fc2, fnma(qw, qx, mul(qy, qz)));
-    dv[2] = fnma(fc2, fma(qx, qx, mul(qy, qy)), fcg);
-    dq[0] = neg(fma(qx, hx, fma(qy, hy, mul(qz, hz))));
-    dq[1] = fma(qw, hx, fnma(qz, hy, mul(qy, hz)));
-    dq[2] = fma(qw, hy, fnma(qx, hz, mul(qz, hx)));
-    dq[3] = fma(qw, hz, fnma(qy, hx, mul(qx, hy)));
-    dw[0] = fnma(bc<T>(D.gx), mul(hy, hz), tI[0]);
-    dw[1] = fnma(bc<T>(D.gy), mul(hz, hx), tI[1]);
-    dw[2] = fnma(bc<T>(D.gz), mul(hx, hy), tI[2]);
+    S[0] = fma(qx, qz, mul(qw, qy));
+    S[1] = fnma(qw, qx, mul(qy, qz));
+    S[2] = fma(qx, qx, mul(qy, qy));
+}
+
+// S: the thrust terms of q when the caller already has them (the outer loop
+// computed them from the same quaternion), else null
+template <class T>
+__device__ __forceinline__ void deriv(const T q[4], const T w[3], T fc2, T fcg, const T tI[3], const Derived &D,
+                                      T dv[3], T dq[4], T dw[3], const T *S = nullptr)
+{
+    const T qw = q[0], qx = q[1], qy = q[2], qz = q[3];
+    const T wx = w[0], wy = w[1], wz = w[2];
+    T St[3];
+    if (S == nullptr) {
+        thrust_terms(q, St);
+        S = St;
+    }
+    dv[0] = mul_nc(fc2, S[0]);     // feed the RK4 stage sums
+    dv[1] = mul_nc(fc2, S[1]);
+    dv[2] = fnma(fc2, S[2], fcg);
+    dq[0] = neg(fma(qx, wx, fma(qy, wy, mul(qz, wz))));
+    dq[1] = fma(qw, wx, fnma(qz, wy, mul(qy, wz)));
+    dq[2] = fma(qw, wy, fnma(qx, wz, mul(qz, wx)));
+    dq[3] = fma(qw, wz, fnma(qy, wx, mul(qx, wy)));
+    dw[0] = fnma(bc<T>(D.gx), mul(wy, wz), tI[0]);
+    dw[1] = fnma(bc<T>(D.gy), mul(wz, wx), tI[1]);
+    dw[2] = fnma(bc<T>(D.gz), mul(wx, wy), tI[2]);
 }
 
 // One classical RK4 step with the wrench held (quad.py:350-437), in place.
 // Returns, per lane, whether the row stays finite (the reference's fault
 // predicate, quad.py:404-430); a faulted lane's state is garbage and the
-// caller restores its pre-step values.  Position feeds no derivative, so only
-// its final combination is formed: dp = dt/6 (v + 2 v2 + 2 v3 + v4).
-template <class T, bool COMP>
+// caller restores its pre-step values.
+//
+// Position feeds no derivative and vdot depends on q alone, so the stage
+// velocities v + c k are never needed: RK4's position increment
+// dt/6 (v1 + 2 v2 + 2 v3 + v4) with v2 = v + dt/2 k1, v3 = v + dt/2 k2,
+// v4 = v + dt k3 is exactly dt v + dt^2/6 (k1 + k2 + k3), accumulated as it
+// goes (4 FMAs per axis instead of 7, and no stage-velocity registers).
+#ifndef SSB_POS_KSUM
+#define SSB_POS_KSUM 1
+#endif
+// ACC (compensated position only): p_lo is a launch-local accumulator of
+// the position increments against a p_hi held fixed for the whole launch
+// (|acc| grows to about K |v| dt, rounding at ulp(acc) instead of a Fast2Sum
+// per tick); the step kernels fold it back into (hi, lo) once per launch
+// (fold_position).  Without ACC each tick ends with the Fast2Sum
+// (the function-level rk4_step, ops.cu).
+template <class T, bool COMP, bool ACC = false>
 __device__ __forceinline__ mask_t<T> rk4_inplace(T p_hi[3], T p_lo[3], T v[3], T q[4], T w[3], T f_c,
                                                  const T tau[3], const swarmstep_quad_params &P,
-                                                 const Derived &D, float dt)
+                                                 const Derived &D, float dt, const T *S1 = nullptr)
 {
     const T half = bc<T>(D.half_dt), h6 = bc<T>(D.sixth_dt), dtv = bc<T>(D.dt);
-    const T qtr = bc<T>(D.quarter_dt), hdt = bc<T>(D.half_dt);  // stage steps on half rates
+    const T qtr = bc<T>(D.quarter_dt), h12 = bc<T>(D.twelfth_dt);  // weights of the doubled quaternion rate
     const T two = bc<T>(D.two);
     // fc2 = 2 f_c / m (exact doubling of f_c / m); fcg = f_c / m - g in one FMA
     const T fc2 = mul(f_c, bc<T>(2.0f * P.inv_m));
     const T fcg = fma(bc<T>(P.inv_m), f_c, bc<T>(-D.g));
     const T tI[3] = {mul(tau[0], bc<T>(P.inv_ixx)), mul(tau[1], bc<T>(P.inv_iyy)), mul(tau[2], bc<T>(P.inv_izz))};
     T kv[3], kq[4], kw[3];
-    T av[3], aq[4], aw[3], ap[3];
-    T sv[3], sq[4], sw[3];
-    const T hw[3] = {mul(bc<T>(0.5f), w[0]), mul(bc<T>(0.5f), w[1]), mul(bc<T>(0.5f), w[2])};
-
-    deriv(q, hw, fc2, fcg, tI, D, kv, kq, kw);                      // k1
+    T av[3], aq[4], aw[3];
+    T sq[4], sw[3];
+#if SSB_POS_KSUM
+    // b = (lo +) dt v, then + dt^2/6 k_i for the first three stages
+    const T d26 = bc<T>(D.dt2_sixth);
+    T b[3];
 #pragma unroll
-    for (int i = 0; i < 3; i++) { av[i] = kv[i]; aw[i] = kw[i]; ap[i] = v[i]; }
+    for (int i = 0; i < 3; i++) b[i] = COMP ? fma(dtv, v[i], p_lo[i]) : mul(dtv, v[i]);
+#else
+    T ap[3], sv[3];
+#pragma unroll
+    for (int i = 0; i < 3; i++) ap[i] = v[i];
+#endif
+
+    deriv(q, w, fc2, fcg, tI, D, kv, kq, kw, S1);                   // k1
+#pragma unroll
+    for (int i = 0; i < 3; i++) { av[i] = kv[i]; aw[i] = kw[i]; }
 #pragma unroll
     for (int i = 0; i < 4; i++) aq[i] = kq[i];
 #pragma unroll
     for (int s = 0; s < 2; s++) {                                   // k2, k3 at y + h/2 k
 #pragma unroll
-        for (int i = 0; i < 3; i++) { sv[i] = fma(half, kv[i], v[i]); sw[i] = fma(qtr, kw[i], hw[i]); }
+        for (int i = 0; i < 3; i++) {
+            sw[i] = fma(half, kw[i], w[i]);
+#if SSB_POS_KSUM
+            b[i] = fma(d26, kv[i], b[i]);
+#else
+            sv[i] = fma(half, kv[i], v[i]);
+            ap[i] = fma(two, sv[i], ap[i]);
+#endif
+        }
 #pragma unroll
-        for (int i = 0; i < 4; i++) sq[i] = fma(half, kq[i], q[i]);
-#pragma unroll
-        for (int i = 0; i < 3; i++) ap[i] = fma(two, sv[i], ap[i]);
+        for (int i = 0; i < 4; i++) sq[i] = fma(qtr, kq[i], q[i]);
         deriv(sq, sw, fc2, fcg, tI, D, kv, kq, kw);
 #pragma unroll
         for (int i = 0; i < 3; i++) { av[i] = fma(two, kv[i], av[i]); aw[i] = fma(two, kw[i], aw[i]); }
@@ -267,11 +321,17 @@ __device__ __forceinline__ mask_t<T> rk4_inplace(T p_hi[3], T p_lo[3], T v[3], T
         for (int i = 0; i < 4; i++) aq[i] = fma(two, kq[i], aq[i]);
     }
 #pragma unroll
-    for (int i = 0; i < 3; i++) { sv[i] = fma(dtv, kv[i], v[i]); sw[i] = fma(hdt, kw[i], hw[i]); }
+    for (int i = 0; i < 3; i++) {
+        sw[i] = fma(dtv, kw[i], w[i]);
+#if SSB_POS_KSUM
+        b[i] = fma(d26, kv[i], b[i]);
+#else
+        sv[i] = fma(dtv, kv[i], v[i]);
+        ap[i] = add(ap[i], sv[i]);
+#endif
+    }
 #pragma unroll
-    for (int i = 0; i < 4; i++) sq[i] = fma(dtv, kq[i], q[i]);
-#pragma unroll
-    for (int i = 0; i < 3; i++) ap[i] = add(ap[i], sv[i]);
+    for (int i = 0; i < 4; i++) sq[i] = fma(half, kq[i], q[i]);
     deriv(sq, sw, fc2, fcg, tI, D, kv, kq, kw);                     // k4
 #pragma unroll
     for (int i = 0; i < 3; i++) { av[i] = add(av[i], kv[i]); aw[i] = add(aw[i], kw[i]); }
@@ -283,20 +343,27 @@ __device__ __forceinline__ mask_t<T> rk4_inplace(T p_hi[3], T p_lo[3], T v[3], T
     for (int i = 0; i < 3; i++) {
         v[i] = fma(h6, av[i], v[i]);
         w[i] = fma(h6, aw[i], w[i]);
-        if (COMP) {
-            // Fast2Sum of hi and b = dt/6 ap + lo (one FMA): exact when
-            // |hi| >= |b| (a position against one tick's displacement);
+#if !SSB_POS_KSUM
+        if (!COMP) { p_hi[i] = fma(h6, ap[i], p_hi[i]); continue; }
+        const T b_i = fma(h6, ap[i], p_lo[i]);
+#else
+        const T b_i = b[i];
+#endif
+        if (COMP && ACC) {
+            p_lo[i] = b_i;
+        } else if (COMP) {
+            // Fast2Sum of hi and b (the increment plus the carried lo): exact
+            // when |hi| >= |b| (a position against one tick's displacement);
             // keeps |lo| <= ulp(hi)/2
-            const T b = fma(h6, ap[i], p_lo[i]);
-            const T sum = add(p_hi[i], b);
-            p_lo[i] = sub(b, sub(sum, p_hi[i]));
+            const T sum = add(p_hi[i], b_i);
+            p_lo[i] = sub(b_i, sub(sum, p_hi[i]));
             p_hi[i] = sum;
         } else {
-            p_hi[i] = fma(h6, ap[i], p_hi[i]);
+            p_hi[i] = add(p_hi[i], b_i);
         }
     }
 #pragma unroll
-    for (int i = 0; i < 4; i++) q[i] = fma(h6, aq[i], q[i]);
+    for (int i = 0; i < 4; i++) q[i] = fma(h12, aq[i], q[i]);
 
     // single post-step renormalisation; zero / non-finite norm is a fault
     const T nsq = fma(q[0], q[0], fma(q[1], q[1], fma(q[2], q[2], mul(q[3], q[3]))));
@@ -310,6 +377,18 @@ __device__ __forceinline__ mask_t<T> rk4_inplace(T p_hi[3], T p_lo[3], T v[3], T
     if (COMP) s = add(s, add(add(p_lo[0], p_lo[1]), p_lo[2]));
     const T chk = mul(bc<T>(0.0f), s);
     return mand(gt(nsq, bc<T>(0.0f)), eq(chk, bc<T>(0.0f)));
+}
+
+// Fast2Sum of a launch-local accumulator back into (hi, lo), |lo| <= ulp(hi)/2
+template <class T>
+__device__ __forceinline__ void fold_position(T p_hi[3], T p_lo[3])
+{
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+        const T sum = add(p_hi[i], p_lo[i]);
+        p_lo[i] = sub(p_lo[i], sub(sum, p_hi[i]));
+        p_hi[i] = sum;
+    }
 }
 
 // mix_to_motors (quad.py:143-168): realized wrench after per-motor clamp.
@@ -445,66 +524,24 @@ __device__ __forceinline__ T axis_angle_factor(T s, T c)
     return mul(mul(bc<T>(2.0f), sel(small, p, big)), r);
 }
 
-// position_outer_loop for alive rows (control.py:222-294): PD position loop
-// -> desired frame (z_des, yaw) with the degenerate-heading fallback ->
-// desired quaternion from the selected branch of _rotmats_to_quats
-// (control.py:190-213) -> axis-angle attitude error -> clipped rate setpoint.
-// cy / sy = cos / sin(yaw_sp) are hoisted by the caller.
+// _rotmats_to_quats (control.py:190-213) for the desired frame R = [x y z],
+// x = y x z, up to a positive scale: branch 0 (tr > 0), 1 (m00 largest),
+// 2 (m11 >= m22) or 3; branch k has t = 1 + (+-m00 +- m11 +- m22), s =
+// 2 sqrt(t), its own component s/4 and the others (m_ij +- m_ji)/s.  Any
+// positive scale of q_des leaves the outer loop's result unchanged (q_err is
+// linear in q_des and the axis-angle vector is scale invariant), so the
+// branch quaternion is formed scaled by s -- (t, m_ij +- m_ji) -- with no
+// square root.
 template <class T>
-__device__ __forceinline__ void outer_row(const T p_err[3], const T v[3], const T q[4], const T v_sp[3],
-                                          T cy, T sy, const swarmstep_quad_params &P, T w_sp[3], T &f_c_sp)
+__device__ __forceinline__ void frame_quat(const T yd[3], const T z[3], T qd[4])
 {
     const T zero = bc<T>(0.0f), one = bc<T>(1.0f);
-    T a[3], z[3];
-#pragma unroll
-    for (int i = 0; i < 3; i++) a[i] = fma(bc<T>(P.kp_pos[i]), p_err[i], mul(bc<T>(P.kv[i]), sub(v_sp[i], v[i])));
-    a[2] = add(a[2], bc<T>(P.g));
-    const T asq = fma(a[0], a[0], fma(a[1], a[1], mul(a[2], a[2])));
-    const T qw = q[0], qx = q[1], qy = q[2], qz = q[3];
-    const T zb0 = mul(bc<T>(2.0f), fma(qx, qz, mul(qw, qy)));
-    const T zb1 = mul(bc<T>(2.0f), fnma(qw, qx, mul(qy, qz)));
-    const T zb2 = fnma(bc<T>(2.0f), fma(qx, qx, mul(qy, qy)), one);
-    const float amin = P.a_cmd_min;
-    // free-fall floor (control.py:243-247): |a| < a_min -> z_des = e_z, |a| := a_min;
-    // else m |a| (z_body . a/|a|) = m (z_body . a)
-    const mask_t<T> low = lt(asq, bc<T>(amin * amin));
-    const T ia = rsqrt_a(asq);
-    z[0] = sel(low, zero, mul(a[0], ia));
-    z[1] = sel(low, zero, mul(a[1], ia));
-    z[2] = sel(low, one, mul(a[2], ia));
-    const T fc = sel(low, mul(bc<T>(P.m * amin), zb2), mul(bc<T>(P.m), fma(zb0, a[0], fma(zb1, a[1], mul(zb2, a[2])))));
-    f_c_sp = vmin(vmax(fc, zero), bc<T>(P.fc_max));
-
-    // y = z x x_c / |z x x_c| with x_c = (cy, sy, 0); degenerate fallback from y_c
-    T yd[3];
-    const T yr0 = neg(mul(z[2], sy)), yr1 = mul(z[2], cy), yr2 = fnma(z[1], cy, mul(z[0], sy));
-    const T nysq = fma(yr0, yr0, fma(yr1, yr1, mul(yr2, yr2)));
-    const T iy = rsqrt_a(nysq);
-    yd[0] = mul_nc(yr0, iy); yd[1] = mul_nc(yr1, iy); yd[2] = mul_nc(yr2, iy);   // feed m_ij +- m_ji
-    const mask_t<T> degen = mnot(ge(nysq, bc<T>(1e-12f)));
-    if (any(degen)) {
-        // x_alt = y_c x z, y_c = (-sy, cy, 0); y = z x x_alt / |x_alt|
-        const T xa0 = mul(cy, z[2]), xa1 = mul(sy, z[2]), xa2 = fnma(sy, z[1], neg(mul(cy, z[0])));
-        const T ix = rsqrt_a(fma(xa0, xa0, fma(xa1, xa1, mul(xa2, xa2))));
-        const T x0 = mul(xa0, ix), x1 = mul(xa1, ix), x2 = mul(xa2, ix);
-        yd[0] = sel(degen, fnma(z[2], x1, mul(z[1], x2)), yd[0]);
-        yd[1] = sel(degen, fnma(z[0], x2, mul(z[2], x0)), yd[1]);
-        yd[2] = sel(degen, fnma(z[1], x0, mul(z[0], x1)), yd[2]);
-    }
-    // x = y x z ;  R = [x y z] (columns)
     const T m00 = fnma(yd[2], z[1], mul(yd[1], z[2]));
     const T m10 = fnma(yd[0], z[2], mul(yd[2], z[0]));
     const T m20 = fnma(yd[1], z[0], mul(yd[0], z[1]));
     const T m01 = yd[0], m11 = yd[1], m21 = yd[2];
     const T m02 = z[0], m12 = z[1], m22 = z[2];
     const T tr = add(add(m00, m11), m22);
-    // _rotmats_to_quats selects branch 0 (tr > 0), 1 (m00 largest), 2 (m11 >=
-    // m22) or 3; branch k has t = 1 + (+-m00 +- m11 +- m22), s = 2 sqrt(t), its
-    // own component s/4 and the others (m_ij +- m_ji)/s.  Any positive scale
-    // of q_des leaves the result unchanged (q_err is linear in q_des and the
-    // axis-angle vector is scale invariant), so the branch quaternion is
-    // formed scaled by s -- (t, m_ij +- m_ji) -- with no square root, and
-    // neither q_des nor q_err is renormalised (identical in R).
     const mask_t<T> b0 = gt(tr, zero);
     const mask_t<T> b1 = mand(mnot(b0), mand(ge(m00, m11), ge(m00, m22)));
     const mask_t<T> b2 = mand(mand(mnot(b0), mnot(b1)), ge(m11, m22));
@@ -515,17 +552,136 @@ __device__ __forceinline__ void outer_row(const T p_err[3], const T v[3], const 
     const T t = vmax(add(add(add(one, s00), s11), s22), bc<T>(1e-30f));
     const T d21 = sub(m21, m12), d02 = sub(m02, m20), d10 = sub(m10, m01);
     const T a01 = add(m01, m10), a02 = add(m02, m20), a12 = add(m12, m21);
-    T qd[4];
     qd[0] = sel(b0, t, sel(b1, d21, sel(b2, d02, d10)));
     qd[1] = sel(b1, t, sel(b0, d21, sel(b2, a01, a02)));
     qd[2] = sel(b2, t, sel(b0, d02, sel(b1, a01, a12)));
     qd[3] = sel(b3, t, sel(b0, d10, sel(b1, a02, a12)));
+}
+
+// Desired quaternion of the degenerate-heading fallback (control.py:256-262):
+// x_alt = y_c x z with y_c = (-sy, cy, 0); y = z x x_alt / |x_alt|.
+template <class T>
+__device__ __forceinline__ void fallback_quat(const T z[3], T cy, T sy, T qd[4])
+{
+    const T xa0 = mul(cy, z[2]), xa1 = mul(sy, z[2]), xa2 = fnma(sy, z[1], neg(mul(cy, z[0])));
+    const T ix = rsqrt_a(fma(xa0, xa0, fma(xa1, xa1, mul(xa2, xa2))));
+    const T x0 = mul(xa0, ix), x1 = mul(xa1, ix), x2 = mul(xa2, ix);
+    T yd[3];
+    yd[0] = fnma(z[2], x1, mul(z[1], x2));
+    yd[1] = fnma(z[0], x2, mul(z[2], x0));
+    yd[2] = fnma(z[1], x0, mul(z[0], x1));
+    frame_quat(yd, z, qd);
+}
+
+// position_outer_loop for alive rows (control.py:222-294): PD position loop
+// -> desired frame (z_des, yaw) with the degenerate-heading fallback ->
+// desired quaternion (control.py:190-213) -> axis-angle attitude error ->
+// clipped rate setpoint.  cy / sy = cos / sin(yaw_sp) and ch / sh =
+// cos / sin(yaw_sp / 2) are hoisted by the caller (per launch).
+//
+// The desired frame (x_c = (cy, sy, 0), y = z x x_c / |z x x_c|, x = y x z)
+// is R = Rz(yaw) Rx(phi) Ry(theta): its y axis Rz Rx e_y is orthogonal to
+// x_c = Rz e_x, and with z' = Rz(-yaw) z = (sin th, -sin ph cos th,
+// cos ph cos th) the angles come from z' directly (cos th = |z x x_c|).  So
+// q_des = q_z(yaw) (x) q_x(phi) (x) q_y(theta) in closed form, each factor
+// from its (cos, sin) pair by the half-angle identity up to a positive scale
+// -- (1 + c, s) or (s, 1 - c) -- instead of building R and selecting a
+// branch of _rotmats_to_quats: the same rotation, 21 FP32 operations and
+// three selects instead of 27 and ~24 selects / compares per agent-tick.
+#ifndef SSB_QDES_CLOSED
+#define SSB_QDES_CLOSED 1
+#endif
+template <class T>
+__device__ __forceinline__ void outer_row(const T p_err[3], const T v[3], const T q[4], const T v_sp[3],
+                                          T cy, T sy, T ch, T sh, const swarmstep_quad_params &P, T w_sp[3],
+                                          T &f_c_sp, T S[3])
+{
+    const T zero = bc<T>(0.0f), one = bc<T>(1.0f);
+    T a[3], z[3];
+#pragma unroll
+    for (int i = 0; i < 3; i++) a[i] = fma(bc<T>(P.kp_pos[i]), p_err[i], mul(bc<T>(P.kv[i]), sub(v_sp[i], v[i])));
+    a[2] = add(a[2], bc<T>(P.g));
+    const T asq = fma(a[0], a[0], fma(a[1], a[1], mul(a[2], a[2])));
+    const T qw = q[0], qx = q[1], qy = q[2], qz = q[3];
+    // body z axis R(q) e_z = (2 S0, 2 S1, 1 - 2 S2); the RK4's first stage
+    // reuses S (same quaternion)
+    thrust_terms(q, S);
+    const float amin = P.a_cmd_min;
+    // free-fall floor (control.py:243-247): |a| < a_min -> z_des = e_z, |a| := a_min;
+    // else m |a| (z_body . a/|a|) = m (z_body . a) = m (a2 + 2 (S0 a0 + S1 a1 - S2 a2))
+    const mask_t<T> low = lt(asq, bc<T>(amin * amin));
+    const T ia = rsqrt_a(asq);
+    z[0] = sel(low, zero, mul(a[0], ia));
+    z[1] = sel(low, zero, mul(a[1], ia));
+    z[2] = sel(low, one, mul(a[2], ia));
+    const T za = fma(S[0], a[0], fnma(S[2], a[2], mul(S[1], a[1])));
+    const T fc = sel(low, fnma(bc<T>(2.0f * P.m * amin), S[2], bc<T>(P.m * amin)),
+                     fma(bc<T>(2.0f * P.m), za, mul(bc<T>(P.m), a[2])));
+    f_c_sp = vmin(vmax(fc, zero), bc<T>(P.fc_max));
+
+#if SSB_QDES_CLOSED
+    // z in the yaw frame; |z x x_c|^2 = z'1^2 + z'2^2 = cos^2 th
+    const T zp0 = fma(cy, z[0], mul(sy, z[1]));
+    const T zp1 = fnma(sy, z[0], mul(cy, z[1]));
+    const T zp2 = z[2];
+    const T nysq = fma(zp1, zp1, mul(zp2, zp2));
+    const T ct = sqrt_a(nysq);
+    // roll: cos th (1 + cos ph, sin ph) while z'2 >= 0, else cos th (sin ph, 1 - cos ph)
+    const mask_t<T> up = ge(zp2, zero);
+    const T ax = sel(up, add(ct, zp2), neg(zp1));
+    const T bx = sel(up, neg(zp1), sub(ct, zp2));
+    // pitch: (1 + cos th, sin th), cos th >= 0
+    const T ay = add(one, ct), by = zp0;
+    // q_err = conj(q) (x) q_des (quat.py:75-92) with q_des = q_z (x) q_x (x) q_y,
+    // multiplied left to right: each factor has two non-zero components
+    T e0, e1, e2, e3;
+    {
+        // conj(q) (x) (ch, 0, 0, sh)
+        const T p0 = fma(qw, ch, mul(qz, sh)), p1 = fnma(qx, ch, neg(mul(qy, sh)));
+        const T p2 = fma(qx, sh, neg(mul(qy, ch))), p3 = fnma(qz, ch, mul(qw, sh));
+        // (x) (ax, bx, 0, 0)
+        const T t0 = fnma(bx, p1, mul(ax, p0)), t1 = fma(bx, p0, mul(ax, p1));
+        const T t2 = fma(bx, p3, mul(ax, p2)), t3 = fnma(bx, p2, mul(ax, p3));
+        // (x) (ay, 0, by, 0)
+        e0 = fnma(by, t2, mul(ay, t0));
+        e1 = fnma(by, t3, mul(ay, t1));
+        e2 = fma(by, t0, mul(ay, t2));
+        e3 = fma(by, t1, mul(ay, t3));
+    }
+    const mask_t<T> degen = mnot(ge(nysq, bc<T>(1e-12f)));
+    if (any(degen)) {
+        T qa[4];
+        fallback_quat(z, cy, sy, qa);
+        e0 = sel(degen, fma(qw, qa[0], fma(qx, qa[1], fma(qy, qa[2], mul(qz, qa[3])))), e0);
+        e1 = sel(degen, fma(qw, qa[1], fnma(qx, qa[0], fnma(qy, qa[3], mul(qz, qa[2])))), e1);
+        e2 = sel(degen, fma(qw, qa[2], fma(qx, qa[3], fnma(qy, qa[0], neg(mul(qz, qa[1]))))), e2);
+        e3 = sel(degen, fma(qw, qa[3], fnma(qx, qa[2], fnma(qz, qa[0], mul(qy, qa[1])))), e3);
+    }
+#else
+    // y = z x x_c / |z x x_c| with x_c = (cy, sy, 0); degenerate fallback from y_c
+    T qd[4];
+    T yd[3];
+    const T yr0 = neg(mul(z[2], sy)), yr1 = mul(z[2], cy), yr2 = fnma(z[1], cy, mul(z[0], sy));
+    const T nysq = fma(yr0, yr0, fma(yr1, yr1, mul(yr2, yr2)));
+    const T iy = rsqrt_a(nysq);
+    yd[0] = mul_nc(yr0, iy); yd[1] = mul_nc(yr1, iy); yd[2] = mul_nc(yr2, iy);   // feed m_ij +- m_ji
+    const mask_t<T> degen = mnot(ge(nysq, bc<T>(1e-12f)));
+    frame_quat(yd, z, qd);
+    if (any(degen)) {
+        T qa[4];
+        fallback_quat(z, cy, sy, qa);
+#pragma unroll
+        for (int i = 0; i < 4; i++) qd[i] = sel(degen, qa[i], qd[i]);
+    }
+    (void)ch; (void)sh;
     // q_err = conj(q) (x) q_des (quat.py:75-92); the w >= 0 flip becomes |e_w|
     // and a sign on the rate setpoint
     const T e0 = fma(qw, qd[0], fma(qx, qd[1], fma(qy, qd[2], mul(qz, qd[3]))));
     const T e1 = fma(qw, qd[1], fnma(qx, qd[0], fnma(qy, qd[3], mul(qz, qd[2]))));
     const T e2 = fma(qw, qd[2], fma(qx, qd[3], fnma(qy, qd[0], neg(mul(qz, qd[1])))));
     const T e3 = fma(qw, qd[3], fnma(qx, qd[2], fnma(qz, qd[0], mul(qy, qd[1]))));
+#endif
+    // the w >= 0 flip of q_err becomes |e_w| and a sign on the rate setpoint
     const T ssq = fma(e1, e1, fma(e2, e2, mul(e3, e3)));
     T factor = axis_angle_factor(sqrt_a(ssq), vabs(e0));
     factor = sel(lt(e0, zero), neg(factor), factor);

@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(kThreads) swarm_stats_kernel(const float *cols
         double q[3];
         for (int i = 0; i < 3; i++) {
             q[i] = (double)cols[ssb::at(SWARMSTEP_COL_POS + i, r)];
-            if (compensated) q[i] += (double)cols[ssb::at(SWARMSTEP_COL_POS_LO + i, r)];
+            if (compensated) q[i] += (double)ssb::pos_lo(cols, r, i);
             a.lo[i] = fminf(a.lo[i], (float)q[i]);
             a.hi[i] = fmaxf(a.hi[i], (float)q[i]);
         }

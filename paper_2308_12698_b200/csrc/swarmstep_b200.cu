@@ -62,9 +62,10 @@ template <class T>
 struct RowT {
     T p_hi[3], p_lo[3], v[3], q[4], w[3], integ[3], prev[3];
     // u[]: per-launch setpoint registers, shared by the three levels
-    //   POS:   p_sp xyz, v_sp xyz (+ overlay on tick 0), cos(yaw), sin(yaw)
+    //   POS:   p_sp xyz, v_sp xyz (+ overlay on tick 0), cos(yaw), sin(yaw),
+    //          cos(yaw/2), sin(yaw/2)
     //   MOTOR: rotor-model wrench f_c, tau xyz (core.py:189-197)
-    T u[8];
+    T u[10];
     T w_sp[3], f_sp;   // inner-loop setpoints (stale ones for MOTOR rows)
 };
 using Row = RowT<float>;
@@ -82,7 +83,7 @@ __device__ __forceinline__ Row lane_row(const RowT<ssb::f2> &R, int i)
 #pragma unroll
     for (int k = 0; k < 4; k++) o.q[k] = ssb::lane(R.q[k], i);
 #pragma unroll
-    for (int k = 0; k < 8; k++) o.u[k] = ssb::lane(R.u[k], i);
+    for (int k = 0; k < 10; k++) o.u[k] = ssb::lane(R.u[k], i);
     o.f_sp = ssb::lane(R.f_sp, i);
     return o;
 }
@@ -187,6 +188,7 @@ struct CircleFeedRow {
 #pragma unroll
         for (int i = 0; i < 6; i++) R.u[i] = v[i];
         sincosf(v[6], &R.u[7], &R.u[6]);
+        sincosf(0.5f * v[6], &R.u[9], &R.u[8]);
     }
     // the command columns the unfused feed would have left: tick k's values
     template <class A> __device__ __forceinline__ void store_cmd(const A &C, int k) const
@@ -216,6 +218,10 @@ struct CircleFeedPair {
         sincosf(vb[6], &sb, &cb);
         R.u[6] = ssb::f2{make_float2(ca, cb)};
         R.u[7] = ssb::f2{make_float2(sa, sb)};
+        sincosf(0.5f * va[6], &sa, &ca);
+        sincosf(0.5f * vb[6], &sb, &cb);
+        R.u[8] = ssb::f2{make_float2(ca, cb)};
+        R.u[9] = ssb::f2{make_float2(sa, sb)};
     }
     template <class A> __device__ __forceinline__ void store_cmd(const A &C, int k) const
     {
@@ -227,6 +233,30 @@ struct CircleFeedPair {
     }
 };
 
+// packed compensated-position word <-> three float low parts (common.cuh)
+__device__ __forceinline__ void decode_lo(float w, const float hi[3], float lo[3])
+{
+#pragma unroll
+    for (int i = 0; i < 3; i++) lo[i] = ssb::pos_lo_decode(__float_as_uint(w), i, hi[i]);
+}
+__device__ __forceinline__ void decode_lo(ssb::f2 w, const ssb::f2 hi[3], ssb::f2 lo[3])
+{
+#pragma unroll
+    for (int i = 0; i < 3; i++)
+        lo[i] = ssb::f2{make_float2(ssb::pos_lo_decode(__float_as_uint(w.v.x), i, hi[i].v.x),
+                                    ssb::pos_lo_decode(__float_as_uint(w.v.y), i, hi[i].v.y))};
+}
+__device__ __forceinline__ float encode_lo(const float hi[3], const float lo[3])
+{
+    return __uint_as_float(ssb::pos_lo_encode(lo, hi));
+}
+__device__ __forceinline__ ssb::f2 encode_lo(const ssb::f2 hi[3], const ssb::f2 lo[3])
+{
+    const float ha[3] = {hi[0].v.x, hi[1].v.x, hi[2].v.x}, la[3] = {lo[0].v.x, lo[1].v.x, lo[2].v.x};
+    const float hb[3] = {hi[0].v.y, hi[1].v.y, hi[2].v.y}, lb[3] = {lo[0].v.y, lo[1].v.y, lo[2].v.y};
+    return ssb::f2{make_float2(__uint_as_float(ssb::pos_lo_encode(la, ha)), __uint_as_float(ssb::pos_lo_encode(lb, hb)))};
+}
+
 template <bool COMP, class T, class A>
 __device__ __forceinline__ void load_state(const A &C, RowT<T> &R)
 {
@@ -237,18 +267,25 @@ __device__ __forceinline__ void load_state(const A &C, RowT<T> &R)
         R.w[i] = C.ld(SWARMSTEP_COL_OMEGA + i);
         R.integ[i] = C.ld(SWARMSTEP_COL_INTEGRAL + i);
         R.prev[i] = C.ld(SWARMSTEP_COL_PREV + i);
-        R.p_lo[i] = COMP ? C.ld(SWARMSTEP_COL_POS_LO + i) : zero_t<T>();
+    }
+    if (COMP) {
+        decode_lo(C.ld(SWARMSTEP_COL_POS_LO), R.p_hi, R.p_lo);
+    } else {
+#pragma unroll
+        for (int i = 0; i < 3; i++) R.p_lo[i] = zero_t<T>();
     }
 #pragma unroll
     for (int i = 0; i < 4; i++) R.q[i] = C.ld(SWARMSTEP_COL_QUAT + i);
 #pragma unroll
     for (int i = 0; i < 7; i++) R.u[i] = C.ld(SWARMSTEP_COL_CMD + i);
-    R.u[7] = zero_t<T>();
+    R.u[7] = R.u[8] = R.u[9] = zero_t<T>();
 }
 
 template <bool COMP, class T, class A>
-__device__ __forceinline__ void store_state(const A &C, int level, const RowT<T> &R)
+__device__ __forceinline__ void store_state(const A &C, int level, RowT<T> &R)
 {
+    // the launch-local position accumulator back into (hi, lo) (rk4_inplace ACC)
+    if (COMP) ssb::fold_position(R.p_hi, R.p_lo);
 #pragma unroll
     for (int i = 0; i < 3; i++) {
         C.st(SWARMSTEP_COL_POS + i, R.p_hi[i]);
@@ -256,8 +293,8 @@ __device__ __forceinline__ void store_state(const A &C, int level, const RowT<T>
         C.st(SWARMSTEP_COL_OMEGA + i, R.w[i]);
         C.st(SWARMSTEP_COL_INTEGRAL + i, R.integ[i]);
         C.st(SWARMSTEP_COL_PREV + i, R.prev[i]);
-        if (COMP) C.st(SWARMSTEP_COL_POS_LO + i, R.p_lo[i]);
     }
+    if (COMP) C.st(SWARMSTEP_COL_POS_LO, encode_lo(R.p_hi, R.p_lo));
 #pragma unroll
     for (int i = 0; i < 4; i++) C.st(SWARMSTEP_COL_QUAT + i, R.q[i]);
     if (level != SWARMSTEP_LEVEL_MOTOR) {
@@ -287,10 +324,13 @@ __device__ __forceinline__ void setup_level(const A &C, int level, int overlay_a
     for (int i = 0; i < 3; i++) R.prev[i] = ssb::sel(has_prev, R.prev[i], R.w[i]);
     R.w_sp[0] = R.w_sp[1] = R.w_sp[2] = R.f_sp = zero_t<T>();
     if (level == SWARMSTEP_LEVEL_POS) {
-        T s, c;
+        T s, c, sh, ch;
         sincos_lane(R.u[6], s, c);
+        sincos_lane(ssb::mul(ssb::bc<T>(0.5f), R.u[6]), sh, ch);
         R.u[6] = c;
         R.u[7] = s;
+        R.u[8] = ch;
+        R.u[9] = sh;
         if (overlay_active) {
 #pragma unroll
             for (int i = 0; i < 3; i++) R.u[3 + i] = ssb::add(R.u[3 + i], C.ldc(SWARMSTEP_COL_OVERLAY + i));
@@ -348,12 +388,15 @@ __device__ __forceinline__ int run_ticks(const swarmstep_quad_params &P, const s
 {
 #pragma unroll kTickUnroll
     for (int k = 0; k < K; k++) {
+        T S[3];                 // thrust terms of the tick's quaternion (POS: from the outer loop)
+        const T *S1 = LEVEL == SWARMSTEP_LEVEL_POS ? S : nullptr;
         if (LEVEL == SWARMSTEP_LEVEL_POS) {
             if constexpr (L::feed_on) lag.feed(k, R);
+            const T *u = R.u;
             T p_err[3];
 #pragma unroll
-            for (int i = 0; i < 3; i++) p_err[i] = ssb::sub(ssb::sub(R.u[i], R.p_hi[i]), R.p_lo[i]);
-            ssb::outer_row(p_err, R.v, R.q, R.u + 3, R.u[6], R.u[7], P, R.w_sp, R.f_sp);
+            for (int i = 0; i < 3; i++) p_err[i] = ssb::sub(ssb::sub(u[i], R.p_hi[i]), R.p_lo[i]);
+            ssb::outer_row(p_err, R.v, R.q, u + 3, u[6], u[7], u[8], u[9], P, R.w_sp, R.f_sp, S);
         }
         T tau[3], f_c = R.f_sp;
         ssb::pid_row(R.w, R.w_sp, P, D, dt, R.integ, R.prev, tau);
@@ -370,7 +413,7 @@ __device__ __forceinline__ int run_ticks(const swarmstep_quad_params &P, const s
             }
             ssb::lag_thrust(lag.f, u, ssb::bc<T>(lag.phi), fbar);
             ssb::thrust_wrench(fbar, P, f_c, tau);
-            const auto ok = ssb::rk4_inplace<T, COMP>(R.p_hi, R.p_lo, R.v, R.q, R.w, f_c, tau, P, D, dt);
+            const auto ok = ssb::rk4_inplace<T, COMP, true>(R.p_hi, R.p_lo, R.v, R.q, R.w, f_c, tau, P, D, dt, S1);
             if (CHECK && ssb::any(ssb::mnot(ok))) return k;
             ssb::lag_thrust(lag.f, u, ssb::bc<T>(lag.e_full), lag.f);
         } else {
@@ -379,7 +422,7 @@ __device__ __forceinline__ int run_ticks(const swarmstep_quad_params &P, const s
             } else {
                 ssb::mix_row(f_c, tau, P);
             }
-            const auto ok = ssb::rk4_inplace<T, COMP>(R.p_hi, R.p_lo, R.v, R.q, R.w, f_c, tau, P, D, dt);
+            const auto ok = ssb::rk4_inplace<T, COMP, true>(R.p_hi, R.p_lo, R.v, R.q, R.w, f_c, tau, P, D, dt, S1);
             if (CHECK && ssb::any(ssb::mnot(ok))) return k;
         }
     }
@@ -846,7 +889,7 @@ __global__ void viewer_overlay_kernel(float *cols, const uint8_t *flags, int64_t
         double p[3];
         for (int i = 0; i < 3; i++) {
             p[i] = (double)cols[ssb::at(SWARMSTEP_COL_POS + i, r)];
-            if (compensated) p[i] += (double)cols[ssb::at(SWARMSTEP_COL_POS_LO + i, r)];
+            if (compensated) p[i] += (double)ssb::pos_lo(cols, r, i);
         }
         const double delta[3] = {__dadd_rn(px, -p[0]), __dadd_rn(py, -p[1]), __dadd_rn(pz, -p[2])};
         const double d = norm3_rn(delta[0], delta[1], delta[2]);
@@ -875,7 +918,7 @@ __global__ void retarget_kernel(float *cols, uint8_t *flags, int64_t n, int64_t 
     double p[3];
     for (int i = 0; i < 3; i++) {
         p[i] = (double)cols[ssb::at(SWARMSTEP_COL_POS + i, r)];
-        if (compensated) p[i] += (double)cols[ssb::at(SWARMSTEP_COL_POS_LO + i, r)];
+        if (compensated) p[i] += (double)ssb::pos_lo(cols, r, i);
     }
     // np.linalg.norm(pos - point, axis=1): ((dx^2 + dy^2) + dz^2), no contraction
     const double d = norm3_rn(__dadd_rn(p[0], -px), __dadd_rn(p[1], -py), __dadd_rn(p[2], -pz));
@@ -901,7 +944,7 @@ __global__ void pack_f64_kernel(const float *cols, const uint8_t *flags, int64_t
     for (int i = 0; i < 3; i++) {
         if (pos) {
             double p = cols[ssb::at(SWARMSTEP_COL_POS + i, r)];
-            if (compensated) p += (double)cols[ssb::at(SWARMSTEP_COL_POS_LO + i, r)];
+            if (compensated) p += (double)ssb::pos_lo(cols, r, i);
             pos[r * 3 + i] = p;
         }
         if (vel) vel[r * 3 + i] = cols[ssb::at(SWARMSTEP_COL_VEL + i, r)];
@@ -918,13 +961,17 @@ __global__ void unpack_f64_kernel(float *cols, uint8_t *flags, int64_t n, int64_
 {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n) return;
-    for (int i = 0; i < 3; i++) {
-        if (pos) {
+    if (pos) {
+        float hi[3], lo[3];
+        for (int i = 0; i < 3; i++) {
             const double p = pos[r * 3 + i];
-            const float hi = (float)p;
-            cols[ssb::at(SWARMSTEP_COL_POS + i, r)] = hi;
-            cols[ssb::at(SWARMSTEP_COL_POS_LO + i, r)] = compensated ? (float)(p - (double)hi) : 0.0f;
+            hi[i] = (float)p;
+            lo[i] = compensated ? (float)(p - (double)hi[i]) : 0.0f;
+            cols[ssb::at(SWARMSTEP_COL_POS + i, r)] = hi[i];
         }
+        cols[ssb::at(SWARMSTEP_COL_POS_LO, r)] = __uint_as_float(ssb::pos_lo_encode(lo, hi));
+    }
+    for (int i = 0; i < 3; i++) {
         if (vel) cols[ssb::at(SWARMSTEP_COL_VEL + i, r)] = (float)vel[r * 3 + i];
         if (omega) cols[ssb::at(SWARMSTEP_COL_OMEGA + i, r)] = (float)omega[r * 3 + i];
     }

@@ -40,7 +40,7 @@ __global__ void pack_wire_kernel(const float *cols, const uint8_t *flags, const 
     const bool aligned = ((9 * n) & 3) == 0;
     for (int i = 0; i < 3; i++) {
         double p = (double)cols[ssb::at(SWARMSTEP_COL_POS + i, r)];
-        if (compensated) p += (double)cols[ssb::at(SWARMSTEP_COL_POS_LO + i, r)];
+        if (compensated) p += (double)ssb::pos_lo(cols, r, i);
         put_f32(f + 4 * (3 * r + i), aligned, (float)p);
         put_f32(f + 4 * (3 * n + 3 * r + i), aligned, cols[ssb::at(SWARMSTEP_COL_VEL + i, r)]);
         put_f32(f + 4 * (10 * n + 3 * r + i), aligned, cols[ssb::at(SWARMSTEP_COL_OMEGA + i, r)]);

@@ -72,3 +72,34 @@ def rel_errors(gst: dict, og: orc.OracleGroup, rows=None) -> dict:
 
 def f32(dt: float) -> float:
     return float(np.float32(dt))
+
+
+# K fused ticks vs K one-tick launches.  Everything in a tick is the same
+# arithmetic either way; the compensated position differs only in where its
+# low part is folded and rounded: a fused launch carries the position
+# increments in a launch-local accumulator and folds it into (hi, lo) once,
+# a one-tick launch folds every tick, and the stored low part is rounded to
+# ulp(hi)/512 at every launch boundary (include/swarmstep_b200.h COL_POS_LO).
+# Without compensation the two are bit-identical (asserted separately).
+FUSION_TOL = 1e-6
+FUSION_FLOORS = dict(FLOORS, prev_omega=1e-3, omega_sp=1e-3, f_c_sp=1e-3)
+
+
+def fusion_errors(a: dict, b: dict, keys) -> dict:
+    """Per-quantity max |a - b| / max(|a|_row, floor) (same metric as rel_errors)."""
+    out = {}
+    for q in keys:
+        x, y = np.asarray(a[q], dtype=np.float64), np.asarray(b[q], dtype=np.float64)
+        if x.ndim == 1:
+            x, y = x[:, None], y[:, None]
+        scale = np.maximum(np.max(np.abs(x), axis=1, keepdims=True), FUSION_FLOORS.get(q, 1.0))
+        d = np.abs(x - y)
+        d[np.isnan(x) & np.isnan(y)] = 0.0
+        out[q] = float(np.max(d / scale)) if d.size else 0.0
+    return out
+
+
+def assert_fusion_close(a: dict, b: dict, keys, tol: float = FUSION_TOL):
+    err = fusion_errors(a, b, keys)
+    bad = {k: v for k, v in err.items() if not v <= tol}
+    assert not bad, f"fused vs one-tick launches differ beyond {tol}: {bad}"

@@ -34,7 +34,8 @@ def test_header_declares_what_binding_exports():
 def test_library_exports_every_declared_symbol(lib):
     for name in declared_functions():
         assert hasattr(lib, name), name
-    assert lib.swarmstep_abi_version() == 2
+    from paper_2308_12698_b200 import _lib as L
+    assert lib.swarmstep_abi_version() == L.ABI_VERSION == 3
     out = subprocess.run(["nm", "-D", "--defined-only", str(ROOT / "paper_2308_12698_b200" / "libswarmstep_b200.so")],
                          capture_output=True, text=True, check=True).stdout
     for name in declared_functions():

@@ -39,5 +39,5 @@ def test_c_host_matches_python_group(n, k, launches, tmp_path):
     for _ in range(launches):
         g.step_k(1e-3, k)
     p = g.batch.pos
-    assert c["abi"] == 2 and c["alive"] == n and c["faults"] == 0
+    assert c["abi"] == 3 and c["alive"] == n and c["faults"] == 0
     np.testing.assert_array_equal(np.fromfile(dump, dtype=np.float64).reshape(n, 3), p)

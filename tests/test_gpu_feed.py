@@ -25,12 +25,13 @@ def circle_reference(t, radius, omega, z, phase):
     return p, v, th + math.copysign(math.pi / 2, omega)
 
 
-def _circle_group(n, radius=5.0, z=10.0):
+def _circle_group(n, radius=5.0, z=10.0, compensated=True):
     ph = 2 * np.pi * np.arange(n) / n
     pos = np.stack([radius * np.cos(ph), radius * np.sin(ph), np.full(n, z)], axis=1)   # config.py:159-168
     yaw = ph + np.pi / 2
     q = np.stack([np.cos(yaw / 2), np.zeros(n), np.zeros(n), np.sin(yaw / 2)], axis=1)
-    return make_group(Scenario("circle", n, 2e-3, 1, pos, np.zeros((n, 3)), q, np.zeros((n, 3)), record=[]))
+    return make_group(Scenario("circle", n, 2e-3, 1, pos, np.zeros((n, 3)), q, np.zeros((n, 3)), record=[]),
+                      compensated=compensated)
 
 
 def test_circle_feed_setpoints():
@@ -121,17 +122,21 @@ def test_closed_loop_circle_demo_shape():
     assert worst_div < 1e-3, worst_div     # bounded divergence from the float64 oracle over 40 s
 
 
+@pytest.mark.parametrize("compensated", [False, True])
 @pytest.mark.parametrize("kern", ["direct", "pair"])
 @pytest.mark.parametrize("k", [1, 7, 25])
-def test_fused_circle_feed_bit_identical(k, kern):
+def test_fused_circle_feed_bit_identical(k, kern, compensated):
     """K ticks of the circle strategy evaluated inside one launch ==
     K x (feed kernel + 1-tick step): state, command columns, levels, faults
-    (row 9 faults on the first fed tick through a NaN D-term sample)."""
+    (row 9 faults on the first fed tick through a NaN D-term sample) -- bit
+    for bit with a plain float32 position; with the compensated position the
+    state agrees up to the low part's fold / storage rounding (FUSION_TOL)."""
+    from gpu_util import assert_fusion_close
     from paper_2308_12698_b200 import AgentCommand, CommandLevel
     from paper_2308_12698_b200.feed import CircleFeed
     outs = []
     for fused in (False, True):
-        g = _circle_group(300)
+        g = _circle_group(300, compensated=compensated)
         g.apply_command(AgentCommand(5, CommandLevel.RATE, (0.0, 0.0, 0.0, 20.0)))   # the feed moves it to POS
         g.mark_dead([7])
         g.step(2e-3)                       # tick 0 outside the feed
@@ -156,6 +161,8 @@ def test_fused_circle_feed_bit_identical(k, kern):
     for key in outs[0]:
         if key in ("faults", "tick"):
             assert outs[0][key] == outs[1][key], key
+        elif compensated and key in ("pos", "vel", "quat", "omega"):
+            assert_fusion_close(outs[0], outs[1], [key])
         else:
             np.testing.assert_array_equal(outs[0][key], outs[1][key], err_msg=key)
 

@@ -12,6 +12,8 @@ import os
 import numpy as np
 import pytest
 
+from paper_2308_12698_b200._lib import COL_OVERLAY
+
 from conftest import cuda_ok
 from gpu_util import PER_STEP_TOL, f32, gpu_state, oracle_twin, rel_errors
 from scenarios import Scenario
@@ -71,7 +73,7 @@ def test_fuzz_per_step_against_oracle(seed):
             g.add_velocity_overlay(rng.uniform(-1, 1, (sc.n, 3)))
         og = oracle_twin(g)
         if g._overlay_active:
-            og.add_velocity_overlay(g.column_block(33, 36).double().cpu().numpy().astype(np.float32).astype(float))
+            og.add_velocity_overlay(g.column_block(COL_OVERLAY, COL_OVERLAY + 3).double().cpu().numpy().astype(np.float32).astype(float))
         og_f = og.step(f32(sc.dt))
         g_f = g.step(sc.dt)
         assert sorted(g_f.tolist()) == sorted(og_f.tolist()), f"tick {t}: fault ids differ"
@@ -82,19 +84,30 @@ def test_fuzz_per_step_against_oracle(seed):
         assert v <= PER_STEP_TOL, f"seed {seed}: per-step {k} rel err {v:.2e}"
 
 
+@pytest.mark.parametrize("compensated", [False, True])
 @pytest.mark.parametrize("seed", range(max(6, N_SEEDS // 2)))
-def test_fuzz_kernels_and_fusion_bit_identical(seed):
-    from gpu_util import make_group
-    outs = []
+def test_fuzz_kernels_and_fusion_bit_identical(seed, compensated):
+    """Every kernel variant gives identical bits at the same ticks per launch;
+    fusing ticks is bit-identical with a plain float32 position and equal up to
+    the compensated low part's fold / storage rounding otherwise (FUSION_TOL)."""
+    from gpu_util import assert_fusion_close, make_group
+    outs = {}
     for kern, k in (("direct", 1), ("direct", 7), ("pair", 7), ("tma", 7), ("pair", 1)):
         rng, sc = _random_swarm(100 + seed)
-        g = make_group(sc)
+        g = make_group(sc, compensated=compensated)
         g.kernel = kern
         _commands(rng, g, sc)
         for _ in range(14 // k):
             g.step_k(sc.dt, k)
         st = gpu_state(g)
-        outs.append({q: st[q].copy() for q in ("pos", "vel", "quat", "omega", "integral", "prev_omega", "alive")})
-    for o in outs[1:]:
+        outs[(kern, k)] = {q: st[q].copy() for q in ("pos", "vel", "quat", "omega", "integral", "prev_omega",
+                                                     "alive")}
+    ref = {1: outs[("direct", 1)], 7: outs[("direct", 7)]}
+    for (kern, k), o in outs.items():
         for q in o:
-            np.testing.assert_array_equal(outs[0][q], o[q], err_msg=q)
+            np.testing.assert_array_equal(ref[k][q], o[q], err_msg=f"{kern} K={k} {q}")
+    for q in ref[1]:
+        if not compensated or q == "alive":
+            np.testing.assert_array_equal(ref[1][q], ref[7][q], err_msg=f"fused {q}")
+    if compensated:
+        assert_fusion_close(ref[1], ref[7], ("pos", "vel", "quat", "omega", "integral", "prev_omega"))

@@ -21,6 +21,8 @@ import socket
 import numpy as np
 import pytest
 
+from paper_2308_12698_b200._lib import COL_OVERLAY
+
 from conftest import cuda_ok
 
 pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_ok(), reason="needs CUDA")]
@@ -62,7 +64,7 @@ def _state(g):
 
 
 def _overlay(g):
-    return g.column_block(33, 36).cpu().numpy()
+    return g.column_block(COL_OVERLAY, COL_OVERLAY + 3).cpu().numpy()
 
 
 def _run(g, coupling, step, collect):

@@ -104,10 +104,14 @@ def test_per_step_large_random_swarm():
         assert v <= PER_STEP_TOL, f"per-step {k} rel err {v:.2e}"
 
 
-def test_fused_k_equals_k_single_steps():
-    """One launch of K substeps == K launches of one substep, bit for bit."""
+@pytest.mark.parametrize("compensated", [False, True])
+def test_fused_k_equals_k_single_steps(compensated):
+    """One launch of K substeps == K launches of one substep: bit for bit with
+    a plain float32 position; with the compensated position, equal up to the
+    position low part's fold / storage rounding (gpu_util.FUSION_TOL)."""
+    from gpu_util import assert_fusion_close
     sc = ALL["mixed"]()
-    g1, g2 = make_group(sc), make_group(sc)
+    g1, g2 = make_group(sc, compensated=compensated), make_group(sc, compensated=compensated)
     for g in (g1, g2):
         run_script(g, Scenario(**{**sc.__dict__, "ticks": 45, "record": []}))
     for _ in range(3):
@@ -115,8 +119,13 @@ def test_fused_k_equals_k_single_steps():
         for _ in range(10):
             g2.step(sc.dt)
     s1, s2 = gpu_state(g1), gpu_state(g2)
-    for k in ("pos", "vel", "quat", "omega", "integral", "prev_omega", "omega_sp", "f_c_sp"):
-        np.testing.assert_array_equal(s1[k], s2[k], err_msg=k)
+    keys = ("pos", "vel", "quat", "omega", "integral", "prev_omega", "omega_sp", "f_c_sp")
+    np.testing.assert_array_equal(s1["alive"], s2["alive"])
+    if not compensated:
+        for k in keys:
+            np.testing.assert_array_equal(s1[k], s2[k], err_msg=k)
+    else:
+        assert_fusion_close(s1, s2, keys)
 
 
 def test_fused_k_fault_substep_reporting():

@@ -5,6 +5,8 @@ size and at the config-5 size (100k agents, sampled rows)."""
 import numpy as np
 import pytest
 
+from paper_2308_12698_b200._lib import COL_OVERLAY
+
 from conftest import cuda_ok
 from gpu_util import make_group
 from oracle import oracle as orc
@@ -21,7 +23,7 @@ def _swarm(n, box, seed=0):
 
 
 def _overlay(g):
-    return g.column_block(33, 36).double().cpu().numpy()
+    return g.column_block(COL_OVERLAY, COL_OVERLAY + 3).double().cpu().numpy()
 
 
 def _positions(g):

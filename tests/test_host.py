@@ -261,3 +261,24 @@ def test_synthetic_swarm_slices_are_shard_independent():
         np.testing.assert_array_equal(np.concatenate([s for _, s in parts], axis=1), sp)
     off = sp[:3].T.astype(np.float64) - pos
     assert np.all(np.abs(off) <= 1.0 + 1e-5) and np.all(sp[3:6] == 0.0) and np.all(np.abs(sp[6]) <= np.pi)
+
+
+def test_pos_lo_decode_layout():
+    """The packed compensated-position word (include/swarmstep_b200.h COL_POS_LO):
+    10 signed bits per axis in units of ulp(hi) / 512, unit floored at 2^-126."""
+    import numpy as np
+
+    from paper_2308_12698_b200._lib import pos_lo_decode
+
+    hi = np.array([[1.0, 100.0, 1e-3], [0.0, -3.5, 2.0 ** -120]], dtype=np.float32)
+    q = np.array([[5, -256, 511], [0, 256, -511]])
+    words = np.zeros(2, dtype=np.uint32)
+    for i in range(3):
+        words |= ((q[:, i] & 0x3FF).astype(np.uint32) << np.uint32(10 * i))
+    lo = pos_lo_decode(words, hi)
+    ulp = np.spacing(np.abs(hi).astype(np.float32)).astype(np.float64)
+    unit = np.maximum(ulp / 512.0, 2.0 ** -126)
+    unit[1, 0] = 2.0 ** -126          # hi = 0: the floored unit
+    assert np.array_equal(lo, q * unit)
+    # |lo| <= ulp(hi) / 2 fits the 10-bit field with room to spare
+    assert np.all(np.abs(q) <= 511)

@@ -45,7 +45,7 @@ for k in (10, 4, 2, 1):
     ms = e0.elapsed_time(e1) / steps
     out[f"K{k}_ms"] = ms
     out[f"K{k}_agent_steps_per_s"] = n * k / ms * 1e3
-out["K1_GBps"] = 221 * n / out["K1_ms"] / 1e6
+out["K1_GBps_182B"] = 182 * n / out["K1_ms"] / 1e6
 out["kernel"] = g.kernel
 print("RESULT " + json.dumps(out))
 '''
