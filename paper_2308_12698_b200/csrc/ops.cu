@@ -183,7 +183,7 @@ __global__ void op_outer_kernel(int64_t n, const float *pos, const float *pos_lo
         sincosf(yaw_sp[r], &s, &c);
         sincosf(0.5f * yaw_sp[r], &sh, &ch);
         float S[3];
-        ssb::outer_row(pe, v, q, vs, c, s, ch, sh, P, w_sp, f, S);
+        ssb::outer_row(pe, v, q, vs, c, s, ch, sh, P, ssb::derive(P, 1.0f), w_sp, f, S);
         float asq = 0.0f;
         for (int i = 0; i < 3; i++) {
             float ai = ssb::fma(P.kp_pos[i], pe[i], ssb::mul(P.kv[i], ssb::sub(vs[i], v[i])));

@@ -170,6 +170,12 @@ template <class T> __device__ __forceinline__ T clip(T x, T lo, T hi)
 {
     return sel(lt(x, lo), lo, sel(gt(x, hi), hi, x));
 }
+// the same with NaN-propagating min / max (two ALU ops instead of two
+// compares and two selects; a -0 input comes out as +0)
+template <class T> __device__ __forceinline__ T clip_nan(T x, T lo, T hi)
+{
+    return vmin_nan(vmax_nan(x, lo), hi);
+}
 
 // ---------------------------------------------------------------------------
 // Per-launch constants derived from the per-type struct on the host and passed
@@ -184,6 +190,9 @@ struct Derived {
     // so the FFMA2s using them read two vector registers (see fma below)
     float dt, half_dt, quarter_dt, sixth_dt, twelfth_dt, two;
     float dt2_sixth;         // dt^2 / 6: the position increment's acceleration weight
+    // parameter combinations the per-tick code would otherwise recompute
+    float two_inv_m, neg_g, two_m, m_amin, two_m_amin, amin_sq, neg_w_sp_max, g_inv2_abs;
+    float neg_i_limit[3];
 };
 
 __host__ __device__ __forceinline__ Derived derive(const swarmstep_quad_params &P, float dt)
@@ -203,6 +212,15 @@ __host__ __device__ __forceinline__ Derived derive(const swarmstep_quad_params &
     d.twelfth_dt = 0.5f * d.sixth_dt;
     d.two = 2.0f;
     d.dt2_sixth = (float)((double)dt * (double)dt / 6.0);
+    d.two_inv_m = 2.0f * P.inv_m;
+    d.neg_g = -P.g;
+    d.two_m = 2.0f * P.m;
+    d.m_amin = P.m * P.a_cmd_min;
+    d.two_m_amin = 2.0f * P.m * P.a_cmd_min;
+    d.amin_sq = P.a_cmd_min * P.a_cmd_min;
+    d.neg_w_sp_max = -P.omega_sp_max;
+    d.g_inv2_abs = fabsf(P.G_inv[2]);
+    for (int i = 0; i < 3; i++) d.neg_i_limit[i] = -P.i_limit[i];
     return d;
 }
 
@@ -226,7 +244,8 @@ __device__ __forceinline__ void thrust_terms(const T q[4], T S[3])
 
 // S: the thrust terms of q when the caller already has them (the outer loop
 // computed them from the same quaternion), else null
-template <class T>
+// AXI: I_xx == I_yy, so D.gz == 0 exactly and wdot_z = tau_z / I_zz
+template <bool AXI = false, class T>
 __device__ __forceinline__ void deriv(const T q[4], const T w[3], T fc2, T fcg, const T tI[3], const Derived &D,
                                       T dv[3], T dq[4], T dw[3], const T *S = nullptr)
 {
@@ -246,7 +265,7 @@ __device__ __forceinline__ void deriv(const T q[4], const T w[3], T fc2, T fcg, 
     dq[3] = fma(qw, wz, fnma(qy, wx, mul(qx, wy)));
     dw[0] = fnma(bc<T>(D.gx), mul(wy, wz), tI[0]);
     dw[1] = fnma(bc<T>(D.gy), mul(wz, wx), tI[1]);
-    dw[2] = fnma(bc<T>(D.gz), mul(wx, wy), tI[2]);
+    dw[2] = AXI ? tI[2] : fnma(bc<T>(D.gz), mul(wx, wy), tI[2]);
 }
 
 // One classical RK4 step with the wrench held (quad.py:350-437), in place.
@@ -268,7 +287,7 @@ __device__ __forceinline__ void deriv(const T q[4], const T w[3], T fc2, T fcg, 
 // per tick); the step kernels fold it back into (hi, lo) once per launch
 // (fold_position).  Without ACC each tick ends with the Fast2Sum
 // (the function-level rk4_step, ops.cu).
-template <class T, bool COMP, bool ACC = false>
+template <class T, bool COMP, bool ACC = false, bool AXI = false>
 __device__ __forceinline__ mask_t<T> rk4_inplace(T p_hi[3], T p_lo[3], T v[3], T q[4], T w[3], T f_c,
                                                  const T tau[3], const swarmstep_quad_params &P,
                                                  const Derived &D, float dt, const T *S1 = nullptr)
@@ -277,8 +296,8 @@ __device__ __forceinline__ mask_t<T> rk4_inplace(T p_hi[3], T p_lo[3], T v[3], T
     const T qtr = bc<T>(D.quarter_dt), h12 = bc<T>(D.twelfth_dt);  // weights of the doubled quaternion rate
     const T two = bc<T>(D.two);
     // fc2 = 2 f_c / m (exact doubling of f_c / m); fcg = f_c / m - g in one FMA
-    const T fc2 = mul(f_c, bc<T>(2.0f * P.inv_m));
-    const T fcg = fma(bc<T>(P.inv_m), f_c, bc<T>(-D.g));
+    const T fc2 = mul(f_c, bc<T>(D.two_inv_m));
+    const T fcg = fma(bc<T>(P.inv_m), f_c, bc<T>(D.neg_g));
     const T tI[3] = {mul(tau[0], bc<T>(P.inv_ixx)), mul(tau[1], bc<T>(P.inv_iyy)), mul(tau[2], bc<T>(P.inv_izz))};
     T kv[3], kq[4], kw[3];
     T av[3], aq[4], aw[3];
@@ -295,7 +314,7 @@ __device__ __forceinline__ mask_t<T> rk4_inplace(T p_hi[3], T p_lo[3], T v[3], T
     for (int i = 0; i < 3; i++) ap[i] = v[i];
 #endif
 
-    deriv(q, w, fc2, fcg, tI, D, kv, kq, kw, S1);                   // k1
+    deriv<AXI>(q, w, fc2, fcg, tI, D, kv, kq, kw, S1);                   // k1
 #pragma unroll
     for (int i = 0; i < 3; i++) { av[i] = kv[i]; aw[i] = kw[i]; }
 #pragma unroll
@@ -314,7 +333,7 @@ __device__ __forceinline__ mask_t<T> rk4_inplace(T p_hi[3], T p_lo[3], T v[3], T
         }
 #pragma unroll
         for (int i = 0; i < 4; i++) sq[i] = fma(qtr, kq[i], q[i]);
-        deriv(sq, sw, fc2, fcg, tI, D, kv, kq, kw);
+        deriv<AXI>(sq, sw, fc2, fcg, tI, D, kv, kq, kw);
 #pragma unroll
         for (int i = 0; i < 3; i++) { av[i] = fma(two, kv[i], av[i]); aw[i] = fma(two, kw[i], aw[i]); }
 #pragma unroll
@@ -332,7 +351,7 @@ __device__ __forceinline__ mask_t<T> rk4_inplace(T p_hi[3], T p_lo[3], T v[3], T
     }
 #pragma unroll
     for (int i = 0; i < 4; i++) sq[i] = fma(half, kq[i], q[i]);
-    deriv(sq, sw, fc2, fcg, tI, D, kv, kq, kw);                     // k4
+    deriv<AXI>(sq, sw, fc2, fcg, tI, D, kv, kq, kw);                // k4
 #pragma unroll
     for (int i = 0; i < 3; i++) { av[i] = add(av[i], kv[i]); aw[i] = add(aw[i], kw[i]); }
 #pragma unroll
@@ -397,11 +416,11 @@ __device__ __forceinline__ void fold_position(T p_hi[3], T p_lo[3])
 // sign pattern of G's columns.  P.G_inv carries the exact inverse; the host
 // checks the pattern (params.py) and the kernel uses c = |G_inv[0][:]|.
 template <class T>
-__device__ __forceinline__ void mix_row(T &f_c, T tau[3], const swarmstep_quad_params &P)
+__device__ __forceinline__ void mix_row(T &f_c, T tau[3], const swarmstep_quad_params &P, const Derived &D)
 {
     // c0 f +- c1 tau_x and c2 tau_y -+ c3 tau_z, one product folded into an FMA
     const T A = mul(bc<T>(P.G_inv[1]), tau[0]), C = mul(bc<T>(P.G_inv[3]), tau[2]);
-    const T c0 = bc<T>(P.G_inv[0]), c2 = bc<T>(fabsf(P.G_inv[2]));
+    const T c0 = bc<T>(P.G_inv[0]), c2 = bc<T>(D.g_inv2_abs);
     const T FpA = fma(c0, f_c, A), FmA = fma(c0, f_c, neg(A)), BmC = fma(c2, tau[1], neg(C)), BpC = fma(c2, tau[1], C);
     T m[4] = {sub(FpA, BmC), sub(FmA, BpC), add(FmA, BpC), add(FpA, BmC)};
     const T lo = vmin(vmin(m[0], m[1]), vmin(m[2], m[3]));
@@ -409,7 +428,7 @@ __device__ __forceinline__ void mix_row(T &f_c, T tau[3], const swarmstep_quad_p
     const mask_t<T> sat = mor(lt(lo, bc<T>(0.0f)), gt(hi, bc<T>(P.f_max)));
     if (any(sat)) {
 #pragma unroll
-        for (int i = 0; i < 4; i++) m[i] = clip(m[i], bc<T>(0.0f), bc<T>(P.f_max));
+        for (int i = 0; i < 4; i++) m[i] = clip_nan(m[i], bc<T>(0.0f), bc<T>(P.f_max));
         const T fc_s = add(add(m[0], m[1]), add(m[2], m[3]));
         f_c = sel(sat, fc_s, f_c);
 #pragma unroll
@@ -449,10 +468,11 @@ __device__ __forceinline__ void motor_wrench(const float rpm[4], const swarmstep
 
 // clamped mixer motor thrusts m = clip(G^-1 [f_c, tau], 0, f_max) (quad.py:153-160)
 template <class T>
-__device__ __forceinline__ void mix_motors(T f_c, const T tau[3], const swarmstep_quad_params &P, T m[4])
+__device__ __forceinline__ void mix_motors(T f_c, const T tau[3], const swarmstep_quad_params &P, const Derived &D,
+                                           T m[4])
 {
     const T A = mul(bc<T>(P.G_inv[1]), tau[0]), C = mul(bc<T>(P.G_inv[3]), tau[2]);
-    const T c0 = bc<T>(P.G_inv[0]), c2 = bc<T>(fabsf(P.G_inv[2]));
+    const T c0 = bc<T>(P.G_inv[0]), c2 = bc<T>(D.g_inv2_abs);
     const T FpA = fma(c0, f_c, A), FmA = fma(c0, f_c, neg(A)), BmC = fma(c2, tau[1], neg(C)), BpC = fma(c2, tau[1], C);
     m[0] = sub(FpA, BmC); m[1] = sub(FmA, BpC); m[2] = add(FmA, BpC); m[3] = add(FpA, BmC);
 #pragma unroll
@@ -492,7 +512,7 @@ __device__ __forceinline__ void pid_row(const T w[3], const T w_sp[3], const swa
         const T e = sub(w_sp[a], w[a]);
         // min/max clamp: a NaN error (NaN rate command) faults the row this
         // tick regardless (tau is NaN), so NaN need not be kept in the state
-        integ[a] = vmin(vmax(fma(bc<T>(dt), e, integ[a]), bc<T>(-P.i_limit[a])), bc<T>(P.i_limit[a]));
+        integ[a] = vmin(vmax(fma(bc<T>(dt), e, integ[a]), bc<T>(D.neg_i_limit[a])), bc<T>(P.i_limit[a]));
         const T t = fma(bc<T>(P.kp[a]), e, mul(bc<T>(P.ki[a]), integ[a]));
         tau[a] = fnma(bc<T>(D.kd_dt[a]), sub(w[a], prev[a]), t);
         prev[a] = w[a];
@@ -501,8 +521,10 @@ __device__ __forceinline__ void pid_row(const T w[3], const T w_sp[3], const swa
 
 // 2 atan2(s, c) / s for s, c >= 0 (the axis-angle factor of control.py:283-285),
 // finite at s = 0 (-> 2/c): atan(t) = t P(t^2) on [0, 1], degree-8 minimax.
+// e0 < 0: the reference flips q_err to w >= 0 first (control.py:280-282),
+// which negates the axis -- folded into the factor's constant 2.
 template <class T>
-__device__ __forceinline__ T axis_angle_factor(T s, T c)
+__device__ __forceinline__ T axis_angle_factor(T s, T c, T e0)
 {
     const mask_t<T> small = le(s, c);
     const T num = sel(small, s, c), den = sel(small, c, s);
@@ -521,7 +543,8 @@ __device__ __forceinline__ T axis_angle_factor(T s, T c)
     // small: atan2 = t p, factor = 2 t p / s = 2 p / c
     // large: atan2 = pi/2 - t p, factor = 2 (pi/2 - t p) / s
     const T big = fnma(t, p, bc<T>(1.5707963267948966f));
-    return mul(mul(bc<T>(2.0f), sel(small, p, big)), r);
+    const T two = sel(lt(e0, bc<T>(0.0f)), bc<T>(-2.0f), bc<T>(2.0f));
+    return mul(mul(two, sel(small, p, big)), r);
 }
 
 // _rotmats_to_quats (control.py:190-213) for the desired frame R = [x y z],
@@ -593,8 +616,8 @@ __device__ __forceinline__ void fallback_quat(const T z[3], T cy, T sy, T qd[4])
 #endif
 template <class T>
 __device__ __forceinline__ void outer_row(const T p_err[3], const T v[3], const T q[4], const T v_sp[3],
-                                          T cy, T sy, T ch, T sh, const swarmstep_quad_params &P, T w_sp[3],
-                                          T &f_c_sp, T S[3])
+                                          T cy, T sy, T ch, T sh, const swarmstep_quad_params &P,
+                                          const Derived &D, T w_sp[3], T &f_c_sp, T S[3])
 {
     const T zero = bc<T>(0.0f), one = bc<T>(1.0f);
     T a[3], z[3];
@@ -606,30 +629,29 @@ __device__ __forceinline__ void outer_row(const T p_err[3], const T v[3], const 
     // body z axis R(q) e_z = (2 S0, 2 S1, 1 - 2 S2); the RK4's first stage
     // reuses S (same quaternion)
     thrust_terms(q, S);
-    const float amin = P.a_cmd_min;
     // free-fall floor (control.py:243-247): |a| < a_min -> z_des = e_z, |a| := a_min;
     // else m |a| (z_body . a/|a|) = m (z_body . a) = m (a2 + 2 (S0 a0 + S1 a1 - S2 a2))
-    const mask_t<T> low = lt(asq, bc<T>(amin * amin));
+    const mask_t<T> low = lt(asq, bc<T>(D.amin_sq));
     const T ia = rsqrt_a(asq);
     z[0] = sel(low, zero, mul(a[0], ia));
     z[1] = sel(low, zero, mul(a[1], ia));
     z[2] = sel(low, one, mul(a[2], ia));
     const T za = fma(S[0], a[0], fnma(S[2], a[2], mul(S[1], a[1])));
-    const T fc = sel(low, fnma(bc<T>(2.0f * P.m * amin), S[2], bc<T>(P.m * amin)),
-                     fma(bc<T>(2.0f * P.m), za, mul(bc<T>(P.m), a[2])));
+    const T fc = sel(low, fnma(bc<T>(D.two_m_amin), S[2], bc<T>(D.m_amin)),
+                     fma(bc<T>(D.two_m), za, mul(bc<T>(P.m), a[2])));
     f_c_sp = vmin(vmax(fc, zero), bc<T>(P.fc_max));
 
 #if SSB_QDES_CLOSED
     // z in the yaw frame; |z x x_c|^2 = z'1^2 + z'2^2 = cos^2 th
     const T zp0 = fma(cy, z[0], mul(sy, z[1]));
-    const T zp1 = fnma(sy, z[0], mul(cy, z[1]));
+    const T nzp1 = fnma(cy, z[1], mul(sy, z[0]));      // -z'1 = cos th sin ph
     const T zp2 = z[2];
-    const T nysq = fma(zp1, zp1, mul(zp2, zp2));
+    const T nysq = fma(nzp1, nzp1, mul(zp2, zp2));
     const T ct = sqrt_a(nysq);
     // roll: cos th (1 + cos ph, sin ph) while z'2 >= 0, else cos th (sin ph, 1 - cos ph)
     const mask_t<T> up = ge(zp2, zero);
-    const T ax = sel(up, add(ct, zp2), neg(zp1));
-    const T bx = sel(up, neg(zp1), sub(ct, zp2));
+    const T ax = sel(up, add(ct, zp2), nzp1);
+    const T bx = sel(up, nzp1, sub(ct, zp2));
     // pitch: (1 + cos th, sin th), cos th >= 0
     const T ay = add(one, ct), by = zp0;
     // q_err = conj(q) (x) q_des (quat.py:75-92) with q_des = q_z (x) q_x (x) q_y,
@@ -683,12 +705,11 @@ __device__ __forceinline__ void outer_row(const T p_err[3], const T v[3], const 
 #endif
     // the w >= 0 flip of q_err becomes |e_w| and a sign on the rate setpoint
     const T ssq = fma(e1, e1, fma(e2, e2, mul(e3, e3)));
-    T factor = axis_angle_factor(sqrt_a(ssq), vabs(e0));
-    factor = sel(lt(e0, zero), neg(factor), factor);
+    const T factor = axis_angle_factor(sqrt_a(ssq), vabs(e0), e0);
     // |w_sp| <= omega_sp_max, NaN propagating (np.clip): a NaN setpoint that
     // reached the device (the bulk feed does not screen) faults its row
     // through the PID and RK4 instead of flying a clamped garbage command
-    const T wm = bc<T>(P.omega_sp_max), nwm = bc<T>(-P.omega_sp_max);
+    const T wm = bc<T>(P.omega_sp_max), nwm = bc<T>(D.neg_w_sp_max);
     w_sp[0] = vmin_nan(vmax_nan(mul(bc<T>(P.k_att[0]), mul(e1, factor)), nwm), wm);
     w_sp[1] = vmin_nan(vmax_nan(mul(bc<T>(P.k_att[1]), mul(e2, factor)), nwm), wm);
     w_sp[2] = vmin_nan(vmax_nan(mul(bc<T>(P.k_att[2]), mul(e3, factor)), nwm), wm);

@@ -117,15 +117,21 @@ template <class T> __device__ __forceinline__ T zero_t() { return ssb::bc<T>(0.0
 // (every hot kernel).  MotorLag: the opt-in first-order rotor lag
 // (quad_math.cuh), scalar rows only; the four rotor thrusts live in their own
 // tiled array (4 columns x 128 rows per tile) next to the state.
-struct NoLag {
-    static constexpr bool lag_on = false, feed_on = false;
+// AXI: the inertia is axisymmetric (I_xx == I_yy, e.g. the default X quad):
+// the yaw gyroscopic coefficient (I_yy - I_xx) / I_zz is exactly 0 and the
+// derivative skips that term (deriv<AXI>).
+template <bool AXI>
+struct NoLagT {
+    static constexpr bool lag_on = false, feed_on = false, axisym = AXI;
     template <class T> __device__ __forceinline__ void feed(int, RowT<T> &) const {}
     template <class A> __device__ __forceinline__ void store_cmd(const A &, int) const {}
     __device__ __forceinline__ void load() {}
     __device__ __forceinline__ void store() const {}
 };
+using NoLag = NoLagT<false>;
+
 struct MotorLag {
-    static constexpr bool lag_on = true, feed_on = false;
+    static constexpr bool lag_on = true, feed_on = false, axisym = false;
     template <class T> __device__ __forceinline__ void feed(int, RowT<T> &) const {}
     template <class A> __device__ __forceinline__ void store_cmd(const A &, int) const {}
     float *p;          // this row's rotor-thrust column 0 (column i at p + 128 i)
@@ -145,7 +151,7 @@ struct MotorLag {
 
 // Two rows' rotor thrusts as one f2 lane pair (the paired kernel).
 struct MotorLagPair {
-    static constexpr bool lag_on = true, feed_on = false;
+    static constexpr bool lag_on = true, feed_on = false, axisym = false;
     template <class T> __device__ __forceinline__ void feed(int, RowT<T> &) const {}
     template <class A> __device__ __forceinline__ void store_cmd(const A &, int) const {}
     float *p0, *p1;          // rows t and t + 64 of one tile (column i at + 128 i)
@@ -172,7 +178,7 @@ struct MotorLagPair {
 // with this row's phase, computed exactly as circle_kernel computes it, so
 // the fused launch is bit-identical to K x (circle_kernel + 1-tick step).
 struct CircleFeedRow {
-    static constexpr bool lag_on = false, feed_on = true;
+    static constexpr bool lag_on = false, feed_on = true, axisym = false;
     int64_t tick0;
     double dt, radius, omega, z, phase;
     __device__ __forceinline__ void load() {}
@@ -202,7 +208,7 @@ struct CircleFeedRow {
 
 // Two rows' circle feeds as one f2 lane pair (the paired kernel).
 struct CircleFeedPair {
-    static constexpr bool lag_on = false, feed_on = true;
+    static constexpr bool lag_on = false, feed_on = true, axisym = false;
     CircleFeedRow a, b;
     __device__ __forceinline__ void load() {}
     __device__ __forceinline__ void store() const {}
@@ -396,7 +402,7 @@ __device__ __forceinline__ int run_ticks(const swarmstep_quad_params &P, const s
             T p_err[3];
 #pragma unroll
             for (int i = 0; i < 3; i++) p_err[i] = ssb::sub(ssb::sub(u[i], R.p_hi[i]), R.p_lo[i]);
-            ssb::outer_row(p_err, R.v, R.q, u + 3, u[6], u[7], u[8], u[9], P, R.w_sp, R.f_sp, S);
+            ssb::outer_row(p_err, R.v, R.q, u + 3, u[6], u[7], u[8], u[9], P, D, R.w_sp, R.f_sp, S);
         }
         T tau[3], f_c = R.f_sp;
         ssb::pid_row(R.w, R.w_sp, P, D, dt, R.integ, R.prev, tau);
@@ -409,20 +415,20 @@ __device__ __forceinline__ int run_ticks(const swarmstep_quad_params &P, const s
 #pragma unroll
                 for (int i = 0; i < 4; i++) u[i] = R.u[i];
             } else {
-                ssb::mix_motors(f_c, tau, P, u);
+                ssb::mix_motors(f_c, tau, P, D, u);
             }
             ssb::lag_thrust(lag.f, u, ssb::bc<T>(lag.phi), fbar);
             ssb::thrust_wrench(fbar, P, f_c, tau);
-            const auto ok = ssb::rk4_inplace<T, COMP, true>(R.p_hi, R.p_lo, R.v, R.q, R.w, f_c, tau, P, D, dt, S1);
+            const auto ok = ssb::rk4_inplace<T, COMP, true, L::axisym>(R.p_hi, R.p_lo, R.v, R.q, R.w, f_c, tau, P, D, dt, S1);
             if (CHECK && ssb::any(ssb::mnot(ok))) return k;
             ssb::lag_thrust(lag.f, u, ssb::bc<T>(lag.e_full), lag.f);
         } else {
             if (LEVEL == SWARMSTEP_LEVEL_MOTOR) {
                 f_c = R.u[0]; tau[0] = R.u[1]; tau[1] = R.u[2]; tau[2] = R.u[3];
             } else {
-                ssb::mix_row(f_c, tau, P);
+                ssb::mix_row(f_c, tau, P, D);
             }
-            const auto ok = ssb::rk4_inplace<T, COMP, true>(R.p_hi, R.p_lo, R.v, R.q, R.w, f_c, tau, P, D, dt, S1);
+            const auto ok = ssb::rk4_inplace<T, COMP, true, L::axisym>(R.p_hi, R.p_lo, R.v, R.q, R.w, f_c, tau, P, D, dt, S1);
             if (CHECK && ssb::any(ssb::mnot(ok))) return k;
         }
     }
@@ -507,7 +513,7 @@ __device__ __forceinline__ uint8_t step_row(const A &C, uint8_t fl, int64_t r, i
 }
 
 // ---- direct kernel: one row per thread, loads/stores straight to HBM -------
-template <bool COMP>
+template <bool COMP, bool AXI>
 __global__ void __launch_bounds__(kBlock, SSB_STEP_MINB)
 quad_step_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t n,
                  uint32_t *__restrict__ counters, uint64_t *__restrict__ fault_log,
@@ -528,7 +534,7 @@ quad_step_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t 
     __threadfence_block();
     if (!(fl & SWARMSTEP_FLAG_ALIVE)) return;  // dead rows are frozen (quad.py:395-437)
     const uint8_t nfl = step_row<COMP>(C, fl, r, overlay_active, P, D, dt, K, tick_base, tick_dev,
-                                       counters, fault_log, fault_cap, R, true);
+                                       counters, fault_log, fault_cap, R, true, NoLagT<AXI>());
     if (nfl != fl) flags[r] = nfl;
 }
 
@@ -647,7 +653,7 @@ __device__ __forceinline__ void pair_body(float *__restrict__ cols, uint8_t *__r
     }
 }
 
-template <bool COMP>
+template <bool COMP, bool AXI>
 __global__ void __launch_bounds__(64, SSB_PAIR_MINB)
 quad_step_pair_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t n,
                       uint32_t *__restrict__ counters, uint64_t *__restrict__ fault_log,
@@ -657,7 +663,7 @@ quad_step_pair_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int
     const int64_t r0 = (int64_t)blockIdx.x * SWARMSTEP_TILE + threadIdx.x;
     if (r0 >= n) return;
     pair_body<COMP>(cols, flags, n, counters, fault_log, fault_cap, overlay_active, tick_base, tick_dev, P, D, dt, K,
-                    r0, NoLag(), NoLag(), NoLag());
+                    r0, NoLagT<AXI>(), NoLagT<AXI>(), NoLagT<AXI>());
 }
 
 // the paired kernel with the opt-in rotor lag
@@ -1084,8 +1090,12 @@ int swarmstep_preload(void)
     // force-load every kernel of this translation unit (lazy module loading
     // must not happen inside a CUDA graph capture)
     cudaFuncAttributes a;
-    const void *fns[] = {(const void *)quad_step_kernel<true>, (const void *)quad_step_kernel<false>,
-                         (const void *)quad_step_pair_kernel<true>, (const void *)quad_step_pair_kernel<false>,
+    const void *fns[] = {(const void *)quad_step_kernel<true, false>, (const void *)quad_step_kernel<false, false>,
+                         (const void *)quad_step_kernel<true, true>, (const void *)quad_step_kernel<false, true>,
+                         (const void *)quad_step_pair_kernel<true, false>,
+                         (const void *)quad_step_pair_kernel<false, false>,
+                         (const void *)quad_step_pair_kernel<true, true>,
+                         (const void *)quad_step_pair_kernel<false, true>,
                          (const void *)quad_step_tma_kernel<true>, (const void *)quad_step_tma_kernel<false>,
                          (const void *)quad_step_lag_kernel<true>, (const void *)quad_step_lag_kernel<false>,
                          (const void *)quad_step_circle_kernel<true>, (const void *)quad_step_circle_kernel<false>,
@@ -1113,6 +1123,7 @@ int swarmstep_quad_step(const swarmstep_group_view *g, const swarmstep_quad_para
     if (!g->counters) return set_err(SWARMSTEP_EINVAL, "null counters");
     if (g->n == 0) return SWARMSTEP_OK;
     const ssb::Derived D = ssb::derive(*p, dt);
+    const bool axi = D.gz == 0.0f;   // I_xx == I_yy: the specialised step kernels (NoLagT)
     const int overlay = launch_flags & SWARMSTEP_STEP_OVERLAY;
     const int motor = (launch_flags & SWARMSTEP_STEP_MOTOR) ? 1 : 0;
     const bool use_tma = (launch_flags & SWARMSTEP_STEP_FORCE_DIRECT) ? false
@@ -1152,13 +1163,15 @@ int swarmstep_quad_step(const swarmstep_group_view *g, const swarmstep_quad_para
     }
     if (!(launch_flags & SWARMSTEP_STEP_FORCE_DIRECT) &&
         ((launch_flags & SWARMSTEP_STEP_FORCE_PAIR) || k_substeps >= SSB_PAIR_MIN_K)) {
-        auto kern = g->compensated ? quad_step_pair_kernel<true> : quad_step_pair_kernel<false>;
+        auto kern = axi ? (g->compensated ? quad_step_pair_kernel<true, true> : quad_step_pair_kernel<false, true>)
+                        : (g->compensated ? quad_step_pair_kernel<true, false> : quad_step_pair_kernel<false, false>);
         kern<<<(unsigned)((g->n + SWARMSTEP_TILE - 1) / SWARMSTEP_TILE), 64, 0, (cudaStream_t)stream>>>(
             g->cols, g->flags, g->n, g->counters, g->fault_log, fcap, overlay, tick_base, tick_dev, *p, D, dt,
             k_substeps);
         return cuda_status("quad_step_pair_kernel");
     }
-    auto kern = g->compensated ? quad_step_kernel<true> : quad_step_kernel<false>;
+    auto kern = axi ? (g->compensated ? quad_step_kernel<true, true> : quad_step_kernel<false, true>)
+                    : (g->compensated ? quad_step_kernel<true, false> : quad_step_kernel<false, false>);
     kern<<<grid_for(g->n, kBlock), kBlock, 0, (cudaStream_t)stream>>>(
         g->cols, g->flags, g->n, g->counters, g->fault_log, fcap, overlay, tick_base, tick_dev, *p, D, dt,
         k_substeps);
