@@ -180,8 +180,7 @@ __global__ void op_outer_kernel(int64_t n, const float *pos, const float *pos_lo
         }
         for (int i = 0; i < 4; i++) q[i] = quat[4 * r + i];
         float s, c, sh, ch;
-        sincosf(yaw_sp[r], &s, &c);
-        sincosf(0.5f * yaw_sp[r], &sh, &ch);
+        ssb::yaw_terms(yaw_sp[r], c, s, ch, sh);
         float S[3];
         ssb::outer_row(pe, v, q, vs, c, s, ch, sh, P, ssb::derive(P, 1.0f), w_sp, f, S);
         float asq = 0.0f;

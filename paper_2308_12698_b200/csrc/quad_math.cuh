@@ -165,6 +165,16 @@ __device__ __forceinline__ float f32_sat(double x)
     return isfinite(x) ? (float)fmin(fmax(x, -3.4028234663852886e38), 3.4028234663852886e38) : (float)x;
 }
 
+// cos / sin of the yaw setpoint and of its half (the outer loop's heading and
+// its quaternion factor): one sincos of yaw/2 and the double-angle formulas
+// (c = (ch - sh)(ch + sh), s = 2 sh ch; ~1e-7 absolute, like sincos itself)
+__device__ __forceinline__ void yaw_terms(float yaw, float &c, float &s, float &ch, float &sh)
+{
+    sincosf(0.5f * yaw, &sh, &ch);
+    c = __fmul_rn(__fsub_rn(ch, sh), __fadd_rn(ch, sh));
+    s = __fmul_rn(__fadd_rn(sh, sh), ch);
+}
+
 // np.clip semantics: NaN passes through
 template <class T> __device__ __forceinline__ T clip(T x, T lo, T hi)
 {
@@ -193,6 +203,11 @@ struct Derived {
     // parameter combinations the per-tick code would otherwise recompute
     float two_inv_m, neg_g, two_m, m_amin, two_m_amin, amin_sq, neg_w_sp_max, g_inv2_abs;
     float neg_i_limit[3];
+    // axisymmetric vehicle: I_xx == I_yy and every x / y gain pair equal (the
+    // default quad).  Kernels instantiated for it (AXI) read the x constants
+    // for y -- fewer distinct constants in the tick loop -- and drop the yaw
+    // gyroscopic term, whose coefficient (I_yy - I_xx) / I_zz is exactly 0.
+    int axisym;
 };
 
 __host__ __device__ __forceinline__ Derived derive(const swarmstep_quad_params &P, float dt)
@@ -221,6 +236,9 @@ __host__ __device__ __forceinline__ Derived derive(const swarmstep_quad_params &
     d.neg_w_sp_max = -P.omega_sp_max;
     d.g_inv2_abs = fabsf(P.G_inv[2]);
     for (int i = 0; i < 3; i++) d.neg_i_limit[i] = -P.i_limit[i];
+    d.axisym = P.ixx == P.iyy && P.inv_ixx == P.inv_iyy && P.kp[0] == P.kp[1] && P.ki[0] == P.ki[1] &&
+               P.kd[0] == P.kd[1] && P.i_limit[0] == P.i_limit[1] && P.kp_pos[0] == P.kp_pos[1] &&
+               P.kv[0] == P.kv[1] && P.k_att[0] == P.k_att[1];
     return d;
 }
 
@@ -231,6 +249,9 @@ __host__ __device__ __forceinline__ Derived derive(const swarmstep_quad_params &
 // returned doubled (the RK4 stage weights carry the 1/2): all three stage
 // inputs are then plain state values, and every product is the reference
 // formula's scaled by an exact power of two.
+// the constant index of axis i: y reads x's constants on an axisymmetric vehicle
+template <bool AXI> __host__ __device__ constexpr int axc(int i) { return (AXI && i == 1) ? 0 : i; }
+
 // thrust direction terms of R(q) e_z = (2 S0, 2 S1, 1 - 2 S2):
 // S0 = qx qz + qw qy, S1 = qy qz - qw qx, S2 = qx^2 + qy^2
 template <class T>
@@ -264,7 +285,8 @@ __device__ __forceinline__ void deriv(const T q[4], const T w[3], T fc2, T fcg, 
     dq[2] = fma(qw, wy, fnma(qx, wz, mul(qz, wx)));
     dq[3] = fma(qw, wz, fnma(qy, wx, mul(qx, wy)));
     dw[0] = fnma(bc<T>(D.gx), mul(wy, wz), tI[0]);
-    dw[1] = fnma(bc<T>(D.gy), mul(wz, wx), tI[1]);
+    // axisymmetric: c_y = (I_xx - I_zz) / I_yy = -c_x exactly
+    dw[1] = AXI ? fma(bc<T>(D.gx), mul(wz, wx), tI[1]) : fnma(bc<T>(D.gy), mul(wz, wx), tI[1]);
     dw[2] = AXI ? tI[2] : fnma(bc<T>(D.gz), mul(wx, wy), tI[2]);
 }
 
@@ -298,7 +320,8 @@ __device__ __forceinline__ mask_t<T> rk4_inplace(T p_hi[3], T p_lo[3], T v[3], T
     // fc2 = 2 f_c / m (exact doubling of f_c / m); fcg = f_c / m - g in one FMA
     const T fc2 = mul(f_c, bc<T>(D.two_inv_m));
     const T fcg = fma(bc<T>(P.inv_m), f_c, bc<T>(D.neg_g));
-    const T tI[3] = {mul(tau[0], bc<T>(P.inv_ixx)), mul(tau[1], bc<T>(P.inv_iyy)), mul(tau[2], bc<T>(P.inv_izz))};
+    const T tI[3] = {mul(tau[0], bc<T>(P.inv_ixx)), mul(tau[1], bc<T>(AXI ? P.inv_ixx : P.inv_iyy)),
+                     mul(tau[2], bc<T>(P.inv_izz))};
     T kv[3], kq[4], kw[3];
     T av[3], aq[4], aw[3];
     T sq[4], sw[3];
@@ -429,14 +452,15 @@ __device__ __forceinline__ void mix_row(T &f_c, T tau[3], const swarmstep_quad_p
     if (any(sat)) {
 #pragma unroll
         for (int i = 0; i < 4; i++) m[i] = clip_nan(m[i], bc<T>(0.0f), bc<T>(P.f_max));
-        const T fc_s = add(add(m[0], m[1]), add(m[2], m[3]));
-        f_c = sel(sat, fc_s, f_c);
-#pragma unroll
-        for (int i = 0; i < 3; i++) {
-            const T t = fma(bc<T>(P.G[(i + 1) * 4 + 0]), m[0], fma(bc<T>(P.G[(i + 1) * 4 + 1]), m[1],
-                        fma(bc<T>(P.G[(i + 1) * 4 + 2]), m[2], mul(bc<T>(P.G[(i + 1) * 4 + 3]), m[3]))));
-            tau[i] = sel(sat, t, tau[i]);
-        }
+        // realized wrench G m (quad.py:160-168) on G's X structure: rows
+        // (1 1 1 1), ls (1 -1 -1 1), lc (-1 -1 1 1), kr (1 -1 1 -1)
+        const T s01 = add(m[0], m[1]), s23 = add(m[2], m[3]);
+        const T s03 = add(m[0], m[3]), s12 = add(m[1], m[2]);
+        const T s02 = add(m[0], m[2]), s13 = add(m[1], m[3]);
+        f_c = sel(sat, add(s01, s23), f_c);
+        tau[0] = sel(sat, mul(bc<T>(P.G[4]), sub(s03, s12)), tau[0]);
+        tau[1] = sel(sat, mul(bc<T>(P.G[11]), sub(s23, s01)), tau[1]);
+        tau[2] = sel(sat, mul(bc<T>(P.G[12]), sub(s02, s13)), tau[2]);
     }
 }
 
@@ -503,7 +527,7 @@ __device__ __forceinline__ void lag_thrust(const T f[4], const T u[4], T e, T ou
 // this (they are frozen: tau = 0, f_c = 0, state untouched).  A row without a
 // previous sample has no D term (control.py:175-177): the caller sets
 // prev := w for it before the first tick, making the difference exactly 0.
-template <class T>
+template <bool AXI = false, class T>
 __device__ __forceinline__ void pid_row(const T w[3], const T w_sp[3], const swarmstep_quad_params &P,
                                         const Derived &D, float dt, T integ[3], T prev[3], T tau[3])
 {
@@ -512,9 +536,10 @@ __device__ __forceinline__ void pid_row(const T w[3], const T w_sp[3], const swa
         const T e = sub(w_sp[a], w[a]);
         // min/max clamp: a NaN error (NaN rate command) faults the row this
         // tick regardless (tau is NaN), so NaN need not be kept in the state
-        integ[a] = vmin(vmax(fma(bc<T>(dt), e, integ[a]), bc<T>(D.neg_i_limit[a])), bc<T>(P.i_limit[a]));
-        const T t = fma(bc<T>(P.kp[a]), e, mul(bc<T>(P.ki[a]), integ[a]));
-        tau[a] = fnma(bc<T>(D.kd_dt[a]), sub(w[a], prev[a]), t);
+        const int c = axc<AXI>(a);
+        integ[a] = vmin(vmax(fma(bc<T>(dt), e, integ[a]), bc<T>(D.neg_i_limit[c])), bc<T>(P.i_limit[c]));
+        const T t = fma(bc<T>(P.kp[c]), e, mul(bc<T>(P.ki[c]), integ[a]));
+        tau[a] = fnma(bc<T>(D.kd_dt[c]), sub(w[a], prev[a]), t);
         prev[a] = w[a];
     }
 }
@@ -614,7 +639,7 @@ __device__ __forceinline__ void fallback_quat(const T z[3], T cy, T sy, T qd[4])
 #ifndef SSB_QDES_CLOSED
 #define SSB_QDES_CLOSED 1
 #endif
-template <class T>
+template <bool AXI = false, class T>
 __device__ __forceinline__ void outer_row(const T p_err[3], const T v[3], const T q[4], const T v_sp[3],
                                           T cy, T sy, T ch, T sh, const swarmstep_quad_params &P,
                                           const Derived &D, T w_sp[3], T &f_c_sp, T S[3])
@@ -622,7 +647,8 @@ __device__ __forceinline__ void outer_row(const T p_err[3], const T v[3], const 
     const T zero = bc<T>(0.0f), one = bc<T>(1.0f);
     T a[3], z[3];
 #pragma unroll
-    for (int i = 0; i < 3; i++) a[i] = fma(bc<T>(P.kp_pos[i]), p_err[i], mul(bc<T>(P.kv[i]), sub(v_sp[i], v[i])));
+    for (int i = 0; i < 3; i++)
+        a[i] = fma(bc<T>(P.kp_pos[axc<AXI>(i)]), p_err[i], mul(bc<T>(P.kv[axc<AXI>(i)]), sub(v_sp[i], v[i])));
     a[2] = add(a[2], bc<T>(P.g));
     const T asq = fma(a[0], a[0], fma(a[1], a[1], mul(a[2], a[2])));
     const T qw = q[0], qx = q[1], qy = q[2], qz = q[3];
@@ -711,7 +737,7 @@ __device__ __forceinline__ void outer_row(const T p_err[3], const T v[3], const 
     // through the PID and RK4 instead of flying a clamped garbage command
     const T wm = bc<T>(P.omega_sp_max), nwm = bc<T>(D.neg_w_sp_max);
     w_sp[0] = vmin_nan(vmax_nan(mul(bc<T>(P.k_att[0]), mul(e1, factor)), nwm), wm);
-    w_sp[1] = vmin_nan(vmax_nan(mul(bc<T>(P.k_att[1]), mul(e2, factor)), nwm), wm);
+    w_sp[1] = vmin_nan(vmax_nan(mul(bc<T>(P.k_att[axc<AXI>(1)]), mul(e2, factor)), nwm), wm);
     w_sp[2] = vmin_nan(vmax_nan(mul(bc<T>(P.k_att[2]), mul(e3, factor)), nwm), wm);
 }
 

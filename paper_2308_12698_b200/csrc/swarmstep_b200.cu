@@ -9,6 +9,7 @@
 #include <math.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <mutex>
@@ -111,6 +112,26 @@ struct PairRow {
     __device__ __forceinline__ void st(int c, ssb::f2 v) const { a.st(c, v.v.x); b.st(c, v.v.y); }
 };
 
+// Two adjacent rows (2t, 2t + 1) of one tile as one f2 lane pair: every
+// column is one 8-byte access per thread, so a warp moves 256 contiguous
+// bytes per column with one LDG.64 / STG.64 (half the memory instructions of
+// two separate rows) and the lanes land directly in the FFMA2 register pair.
+struct VecPairRow {
+    float *p;     // row 2t, column 0 (8-byte aligned: tiles are 512 B per column)
+    __device__ __forceinline__ ssb::f2 ld(int c) const
+    {
+        return ssb::f2{__ldcs(reinterpret_cast<const float2 *>(p + c * SWARMSTEP_TILE))};
+    }
+    __device__ __forceinline__ ssb::f2 ldc(int c) const
+    {
+        return ssb::f2{__ldg(reinterpret_cast<const float2 *>(p + c * SWARMSTEP_TILE))};
+    }
+    __device__ __forceinline__ void st(int c, ssb::f2 v) const
+    {
+        __stcs(reinterpret_cast<float2 *>(p + c * SWARMSTEP_TILE), v.v);
+    }
+};
+
 template <class T> __device__ __forceinline__ T zero_t() { return ssb::bc<T>(0.0f); }
 
 // Motor-lag policy of a launch.  NoLag: the reference's instantaneous mixer
@@ -154,7 +175,7 @@ struct MotorLagPair {
     static constexpr bool lag_on = true, feed_on = false, axisym = false;
     template <class T> __device__ __forceinline__ void feed(int, RowT<T> &) const {}
     template <class A> __device__ __forceinline__ void store_cmd(const A &, int) const {}
-    float *p0, *p1;          // rows t and t + 64 of one tile (column i at + 128 i)
+    float *p0, *p1;          // rows 2t and 2t + 1 of one tile (column i at + 128 i)
     float phi, e_full;
     ssb::f2 f[4];
     __device__ __forceinline__ void load()
@@ -193,8 +214,7 @@ struct CircleFeedRow {
         values(k, v);
 #pragma unroll
         for (int i = 0; i < 6; i++) R.u[i] = v[i];
-        sincosf(v[6], &R.u[7], &R.u[6]);
-        sincosf(0.5f * v[6], &R.u[9], &R.u[8]);
+        ssb::yaw_terms(v[6], R.u[6], R.u[7], R.u[8], R.u[9]);
     }
     // the command columns the unfused feed would have left: tick k's values
     template <class A> __device__ __forceinline__ void store_cmd(const A &C, int k) const
@@ -219,15 +239,13 @@ struct CircleFeedPair {
         b.values(k, vb);
 #pragma unroll
         for (int i = 0; i < 6; i++) R.u[i] = ssb::f2{make_float2(va[i], vb[i])};
-        float sa, ca, sb, cb;
-        sincosf(va[6], &sa, &ca);
-        sincosf(vb[6], &sb, &cb);
+        float ca, sa, cha, sha, cb, sb, chb, shb;
+        ssb::yaw_terms(va[6], ca, sa, cha, sha);
+        ssb::yaw_terms(vb[6], cb, sb, chb, shb);
         R.u[6] = ssb::f2{make_float2(ca, cb)};
         R.u[7] = ssb::f2{make_float2(sa, sb)};
-        sincosf(0.5f * va[6], &sa, &ca);
-        sincosf(0.5f * vb[6], &sb, &cb);
-        R.u[8] = ssb::f2{make_float2(ca, cb)};
-        R.u[9] = ssb::f2{make_float2(sa, sb)};
+        R.u[8] = ssb::f2{make_float2(cha, chb)};
+        R.u[9] = ssb::f2{make_float2(sha, shb)};
     }
     template <class A> __device__ __forceinline__ void store_cmd(const A &C, int k) const
     {
@@ -312,11 +330,14 @@ __device__ __forceinline__ void store_state(const A &C, int level, RowT<T> &R)
     }
 }
 
-__device__ __forceinline__ void sincos_lane(float x, float &s, float &c) { sincosf(x, &s, &c); }
-__device__ __forceinline__ void sincos_lane(ssb::f2 x, ssb::f2 &s, ssb::f2 &c)
+__device__ __forceinline__ void yaw_lane(float yaw, float &c, float &s, float &ch, float &sh)
 {
-    sincosf(x.v.x, &s.v.x, &c.v.x);
-    sincosf(x.v.y, &s.v.y, &c.v.y);
+    ssb::yaw_terms(yaw, c, s, ch, sh);
+}
+__device__ __forceinline__ void yaw_lane(ssb::f2 yaw, ssb::f2 &c, ssb::f2 &s, ssb::f2 &ch, ssb::f2 &sh)
+{
+    ssb::yaw_terms(yaw.v.x, c.v.x, s.v.x, ch.v.x, sh.v.x);
+    ssb::yaw_terms(yaw.v.y, c.v.y, s.v.y, ch.v.y, sh.v.y);
 }
 
 // Per-launch setpoint preparation (commands are fixed across the K ticks).
@@ -331,8 +352,7 @@ __device__ __forceinline__ void setup_level(const A &C, int level, int overlay_a
     R.w_sp[0] = R.w_sp[1] = R.w_sp[2] = R.f_sp = zero_t<T>();
     if (level == SWARMSTEP_LEVEL_POS) {
         T s, c, sh, ch;
-        sincos_lane(R.u[6], s, c);
-        sincos_lane(ssb::mul(ssb::bc<T>(0.5f), R.u[6]), sh, ch);
+        yaw_lane(R.u[6], c, s, ch, sh);
         R.u[6] = c;
         R.u[7] = s;
         R.u[8] = ch;
@@ -402,10 +422,10 @@ __device__ __forceinline__ int run_ticks(const swarmstep_quad_params &P, const s
             T p_err[3];
 #pragma unroll
             for (int i = 0; i < 3; i++) p_err[i] = ssb::sub(ssb::sub(u[i], R.p_hi[i]), R.p_lo[i]);
-            ssb::outer_row(p_err, R.v, R.q, u + 3, u[6], u[7], u[8], u[9], P, D, R.w_sp, R.f_sp, S);
+            ssb::outer_row<L::axisym>(p_err, R.v, R.q, u + 3, u[6], u[7], u[8], u[9], P, D, R.w_sp, R.f_sp, S);
         }
         T tau[3], f_c = R.f_sp;
-        ssb::pid_row(R.w, R.w_sp, P, D, dt, R.integ, R.prev, tau);
+        ssb::pid_row<L::axisym>(R.w, R.w_sp, P, D, dt, R.integ, R.prev, tau);
         if (RERUN && k == pid_only_at) return -1;
         if constexpr (L::lag_on) {
             // commanded rotor thrusts u; the body integrates the wrench of the
@@ -583,7 +603,7 @@ quad_step_circle_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, i
 }
 
 // ---- paired kernel: two rows per thread on packed FP32x2 (FFMA2) -------------
-// Thread t of a 64-thread CTA owns rows t and t + 64 of one 128-agent tile.
+// Thread t of a 64-thread CTA owns rows 2t and 2t + 1 of one 128-agent tile.
 // When both rows are alive at the same POS or RATE level (the common case)
 // they run as one f2 lane pair: every FFMA / FADD / FMUL of the step becomes
 // one FFMA2 / FADD2 / FMUL2 for both agents, halving the issued FP
@@ -597,24 +617,21 @@ quad_step_circle_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, i
 // The paired kernel's per-thread body.  PF / RF: the launch's policy for the
 // f2 pair and for a scalar row (NoLag, or the in-kernel circle feed, which
 // puts every alive row at POS level).
-template <bool COMP, class PF, class RF>
-__device__ __forceinline__ void pair_body(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t n,
-                                          uint32_t *__restrict__ counters, uint64_t *__restrict__ fault_log,
-                                          int64_t fault_cap, int overlay_active, uint32_t tick_base,
-                                          const int64_t *tick_dev, const swarmstep_quad_params &P,
-                                          const ssb::Derived &D, float dt, int K, int64_t r0, PF pf, RF rf0, RF rf1)
+// The paired kernels' per-thread work once rows r0 and r1 (flag bytes f0,
+// f1) are in registers (R): the f2 lane pair or the scalar path per row.  C
+// addresses the pair in global memory, C0 / C1 the single rows (stores, and
+// the re-reads of a faulted row's launch inputs).
+template <bool COMP, class PA, class PF, class RF>
+__device__ __forceinline__ void pair_rows(uint8_t *__restrict__ flags, uint32_t *__restrict__ counters,
+                                          uint64_t *__restrict__ fault_log, int64_t fault_cap, int overlay_active,
+                                          uint32_t tick_base, const int64_t *tick_dev, const swarmstep_quad_params &P,
+                                          const ssb::Derived &D, float dt, int K, int64_t r0, int64_t r1, uint8_t f0,
+                                          uint8_t f1, const PA &C, const GlobalRow &C0, const GlobalRow &C1,
+                                          RowT<ssb::f2> &R, PF pf, RF rf0, RF rf1)
 {
-    const int64_t r1 = r0 + 64;
-    const uint8_t f0 = flags[r0], f1 = r1 < n ? flags[r1] : 0;
     const bool a0 = f0 & SWARMSTEP_FLAG_ALIVE, a1 = f1 & SWARMSTEP_FLAG_ALIVE;
     const int l0 = PF::feed_on ? SWARMSTEP_LEVEL_POS : (f0 & SWARMSTEP_LEVEL_MASK) >> SWARMSTEP_LEVEL_SHIFT;
     const int l1 = PF::feed_on ? SWARMSTEP_LEVEL_POS : (f1 & SWARMSTEP_LEVEL_MASK) >> SWARMSTEP_LEVEL_SHIFT;
-    const GlobalRow C0{cols + ssb::tile_base(r0)}, C1{cols + ssb::tile_base(r1)};
-    const PairRow<GlobalRow> C{C0, C1};
-    // both rows' loads in flight before any decision (see quad_step_kernel)
-    RowT<ssb::f2> R;
-    load_state<COMP>(C, R);
-    __threadfence_block();
     const bool paired = a0 && a1 && l0 == l1 && l0 != SWARMSTEP_LEVEL_MOTOR;
     if (paired) pf.load();
     bool reload = false;
@@ -653,6 +670,31 @@ __device__ __forceinline__ void pair_body(float *__restrict__ cols, uint8_t *__r
     }
 }
 
+// adjacent rows r0 = 2t, r0 + 1 of a tile loaded straight from HBM (one
+// 8-byte load per column), then pair_rows.  Rows in [n, stride) are dead
+// padding (flags 0), so the pair's second row needs no bound check.
+template <bool COMP, class PF, class RF>
+__device__ __forceinline__ void pair_body(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t n,
+                                          uint32_t *__restrict__ counters, uint64_t *__restrict__ fault_log,
+                                          int64_t fault_cap, int overlay_active, uint32_t tick_base,
+                                          const int64_t *tick_dev, const swarmstep_quad_params &P,
+                                          const ssb::Derived &D, float dt, int K, int64_t r0, PF pf, RF rf0, RF rf1)
+{
+    const int64_t r1 = r0 + 1;
+    const uint16_t ff = *reinterpret_cast<const uint16_t *>(flags + r0);
+    const uint8_t f0 = (uint8_t)(ff & 0xFFu), f1 = (uint8_t)(ff >> 8);
+    float *base = cols + ssb::tile_base(r0);
+    const VecPairRow C{base};
+    const GlobalRow C0{base}, C1{base + 1};
+    // both rows' loads in flight before any decision (see quad_step_kernel)
+    RowT<ssb::f2> R;
+    load_state<COMP>(C, R);
+    __threadfence_block();
+    pair_rows<COMP>(flags, counters, fault_log, fault_cap, overlay_active, tick_base, tick_dev, P, D, dt, K, r0, r1,
+                    f0, f1, C, C0, C1, R, pf, rf0, rf1);
+    (void)n;
+}
+
 template <bool COMP, bool AXI>
 __global__ void __launch_bounds__(64, SSB_PAIR_MINB)
 quad_step_pair_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t n,
@@ -660,7 +702,7 @@ quad_step_pair_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int
                       int64_t fault_cap, int overlay_active, uint32_t tick_base, const int64_t *tick_dev,
                       const swarmstep_quad_params P, const ssb::Derived D, float dt, int K)
 {
-    const int64_t r0 = (int64_t)blockIdx.x * SWARMSTEP_TILE + threadIdx.x;
+    const int64_t r0 = (int64_t)blockIdx.x * SWARMSTEP_TILE + 2 * threadIdx.x;
     if (r0 >= n) return;
     pair_body<COMP>(cols, flags, n, counters, fault_log, fault_cap, overlay_active, tick_base, tick_dev, P, D, dt, K,
                     r0, NoLagT<AXI>(), NoLagT<AXI>(), NoLagT<AXI>());
@@ -675,9 +717,9 @@ quad_step_pair_lag_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags,
                           const swarmstep_quad_params P, const ssb::Derived D, float phi, float e_full, float dt,
                           int K)
 {
-    const int64_t r0 = (int64_t)blockIdx.x * SWARMSTEP_TILE + threadIdx.x;
+    const int64_t r0 = (int64_t)blockIdx.x * SWARMSTEP_TILE + 2 * threadIdx.x;
     if (r0 >= n) return;
-    float *m0 = motor + (r0 >> 7) * (4 * SWARMSTEP_TILE) + (r0 & (SWARMSTEP_TILE - 1)), *m1 = m0 + 64;
+    float *m0 = motor + (r0 >> 7) * (4 * SWARMSTEP_TILE) + (r0 & (SWARMSTEP_TILE - 1)), *m1 = m0 + 1;
     pair_body<COMP>(cols, flags, n, counters, fault_log, fault_cap, overlay_active, tick_base, tick_dev, P, D, dt, K,
                     r0, MotorLagPair{m0, m1, phi, e_full, {}}, MotorLag{m0, phi, e_full, {}},
                     MotorLag{m1, phi, e_full, {}});
@@ -691,12 +733,12 @@ quad_step_pair_circle_kernel(float *__restrict__ cols, uint8_t *__restrict__ fla
                              uint32_t tick_base, const int64_t *tick_dev, const swarmstep_quad_params P,
                              const ssb::Derived D, swarmstep_circle_feed feed, float dt, int K)
 {
-    const int64_t r0 = (int64_t)blockIdx.x * SWARMSTEP_TILE + threadIdx.x;
+    const int64_t r0 = (int64_t)blockIdx.x * SWARMSTEP_TILE + 2 * threadIdx.x;
     if (r0 >= n) return;
     const int64_t tick0 = *tick_dev + (int64_t)tick_base;
     const CircleFeedRow c0{tick0, feed.dt, feed.radius, feed.omega, feed.z, feed.phase0 + feed.dphase * (double)r0};
     const CircleFeedRow c1{tick0, feed.dt, feed.radius, feed.omega, feed.z,
-                           feed.phase0 + feed.dphase * (double)(r0 + 64)};
+                           feed.phase0 + feed.dphase * (double)(r0 + 1)};
     pair_body<COMP>(cols, flags, n, counters, fault_log, fault_cap, 0, tick_base, tick_dev, P, D, dt, K, r0,
                     CircleFeedPair{c0, c1}, c0, c1);
 }
@@ -1123,7 +1165,7 @@ int swarmstep_quad_step(const swarmstep_group_view *g, const swarmstep_quad_para
     if (!g->counters) return set_err(SWARMSTEP_EINVAL, "null counters");
     if (g->n == 0) return SWARMSTEP_OK;
     const ssb::Derived D = ssb::derive(*p, dt);
-    const bool axi = D.gz == 0.0f;   // I_xx == I_yy: the specialised step kernels (NoLagT)
+    const bool axi = D.axisym != 0;   // the axisymmetric-vehicle step kernels (NoLagT<true>)
     const int overlay = launch_flags & SWARMSTEP_STEP_OVERLAY;
     const int motor = (launch_flags & SWARMSTEP_STEP_MOTOR) ? 1 : 0;
     const bool use_tma = (launch_flags & SWARMSTEP_STEP_FORCE_DIRECT) ? false
@@ -1163,9 +1205,10 @@ int swarmstep_quad_step(const swarmstep_group_view *g, const swarmstep_quad_para
     }
     if (!(launch_flags & SWARMSTEP_STEP_FORCE_DIRECT) &&
         ((launch_flags & SWARMSTEP_STEP_FORCE_PAIR) || k_substeps >= SSB_PAIR_MIN_K)) {
+        const int64_t ntiles = (g->n + SWARMSTEP_TILE - 1) / SWARMSTEP_TILE;
         auto kern = axi ? (g->compensated ? quad_step_pair_kernel<true, true> : quad_step_pair_kernel<false, true>)
                         : (g->compensated ? quad_step_pair_kernel<true, false> : quad_step_pair_kernel<false, false>);
-        kern<<<(unsigned)((g->n + SWARMSTEP_TILE - 1) / SWARMSTEP_TILE), 64, 0, (cudaStream_t)stream>>>(
+        kern<<<(unsigned)ntiles, 64, 0, (cudaStream_t)stream>>>(
             g->cols, g->flags, g->n, g->counters, g->fault_log, fcap, overlay, tick_base, tick_dev, *p, D, dt,
             k_substeps);
         return cuda_status("quad_step_pair_kernel");
