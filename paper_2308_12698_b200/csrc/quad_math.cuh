@@ -166,13 +166,13 @@ __device__ __forceinline__ float f32_sat(double x)
 }
 
 // cos / sin of the yaw setpoint and of its half (the outer loop's heading and
-// its quaternion factor): one sincos of yaw/2 and the double-angle formulas
-// (c = (ch - sh)(ch + sh), s = 2 sh ch; ~1e-7 absolute, like sincos itself)
+// its quaternion factor), once per launch.  (Deriving the pair from the half
+// angle by the double-angle formulas saves a sincos but measured 1 % slower per
+// K = 10 launch: profiles/tune_r02/r02n_*.)
 __device__ __forceinline__ void yaw_terms(float yaw, float &c, float &s, float &ch, float &sh)
 {
+    sincosf(yaw, &s, &c);
     sincosf(0.5f * yaw, &sh, &ch);
-    c = __fmul_rn(__fsub_rn(ch, sh), __fadd_rn(ch, sh));
-    s = __fmul_rn(__fadd_rn(sh, sh), ch);
 }
 
 // np.clip semantics: NaN passes through
@@ -250,7 +250,10 @@ __host__ __device__ __forceinline__ Derived derive(const swarmstep_quad_params &
 // inputs are then plain state values, and every product is the reference
 // formula's scaled by an exact power of two.
 // the constant index of axis i: y reads x's constants on an axisymmetric vehicle
-template <bool AXI> __host__ __device__ constexpr int axc(int i) { return (AXI && i == 1) ? 0 : i; }
+#ifndef SSB_AXI_GAINS
+#define SSB_AXI_GAINS 1
+#endif
+template <bool AXI> __host__ __device__ constexpr int axc(int i) { return (SSB_AXI_GAINS && AXI && i == 1) ? 0 : i; }
 
 // thrust direction terms of R(q) e_z = (2 S0, 2 S1, 1 - 2 S2):
 // S0 = qx qz + qw qy, S1 = qy qz - qw qx, S2 = qx^2 + qy^2
@@ -433,6 +436,9 @@ __device__ __forceinline__ void fold_position(T p_hi[3], T p_lo[3])
     }
 }
 
+#ifndef SSB_WRENCH_STRUCT
+#define SSB_WRENCH_STRUCT 1
+#endif
 // mix_to_motors (quad.py:143-168): realized wrench after per-motor clamp.
 // G (quad.py:106-122) has mutually orthogonal rows, so G^-1 = G^T diag(c):
 // motor i = c0 f + s_i1 c1 tau_x + s_i2 c2 tau_y + s_i3 c3 tau_z with the
@@ -454,6 +460,7 @@ __device__ __forceinline__ void mix_row(T &f_c, T tau[3], const swarmstep_quad_p
         for (int i = 0; i < 4; i++) m[i] = clip_nan(m[i], bc<T>(0.0f), bc<T>(P.f_max));
         // realized wrench G m (quad.py:160-168) on G's X structure: rows
         // (1 1 1 1), ls (1 -1 -1 1), lc (-1 -1 1 1), kr (1 -1 1 -1)
+#if SSB_WRENCH_STRUCT
         const T s01 = add(m[0], m[1]), s23 = add(m[2], m[3]);
         const T s03 = add(m[0], m[3]), s12 = add(m[1], m[2]);
         const T s02 = add(m[0], m[2]), s13 = add(m[1], m[3]);
@@ -461,6 +468,15 @@ __device__ __forceinline__ void mix_row(T &f_c, T tau[3], const swarmstep_quad_p
         tau[0] = sel(sat, mul(bc<T>(P.G[4]), sub(s03, s12)), tau[0]);
         tau[1] = sel(sat, mul(bc<T>(P.G[11]), sub(s23, s01)), tau[1]);
         tau[2] = sel(sat, mul(bc<T>(P.G[12]), sub(s02, s13)), tau[2]);
+#else
+        f_c = sel(sat, add(add(m[0], m[1]), add(m[2], m[3])), f_c);
+#pragma unroll
+        for (int i = 0; i < 3; i++) {
+            const T t = fma(bc<T>(P.G[(i + 1) * 4 + 0]), m[0], fma(bc<T>(P.G[(i + 1) * 4 + 1]), m[1],
+                        fma(bc<T>(P.G[(i + 1) * 4 + 2]), m[2], mul(bc<T>(P.G[(i + 1) * 4 + 3]), m[3]))));
+            tau[i] = sel(sat, t, tau[i]);
+        }
+#endif
     }
 }
 

@@ -1,0 +1,52 @@
+// step_launch.h -- internal: the step kernels' launchers, one translation unit
+// per kernel family (step_pair.cu: the paired FFMA2 kernels; step_direct.cu:
+// one row per thread, TMA-staged), called by the C ABI in swarmstep_b200.cu.
+// Each returns an int status like the ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "swarmstep_b200.h"
+#include "quad_math.cuh"
+
+#ifndef SSB_PAIR_MIN_K
+#define SSB_PAIR_MIN_K 2   // auto picks the paired (FFMA2) kernel from this many ticks per launch
+#endif
+#ifndef SSB_TMA_MAX_K
+#define SSB_TMA_MAX_K 0   // auto never picks the TMA-staged kernel (measured slower)
+#endif
+
+namespace ssbl {
+
+struct StepArgs {
+    float *cols;
+    uint8_t *flags;
+    int64_t n;
+    uint32_t *counters;
+    uint64_t *fault_log;
+    int64_t fault_cap;
+    int overlay;
+    uint32_t tick_base;
+    const int64_t *tick_dev;
+    float dt;
+    int k;
+    bool compensated;
+};
+
+int launch_pair(const StepArgs &a, bool axi, const swarmstep_quad_params &P, const ssb::Derived &D, cudaStream_t s);
+int launch_pair_lag(const StepArgs &a, float *motor, float phi, float e_full, const swarmstep_quad_params &P,
+                    const ssb::Derived &D, cudaStream_t s);
+int launch_pair_circle(const StepArgs &a, const swarmstep_circle_feed &feed, const swarmstep_quad_params &P,
+                       const ssb::Derived &D, cudaStream_t s);
+int preload_pair();
+
+int launch_direct(const StepArgs &a, bool axi, const swarmstep_quad_params &P, const ssb::Derived &D, cudaStream_t s);
+int launch_lag(const StepArgs &a, float *motor, float phi, float e_full, const swarmstep_quad_params &P,
+               const ssb::Derived &D, cudaStream_t s);
+int launch_circle(const StepArgs &a, const swarmstep_circle_feed &feed, const swarmstep_quad_params &P,
+                  const ssb::Derived &D, cudaStream_t s);
+int launch_tma(const StepArgs &a, int motor_possible, const swarmstep_quad_params &P, const ssb::Derived &D,
+               cudaStream_t s);
+int preload_direct();
+
+}  // namespace ssbl
