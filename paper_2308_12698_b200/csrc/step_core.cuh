@@ -226,8 +226,9 @@ __device__ __forceinline__ void circle_advance(RowT<T> &R, const CircleRot &r)
     R.u[4] = ssb::mul(bc<T>(r.rws), R.u[7]);
 }
 
-struct CircleFeedRow {
-    static constexpr bool lag_on = false, feed_on = true, axisym = false;
+template <bool AXI>
+struct CircleFeedRowT {
+    static constexpr bool lag_on = false, feed_on = true, axisym = AXI;
     int64_t tick0;
     double dt, radius, omega, z, phase;
     CircleRot rot;
@@ -260,9 +261,10 @@ struct CircleFeedRow {
 };
 
 // Two rows' circle feeds as one f2 lane pair (the paired kernel).
-struct CircleFeedPair {
-    static constexpr bool lag_on = false, feed_on = true, axisym = false;
-    CircleFeedRow a, b;
+template <bool AXI>
+struct CircleFeedPairT {
+    static constexpr bool lag_on = false, feed_on = true, axisym = AXI;
+    CircleFeedRowT<AXI> a, b;
     __device__ __forceinline__ void load() {}
     __device__ __forceinline__ void store() const {}
     __device__ __forceinline__ void feed(int k, RowT<ssb::f2> &R) const
@@ -619,7 +621,7 @@ quad_step_lag_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, floa
 }
 
 // ---- circle-feed kernel: K ticks of the device circle strategy, fused -------
-template <bool COMP>
+template <bool COMP, bool AXI>
 __global__ void __launch_bounds__(kBlock, 4)
 quad_step_circle_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t n,
                         uint32_t *__restrict__ counters, uint64_t *__restrict__ fault_log, int64_t fault_cap,
@@ -631,8 +633,8 @@ quad_step_circle_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, i
     const uint8_t fl = flags[r];
     if (!(fl & SWARMSTEP_FLAG_ALIVE)) return;    // the strategy skips dead agents (client.py:66-67)
     const GlobalRow C{cols + ssb::tile_base(r)};
-    const CircleFeedRow cf{*tick_dev + (int64_t)tick_base, feed.dt, feed.radius, feed.omega, feed.z,
-                           feed.phase0 + feed.dphase * (double)r, circle_rot(feed.dt, feed.radius, feed.omega)};
+    const CircleFeedRowT<AXI> cf{*tick_dev + (int64_t)tick_base, feed.dt, feed.radius, feed.omega, feed.z,
+                                 feed.phase0 + feed.dphase * (double)r, circle_rot(feed.dt, feed.radius, feed.omega)};
     Row R;
     const uint8_t nfl = step_row<COMP>(C, fl, r, 0, P, D, dt, K, tick_base, tick_dev, counters, fault_log,
                                        fault_cap, R, false, cf);
@@ -763,7 +765,7 @@ quad_step_pair_lag_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags,
 }
 
 // the paired kernel with the in-kernel circle feed (every alive row at POS)
-template <bool COMP>
+template <bool COMP, bool AXI>
 __global__ void __launch_bounds__(64, SSB_PAIR_MINB)
 quad_step_pair_circle_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t n,
                              uint32_t *__restrict__ counters, uint64_t *__restrict__ fault_log, int64_t fault_cap,
@@ -774,11 +776,12 @@ quad_step_pair_circle_kernel(float *__restrict__ cols, uint8_t *__restrict__ fla
     if (r0 >= n) return;
     const int64_t tick0 = *tick_dev + (int64_t)tick_base;
     const CircleRot rot = circle_rot(feed.dt, feed.radius, feed.omega);
-    const CircleFeedRow c0{tick0, feed.dt, feed.radius, feed.omega, feed.z, feed.phase0 + feed.dphase * (double)r0, rot};
-    const CircleFeedRow c1{tick0, feed.dt, feed.radius, feed.omega, feed.z,
-                           feed.phase0 + feed.dphase * (double)(r0 + 1), rot};
+    const CircleFeedRowT<AXI> c0{tick0, feed.dt, feed.radius, feed.omega, feed.z,
+                                 feed.phase0 + feed.dphase * (double)r0, rot};
+    const CircleFeedRowT<AXI> c1{tick0, feed.dt, feed.radius, feed.omega, feed.z,
+                                 feed.phase0 + feed.dphase * (double)(r0 + 1), rot};
     pair_body<COMP>(cols, flags, n, counters, fault_log, fault_cap, 0, tick_base, tick_dev, P, D, dt, K, r0,
-                    CircleFeedPair{c0, c1}, c0, c1);
+                    CircleFeedPairT<AXI>{c0, c1}, c0, c1);
 }
 
 // ---- TMA kernel: persistent CTAs, tiles staged through shared memory --------

@@ -42,7 +42,9 @@ int launch_lag(const StepArgs &a, float *motor, float phi, float e_full, const s
 int launch_circle(const StepArgs &a, const swarmstep_circle_feed &feed, const swarmstep_quad_params &P,
                   const ssb::Derived &D, cudaStream_t s)
 {
-    auto kern = a.compensated ? quad_step_circle_kernel<true> : quad_step_circle_kernel<false>;
+    const bool axi = D.axisym != 0;
+    auto kern = axi ? (a.compensated ? quad_step_circle_kernel<true, true> : quad_step_circle_kernel<false, true>)
+                    : (a.compensated ? quad_step_circle_kernel<true, false> : quad_step_circle_kernel<false, false>);
     kern<<<grid_for(a.n, kBlock), kBlock, 0, s>>>(a.cols, a.flags, a.n, a.counters, a.fault_log, a.fault_cap,
                                                   a.tick_base, a.tick_dev, P, D, feed, a.dt, a.k);
     return ssb::cuda_status("quad_step_circle_kernel");
@@ -89,7 +91,10 @@ int preload_direct()
                          (const void *)quad_step_kernel<true, true>, (const void *)quad_step_kernel<false, true>,
                          (const void *)quad_step_tma_kernel<true>, (const void *)quad_step_tma_kernel<false>,
                          (const void *)quad_step_lag_kernel<true>, (const void *)quad_step_lag_kernel<false>,
-                         (const void *)quad_step_circle_kernel<true>, (const void *)quad_step_circle_kernel<false>};
+                         (const void *)quad_step_circle_kernel<true, false>,
+                         (const void *)quad_step_circle_kernel<false, false>,
+                         (const void *)quad_step_circle_kernel<true, true>,
+                         (const void *)quad_step_circle_kernel<false, true>};
     for (const void *f : fns)
         if (cudaFuncGetAttributes(&attr, f) != cudaSuccess) return ssb::cuda_status("cudaFuncGetAttributes");
     return SWARMSTEP_OK;

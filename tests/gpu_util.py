@@ -40,10 +40,11 @@ class _Batch:
         self.alive = st["alive"]
 
 
-def oracle_twin(g, st=None) -> orc.OracleGroup:
-    """float64 oracle group holding exactly the GPU group's current (float32) state."""
+def oracle_twin(g, st=None, params=None) -> orc.OracleGroup:
+    """float64 oracle group holding exactly the GPU group's current (float32) state
+    (``params``: the (QuadParams, PidGains, OuterGains) the group was built with)."""
     st = st or gpu_state(g)
-    og = orc.OracleGroup(0, _Batch(st))
+    og = orc.OracleGroup(0, _Batch(st), *(params or ()))
     og.integral[:] = st["integral"]
     og.prev_omega[:] = st["prev_omega"]
     og.has_prev[:] = st["has_prev"].astype(np.uint8)

@@ -111,3 +111,55 @@ def test_fuzz_kernels_and_fusion_bit_identical(seed, compensated):
             np.testing.assert_array_equal(ref[1][q], ref[7][q], err_msg=f"fused {q}")
     if compensated:
         assert_fusion_close(ref[1], ref[7], ("pos", "vel", "quat", "omega", "integral", "prev_omega"))
+
+
+def _asym_params():
+    """A vehicle that is NOT axisymmetric (I_xx != I_yy, different x / y
+    gains): the general step kernels, not the axisymmetric instantiation."""
+    from paper_2308_12698_b200.params import OuterGains, PidGains, QuadParams
+    quad = QuadParams(m=1.2, i_diag=(0.011, 0.0093, 0.021))
+    rate = PidGains(kp=(0.27, 0.22, 0.11), ki=(0.05, 0.04, 0.02), kd=(0.0021, 0.0018, 0.001),
+                    i_limit=(0.2, 0.15, 0.2))
+    outer = OuterGains(kp_pos=(15.0, 17.0, 16.0), kv=(8.0, 7.5, 8.5), k_att=(12.0, 11.0, 3.0))
+    return quad, rate, outer
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_fuzz_non_axisymmetric_vehicle_per_step(seed):
+    """Per-step parity (and identical fault ids) for a non-axisymmetric vehicle,
+    paired (K = 7) and direct kernels alike."""
+    from paper_2308_12698_b200 import B200QuadGroup, batch_create
+    params = _asym_params()
+    rng, sc = _random_swarm(300 + seed)
+    g = B200QuadGroup(0, batch_create(0, sc.n, sc.pos, quat=sc.quat, vel=sc.vel, omega=sc.omega), *params)
+    _commands(rng, g, sc)
+    g.step_k(sc.dt, 7)                     # the paired kernel on the general (non-AXI) instantiation
+    worst = {}
+    for t in range(6):
+        og = oracle_twin(g, params=params)
+        og_f = og.step(f32(sc.dt))
+        g_f = g.step(sc.dt)
+        assert sorted(g_f.tolist()) == sorted(og_f.tolist()), f"tick {t}: fault ids differ"
+        for k, v in rel_errors(gpu_state(g), og).items():
+            worst[k] = max(worst.get(k, 0.0), v)
+    for k, v in worst.items():
+        assert v <= PER_STEP_TOL, f"seed {seed}: per-step {k} rel err {v:.2e}"
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_non_axisymmetric_kernels_bit_identical(seed):
+    from paper_2308_12698_b200 import B200QuadGroup, batch_create
+    params = _asym_params()
+    outs = []
+    for kern in ("direct", "pair", "tma"):
+        rng, sc = _random_swarm(400 + seed)
+        g = B200QuadGroup(0, batch_create(0, sc.n, sc.pos, quat=sc.quat, vel=sc.vel, omega=sc.omega), *params)
+        g.kernel = kern
+        _commands(rng, g, sc)
+        for _ in range(2):
+            g.step_k(sc.dt, 5)
+        st = gpu_state(g)
+        outs.append({q: st[q].copy() for q in ("pos", "vel", "quat", "omega", "integral", "alive")})
+    for o in outs[1:]:
+        for q in o:
+            np.testing.assert_array_equal(outs[0][q], o[q], err_msg=q)
