@@ -382,6 +382,31 @@ def run_b200(args, rank: int, world: int) -> None:
                "h2d_bytes_per_step": int(7 * 4 * n_total), "d2h_bytes_per_step": 16 * world,
                "ms_per_step": el / args.steps * 1e3,
                "path": "B200QuadGroup.set_setpoints(pinned host) + step_async(dt, K) + collect_faults() per rank"}
+        # informative: the same public-API loop with the setpoints generated on
+        # the device (the circle strategy fused into the step,
+        # CircleFeed.step_fused) -- no per-step setpoint upload, so this is NOT
+        # the e2e figure above (a different setpoint stream, inputs on device)
+        if args.motor_tau == 0.0:
+            from paper_2308_12698_b200.feed import CircleFeed
+            feed = CircleFeed(g, dt)
+
+            def feed_run(steps):
+                for _ in range(steps):
+                    feed.step_fused(k)
+                    g.collect_faults()
+
+            feed_run(args.warmup)
+            barrier()
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            feed_run(args.steps)
+            torch.cuda.synchronize(dev)
+            el = max_over_ranks(time.perf_counter() - t0)
+            barrier()
+            e2e["device_feed"] = {"value": n_total * k * args.steps / el, "ms_per_step": el / args.steps * 1e3,
+                                  "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 16 * world,
+                                  "path": "CircleFeed.step_fused(K) + collect_faults() per rank (setpoints "
+                                          "generated on the device; informative, not the e2e figure)"}
 
     # ---- the reference's CPU path beside the GPU number (rank 0, after the
     # timed regions; every N): the unmodified reference QuadGroup.step on this

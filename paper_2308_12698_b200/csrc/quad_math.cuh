@@ -250,10 +250,7 @@ __host__ __device__ __forceinline__ Derived derive(const swarmstep_quad_params &
 // inputs are then plain state values, and every product is the reference
 // formula's scaled by an exact power of two.
 // the constant index of axis i: y reads x's constants on an axisymmetric vehicle
-#ifndef SSB_AXI_GAINS
-#define SSB_AXI_GAINS 1
-#endif
-template <bool AXI> __host__ __device__ constexpr int axc(int i) { return (SSB_AXI_GAINS && AXI && i == 1) ? 0 : i; }
+template <bool AXI> __host__ __device__ constexpr int axc(int i) { return (AXI && i == 1) ? 0 : i; }
 
 // thrust direction terms of R(q) e_z = (2 S0, 2 S1, 1 - 2 S2):
 // S0 = qx qz + qw qy, S1 = qy qz - qw qx, S2 = qx^2 + qy^2
@@ -303,9 +300,6 @@ __device__ __forceinline__ void deriv(const T q[4], const T w[3], T fc2, T fcg, 
 // dt/6 (v1 + 2 v2 + 2 v3 + v4) with v2 = v + dt/2 k1, v3 = v + dt/2 k2,
 // v4 = v + dt k3 is exactly dt v + dt^2/6 (k1 + k2 + k3), accumulated as it
 // goes (4 FMAs per axis instead of 7, and no stage-velocity registers).
-#ifndef SSB_POS_KSUM
-#define SSB_POS_KSUM 1
-#endif
 // ACC (compensated position only): p_lo is a launch-local accumulator of
 // the position increments against a p_hi held fixed for the whole launch
 // (|acc| grows to about K |v| dt, rounding at ulp(acc) instead of a Fast2Sum
@@ -328,17 +322,11 @@ __device__ __forceinline__ mask_t<T> rk4_inplace(T p_hi[3], T p_lo[3], T v[3], T
     T kv[3], kq[4], kw[3];
     T av[3], aq[4], aw[3];
     T sq[4], sw[3];
-#if SSB_POS_KSUM
     // b = (lo +) dt v, then + dt^2/6 k_i for the first three stages
     const T d26 = bc<T>(D.dt2_sixth);
     T b[3];
 #pragma unroll
     for (int i = 0; i < 3; i++) b[i] = COMP ? fma(dtv, v[i], p_lo[i]) : mul(dtv, v[i]);
-#else
-    T ap[3], sv[3];
-#pragma unroll
-    for (int i = 0; i < 3; i++) ap[i] = v[i];
-#endif
 
     deriv<AXI>(q, w, fc2, fcg, tI, D, kv, kq, kw, S1);                   // k1
 #pragma unroll
@@ -350,12 +338,7 @@ __device__ __forceinline__ mask_t<T> rk4_inplace(T p_hi[3], T p_lo[3], T v[3], T
 #pragma unroll
         for (int i = 0; i < 3; i++) {
             sw[i] = fma(half, kw[i], w[i]);
-#if SSB_POS_KSUM
             b[i] = fma(d26, kv[i], b[i]);
-#else
-            sv[i] = fma(half, kv[i], v[i]);
-            ap[i] = fma(two, sv[i], ap[i]);
-#endif
         }
 #pragma unroll
         for (int i = 0; i < 4; i++) sq[i] = fma(qtr, kq[i], q[i]);
@@ -368,12 +351,7 @@ __device__ __forceinline__ mask_t<T> rk4_inplace(T p_hi[3], T p_lo[3], T v[3], T
 #pragma unroll
     for (int i = 0; i < 3; i++) {
         sw[i] = fma(dtv, kw[i], w[i]);
-#if SSB_POS_KSUM
         b[i] = fma(d26, kv[i], b[i]);
-#else
-        sv[i] = fma(dtv, kv[i], v[i]);
-        ap[i] = add(ap[i], sv[i]);
-#endif
     }
 #pragma unroll
     for (int i = 0; i < 4; i++) sq[i] = fma(half, kq[i], q[i]);
@@ -388,12 +366,7 @@ __device__ __forceinline__ mask_t<T> rk4_inplace(T p_hi[3], T p_lo[3], T v[3], T
     for (int i = 0; i < 3; i++) {
         v[i] = fma(h6, av[i], v[i]);
         w[i] = fma(h6, aw[i], w[i]);
-#if !SSB_POS_KSUM
-        if (!COMP) { p_hi[i] = fma(h6, ap[i], p_hi[i]); continue; }
-        const T b_i = fma(h6, ap[i], p_lo[i]);
-#else
         const T b_i = b[i];
-#endif
         if (COMP && ACC) {
             p_lo[i] = b_i;
         } else if (COMP) {
@@ -436,9 +409,6 @@ __device__ __forceinline__ void fold_position(T p_hi[3], T p_lo[3])
     }
 }
 
-#ifndef SSB_WRENCH_STRUCT
-#define SSB_WRENCH_STRUCT 1
-#endif
 // mix_to_motors (quad.py:143-168): realized wrench after per-motor clamp.
 // G (quad.py:106-122) has mutually orthogonal rows, so G^-1 = G^T diag(c):
 // motor i = c0 f + s_i1 c1 tau_x + s_i2 c2 tau_y + s_i3 c3 tau_z with the
@@ -460,7 +430,6 @@ __device__ __forceinline__ void mix_row(T &f_c, T tau[3], const swarmstep_quad_p
         for (int i = 0; i < 4; i++) m[i] = clip_nan(m[i], bc<T>(0.0f), bc<T>(P.f_max));
         // realized wrench G m (quad.py:160-168) on G's X structure: rows
         // (1 1 1 1), ls (1 -1 -1 1), lc (-1 -1 1 1), kr (1 -1 1 -1)
-#if SSB_WRENCH_STRUCT
         const T s01 = add(m[0], m[1]), s23 = add(m[2], m[3]);
         const T s03 = add(m[0], m[3]), s12 = add(m[1], m[2]);
         const T s02 = add(m[0], m[2]), s13 = add(m[1], m[3]);
@@ -468,15 +437,6 @@ __device__ __forceinline__ void mix_row(T &f_c, T tau[3], const swarmstep_quad_p
         tau[0] = sel(sat, mul(bc<T>(P.G[4]), sub(s03, s12)), tau[0]);
         tau[1] = sel(sat, mul(bc<T>(P.G[11]), sub(s23, s01)), tau[1]);
         tau[2] = sel(sat, mul(bc<T>(P.G[12]), sub(s02, s13)), tau[2]);
-#else
-        f_c = sel(sat, add(add(m[0], m[1]), add(m[2], m[3])), f_c);
-#pragma unroll
-        for (int i = 0; i < 3; i++) {
-            const T t = fma(bc<T>(P.G[(i + 1) * 4 + 0]), m[0], fma(bc<T>(P.G[(i + 1) * 4 + 1]), m[1],
-                        fma(bc<T>(P.G[(i + 1) * 4 + 2]), m[2], mul(bc<T>(P.G[(i + 1) * 4 + 3]), m[3]))));
-            tau[i] = sel(sat, t, tau[i]);
-        }
-#endif
     }
 }
 
@@ -652,9 +612,6 @@ __device__ __forceinline__ void fallback_quat(const T z[3], T cy, T sy, T qd[4])
 // -- (1 + c, s) or (s, 1 - c) -- instead of building R and selecting a
 // branch of _rotmats_to_quats: the same rotation, 21 FP32 operations and
 // three selects instead of 27 and ~24 selects / compares per agent-tick.
-#ifndef SSB_QDES_CLOSED
-#define SSB_QDES_CLOSED 1
-#endif
 template <bool AXI = false, class T>
 __device__ __forceinline__ void outer_row(const T p_err[3], const T v[3], const T q[4], const T v_sp[3],
                                           T cy, T sy, T ch, T sh, const swarmstep_quad_params &P,
@@ -683,7 +640,6 @@ __device__ __forceinline__ void outer_row(const T p_err[3], const T v[3], const 
                      fma(bc<T>(D.two_m), za, mul(bc<T>(P.m), a[2])));
     f_c_sp = vmin(vmax(fc, zero), bc<T>(P.fc_max));
 
-#if SSB_QDES_CLOSED
     // z in the yaw frame; |z x x_c|^2 = z'1^2 + z'2^2 = cos^2 th
     const T zp0 = fma(cy, z[0], mul(sy, z[1]));
     const T nzp1 = fnma(cy, z[1], mul(sy, z[0]));      // -z'1 = cos th sin ph
@@ -721,30 +677,6 @@ __device__ __forceinline__ void outer_row(const T p_err[3], const T v[3], const 
         e2 = sel(degen, fma(qw, qa[2], fma(qx, qa[3], fnma(qy, qa[0], neg(mul(qz, qa[1]))))), e2);
         e3 = sel(degen, fma(qw, qa[3], fnma(qx, qa[2], fnma(qz, qa[0], mul(qy, qa[1])))), e3);
     }
-#else
-    // y = z x x_c / |z x x_c| with x_c = (cy, sy, 0); degenerate fallback from y_c
-    T qd[4];
-    T yd[3];
-    const T yr0 = neg(mul(z[2], sy)), yr1 = mul(z[2], cy), yr2 = fnma(z[1], cy, mul(z[0], sy));
-    const T nysq = fma(yr0, yr0, fma(yr1, yr1, mul(yr2, yr2)));
-    const T iy = rsqrt_a(nysq);
-    yd[0] = mul_nc(yr0, iy); yd[1] = mul_nc(yr1, iy); yd[2] = mul_nc(yr2, iy);   // feed m_ij +- m_ji
-    const mask_t<T> degen = mnot(ge(nysq, bc<T>(1e-12f)));
-    frame_quat(yd, z, qd);
-    if (any(degen)) {
-        T qa[4];
-        fallback_quat(z, cy, sy, qa);
-#pragma unroll
-        for (int i = 0; i < 4; i++) qd[i] = sel(degen, qa[i], qd[i]);
-    }
-    (void)ch; (void)sh;
-    // q_err = conj(q) (x) q_des (quat.py:75-92); the w >= 0 flip becomes |e_w|
-    // and a sign on the rate setpoint
-    const T e0 = fma(qw, qd[0], fma(qx, qd[1], fma(qy, qd[2], mul(qz, qd[3]))));
-    const T e1 = fma(qw, qd[1], fnma(qx, qd[0], fnma(qy, qd[3], mul(qz, qd[2]))));
-    const T e2 = fma(qw, qd[2], fma(qx, qd[3], fnma(qy, qd[0], neg(mul(qz, qd[1])))));
-    const T e3 = fma(qw, qd[3], fnma(qx, qd[2], fnma(qz, qd[0], mul(qy, qd[1]))));
-#endif
     // the w >= 0 flip of q_err becomes |e_w| and a sign on the rate setpoint
     const T ssq = fma(e1, e1, fma(e2, e2, mul(e3, e3)));
     const T factor = axis_angle_factor(sqrt_a(ssq), vabs(e0), e0);
