@@ -112,7 +112,7 @@ typedef struct swarmstep_group_view {
     int64_t n;              /* live rows                                    */
     int64_t stride;         /* row capacity (>= n, multiple of 128)         */
     float *cols;            /* [stride/128][SWARMSTEP_NCOL][128] float32    */
-    uint8_t *flags;         /* [stride]                                     */
+    uint8_t *flags;         /* [stride], 2-byte aligned                     */
     uint32_t *counters;     /* device [4]: 0 faults logged (monotonic), 1 retarget count, 2 viewer count */
     uint64_t *fault_log;    /* device [fault_cap]: (tick << 40) | row       */
     int64_t fault_cap;

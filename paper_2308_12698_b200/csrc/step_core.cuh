@@ -185,24 +185,6 @@ struct MotorLagPair {
 // One launch of K ticks agrees with K x (circle_kernel + 1-tick step) to the
 // rotation's rounding (~1e-7 relative over 25 ticks; a one-tick launch is
 // bit-identical), and the command columns it leaves are tick K-1's exact values.
-struct CircleRot {
-    float omc, sd, omc2, sd2;   // 1 - cos d, sin d, and the same for d / 2 (d = omega dt)
-    float rs, nrs, rws;         // sign(omega) R, -sign(omega) R, sign(omega) R omega
-};
-__device__ __forceinline__ CircleRot circle_rot(double dt, double radius, double omega)
-{
-    const double d = omega * dt, sg = copysign(1.0, omega);
-    const double sh = sin(0.5 * d), sq = sin(0.25 * d);
-    CircleRot r;
-    r.omc = (float)(2.0 * sh * sh);        // 1 - cos d without cancellation
-    r.sd = (float)sin(d);
-    r.omc2 = (float)(2.0 * sq * sq);
-    r.sd2 = (float)sh;
-    r.rs = (float)(sg * radius);
-    r.nrs = -r.rs;
-    r.rws = (float)(sg * radius) * (float)omega;
-    return r;
-}
 // (c, s) turned by the angle with 1 - cos = omc, sin = sd
 template <class T>
 __device__ __forceinline__ void rotate_cs(T &c, T &s, T omc, T sd)
@@ -214,7 +196,7 @@ __device__ __forceinline__ void rotate_cs(T &c, T &s, T omc, T sd)
 }
 // tick k >= 1 of a fused circle launch: u[0..9] of tick k-1 advanced by one tick
 template <class T>
-__device__ __forceinline__ void circle_advance(RowT<T> &R, const CircleRot &r)
+__device__ __forceinline__ void circle_advance(RowT<T> &R, const ssbl::CircleRot &r)
 {
     using ssb::bc;
     rotate_cs(R.u[6], R.u[7], bc<T>(r.omc), bc<T>(r.sd));
@@ -231,7 +213,7 @@ struct CircleFeedRowT {
     static constexpr bool lag_on = false, feed_on = true, axisym = AXI;
     int64_t tick0;
     double dt, radius, omega, z, phase;
-    CircleRot rot;
+    ssbl::CircleRot rot;
     __device__ __forceinline__ void load() {}
     __device__ __forceinline__ void store() const {}
     __device__ __forceinline__ void values(int k, float vals[7]) const
@@ -626,7 +608,8 @@ __global__ void __launch_bounds__(kBlock, 4)
 quad_step_circle_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t n,
                         uint32_t *__restrict__ counters, uint64_t *__restrict__ fault_log, int64_t fault_cap,
                         uint32_t tick_base, const int64_t *tick_dev, const swarmstep_quad_params P,
-                        const ssb::Derived D, swarmstep_circle_feed feed, float dt, int K)
+                        const ssb::Derived D, swarmstep_circle_feed feed, const ssbl::CircleRot rot, float dt,
+                        int K)
 {
     const int64_t r = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     if (r >= n) return;
@@ -634,7 +617,7 @@ quad_step_circle_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, i
     if (!(fl & SWARMSTEP_FLAG_ALIVE)) return;    // the strategy skips dead agents (client.py:66-67)
     const GlobalRow C{cols + ssb::tile_base(r)};
     const CircleFeedRowT<AXI> cf{*tick_dev + (int64_t)tick_base, feed.dt, feed.radius, feed.omega, feed.z,
-                                 feed.phase0 + feed.dphase * (double)r, circle_rot(feed.dt, feed.radius, feed.omega)};
+                                 feed.phase0 + feed.dphase * (double)r, rot};
     Row R;
     const uint8_t nfl = step_row<COMP>(C, fl, r, 0, P, D, dt, K, tick_base, tick_dev, counters, fault_log,
                                        fault_cap, R, false, cf);
@@ -770,12 +753,12 @@ __global__ void __launch_bounds__(64, SSB_PAIR_MINB)
 quad_step_pair_circle_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t n,
                              uint32_t *__restrict__ counters, uint64_t *__restrict__ fault_log, int64_t fault_cap,
                              uint32_t tick_base, const int64_t *tick_dev, const swarmstep_quad_params P,
-                             const ssb::Derived D, swarmstep_circle_feed feed, float dt, int K)
+                             const ssb::Derived D, swarmstep_circle_feed feed, const ssbl::CircleRot rot, float dt,
+                             int K)
 {
     const int64_t r0 = (int64_t)blockIdx.x * SWARMSTEP_TILE + 2 * threadIdx.x;
     if (r0 >= n) return;
     const int64_t tick0 = *tick_dev + (int64_t)tick_base;
-    const CircleRot rot = circle_rot(feed.dt, feed.radius, feed.omega);
     const CircleFeedRowT<AXI> c0{tick0, feed.dt, feed.radius, feed.omega, feed.z,
                                  feed.phase0 + feed.dphase * (double)r0, rot};
     const CircleFeedRowT<AXI> c1{tick0, feed.dt, feed.radius, feed.omega, feed.z,

@@ -46,7 +46,8 @@ int launch_circle(const StepArgs &a, const swarmstep_circle_feed &feed, const sw
     auto kern = axi ? (a.compensated ? quad_step_circle_kernel<true, true> : quad_step_circle_kernel<false, true>)
                     : (a.compensated ? quad_step_circle_kernel<true, false> : quad_step_circle_kernel<false, false>);
     kern<<<grid_for(a.n, kBlock), kBlock, 0, s>>>(a.cols, a.flags, a.n, a.counters, a.fault_log, a.fault_cap,
-                                                  a.tick_base, a.tick_dev, P, D, feed, a.dt, a.k);
+                                                  a.tick_base, a.tick_dev, P, D, feed,
+                                                  circle_rot(feed.dt, feed.radius, feed.omega), a.dt, a.k);
     return ssb::cuda_status("quad_step_circle_kernel");
 }
 

@@ -4,6 +4,7 @@
 // Each returns an int status like the ABI.
 #pragma once
 #include <cuda_runtime.h>
+#include <math.h>
 #include <stdint.h>
 
 #include "swarmstep_b200.h"
@@ -32,6 +33,27 @@ struct StepArgs {
     int k;
     bool compensated;
 };
+
+// Per-launch constants of the fused circle feed's rotation (step_core.cuh
+// circle_advance), computed once on the host in double precision.
+struct CircleRot {
+    float omc, sd, omc2, sd2;   // 1 - cos d, sin d, and the same for d / 2 (d = omega dt)
+    float rs, nrs, rws;         // sign(omega) R, -sign(omega) R, sign(omega) R omega
+};
+inline CircleRot circle_rot(double dt, double radius, double omega)
+{
+    const double d = omega * dt, sg = copysign(1.0, omega);
+    const double sh = sin(0.5 * d), sq = sin(0.25 * d);
+    CircleRot r;
+    r.omc = (float)(2.0 * sh * sh);        // 1 - cos d without cancellation
+    r.sd = (float)sin(d);
+    r.omc2 = (float)(2.0 * sq * sq);
+    r.sd2 = (float)sh;
+    r.rs = (float)(sg * radius);
+    r.nrs = -r.rs;
+    r.rws = (float)(sg * radius) * (float)omega;
+    return r;
+}
 
 int launch_pair(const StepArgs &a, bool axi, const swarmstep_quad_params &P, const ssb::Derived &D, cudaStream_t s);
 int launch_pair_lag(const StepArgs &a, float *motor, float phi, float e_full, const swarmstep_quad_params &P,

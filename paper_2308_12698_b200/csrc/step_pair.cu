@@ -34,7 +34,8 @@ int launch_pair_circle(const StepArgs &a, const swarmstep_circle_feed &feed, con
                     : (a.compensated ? quad_step_pair_circle_kernel<true, false>
                                      : quad_step_pair_circle_kernel<false, false>);
     kern<<<(unsigned)((a.n + SWARMSTEP_TILE - 1) / SWARMSTEP_TILE), 64, 0, s>>>(
-        a.cols, a.flags, a.n, a.counters, a.fault_log, a.fault_cap, a.tick_base, a.tick_dev, P, D, feed, a.dt, a.k);
+        a.cols, a.flags, a.n, a.counters, a.fault_log, a.fault_cap, a.tick_base, a.tick_dev, P, D, feed,
+        circle_rot(feed.dt, feed.radius, feed.omega), a.dt, a.k);
     return ssb::cuda_status("quad_step_pair_circle_kernel");
 }
 

@@ -29,6 +29,8 @@ int check_view(const swarmstep_group_view *g)
         return set_err(SWARMSTEP_EINVAL, "bad n/stride (stride must be >= n and a multiple of 128)");
     if ((reinterpret_cast<uintptr_t>(g->cols) & 15u) != 0)
         return set_err(SWARMSTEP_EINVAL, "cols must be 16-byte aligned");
+    if ((reinterpret_cast<uintptr_t>(g->flags) & 1u) != 0)    // the paired kernels read two flag bytes at once
+        return set_err(SWARMSTEP_EINVAL, "flags must be 2-byte aligned");
     return SWARMSTEP_OK;
 }
 
