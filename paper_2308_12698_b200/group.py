@@ -669,9 +669,9 @@ class B200QuadGroup:
         self._flush_commands()
         self._launch(dt, k, self._launch_flags(), self._tick & 0xFFFFFF, None)
         self._overlay_reset()
-        # fault counter to pinned host memory, in stream order (read by collect_faults)
-        _lib.check(self._lib.swarmstep_memcpy_async(self._counters_host.data_ptr(), self._counters.data_ptr(),
-                                                    self._counters.numel() * 4, self._stream_h))
+        # no per-launch read-back: back-to-back launches stay back to back on the
+        # stream; collect_faults copies the fault counter once (the log entries
+        # carry their tick)
         self._launched.append((self._tick, k))
         self._tick += k
         self._state_stale = True
@@ -749,6 +749,9 @@ class B200QuadGroup:
 
     def collect_faults(self) -> list[np.ndarray]:
         """Wait for the launches since the last call; fault ids per tick, in row order."""
+        # the fault counter to pinned host memory, stream-ordered after every launch
+        _lib.check(self._lib.swarmstep_memcpy_async(self._counters_host.data_ptr(), self._counters.data_ptr(),
+                                                    self._counters.numel() * 4, self._stream_h))
         self._sync()
         launched, self._launched = self._launched, []
         return self._faults_for([t0 + j for t0, k in launched for j in range(k)])

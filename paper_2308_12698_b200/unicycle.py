@@ -90,8 +90,6 @@ class B200UnicycleGroup(B200QuadGroup):
                    ctypes.c_float(self.params.omega_max), ctypes.c_float(dt), int(k),
                    STEP_OVERLAY if self._overlay_active else 0, self._stream_h)
         self._overlay_reset()
-        _lib.check(self._lib.swarmstep_memcpy_async(self._counters_host.data_ptr(), self._counters.data_ptr(),
-                                                    self._counters.numel() * 4, self._stream_h))
-        self._launched.append((self._tick, k))
+        self._launched.append((self._tick, k))     # collect_faults reads the fault counter
         self._tick += k
         self._state_stale = True
