@@ -77,12 +77,17 @@ class CircleFeed:
         g._flush_commands()
         fp = _lib.CircleFeedParams(self.dt, self.radius, self.omega, self.z, self.phase0, self.dphase)
         with torch.cuda.device(g.device), torch.cuda.stream(g.stream):
-            self.tick.fill_(g._tick)
+            if g._tick < (1 << 31):
+                # the absolute tick as the launch's base over a device zero: no
+                # fill kernel between back-to-back launches
+                tick_ptr, base = self._zero.data_ptr(), g._tick
+            else:
+                self.tick.fill_(g._tick)
+                tick_ptr, base = self.tick.data_ptr(), 0
             _lib.check(self._lib.swarmstep_quad_step_circle(
-                g._view_ref, g._params_ref, ctypes.c_float(self.dt), int(k), g._launch_flags(), ctypes.c_uint32(0),
-                self.tick.data_ptr(), ctypes.byref(fp), ctypes.c_void_p(g.stream.cuda_stream)))
-            g._counters_host.copy_(g._counters, non_blocking=True)
-        g._launched.append((g._tick, k))
+                g._view_ref, g._params_ref, ctypes.c_float(self.dt), int(k), g._launch_flags(),
+                ctypes.c_uint32(base), tick_ptr, ctypes.byref(fp), ctypes.c_void_p(g.stream.cuda_stream)))
+        g._launched.append((g._tick, k))     # collect_faults reads the fault counter
         g._tick += k
         g._state_stale = True
         g._cmd_stale = True
@@ -155,7 +160,6 @@ class TickGraph:
         with torch.cuda.device(g.device), torch.cuda.stream(g.stream):
             self.tick.fill_(g._tick)       # the graph's tick counter follows the group's
             self.graph.replay()
-            g._counters_host.copy_(g._counters, non_blocking=True)
         g._launched.append((g._tick, self.ticks))
         g._tick += self.ticks
         g._state_stale = True
