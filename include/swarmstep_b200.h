@@ -176,6 +176,22 @@ int swarmstep_quad_step(const swarmstep_group_view *g, const swarmstep_quad_para
                         float dt, int k_substeps, int launch_flags, uint32_t tick_base,
                         const int64_t *tick_dev, void *stream);
 
+/* swarmstep_quad_step (tick_dev = NULL) for launches issued back to back on
+ * one stream: the launch may start while the previous overlapped launch of the
+ * same group is still finishing (programmatic dependent launch), each 128-row
+ * tile waiting only for ITS tile of the previous launch.  tile_epoch: one
+ * uint32 per tile (stride / 128), zeroed once, owned by the group; the launch
+ * waits until tile_epoch[t] >= wait_epoch (0: no wait -- the first overlapped
+ * launch) and stores set_epoch (non-zero, after wait_epoch in wrapping order)
+ * when tile t is done.  Kernels other than these step launches keep full
+ * stream ordering, so commands, setpoints or reads enqueued in between need
+ * nothing special.  Not for CUDA-graph capture (the epochs are per launch) and
+ * not with SWARMSTEP_STEP_FORCE_TMA.  Same results as swarmstep_quad_step. */
+int swarmstep_quad_step_overlapped(const swarmstep_group_view *g, const swarmstep_quad_params *p,
+                                   float dt, int k_substeps, int launch_flags, uint32_t tick_base,
+                                   uint32_t *tile_epoch, uint32_t wait_epoch, uint32_t set_epoch,
+                                   void *stream);
+
 /* The synchronous World tick in one call: swarmstep_quad_step(..., tick_dev =
  * NULL, ...), then the four counters copied to counters_host (pinned host
  * memory) and the stream synchronised.  counters_host[0] is the fault-log

@@ -553,30 +553,91 @@ __device__ __forceinline__ uint8_t step_row(const A &C, uint8_t fl, int64_t r, i
     return (uint8_t)(lv | (alive ? SWARMSTEP_FLAG_ALIVE : 0u) | SWARMSTEP_FLAG_HAS_PREV);
 }
 
+// Launch a step kernel, with the programmatic-stream-serialization attribute
+// when `pdl` (the kernel then lets the next such launch start early).
+template <class... KArgs, class... Args>
+int launch_step(void (*kern)(KArgs...), unsigned grid, unsigned block, cudaStream_t s, bool pdl, const char *name,
+                Args... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    if (cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...) != cudaSuccess) return ssb::cuda_status(name);
+    return ssb::cuda_status(name);
+}
+
+// ---- back-to-back step launches that overlap (programmatic dependent launch)
+// A step launch only reads and writes its own tiles, and tile b of launch L+1
+// depends on tile b of launch L alone.  With PDL (the launch attribute set by
+// the host, step_*.cu) every CTA of a step launch lets the next step launch
+// start right away (griddepcontrol.launch_dependents), and a CTA of the next
+// launch waits for its own tile's epoch (acquire) instead of the whole
+// previous grid, so one launch's last wave overlaps the next launch's first.
+// Each CTA publishes its tile's epoch (release) after its stores.  Only step
+// kernels launched this way trigger early; any other kernel in between keeps
+// full stream ordering.  A null tile_epoch disables all of it.
+__device__ __forceinline__ void pdl_enter(const ssbl::Pdl &pdl, int64_t tile)
+{
+    if (!pdl.tile_epoch) return;
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (!pdl.wait) return;
+    if (threadIdx.x == 0) {
+        const long long t0 = clock64();
+        for (;;) {
+            uint32_t v;
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(pdl.tile_epoch + tile) : "memory");
+            if ((int32_t)(v - pdl.wait) >= 0) break;
+            if (clock64() - t0 > (1ll << 35)) __trap();   // ~18 s: a broken chain fails loudly
+            __nanosleep(256);
+        }
+    }
+    __syncthreads();
+}
+__device__ __forceinline__ void pdl_exit(const ssbl::Pdl &pdl, int64_t tile)
+{
+    if (!pdl.tile_epoch) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(pdl.tile_epoch + tile), "r"(pdl.set) : "memory");
+    }
+}
+
 // ---- direct kernel: one row per thread, loads/stores straight to HBM -------
 template <bool COMP, bool AXI>
 __global__ void __launch_bounds__(kBlock, SSB_STEP_MINB)
 quad_step_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t n,
                  uint32_t *__restrict__ counters, uint64_t *__restrict__ fault_log,
                  int64_t fault_cap, int overlay_active, uint32_t tick_base, const int64_t *tick_dev,
-                 const swarmstep_quad_params P, const ssb::Derived D, float dt, int K)
+                 const swarmstep_quad_params P, const ssb::Derived D, float dt, int K, const ssbl::Pdl pdl)
 {
+    pdl_enter(pdl, blockIdx.x);      // kBlock == one tile
     const int64_t r = (int64_t)blockIdx.x * kBlock + threadIdx.x;
-    if (r >= n) return;
-    // every state load is issued before the flag test: one memory round trip
-    // per row (dead rows are rare; their loads are discarded)
-    const uint8_t fl = flags[r];
-    const GlobalRow C{cols + ssb::tile_base(r)};
-    Row R;
-    load_state<COMP>(C, R);
-    // Keep every load of the row ahead of the first use: without this fence
-    // ptxas sinks the level-specific command loads behind the level branch,
-    // adding a second dependent memory round trip to the HBM-bound K = 1 case.
-    __threadfence_block();
-    if (!(fl & SWARMSTEP_FLAG_ALIVE)) return;  // dead rows are frozen (quad.py:395-437)
-    const uint8_t nfl = step_row<COMP>(C, fl, r, overlay_active, P, D, dt, K, tick_base, tick_dev,
-                                       counters, fault_log, fault_cap, R, true, NoLagT<AXI>());
-    if (nfl != fl) flags[r] = nfl;
+    if (r < n) {
+        // every state load is issued before the flag test: one memory round trip
+        // per row (dead rows are rare; their loads are discarded)
+        const uint8_t fl = flags[r];
+        const GlobalRow C{cols + ssb::tile_base(r)};
+        Row R;
+        load_state<COMP>(C, R);
+        // Keep every load of the row ahead of the first use: without this fence
+        // ptxas sinks the level-specific command loads behind the level branch,
+        // adding a second dependent memory round trip to the HBM-bound K = 1 case.
+        __threadfence_block();
+        if (fl & SWARMSTEP_FLAG_ALIVE) {   // dead rows are frozen (quad.py:395-437)
+            const uint8_t nfl = step_row<COMP>(C, fl, r, overlay_active, P, D, dt, K, tick_base, tick_dev,
+                                               counters, fault_log, fault_cap, R, true, NoLagT<AXI>());
+            if (nfl != fl) flags[r] = nfl;
+        }
+    }
+    pdl_exit(pdl, blockIdx.x);
 }
 
 // ---- motor-lag kernel: the direct kernel with the opt-in rotor lag -----------
@@ -722,12 +783,14 @@ __global__ void __launch_bounds__(64, SSB_PAIR_MINB)
 quad_step_pair_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, int64_t n,
                       uint32_t *__restrict__ counters, uint64_t *__restrict__ fault_log,
                       int64_t fault_cap, int overlay_active, uint32_t tick_base, const int64_t *tick_dev,
-                      const swarmstep_quad_params P, const ssb::Derived D, float dt, int K)
+                      const swarmstep_quad_params P, const ssb::Derived D, float dt, int K, const ssbl::Pdl pdl)
 {
+    pdl_enter(pdl, blockIdx.x);
     const int64_t r0 = (int64_t)blockIdx.x * SWARMSTEP_TILE + 2 * threadIdx.x;
-    if (r0 >= n) return;
-    pair_body<COMP>(cols, flags, n, counters, fault_log, fault_cap, overlay_active, tick_base, tick_dev, P, D, dt, K,
-                    r0, NoLagT<AXI>(), NoLagT<AXI>(), NoLagT<AXI>());
+    if (r0 < n)
+        pair_body<COMP>(cols, flags, n, counters, fault_log, fault_cap, overlay_active, tick_base, tick_dev, P, D, dt,
+                        K, r0, NoLagT<AXI>(), NoLagT<AXI>(), NoLagT<AXI>());
+    pdl_exit(pdl, blockIdx.x);
 }
 
 // the paired kernel with the opt-in rotor lag

@@ -21,13 +21,14 @@ std::mutex g_tma_mu;
 
 namespace ssbl {
 
-int launch_direct(const StepArgs &a, bool axi, const swarmstep_quad_params &P, const ssb::Derived &D, cudaStream_t s)
+int launch_direct(const StepArgs &a, bool axi, const swarmstep_quad_params &P, const ssb::Derived &D, cudaStream_t s,
+                  const Pdl &pdl)
 {
     auto kern = axi ? (a.compensated ? quad_step_kernel<true, true> : quad_step_kernel<false, true>)
                     : (a.compensated ? quad_step_kernel<true, false> : quad_step_kernel<false, false>);
-    kern<<<grid_for(a.n, kBlock), kBlock, 0, s>>>(a.cols, a.flags, a.n, a.counters, a.fault_log, a.fault_cap,
-                                                  a.overlay, a.tick_base, a.tick_dev, P, D, a.dt, a.k);
-    return ssb::cuda_status("quad_step_kernel");
+    return launch_step(kern, grid_for(a.n, kBlock), kBlock, s, pdl.tile_epoch != nullptr, "quad_step_kernel", a.cols,
+                       a.flags, a.n, a.counters, a.fault_log, a.fault_cap, a.overlay, a.tick_base, a.tick_dev, P, D,
+                       a.dt, a.k, pdl);
 }
 
 int launch_lag(const StepArgs &a, float *motor, float phi, float e_full, const swarmstep_quad_params &P,

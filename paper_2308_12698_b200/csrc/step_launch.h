@@ -34,6 +34,14 @@ struct StepArgs {
     bool compensated;
 };
 
+// Overlapping back-to-back step launches (step_core.cuh pdl_enter / pdl_exit):
+// per-tile epochs in device memory, the epoch this launch waits for (0: none)
+// and the one it publishes.  tile_epoch == nullptr: a plain launch.
+struct Pdl {
+    uint32_t *tile_epoch;
+    uint32_t wait, set;
+};
+
 // Per-launch constants of the fused circle feed's rotation (step_core.cuh
 // circle_advance), computed once on the host in double precision.
 struct CircleRot {
@@ -55,14 +63,16 @@ inline CircleRot circle_rot(double dt, double radius, double omega)
     return r;
 }
 
-int launch_pair(const StepArgs &a, bool axi, const swarmstep_quad_params &P, const ssb::Derived &D, cudaStream_t s);
+int launch_pair(const StepArgs &a, bool axi, const swarmstep_quad_params &P, const ssb::Derived &D, cudaStream_t s,
+                const Pdl &pdl = Pdl{nullptr, 0, 0});
 int launch_pair_lag(const StepArgs &a, float *motor, float phi, float e_full, const swarmstep_quad_params &P,
                     const ssb::Derived &D, cudaStream_t s);
 int launch_pair_circle(const StepArgs &a, const swarmstep_circle_feed &feed, const swarmstep_quad_params &P,
                        const ssb::Derived &D, cudaStream_t s);
 int preload_pair();
 
-int launch_direct(const StepArgs &a, bool axi, const swarmstep_quad_params &P, const ssb::Derived &D, cudaStream_t s);
+int launch_direct(const StepArgs &a, bool axi, const swarmstep_quad_params &P, const ssb::Derived &D, cudaStream_t s,
+                  const Pdl &pdl = Pdl{nullptr, 0, 0});
 int launch_lag(const StepArgs &a, float *motor, float phi, float e_full, const swarmstep_quad_params &P,
                const ssb::Derived &D, cudaStream_t s);
 int launch_circle(const StepArgs &a, const swarmstep_circle_feed &feed, const swarmstep_quad_params &P,

@@ -6,14 +6,14 @@
 
 namespace ssbl {
 
-int launch_pair(const StepArgs &a, bool axi, const swarmstep_quad_params &P, const ssb::Derived &D, cudaStream_t s)
+int launch_pair(const StepArgs &a, bool axi, const swarmstep_quad_params &P, const ssb::Derived &D, cudaStream_t s,
+                const Pdl &pdl)
 {
     auto kern = axi ? (a.compensated ? quad_step_pair_kernel<true, true> : quad_step_pair_kernel<false, true>)
                     : (a.compensated ? quad_step_pair_kernel<true, false> : quad_step_pair_kernel<false, false>);
-    kern<<<(unsigned)((a.n + SWARMSTEP_TILE - 1) / SWARMSTEP_TILE), 64, 0, s>>>(
-        a.cols, a.flags, a.n, a.counters, a.fault_log, a.fault_cap, a.overlay, a.tick_base, a.tick_dev, P, D, a.dt,
-        a.k);
-    return ssb::cuda_status("quad_step_pair_kernel");
+    return launch_step(kern, (unsigned)((a.n + SWARMSTEP_TILE - 1) / SWARMSTEP_TILE), 64, s, pdl.tile_epoch != nullptr,
+                       "quad_step_pair_kernel", a.cols, a.flags, a.n, a.counters, a.fault_log, a.fault_cap, a.overlay,
+                       a.tick_base, a.tick_dev, P, D, a.dt, a.k, pdl);
 }
 
 int launch_pair_lag(const StepArgs &a, float *motor, float phi, float e_full, const swarmstep_quad_params &P,

@@ -322,6 +322,33 @@ int swarmstep_quad_step(const swarmstep_group_view *g, const swarmstep_quad_para
     return ssbl::launch_direct(args, axi, *p, D, (cudaStream_t)stream);
 }
 
+int swarmstep_quad_step_overlapped(const swarmstep_group_view *g, const swarmstep_quad_params *p, float dt,
+                                   int k_substeps, int launch_flags, uint32_t tick_base, uint32_t *tile_epoch,
+                                   uint32_t wait_epoch, uint32_t set_epoch, void *stream)
+{
+    int st = check_view(g);
+    if (st) return st;
+    if (!p || !tile_epoch) return set_err(SWARMSTEP_EINVAL, "null params / tile_epoch");
+    if (!(dt > 0.0f)) return set_err(SWARMSTEP_EINVAL, "dt must be positive");
+    if (k_substeps < 1) return set_err(SWARMSTEP_EINVAL, "k_substeps must be >= 1");
+    if (!g->counters) return set_err(SWARMSTEP_EINVAL, "null counters");
+    if (set_epoch == 0 || (int32_t)(set_epoch - wait_epoch) <= 0)
+        return set_err(SWARMSTEP_EINVAL, "set_epoch must be non-zero and follow wait_epoch");
+    if (launch_flags & SWARMSTEP_STEP_FORCE_TMA)
+        return set_err(SWARMSTEP_EINVAL, "the TMA-staged kernel does not overlap launches");
+    if (g->n == 0) return SWARMSTEP_OK;
+    const ssb::Derived D = ssb::derive(*p, dt);
+    const bool axi = D.axisym != 0;
+    const ssbl::StepArgs args{g->cols, g->flags, g->n, g->counters, g->fault_log, g->fault_log ? g->fault_cap : 0,
+                              launch_flags & SWARMSTEP_STEP_OVERLAY, tick_base, nullptr, dt, k_substeps,
+                              g->compensated != 0};
+    const ssbl::Pdl pdl{tile_epoch, wait_epoch, set_epoch};
+    if (!(launch_flags & SWARMSTEP_STEP_FORCE_DIRECT) &&
+        ((launch_flags & SWARMSTEP_STEP_FORCE_PAIR) || k_substeps >= SSB_PAIR_MIN_K))
+        return ssbl::launch_pair(args, axi, *p, D, (cudaStream_t)stream, pdl);
+    return ssbl::launch_direct(args, axi, *p, D, (cudaStream_t)stream, pdl);
+}
+
 int swarmstep_quad_step_collect(const swarmstep_group_view *g, const swarmstep_quad_params *p, float dt,
                                 int k_substeps, int launch_flags, uint32_t tick_base, uint32_t *counters_host,
                                 void *stream)

@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from typing import Iterable
 
 import numpy as np
@@ -148,6 +149,13 @@ class DeviceBatchView:
         return self._g.rows_for(agent_id)
 
 
+# Overlapped launches from this many ticks per launch: the compute-bound
+# paired kernel gains (1M agents, K = 10: +6%, profiles/pdl_r02/), while the
+# HBM-bound K = 1 launch loses to the per-tile epoch handshake (0.90 -> 0.81
+# of the copy bandwidth), so short launches keep plain stream order.
+_OVERLAP_MIN_K = 4
+
+
 class B200QuadGroup:
     """One quadrotor type stepped by the sm_100a fused kernel."""
 
@@ -201,6 +209,13 @@ class B200QuadGroup:
                                counters=_ptr(self._counters), fault_log=_ptr(self._fault_log),
                                fault_cap=self._fault_cap, compensated=int(self.compensated))
         self._view_ref = ctypes.byref(self._view)
+        # overlapped step launches (swarmstep_quad_step_overlapped): one epoch
+        # word per tile, the chain's last published epoch (0: no launch yet)
+        with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
+            self._tile_epoch = torch.zeros(self.ntiles, dtype=torch.int32, device=self.device)
+        self._tile_epoch_ptr = _ptr(self._tile_epoch)
+        self._pdl_epoch = 0
+        self.overlap_launches = os.environ.get("SWARMSTEP_B200_NO_OVERLAP", "") != "1"
         self._dev_idx = self.device.index
         self._stream_h = ctypes.c_void_p(self.stream.cuda_stream)
         self._params_ref = ctypes.byref(self._dparams)
@@ -667,7 +682,19 @@ class B200QuadGroup:
             self._overlay_reset()
             raise InvalidStateError("non-finite quaternion input")
         self._flush_commands()
-        self._launch(dt, k, self._launch_flags(), self._tick & 0xFFFFFF, None)
+        flags = self._launch_flags()
+        if (self.overlap_launches and k >= _OVERLAP_MIN_K and self._motor is None
+                and not flags & (STEP_FORCE_TMA | STEP_FORCE_DIRECT)):
+            # back-to-back step launches overlap: each tile of this launch waits
+            # for its own tile of the previous one instead of the whole grid
+            wait = self._pdl_epoch
+            nxt = (wait + 1) & 0xFFFFFFFF or 1
+            self._call(self._lib.swarmstep_quad_step_overlapped, self._params_ref, ctypes.c_float(dt), int(k), flags,
+                       ctypes.c_uint32(self._tick & 0xFFFFFF), self._tile_epoch_ptr, ctypes.c_uint32(wait),
+                       ctypes.c_uint32(nxt), self._stream_h)
+            self._pdl_epoch = nxt
+        else:
+            self._launch(dt, k, flags, self._tick & 0xFFFFFF, None)
         self._overlay_reset()
         # no per-launch read-back: back-to-back launches stay back to back on the
         # stream; collect_faults copies the fault counter once (the log entries
