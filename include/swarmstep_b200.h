@@ -216,6 +216,14 @@ typedef struct swarmstep_circle_feed {
 int swarmstep_quad_step_circle(const swarmstep_group_view *g, const swarmstep_quad_params *p, float dt,
                                int k_substeps, int launch_flags, uint32_t tick_base, const int64_t *tick_dev,
                                const swarmstep_circle_feed *feed, void *stream);
+/* swarmstep_quad_step_circle whose back-to-back launches overlap, with the
+ * tile_epoch / wait_epoch / set_epoch chain of swarmstep_quad_step_overlapped
+ * (the two share one chain per group). */
+int swarmstep_quad_step_circle_overlapped(const swarmstep_group_view *g, const swarmstep_quad_params *p, float dt,
+                                          int k_substeps, int launch_flags, uint32_t tick_base,
+                                          const int64_t *tick_dev, const swarmstep_circle_feed *feed,
+                                          uint32_t *tile_epoch, uint32_t wait_epoch, uint32_t set_epoch,
+                                          void *stream);
 
 /* swarmstep_quad_step with the opt-in first-order rotor lag of the north star
  * (absent in the reference; tau_m = 0 is swarmstep_quad_step

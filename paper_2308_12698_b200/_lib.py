@@ -35,7 +35,7 @@ STEP_OVERLAY, STEP_MOTOR, STEP_FORCE_DIRECT, STEP_FORCE_TMA, STEP_FORCE_PAIR = 0
 EXPORTS = (
     "swarmstep_abi_version", "swarmstep_last_error", "swarmstep_device_info", "swarmstep_preload",
     "swarmstep_memcpy_async", "swarmstep_stream_sync", "swarmstep_quad_params_init",
-    "swarmstep_quad_step", "swarmstep_quad_step_overlapped", "swarmstep_quad_step_collect", "swarmstep_quad_step_lag", "swarmstep_quad_step_circle",
+    "swarmstep_quad_step", "swarmstep_quad_step_overlapped", "swarmstep_quad_step_collect", "swarmstep_quad_step_lag", "swarmstep_quad_step_circle", "swarmstep_quad_step_circle_overlapped",
     "swarmstep_quad_apply_commands", "swarmstep_quad_set_setpoints",
     "swarmstep_quad_mark_dead", "swarmstep_quad_retarget_waypoint", "swarmstep_quad_viewer_overlay",
     "swarmstep_quad_pack_f64", "swarmstep_quad_unpack_f64",
@@ -117,6 +117,9 @@ def _declare(lib) -> None:
     lib.swarmstep_quad_swarm_stats.argtypes = [view, vp, vp, ctypes.c_uint64, vp]
     lib.swarmstep_quad_step_circle.restype = i32
     lib.swarmstep_quad_step_circle.argtypes = [view, vp, f32, i32, i32, ctypes.c_uint32, vp, vp, vp]
+    lib.swarmstep_quad_step_circle_overlapped.restype = i32
+    lib.swarmstep_quad_step_circle_overlapped.argtypes = [view, vp, f32, i32, i32, ctypes.c_uint32, vp, vp, vp,
+                                                          ctypes.c_uint32, ctypes.c_uint32, vp]
     lib.swarmstep_quad_step_lag.restype = i32
     lib.swarmstep_quad_step_lag.argtypes = [view, vp, vp, f32, f32, i32, i32, ctypes.c_uint32, vp, vp]
     lib.swarmstep_quad_apply_commands.restype = i32

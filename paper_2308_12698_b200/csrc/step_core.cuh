@@ -670,19 +670,21 @@ quad_step_circle_kernel(float *__restrict__ cols, uint8_t *__restrict__ flags, i
                         uint32_t *__restrict__ counters, uint64_t *__restrict__ fault_log, int64_t fault_cap,
                         uint32_t tick_base, const int64_t *tick_dev, const swarmstep_quad_params P,
                         const ssb::Derived D, swarmstep_circle_feed feed, const ssbl::CircleRot rot, float dt,
-                        int K)
+                        int K, const ssbl::Pdl pdl)
 {
+    pdl_enter(pdl, blockIdx.x);
     const int64_t r = (int64_t)blockIdx.x * kBlock + threadIdx.x;
-    if (r >= n) return;
-    const uint8_t fl = flags[r];
-    if (!(fl & SWARMSTEP_FLAG_ALIVE)) return;    // the strategy skips dead agents (client.py:66-67)
-    const GlobalRow C{cols + ssb::tile_base(r)};
-    const CircleFeedRowT<AXI> cf{*tick_dev + (int64_t)tick_base, feed.dt, feed.radius, feed.omega, feed.z,
-                                 feed.phase0 + feed.dphase * (double)r, rot};
-    Row R;
-    const uint8_t nfl = step_row<COMP>(C, fl, r, 0, P, D, dt, K, tick_base, tick_dev, counters, fault_log,
-                                       fault_cap, R, false, cf);
-    if (nfl != fl) flags[r] = nfl;
+    const uint8_t fl = r < n ? flags[r] : (uint8_t)0;
+    if (fl & SWARMSTEP_FLAG_ALIVE) {              // the strategy skips dead agents (client.py:66-67)
+        const GlobalRow C{cols + ssb::tile_base(r)};
+        const CircleFeedRowT<AXI> cf{*tick_dev + (int64_t)tick_base, feed.dt, feed.radius, feed.omega, feed.z,
+                                     feed.phase0 + feed.dphase * (double)r, rot};
+        Row R;
+        const uint8_t nfl = step_row<COMP>(C, fl, r, 0, P, D, dt, K, tick_base, tick_dev, counters, fault_log,
+                                           fault_cap, R, false, cf);
+        if (nfl != fl) flags[r] = nfl;
+    }
+    pdl_exit(pdl, blockIdx.x);
 }
 
 // ---- paired kernel: two rows per thread on packed FP32x2 (FFMA2) -------------
@@ -817,17 +819,20 @@ quad_step_pair_circle_kernel(float *__restrict__ cols, uint8_t *__restrict__ fla
                              uint32_t *__restrict__ counters, uint64_t *__restrict__ fault_log, int64_t fault_cap,
                              uint32_t tick_base, const int64_t *tick_dev, const swarmstep_quad_params P,
                              const ssb::Derived D, swarmstep_circle_feed feed, const ssbl::CircleRot rot, float dt,
-                             int K)
+                             int K, const ssbl::Pdl pdl)
 {
+    pdl_enter(pdl, blockIdx.x);
     const int64_t r0 = (int64_t)blockIdx.x * SWARMSTEP_TILE + 2 * threadIdx.x;
-    if (r0 >= n) return;
-    const int64_t tick0 = *tick_dev + (int64_t)tick_base;
-    const CircleFeedRowT<AXI> c0{tick0, feed.dt, feed.radius, feed.omega, feed.z,
-                                 feed.phase0 + feed.dphase * (double)r0, rot};
-    const CircleFeedRowT<AXI> c1{tick0, feed.dt, feed.radius, feed.omega, feed.z,
-                                 feed.phase0 + feed.dphase * (double)(r0 + 1), rot};
-    pair_body<COMP>(cols, flags, n, counters, fault_log, fault_cap, 0, tick_base, tick_dev, P, D, dt, K, r0,
-                    CircleFeedPairT<AXI>{c0, c1}, c0, c1);
+    if (r0 < n) {
+        const int64_t tick0 = *tick_dev + (int64_t)tick_base;
+        const CircleFeedRowT<AXI> c0{tick0, feed.dt, feed.radius, feed.omega, feed.z,
+                                     feed.phase0 + feed.dphase * (double)r0, rot};
+        const CircleFeedRowT<AXI> c1{tick0, feed.dt, feed.radius, feed.omega, feed.z,
+                                     feed.phase0 + feed.dphase * (double)(r0 + 1), rot};
+        pair_body<COMP>(cols, flags, n, counters, fault_log, fault_cap, 0, tick_base, tick_dev, P, D, dt, K, r0,
+                        CircleFeedPairT<AXI>{c0, c1}, c0, c1);
+    }
+    pdl_exit(pdl, blockIdx.x);
 }
 
 // ---- TMA kernel: persistent CTAs, tiles staged through shared memory --------

@@ -41,15 +41,14 @@ int launch_lag(const StepArgs &a, float *motor, float phi, float e_full, const s
 }
 
 int launch_circle(const StepArgs &a, const swarmstep_circle_feed &feed, const swarmstep_quad_params &P,
-                  const ssb::Derived &D, cudaStream_t s)
+                  const ssb::Derived &D, cudaStream_t s, const Pdl &pdl)
 {
     const bool axi = D.axisym != 0;
     auto kern = axi ? (a.compensated ? quad_step_circle_kernel<true, true> : quad_step_circle_kernel<false, true>)
                     : (a.compensated ? quad_step_circle_kernel<true, false> : quad_step_circle_kernel<false, false>);
-    kern<<<grid_for(a.n, kBlock), kBlock, 0, s>>>(a.cols, a.flags, a.n, a.counters, a.fault_log, a.fault_cap,
-                                                  a.tick_base, a.tick_dev, P, D, feed,
-                                                  circle_rot(feed.dt, feed.radius, feed.omega), a.dt, a.k);
-    return ssb::cuda_status("quad_step_circle_kernel");
+    return launch_step(kern, grid_for(a.n, kBlock), kBlock, s, pdl.tile_epoch != nullptr, "quad_step_circle_kernel",
+                       a.cols, a.flags, a.n, a.counters, a.fault_log, a.fault_cap, a.tick_base, a.tick_dev, P, D, feed,
+                       circle_rot(feed.dt, feed.radius, feed.omega), a.dt, a.k, pdl);
 }
 
 int launch_tma(const StepArgs &a, int motor_possible, const swarmstep_quad_params &P, const ssb::Derived &D,

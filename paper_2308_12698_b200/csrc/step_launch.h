@@ -68,7 +68,8 @@ int launch_pair(const StepArgs &a, bool axi, const swarmstep_quad_params &P, con
 int launch_pair_lag(const StepArgs &a, float *motor, float phi, float e_full, const swarmstep_quad_params &P,
                     const ssb::Derived &D, cudaStream_t s);
 int launch_pair_circle(const StepArgs &a, const swarmstep_circle_feed &feed, const swarmstep_quad_params &P,
-                       const ssb::Derived &D, cudaStream_t s);
+                       const ssb::Derived &D, cudaStream_t s,
+                       const Pdl &pdl = Pdl{nullptr, 0, 0});
 int preload_pair();
 
 int launch_direct(const StepArgs &a, bool axi, const swarmstep_quad_params &P, const ssb::Derived &D, cudaStream_t s,
@@ -76,7 +77,8 @@ int launch_direct(const StepArgs &a, bool axi, const swarmstep_quad_params &P, c
 int launch_lag(const StepArgs &a, float *motor, float phi, float e_full, const swarmstep_quad_params &P,
                const ssb::Derived &D, cudaStream_t s);
 int launch_circle(const StepArgs &a, const swarmstep_circle_feed &feed, const swarmstep_quad_params &P,
-                  const ssb::Derived &D, cudaStream_t s);
+                  const ssb::Derived &D, cudaStream_t s,
+                       const Pdl &pdl = Pdl{nullptr, 0, 0});
 int launch_tma(const StepArgs &a, int motor_possible, const swarmstep_quad_params &P, const ssb::Derived &D,
                cudaStream_t s);
 int preload_direct();

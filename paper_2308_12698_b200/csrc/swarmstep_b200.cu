@@ -391,9 +391,9 @@ int swarmstep_quad_step_lag(const swarmstep_group_view *g, const swarmstep_quad_
     return ssbl::launch_lag(args, motor, phi, e_full, *p, D, (cudaStream_t)stream);
 }
 
-int swarmstep_quad_step_circle(const swarmstep_group_view *g, const swarmstep_quad_params *p, float dt,
-                               int k_substeps, int launch_flags, uint32_t tick_base, const int64_t *tick_dev,
-                               const swarmstep_circle_feed *feed, void *stream)
+static int quad_step_circle(const swarmstep_group_view *g, const swarmstep_quad_params *p, float dt, int k_substeps,
+                            int launch_flags, uint32_t tick_base, const int64_t *tick_dev,
+                            const swarmstep_circle_feed *feed, const ssbl::Pdl &pdl, void *stream)
 {
     int st = check_view(g);
     if (st) return st;
@@ -409,8 +409,29 @@ int swarmstep_quad_step_circle(const swarmstep_group_view *g, const swarmstep_qu
                               0, tick_base, tick_dev, dt, k_substeps, g->compensated != 0};
     if (!(launch_flags & SWARMSTEP_STEP_FORCE_DIRECT) &&
         ((launch_flags & SWARMSTEP_STEP_FORCE_PAIR) || k_substeps >= SSB_PAIR_MIN_K))
-        return ssbl::launch_pair_circle(args, *feed, *p, D, (cudaStream_t)stream);
-    return ssbl::launch_circle(args, *feed, *p, D, (cudaStream_t)stream);
+        return ssbl::launch_pair_circle(args, *feed, *p, D, (cudaStream_t)stream, pdl);
+    return ssbl::launch_circle(args, *feed, *p, D, (cudaStream_t)stream, pdl);
+}
+
+int swarmstep_quad_step_circle(const swarmstep_group_view *g, const swarmstep_quad_params *p, float dt,
+                               int k_substeps, int launch_flags, uint32_t tick_base, const int64_t *tick_dev,
+                               const swarmstep_circle_feed *feed, void *stream)
+{
+    return quad_step_circle(g, p, dt, k_substeps, launch_flags, tick_base, tick_dev, feed, ssbl::Pdl{nullptr, 0, 0},
+                            stream);
+}
+
+int swarmstep_quad_step_circle_overlapped(const swarmstep_group_view *g, const swarmstep_quad_params *p, float dt,
+                                          int k_substeps, int launch_flags, uint32_t tick_base,
+                                          const int64_t *tick_dev, const swarmstep_circle_feed *feed,
+                                          uint32_t *tile_epoch, uint32_t wait_epoch, uint32_t set_epoch,
+                                          void *stream)
+{
+    if (!tile_epoch) return set_err(SWARMSTEP_EINVAL, "null tile_epoch");
+    if (set_epoch == 0 || (int32_t)(set_epoch - wait_epoch) <= 0)
+        return set_err(SWARMSTEP_EINVAL, "set_epoch must be non-zero and follow wait_epoch");
+    return quad_step_circle(g, p, dt, k_substeps, launch_flags, tick_base, tick_dev, feed,
+                            ssbl::Pdl{tile_epoch, wait_epoch, set_epoch}, stream);
 }
 
 int swarmstep_quad_apply_commands(const swarmstep_group_view *g, const int64_t *rows, const uint8_t *levels,

@@ -44,6 +44,9 @@ class CircleFeed:
         with torch.cuda.device(group.device):
             self.tick = torch.full((1,), group._tick, dtype=torch.int64, device=group.device)
             self._zero = torch.zeros(1, dtype=torch.int64, device=group.device)
+        self._zero_ptr = ctypes.c_void_p(self._zero.data_ptr())
+        self._tick_ptr = ctypes.c_void_p(self.tick.data_ptr())
+        self._fp_key = None
 
     def apply(self, tick_offset: int = 0, sync_tick: bool = True) -> None:
         """Write the setpoints of the group's current tick (the next one to
@@ -75,18 +78,30 @@ class CircleFeed:
         if getattr(g, "_motor", None) is not None:
             raise ValidationError("the fused circle feed runs the reference mixer (motor_tau = 0)")
         g._flush_commands()
-        fp = _lib.CircleFeedParams(self.dt, self.radius, self.omega, self.z, self.phase0, self.dphase)
-        with torch.cuda.device(g.device), torch.cuda.stream(g.stream):
-            if g._tick < (1 << 31):
-                # the absolute tick as the launch's base over a device zero: no
-                # fill kernel between back-to-back launches
-                tick_ptr, base = self._zero.data_ptr(), g._tick
-            else:
+        # lean per-launch host path (a launch at <= 100k agents is shorter than
+        # the Python around it): the feed struct is rebuilt only when the
+        # feed's attributes change, no torch device / stream guards
+        key = (self.dt, self.radius, self.omega, self.z, self.phase0, self.dphase)
+        if key != self._fp_key:
+            self._fp = _lib.CircleFeedParams(*key)
+            self._fp_ref, self._fp_key = ctypes.byref(self._fp), key
+        if g._tick < (1 << 31):
+            # the absolute tick as the launch's base over a device zero: no
+            # fill kernel between back-to-back launches
+            tick_ptr, base = self._zero_ptr, g._tick
+        else:
+            with torch.cuda.device(g.device), torch.cuda.stream(g.stream):
                 self.tick.fill_(g._tick)
-                tick_ptr, base = self.tick.data_ptr(), 0
-            _lib.check(self._lib.swarmstep_quad_step_circle(
-                g._view_ref, g._params_ref, ctypes.c_float(self.dt), int(k), g._launch_flags(),
-                ctypes.c_uint32(base), tick_ptr, ctypes.byref(fp), ctypes.c_void_p(g.stream.cuda_stream)))
+            tick_ptr, base = self._tick_ptr, 0
+        flags = g._launch_flags()
+        ep = g._overlap_epochs(k, flags)
+        if ep is None:
+            g._call(self._lib.swarmstep_quad_step_circle, g._params_ref, ctypes.c_float(self.dt), int(k), flags,
+                    ctypes.c_uint32(base), tick_ptr, self._fp_ref, g._stream_h)
+        else:    # overlapping the group's previous step launch (group.step_async)
+            g._call(self._lib.swarmstep_quad_step_circle_overlapped, g._params_ref, ctypes.c_float(self.dt), int(k),
+                    flags, ctypes.c_uint32(base), tick_ptr, self._fp_ref, g._tile_epoch_ptr, *ep, g._stream_h)
+            g._pdl_epoch = ep[1].value
         g._launched.append((g._tick, k))     # collect_faults reads the fault counter
         g._tick += k
         g._state_stale = True

@@ -683,16 +683,11 @@ class B200QuadGroup:
             raise InvalidStateError("non-finite quaternion input")
         self._flush_commands()
         flags = self._launch_flags()
-        if (self.overlap_launches and k >= _OVERLAP_MIN_K and self._motor is None
-                and not flags & (STEP_FORCE_TMA | STEP_FORCE_DIRECT)):
-            # back-to-back step launches overlap: each tile of this launch waits
-            # for its own tile of the previous one instead of the whole grid
-            wait = self._pdl_epoch
-            nxt = (wait + 1) & 0xFFFFFFFF or 1
+        ep = self._overlap_epochs(k, flags)
+        if ep is not None:
             self._call(self._lib.swarmstep_quad_step_overlapped, self._params_ref, ctypes.c_float(dt), int(k), flags,
-                       ctypes.c_uint32(self._tick & 0xFFFFFF), self._tile_epoch_ptr, ctypes.c_uint32(wait),
-                       ctypes.c_uint32(nxt), self._stream_h)
-            self._pdl_epoch = nxt
+                       ctypes.c_uint32(self._tick & 0xFFFFFF), self._tile_epoch_ptr, *ep, self._stream_h)
+            self._pdl_epoch = ep[1].value
         else:
             self._launch(dt, k, flags, self._tick & 0xFFFFFF, None)
         self._overlay_reset()
@@ -702,6 +697,17 @@ class B200QuadGroup:
         self._launched.append((self._tick, k))
         self._tick += k
         self._state_stale = True
+
+    def _overlap_epochs(self, k: int, flags: int):
+        """(wait, set) epochs for an overlapped launch (each tile of the launch
+        waits for its own tile of the previous one instead of the whole grid),
+        or None for a plain stream-ordered launch; the caller stores set into
+        _pdl_epoch once the launch is queued."""
+        if not (self.overlap_launches and k >= _OVERLAP_MIN_K and self._motor is None
+                and not flags & (STEP_FORCE_TMA | STEP_FORCE_DIRECT)):
+            return None
+        wait = self._pdl_epoch
+        return ctypes.c_uint32(wait), ctypes.c_uint32((wait + 1) & 0xFFFFFFFF or 1)
 
     def _launch(self, dt: float, k: int, flags: int, tick_base: int, tick_dev) -> None:
         """One step launch on the group's stream (no host bookkeeping)."""

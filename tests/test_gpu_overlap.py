@@ -84,3 +84,26 @@ def test_overlapped_long_chain_matches_ordered():
     cb, flb = _device_state(b)
     np.testing.assert_array_equal(fla, flb)
     assert ca.tobytes() == cb.tobytes()
+
+
+def test_overlapped_circle_feed_chain():
+    """Fused circle-feed launches share the group's overlap chain with plain
+    step launches: the mixed sequence is bit-identical to ordered launches."""
+    from paper_2308_12698_b200.feed import CircleFeed
+    a, b = _groups(300_000, seed=4)
+    fa, fb = CircleFeed(a, 1e-3), CircleFeed(b, 1e-3)
+    for feed, g in ((fa, a), (fb, b)):
+        for _ in range(3):
+            feed.step_fused(10)
+        g.step_async(1e-3, 10)
+        feed.step_fused(5)
+        g.step_async(1e-3, 1)
+        feed.step_fused(10)
+        feed.step_fused(2)
+        feed.step_fused(10)
+        g.collect_faults()
+    assert a._pdl_epoch == 7 and b._pdl_epoch == 0
+    ca, fla = _device_state(a)
+    cb, flb = _device_state(b)
+    np.testing.assert_array_equal(fla, flb)
+    assert ca.tobytes() == cb.tobytes()

@@ -13,7 +13,9 @@ three ways:
   * kernel: the fused step kernel alone at K = 1 (device time per launch);
   * fused:  CircleFeed.step_fused(10) -- the circle strategy evaluated per
             tick inside the step kernel, 10 ticks per launch (device time per
-            tick): the state stays in registers across the ticks.
+            tick): the state stays in registers across the ticks;
+  * plain:  step_async(dt, 10) on the same swarm without the feed (fixed
+            setpoints), the fused feed's own cost by difference.
 Writes JSON to argv[1] (default gpurun_out/latency.json).
 """
 
@@ -82,8 +84,11 @@ def measure(n: int, dt: float = 2e-3, T: int = 100) -> dict:
     g.collect_faults()
     fused_ms = ev_ms(lambda: feed.step_fused(10), 20, g.stream) / 10
     g.collect_faults()
+    # the same launches without the feed (the commands the fused launches left)
+    plain_ms = ev_ms(lambda: g.step_async(dt, 10), 20, g.stream) / 10
+    g.collect_faults()
     return {"n": n, "graph_ms_per_tick": graph_ms, "eager_ms_per_tick": eager_ms, "kernel_ms": kern_ms,
-            "fused_k10_ms_per_tick": fused_ms,
+            "fused_k10_ms_per_tick": fused_ms, "plain_k10_ms_per_tick": plain_ms,
             "graph_agent_steps_per_s": n / (graph_ms * 1e-3), "alive": int(g.batch.alive.sum())}
 
 
