@@ -186,7 +186,10 @@ int swarmstep_quad_step(const swarmstep_group_view *g, const swarmstep_quad_para
  * when tile t is done.  Kernels other than these step launches keep full
  * stream ordering, so commands, setpoints or reads enqueued in between need
  * nothing special.  Not for CUDA-graph capture (the epochs are per launch) and
- * not with SWARMSTEP_STEP_FORCE_TMA.  Same results as swarmstep_quad_step. */
+ * not with SWARMSTEP_STEP_FORCE_TMA.  Same results as swarmstep_quad_step.
+ * A tile that waits ~18 s for its epoch traps (a broken chain fails loudly
+ * instead of hanging): keep overlapped launches to K <= 4096 ticks, and never
+ * pass wait_epoch = 0 after an overlapped launch on the same stream. */
 int swarmstep_quad_step_overlapped(const swarmstep_group_view *g, const swarmstep_quad_params *p,
                                    float dt, int k_substeps, int launch_flags, uint32_t tick_base,
                                    uint32_t *tile_epoch, uint32_t wait_epoch, uint32_t set_epoch,

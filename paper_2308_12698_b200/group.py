@@ -154,6 +154,10 @@ class DeviceBatchView:
 # HBM-bound K = 1 launch loses to the per-tile epoch handshake (0.90 -> 0.81
 # of the copy bandwidth), so short launches keep plain stream order.
 _OVERLAP_MIN_K = 4
+# ... and up to this many: a waiting tile traps after ~18 s (a broken chain
+# fails loudly), far beyond one CTA's K <= 4096 ticks; longer launches keep
+# plain stream order
+_OVERLAP_MAX_K = 4096
 
 
 class B200QuadGroup:
@@ -703,7 +707,7 @@ class B200QuadGroup:
         waits for its own tile of the previous one instead of the whole grid),
         or None for a plain stream-ordered launch; the caller stores set into
         _pdl_epoch once the launch is queued."""
-        if not (self.overlap_launches and k >= _OVERLAP_MIN_K and self._motor is None
+        if not (self.overlap_launches and _OVERLAP_MIN_K <= k <= _OVERLAP_MAX_K and self._motor is None
                 and not flags & (STEP_FORCE_TMA | STEP_FORCE_DIRECT)):
             return None
         wait = self._pdl_epoch
