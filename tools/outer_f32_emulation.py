@@ -1,3 +1,7 @@
+"""Re-run the position outer loop of one diagnosed row in float32 (tuning aid):
+python tools/outer_f32_emulation.py fuzz_diag_SEED.npz -- numpy float32 with
+FMAs emulated through float64 (one rounding), to show that a parity outlier of
+profiles/fuzz_outliers_r02/ is float32 conditioning, not a kernel error."""
 import numpy as np, sys
 d=np.load(sys.argv[1])
 F=np.float32
