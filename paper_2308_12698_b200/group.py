@@ -161,7 +161,13 @@ _OVERLAP_MAX_K = 4096
 
 
 class B200QuadGroup:
-    """One quadrotor type stepped by the sm_100a fused kernel."""
+    """One quadrotor type stepped by the sm_100a fused kernel.
+
+    ``overlap_launches`` (default True; env ``SWARMSTEP_B200_NO_OVERLAP=1``
+    turns it off for new groups) lets back-to-back ``step_async`` launches of
+    4 to 4096 ticks overlap tile by tile (swarmstep_quad_step_overlapped);
+    results are bit-identical either way.
+    """
 
     kind = "quadrotor"
 
