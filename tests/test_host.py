@@ -282,3 +282,33 @@ def test_pos_lo_decode_layout():
     assert np.array_equal(lo, q * unit)
     # |lo| <= ulp(hi) / 2 fits the 10-bit field with room to spare
     assert np.all(np.abs(q) <= 511)
+
+
+def test_overlap_epoch_policy():
+    """Which step launches join the overlapped chain (group._overlap_epochs):
+    4..4096 ticks, no rotor lag, not forced onto the TMA / direct kernels; the
+    epoch chain skips 0 when it wraps (0 means "no wait")."""
+    from types import SimpleNamespace
+
+    from paper_2308_12698_b200._lib import STEP_FORCE_DIRECT, STEP_FORCE_PAIR, STEP_FORCE_TMA, STEP_OVERLAY
+    from paper_2308_12698_b200.group import B200QuadGroup
+    g = SimpleNamespace(overlap_launches=True, _motor=None, _pdl_epoch=0)
+    ep = B200QuadGroup._overlap_epochs
+
+    def val(e):
+        return None if e is None else (e[0].value, e[1].value)
+
+    assert val(ep(g, 10, 0)) == (0, 1)
+    assert val(ep(g, 4, STEP_OVERLAY | STEP_FORCE_PAIR)) == (0, 1)
+    assert val(ep(g, 4096, 0)) == (0, 1)
+    for k in (1, 2, 3, 4097):
+        assert ep(g, k, 0) is None, k
+    assert ep(g, 10, STEP_FORCE_TMA) is None and ep(g, 10, STEP_FORCE_DIRECT) is None
+    g._pdl_epoch = 0xFFFFFFFF
+    assert val(ep(g, 10, 0)) == (0xFFFFFFFF, 1)
+    g._pdl_epoch = 41
+    assert val(ep(g, 10, 0)) == (41, 42)
+    g._motor = object()
+    assert ep(g, 10, 0) is None
+    g._motor, g.overlap_launches = None, False
+    assert ep(g, 10, 0) is None
