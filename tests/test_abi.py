@@ -139,3 +139,39 @@ def test_c_params_packer_matches_python(lib):
         np.testing.assert_allclose(a, b, rtol=2e-7, atol=0)
     bad = Phys(0.0, 0.01, 0.01, 0.02, 9.81, 1e-8, 1e-10, 0.2, 0.78, 4e4)
     assert lib.swarmstep_quad_params_init(ctypes.byref(DeviceParams()), ctypes.byref(bad), ctypes.byref(Gains())) != 0
+
+
+def test_overlapped_step_argument_checks(lib):
+    """swarmstep_quad_step_overlapped / _circle_overlapped reject a broken
+    epoch chain before anything reaches the device (host-side checks only:
+    the views point at host memory and no call gets as far as a launch)."""
+    from paper_2308_12698_b200 import _lib as L
+    from paper_2308_12698_b200.params import DeviceParams
+    cols = (ctypes.c_float * (L.NCOL * 128))()
+    flags = (ctypes.c_uint16 * 64)()
+    counters = (ctypes.c_uint32 * 4)()
+    epochs = (ctypes.c_uint32 * 1)()
+    p = DeviceParams()
+
+    def view(n):
+        return L.GroupView(n=n, stride=128, cols=ctypes.addressof(cols), flags=ctypes.addressof(flags),
+                           counters=ctypes.addressof(counters), fault_log=None, fault_cap=0, compensated=1)
+
+    def step(n=1, dt=1e-3, k=10, fl=0, ep=epochs, wait=0, set_=1):
+        return lib.swarmstep_quad_step_overlapped(ctypes.byref(view(n)), ctypes.byref(p), ctypes.c_float(dt), k, fl,
+                                                  ctypes.c_uint32(0), ep, ctypes.c_uint32(wait),
+                                                  ctypes.c_uint32(set_), None)
+
+    for kw, msg in ((dict(set_=0), b"set_epoch"), (dict(wait=5, set_=5), b"set_epoch"),
+                    (dict(wait=7, set_=3), b"set_epoch"), (dict(ep=None), b"tile_epoch"),
+                    (dict(fl=L.STEP_FORCE_TMA), b"TMA"), (dict(dt=0.0), b"dt"), (dict(k=0), b"k_substeps")):
+        assert step(**kw) == L.SWARMSTEP_EINVAL, kw
+        assert msg in lib.swarmstep_last_error(), (kw, lib.swarmstep_last_error())
+    assert step(n=0) == L.SWARMSTEP_OK                     # nothing to launch
+    assert step(n=0, wait=0xFFFFFFFF, set_=1) == L.SWARMSTEP_OK   # the chain wraps past 0
+    feed = L.CircleFeedParams(1e-3, 5.0, 0.3, 10.0, 0.0, 0.01)
+    tick = (ctypes.c_int64 * 1)()
+    assert lib.swarmstep_quad_step_circle_overlapped(
+        ctypes.byref(view(1)), ctypes.byref(p), ctypes.c_float(1e-3), 10, 0, ctypes.c_uint32(0), tick,
+        ctypes.byref(feed), None, ctypes.c_uint32(0), ctypes.c_uint32(1), None) == L.SWARMSTEP_EINVAL
+    assert b"tile_epoch" in lib.swarmstep_last_error()
