@@ -103,7 +103,10 @@ def config(args, world: int) -> dict:
             "l2": f"inputs larger than L2 ({-(-n_total // world) * BYTES_WITH_OVERHEAD / 1e9:.2f} GB touched per "
                   f"launch per GPU vs 0.126 GB L2)" if -(-n_total // world) * BYTES_WITH_OVERHEAD > 126e6 else
                   "per-GPU state smaller than L2: launches may hit L2 (not an HBM measurement)",
-            "parallelism": f"agent-index shards x{world}, no collective"}
+            "parallelism": f"agent-index shards x{world}, no collective",
+            "launch_overlap": ("back-to-back K >= 4 launches overlap tile by tile (programmatic dependent launch, "
+                               "per-tile epochs; bit-identical to ordered launches)"
+                               if os.environ.get("SWARMSTEP_B200_NO_OVERLAP", "") != "1" else "off")}
 
 
 class _Batch:
