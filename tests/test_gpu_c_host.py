@@ -16,13 +16,13 @@ pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_ok(), reason="needs C
 DEMO = Path(__file__).resolve().parent.parent / "tools" / "c_host_demo"
 
 
-@pytest.mark.parametrize("n,k,launches", [(1000, 10, 10), (300, 1, 7)])
-def test_c_host_matches_python_group(n, k, launches, tmp_path):
+@pytest.mark.parametrize("n,k,launches,overlap", [(1000, 10, 10, 0), (300, 1, 7, 0), (200_000, 10, 12, 1)])
+def test_c_host_matches_python_group(n, k, launches, overlap, tmp_path):
     if not DEMO.exists():
         pytest.fail("tools/c_host_demo not built (run __graft_entry__.build())")
     dump = tmp_path / "pos.bin"
-    out = subprocess.run([str(DEMO), str(n), str(k), str(launches), str(dump)], capture_output=True, text=True,
-                         timeout=120)
+    out = subprocess.run([str(DEMO), str(n), str(k), str(launches), str(dump), str(overlap)], capture_output=True,
+                         text=True, timeout=120)
     assert out.returncode == 0, out.stderr
     c = json.loads(out.stdout.strip().splitlines()[-1])
 

@@ -108,8 +108,21 @@ int main(int argc, char **argv)
 
     CHECK(swarmstep_quad_unpack_f64(&g, d_pos, d_vel, d_quat, d_omega, d_alive, s));
     CHECK(swarmstep_quad_set_setpoints(&g, 0, n, 0 /* POS */, d_sp, n, s));
-    for (int l = 0; l < launches; l++)
-        CHECK(swarmstep_quad_step(&g, &p, dt, k, 0, (uint32_t)(l * k), NULL, s));
+    /* argv[5] = 1: back-to-back launches overlap tile by tile (one zeroed
+       epoch word per tile; launch l waits for epoch l, publishes l + 1) */
+    const int overlap = argc > 5 ? atoi(argv[5]) : 0;
+    uint32_t *d_epoch = NULL;
+    if (overlap) {
+        CUDA(cudaMalloc((void **)&d_epoch, sizeof(uint32_t) * (size_t)(stride / SWARMSTEP_TILE)));
+        CUDA(cudaMemset(d_epoch, 0, sizeof(uint32_t) * (size_t)(stride / SWARMSTEP_TILE)));
+    }
+    for (int l = 0; l < launches; l++) {
+        if (overlap)
+            CHECK(swarmstep_quad_step_overlapped(&g, &p, dt, k, 0, (uint32_t)(l * k), d_epoch, (uint32_t)l,
+                                                 (uint32_t)(l + 1), s));
+        else
+            CHECK(swarmstep_quad_step(&g, &p, dt, k, 0, (uint32_t)(l * k), NULL, s));
+    }
     CHECK(swarmstep_quad_pack_f64(&g, d_pos, d_vel, d_quat, d_omega, d_alive, s));
     CHECK(swarmstep_stream_sync(s));
     CUDA(cudaMemcpy(pos, d_pos, sizeof(double) * 3 * (size_t)n, cudaMemcpyDeviceToHost));
