@@ -138,3 +138,26 @@ def test_overlapped_chain_with_faults():
     cb, flb = _device_state(b)
     np.testing.assert_array_equal(fla, flb)
     assert ca.tobytes() == cb.tobytes()
+
+
+def test_overlapped_chain_around_graph_replays():
+    """CUDA-graph tick loops (plain launches) between overlapped launches: the
+    chain resumes on the epoch it left, bit-identical to ordered launches."""
+    from paper_2308_12698_b200.feed import CircleFeed, TickGraph
+    a, b = _groups(300_000, seed=9)
+    for g in (a, b):
+        feed = CircleFeed(g, 1e-3)
+        g.step_async(1e-3, 10)
+        tg = TickGraph(g, 1e-3, 5, feed=feed)
+        tg.replay()
+        g.step_async(1e-3, 10)
+        feed.step_fused(10)
+        tg.replay()
+        tg.replay()
+        g.step_async(1e-3, 8)
+        g.collect_faults()
+    assert a._pdl_epoch == 4 and b._pdl_epoch == 0
+    ca, fla = _device_state(a)
+    cb, flb = _device_state(b)
+    np.testing.assert_array_equal(fla, flb)
+    assert ca.tobytes() == cb.tobytes()
